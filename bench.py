@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the RT-GuIDE trajectory-scoring hot path on B200 (BASELINE.json metric).
+
+One step = one planning cycle through the C ABI, every §8(a) row:
+  a1+a2 rtg_map_create   (pack + classify + grids, from device-resident raw map arrays)
+  a3    rtg_traj_upload  (device-resident waypoints of this rank's shard)
+  a4-a6 rtg_score        (collision, visibility + gain, per-trajectory reduction)
+  a7    rtg_best (+ NCCL all_gather of (score, index) across ranks when N > 1)
+Workload: BASELINE.json configs[3] "outdoor" (N=2,000,000 Gaussians, K=16,384 trajectories,
+T=100 waypoints) per GPU; trajectories of the global set are interleaved over ranks
+(k = rank mod N): weak scaling, global K = 16,384 * N.
+
+value = nominal waypoint x Gaussian pair-tests per second over all ranks (K*T*N / step time,
+every pair counted once whether or not it was culled); ms_per_step = planning-cycle latency.
+e2e   = the same step from pinned HOST buffers (H2D copies + 16-byte D2H result inside).
+
+`--impl reference` times the CPU oracle (oracle/, the test-only FP64 reference) on a bounded
+sample of the same workload and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "waypoint x Gaussian pair-tests/s (planning cycle, nominal pairs)"
+UNIT = "pair-tests/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="rtg", choices=["rtg", "reference"])
+    ap.add_argument("--config", default="outdoor", choices=["tiny", "room", "multi_room", "outdoor", "scale"])
+    ap.add_argument("--mode", default="culled", choices=["culled", "dense"])
+    ap.add_argument("--stride", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=-1, help="steps timed per phase (default: all)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- reference arm (CPU oracle)
+def oracle_sample(wl, n_traj, seed=7):
+    import numpy as np
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(wl.K, size=min(n_traj, wl.K), replace=False))
+    t0 = time.perf_counter()
+    O.score(wl, traj_idx=idx)
+    dt = time.perf_counter() - t0
+    pairs = len(idx) * wl.T * wl.N
+    return pairs / dt, dt, len(idx)
+
+
+def oracle_threads():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2409_18122_b200 import workloads as W
+    O.build()
+    wl = W.make(args.config)
+    cores = oracle_threads()
+    n_traj = max(1, min(wl.K, cores))
+    vals, times = [], []
+    for i in range(args.warmup + args.steps):
+        v, dt, nt = oracle_sample(wl, n_traj, seed=100 + i)
+        if i >= args.warmup:
+            vals.append(v)
+            times.append(dt)
+    value = statistics.median(vals)
+    sample = f"{n_traj} random trajectories x T={wl.T} x N={wl.N} per step (full K={wl.K} extrapolated linearly)"
+    ms_full = 1000.0 * wl.K * wl.T * wl.N / value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_full, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} (BASELINE.json configs[3])" if args.config == "outdoor"
+                       else args.config, "N": wl.N, "K": wl.K, "T": wl.T},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- rtg arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2409_18122_b200 import build as B
+    B.build()
+    from paper_2409_18122_b200 import rtg as R
+    from paper_2409_18122_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- workload: the map is replicated; the global trajectory set is interleaved over ranks
+    base = W.make(args.config)
+    Kr = base.K
+    if world > 1:
+        glob = W.make(args.config, K=base.K * world)
+        sel = np.arange(rank, glob.K, world)
+        wl = W.subset_trajectories(glob, sel)
+    else:
+        wl = base
+    N, K, T = wl.N, wl.K, wl.T
+    cam = R.make_camera(wl.camera)
+    params = R.make_params(mode=R.MODE_CULLED if args.mode == "culled" else R.MODE_DENSE,
+                           info_stride=args.stride)
+    to_dev = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    dmap = [to_dev(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)]
+    dtraj = [to_dev(a) for a in (wl.x, wl.y, wl.z, wl.yaw)]
+    pin = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hmap = [pin(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)]
+    htraj = [pin(a) for a in (wl.x, wl.y, wl.z, wl.yaw)]
+    h2d_bytes = sum(a.numel() * a.element_size() for a in hmap + htraj if a is not None)
+    outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
+            torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    gather = torch.zeros(2 * world, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def global_best(score, idx):
+        gidx = rank + idx * world if idx >= 0 else -1
+        if world == 1:
+            return score, gidx
+        mine = torch.tensor([score, float(gidx)], dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(gather, mine)
+        g = gather.view(world, 2).cpu().numpy()
+        top = g[:, 0].max()
+        cands = [int(i) for s, i in g if s == top and i >= 0]
+        return float(top), (min(cands) if cands else -1)
+
+    def step(host: bool):
+        src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
+        m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
+                  device=local)
+        tr = R.Traj.upload(*src_traj, device=local)
+        R.score(m, tr, cam, params, *outs)
+        s, i = R.best(outs[3])
+        res = global_best(s, i)
+        m.close()
+        tr.close()
+        return res
+
+    def timed(host: bool, steps: int, warmup: int):
+        for _ in range(warmup):
+            step(host)
+        torch.cuda.synchronize()
+        total_ms = 0.0
+        res = None
+        for _ in range(steps):
+            flush.fill_(1.0)                     # L2 flush between timed steps (not timed)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            res = step(host)
+            b.record(stream)
+            torch.cuda.synchronize()
+            total_ms += a.elapsed_time(b)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / steps, res
+
+    # ---- device-resident timing (value), with clocks and per-phase events
+    R.profile_read(reset=True)
+    R.profile_enable(True)
+    with ClockSampler(local) as clocks:
+        ms, res = timed(False, args.steps, args.warmup)
+    R.profile_enable(False)
+    prof = R.profile_read(reset=True)
+    # the warm-up steps ran with profiling on as well: per-step phase times use all profiled calls
+    nprof = max(1, prof["calls"]["collision"] or prof["calls"]["visibility_gain"] or 1)
+    launches_per_step = prof["launches"] / (args.steps + args.warmup)
+    clock = clocks.summary()
+    pairs = float(K) * T * N * world
+    value = pairs / (ms / 1000.0)
+
+    # ---- e2e through the same public API from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        ms_e2e, res_e2e = timed(True, args.steps, 1)
+        assert res_e2e == res, (res_e2e, res)
+        e2e = {"value": pairs / (ms_e2e / 1000.0), "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 16 + 68}
+
+    # ---- roofline of the dominant phase
+    phase_ms = {k: v / nprof for k, v in prof["ms"].items()}
+    dom = max(("collision", "visibility_gain", "map_build"), key=lambda k: phase_ms[k])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof = roofline(dom, phase_ms[dom], wl, outs, clock, hbm_peak, R, dev)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cores = oracle_threads()
+        n_traj = max(1, min(K, cores))
+        v, dt, nt = oracle_sample(wl, n_traj)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{nt} random trajectories x T={T} x N={N} of this workload ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "outdoor (BASELINE.json configs[3])" if args.config == "outdoor" else args.config,
+                           "N": N, "K_per_gpu": Kr, "T": T, "mode": args.mode, "info_stride": args.stride,
+                           "parallelism": f"traj-shard x{world}, map replicated",
+                           "l2": "flushed (512 MiB write) between timed steps"},
+                "best": {"score": res[0], "index": res[1]},
+                "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+                "gpu_launches": int(round(launches_per_step)),
+                "clocks": clock, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(phase, ms, wl, outs, clock, hbm_peak, R, dev):
+    """Roofline object for the dominant phase; algorithmic work per unit as in DESIGN.md."""
+    sm_mhz = (clock.get("sm_mhz") or 1965.0)
+    if phase == "map_build":
+        # read 49 B/G raw input, write the packed records; bound: HBM
+        n = wl.N
+        alg_bytes = n * 49 + n * (16 + 8 + 4) + (n // 2) * (16 + 48 + 72)
+        gbs = alg_bytes / (ms / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                "traffic": None, "phase": phase, "ms": ms}
+    # FP32-pipe issue roofline: nominal pairs x the kernel's FP32 instruction budget per pair
+    # would exceed the peak for the culled kernels (they skip pairs), so report pair tests
+    # actually executed is impossible live; we report nominal-pair rate against the dense-kernel
+    # budget as "equivalent" and say so in DESIGN.md.
+    K, T, N = wl.K, wl.T, wl.N
+    feas = float(outs[1].float().mean().item())
+    if phase == "collision":
+        instr_per_pair = 8.0
+        pairs = K * T * wl.flags.astype(bool).__invert__().sum() if wl.flags is not None else K * T * N
+    else:
+        instr_per_pair = 21.0
+        pairs = K * feas * T * N
+    peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # T lane-instr/s
+    ach = pairs * instr_per_pair / (ms / 1e3) / 1e12
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "T FP32-lane-instr/s (dense-equivalent)",
+            "frac": ach / peak, "traffic": None, "phase": phase, "ms": ms}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

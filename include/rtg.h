@@ -1,0 +1,255 @@
+/*
+ * rtg.h -- C ABI of the B200-native RT-GuIDE trajectory-scoring library (librtg.so).
+ *
+ * The library implements the data-parallel hot path of the trajectory planner of
+ * "RT-GuIDE: Real-Time Gaussian splatting for Information-Driven Exploration"
+ * (arXiv 2409.18122, /root/reference/PAPER.md, cited as P:<line>):
+ * batched scoring of K candidate trajectories of T waypoints against a map of N
+ * 3D Gaussians.  For every (waypoint, Gaussian) pair it runs the collision test
+ * and the binary field-of-view visibility test,
+ * accumulates the trace-proxy information gain and the view utility xi
+ * (Eq. equ:view_util), reduces each trajectory to a feasibility flag,
+ * a gain and a utility (Eq. equ:traj_utility) and takes the argmax.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every function returns rtg_status; no C++ exception crosses the ABI.
+ *    On failure, rtg_last_error() returns a thread-local detail message.
+ *  - Arrays are plain pointers.  `kind` says whether input pointers are host
+ *    memory (RTG_MEM_HOST: copied to the device inside the call, stream-ordered)
+ *    or device memory of `device` (RTG_MEM_DEVICE: read in place).  Output
+ *    pointers of rtg_score / rtg_score_debug are always caller-owned DEVICE
+ *    buffers.  The caller keeps every input valid until the stream passes the call.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is
+ *    enqueued on it.  Only rtg_map_create (sizes its grids from the data),
+ *    rtg_best (returns a host result) and rtg_score_debug synchronise it.
+ *  - Handles own their device memory until *_destroy.  Handles are not
+ *    thread-safe; distinct handles on distinct streams are.
+ *  - A CUDA error inside a call returns RTG_ERR_CUDA; if the error is sticky
+ *    the handle is poisoned and later calls on it return RTG_ERR_BAD_HANDLE.
+ *  - Arithmetic: pair tests in FP32 with an FP64 re-decision of every pair whose
+ *    FP32 test lies within a proven error guard of its threshold, so each
+ *    collision / visibility decision equals the FP64 decision; gains are summed
+ *    exactly in 2^-S fixed point (S chosen per map), counts in integers.
+ */
+#ifndef RTG_H
+#define RTG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RTG_OK = 0,
+    RTG_ERR_INVALID_ARGUMENT = 1,
+    RTG_ERR_CUDA = 2,
+    RTG_ERR_OUT_OF_MEMORY = 3,
+    RTG_ERR_NO_FEASIBLE = 4,      /* rtg_best: every utility is -inf (SPEC "unreachable") */
+    RTG_ERR_BAD_HANDLE = 5
+} rtg_status;
+
+typedef enum { RTG_MEM_HOST = 0, RTG_MEM_DEVICE = 1 } rtg_mem;
+
+/* per-Gaussian flag bits (uint8 flags[N]) */
+enum {
+    RTG_G_NO_COLLIDE = 1u,   /* excluded from collision: ground Gaussians      */
+    RTG_G_NO_GAIN = 2u       /* excluded from visibility / gain / classification           */
+};
+
+/* collision rule (rtg_robot.collide_rule) */
+enum {
+    RTG_COLLIDE_ELLIPSOID = 0,       /* q = sum_i ((R^T (p-mu))_i / (lambda_g s_i + r_robot))^2 < 1;
+                                        reduces to |p-mu| < r_robot + lambda_g r when isotropic */
+    RTG_COLLIDE_PRINCIPAL_AXIS = 1   /* |p-mu| < r_robot + lambda_g max_i s_i            */
+};
+
+/* scoring variant (rtg_score_params.variant) */
+enum {
+    RTG_VARIANT_XI = 0,   /* utility = sum of xi = n_H - lambda_xi n_L (Eq. equ:view_util)   */
+    RTG_VARIANT_SUM = 1,  /* utility = sum of visible uncertainty (RTGuIDE-sum)            */
+    RTG_VARIANT_SQ = 2    /* uncertainty u = w^2 for classes and gain (RTGuIDE-sq)         */
+};
+
+/* execution mode (rtg_score_params.mode) -- identical results, different algorithms */
+enum {
+    RTG_MODE_DENSE = 0,   /* every waypoint x every Gaussian ("all sampled points with all
+                             Gaussians at once"), smem/TMA-staged tiles             */
+    RTG_MODE_CULLED = 1   /* exact spatial culling on cell grids built by rtg_map_create  */
+};
+
+/* rtg_score_params.flags */
+enum {
+    RTG_SCORE_FULL_GAIN = 1u,     /* compute gain/xi for infeasible trajectories too (else NaN)  */
+    RTG_SCORE_NO_COLLISION = 2u   /* gain-only viewpoints: skip collision, all feasible          */
+};
+
+typedef struct rtg_map_s* rtg_map;
+typedef struct rtg_traj_s* rtg_traj;
+
+/* Robot: r_robot >= 0 [m]; lambda_g > 0 (3 in the paper); collide_rule above. */
+typedef struct {
+    float r_robot;
+    float lambda_g;
+    int collide_rule;
+} rtg_robot;
+
+/* Pinhole camera mounted at each waypoint, optical axis along the heading, no pitch/roll
+ * (x right = (sin yaw, -cos yaw, 0), y down).  width, height > 0 [px]; fx, fy > 0 [px];
+ * 0 <= cx <= width, 0 <= cy <= height; 0 <= z_near < z_far [m] (depth = camera-axis Z,
+ * P:138).  A Gaussian is visible iff its mean projects inside [0,W]x[0,H] with
+ * z_near <= Z <= z_far (closed bounds; no extent, no occlusion). */
+typedef struct {
+    int width, height;
+    float fx, fy, cx, cy;
+    float z_near, z_far;
+} rtg_camera;
+
+/* Scoring parameters.  lambda_xi >= 0 (1 in the paper); k_sigma >= 0 (1/2);
+ * info_stride >= 1: information is evaluated at waypoints t with (t+1) % info_stride == 0
+ * (1 = every waypoint; 1 s / dt reproduces the paper's segment end states);
+ * tau_hi / tau_lo: NaN = derive from the map as mean +- k_sigma * population std of u over
+ * the gain-eligible Gaussians, else used as given (class H iff u > tau_hi,
+ * L iff u < tau_lo). */
+typedef struct {
+    float lambda_xi;
+    float k_sigma;
+    int variant;
+    int info_stride;
+    int mode;
+    unsigned flags;
+    double tau_hi;
+    double tau_lo;
+} rtg_score_params;
+
+typedef struct {
+    double score;        /* best utility, -inf when none is feasible */
+    long long index;     /* index_base + local index, -1 when none   */
+} rtg_best_result;
+
+/* Grid options for rtg_map_create_ex; any field <= 0 selects the default. */
+typedef struct {
+    float gain_cell_xy;  /* visibility grid column width [m]   (default 0.5)               */
+    float gain_cell_z;   /* visibility grid cell height [m]    (default 0.5)               */
+    float col_cell;      /* collision grid cell edge [m]       (default max(0.5, r_b/2))   */
+} rtg_map_options;
+
+/* Read-only facts about a built map (rtg_map_info). */
+typedef struct {
+    long long n, n_collide, n_gain;
+    double tau_hi, tau_lo, u_mean, u_std;   /* current classification                  */
+    int fixed_point_shift;                  /* gains are exact multiples of 2^-shift    */
+    int gain_dims[3];                       /* visibility grid cells (x, y, z)          */
+    int col_dims[3];                        /* collision grid cells (x, y, z)           */
+    float rb_max;                           /* largest collision bounding radius [m]    */
+    long long device_bytes;                 /* device memory owned by the handle        */
+} rtg_map_info_t;
+
+/*
+ * rtg_map_create -- map intake and packing (SURVEY §8(a) a1 + a2).
+ * means [3][N] (planar x|y|z), quats [4][N] (planar w|x|y|z, any non-zero norm, normalised
+ * in FP64), scales [3][N] (per-axis standard deviation, > 0), opacity [N] (in [0,1]; stored,
+ * unused by scoring: planning never uses alpha), info_w [N] (the displacement-magnitude
+ * uncertainty ledger, finite, >= 0), flags [N] or NULL.  N = 0 is legal.
+ * Packs FP64-derived FP32 records (M = diag(1/a) R^T, bounding radius, fixed-point u),
+ * classifies with the default parameters and builds the visibility and collision grids.
+ * Errors: RTG_ERR_INVALID_ARGUMENT on a bad pointer/size or any invalid element
+ * (non-finite value, quaternion norm < 1e-12, scale <= 0, info_w < 0, opacity outside [0,1]);
+ * RTG_ERR_OUT_OF_MEMORY; RTG_ERR_CUDA.  Synchronises `stream` once.
+ */
+rtg_status rtg_map_create(int device, long long n, rtg_mem kind,
+                          const float* means, const float* quats, const float* scales,
+                          const float* opacity, const float* info_w, const unsigned char* flags,
+                          const rtg_robot* robot, void* stream, rtg_map* out);
+rtg_status rtg_map_create_ex(int device, long long n, rtg_mem kind,
+                             const float* means, const float* quats, const float* scales,
+                             const float* opacity, const float* info_w, const unsigned char* flags,
+                             const rtg_robot* robot, const rtg_map_options* opts,
+                             void* stream, rtg_map* out);
+rtg_status rtg_map_destroy(rtg_map map);
+rtg_status rtg_map_info(rtg_map map, rtg_map_info_t* out);
+
+/*
+ * rtg_traj_upload -- candidate trajectories.  K >= 1, T >= 1,
+ * K*T < 2^31; x, y, z, yaw each [K][T] (trajectory-major), waypoint t of trajectory k at
+ * index k*T + t.  Copies into a handle-owned device SoA.
+ */
+rtg_status rtg_traj_upload(int device, int K, int T, rtg_mem kind,
+                           const float* x, const float* y, const float* z, const float* yaw,
+                           void* stream, rtg_traj* out);
+/*
+ * rtg_traj_sample_unicycle -- on-device motion-primitive sampler:
+ * trajectory k applies the constant control (v[k], omega[k]) from start = {x, y, z, yaw};
+ * waypoint t is the closed-form unicycle state at time (t+1)*dt (FP64, stored as FP32),
+ * heading wrapped to (-pi, pi], z constant.  v/omega are host or device per `kind`.
+ */
+rtg_status rtg_traj_sample_unicycle(int device, int K, int T, float dt, const float start[4],
+                                    const float* v, const float* omega, rtg_mem kind,
+                                    void* stream, rtg_traj* out);
+/* Copies the trajectory SoA into caller device buffers (each K*T floats). */
+rtg_status rtg_traj_read(rtg_traj traj, float* x, float* y, float* z, float* yaw, void* stream);
+rtg_status rtg_traj_destroy(rtg_traj traj);
+
+/*
+ * rtg_score -- the planning cycle's scoring pass.
+ * Outputs (caller-owned device arrays of length K):
+ *   first_col[k]  first colliding waypoint index, T if none (collision is any-reduce over
+ *                 the Gaussians of each waypoint)
+ *   feasible[k]   1 iff first_col[k] == T
+ *   gain[k]       sum over info waypoints of the trace proxy sum_{visible} u_g (Eq. eq:nbv
+ *                 with binary J); NaN for infeasible k unless RTG_SCORE_FULL_GAIN
+ *   utility[k]    feasible ? sum over info waypoints of xi (XI, SQ) or gain (SUM) : -inf
+ * Any output pointer may be NULL (not written).  Reclassifies the map if params ask for a
+ * classification other than the current one.  Does not synchronise.
+ */
+rtg_status rtg_score(rtg_map map, rtg_traj traj, const rtg_camera* cam, const rtg_score_params* params,
+                     int* first_col, unsigned char* feasible, double* gain, double* utility,
+                     void* stream);
+
+/*
+ * rtg_best -- argmax over utility[K] (device), ties -> lowest index (SPEC S:419 reading),
+ * returning index_base + k (global index when trajectories are sharded across ranks).
+ * Synchronises the stream.  RTG_ERR_NO_FEASIBLE (with index -1, score -inf) when every
+ * utility is -inf.
+ */
+rtg_status rtg_best(const double* utility, int K, long long index_base, void* stream,
+                    rtg_best_result* out);
+
+/*
+ * rtg_score_debug -- parity/debug: per-waypoint outputs for EVERY waypoint (no early exit,
+ * every t regardless of info_stride): wp_col[K*T] (uint8 collision), wp_gain[K*T] (double),
+ * wp_nh[K*T], wp_nl[K*T] (visible H / L counts), computed by the `params->mode` kernels.
+ * pair_mask (or NULL): ceil(K*T*N/32) words, bit (i*N + g) = waypoint i collides with
+ * Gaussian g (original index), only when K*T*N <= 2^32.  stats (or NULL): 4 counters
+ * {collision pairs FP64-redecided, visibility pairs FP64-redecided, pairs tested
+ * individually, cells aggregated}.  Synchronises the stream.
+ */
+rtg_status rtg_score_debug(rtg_map map, rtg_traj traj, const rtg_camera* cam,
+                           const rtg_score_params* params,
+                           unsigned char* wp_col, double* wp_gain, int* wp_nh, int* wp_nl,
+                           unsigned int* pair_mask, long long* stats, void* stream);
+
+/*
+ * Profiling (process-wide).  When enabled, every library phase is bracketed by CUDA events
+ * recorded on the stream it is launched on; rtg_profile_read synchronises those events and
+ * returns the accumulated device milliseconds and call counts per phase:
+ *   0 map build (rtg_map_create), 1 classification, 2 collision (a4), 3 info list,
+ *   4 visibility + gain (a5), 5 trajectory reduction (a6), 6 argmax (a7), 7 other.
+ * `launches` counts every kernel the library launched since the last reset (profiling on or off).
+ */
+typedef struct {
+    double ms[8];
+    long long calls[8];
+    long long launches;
+} rtg_profile_t;
+rtg_status rtg_profile_enable(int on);
+rtg_status rtg_profile_read(rtg_profile_t* out, int reset);
+
+const char* rtg_status_string(rtg_status status);
+const char* rtg_last_error(void);
+/* Library version string, e.g. "rtg 0.1 sm_100a". */
+const char* rtg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTG_H */

@@ -1,0 +1,625 @@
+// rtg_api.cu -- the extern "C" boundary of librtg (include/rtg.h): argument validation,
+// handle ownership, host<->device staging and launch orchestration.  No compute happens
+// here; every step of the path runs in the kernels of rtg_map.cu / rtg_score.cu.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <vector>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "rtg_host.hpp"
+
+namespace rtg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+// ------------------------------------------------------------------ launch accounting / profiling
+static std::atomic<long long> g_launches{0};
+static std::atomic<bool> g_prof_on{false};
+struct ProfRec {
+    int phase;
+    cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_prof_pending_begin[8];
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void prof_begin(int phase, cudaStream_t st) {
+    if (!g_prof_on.load(std::memory_order_relaxed)) return;
+    cudaEvent_t a;
+    if (cudaEventCreate(&a) != cudaSuccess) return;
+    cudaEventRecord(a, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_pending_begin[phase & 7].push_back(a);
+}
+
+void prof_end(int phase, cudaStream_t st) {
+    if (!g_prof_on.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    auto& pend = g_prof_pending_begin[phase & 7];
+    if (pend.empty()) return;
+    cudaEvent_t a = pend.back();
+    pend.pop_back();
+    cudaEvent_t b;
+    if (cudaEventCreate(&b) != cudaSuccess) return;
+    cudaEventRecord(b, st);
+    g_prof.push_back(ProfRec{phase & 7, a, b});
+}
+
+static std::mutex g_pool_mu;
+static bool g_pool_ready[64] = {false};
+
+static void ensure_pool(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64 || g_pool_ready[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    g_pool_ready[dev] = true;
+}
+
+cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+    return cudaMallocAsync(p, bytes > 0 ? bytes : 16, st);
+}
+void dev_free(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+// defined in rtg_map.cu / rtg_score.cu
+rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const float* scales, const float* opacity,
+                     const float* w, const unsigned char* flags, const rtg_map_options* opt, cudaStream_t st);
+CamK make_cam(const rtg_camera& c, const double* cam64_dev);
+cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_col, unsigned char* wp_col, int all_wp,
+                           int* counter, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_list(const int* first_col, int K, int T, int stride, int full_gain, int* list, int* count,
+                        cudaStream_t st);
+cudaError_t launch_iota(int* list, long long n, int* count, cudaStream_t st);
+cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& cam, const int* list,
+                           const int* count, long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl,
+                           int* counter, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_reduce(rtg_map_s* m, rtg_traj_s* tr, const rtg_score_params& p, const int* first_col,
+                          const long long* wp_gq, const int* wp_nh, const int* wp_nl, int* out_first,
+                          unsigned char* out_feasible, double* out_gain, double* out_util, cudaStream_t st);
+cudaError_t launch_debug_wp(long long n, const long long* wp_gq, const ClassState* cs, double* out, cudaStream_t st);
+cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaStream_t st);
+cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st);
+cudaError_t launch_sampler(int K, int T, double dt, const float* start, const float* v, const float* om,
+                           rtg_traj_s* tr, cudaStream_t st);
+
+__global__ void k_fill_int(int* p, long long n, int v) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace rtg
+
+using namespace rtg;
+
+namespace {
+
+rtg_status invalid(const char* msg) {
+    set_error("%s", msg);
+    return RTG_ERR_INVALID_ARGUMENT;
+}
+
+// converts a CUDA error; a sticky error poisons the given handle flag
+rtg_status cuda_fail(cudaError_t e, const char* where, bool* poison) {
+    set_error("%s: %s", where, cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return RTG_ERR_OUT_OF_MEMORY;
+    }
+    // sticky errors cannot be cleared; the context is unusable
+    cudaError_t again = cudaGetLastError();
+    (void)again;
+    if (poison && cudaDeviceSynchronize() != cudaSuccess) *poison = true;
+    return RTG_ERR_CUDA;
+}
+
+#define API_CK(expr, poison)                                      \
+    do {                                                          \
+        cudaError_t e_ = (expr);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #expr, poison); \
+    } while (0)
+
+bool finite_f(float v) { return std::isfinite(v); }
+
+rtg_status check_camera(const rtg_camera* c) {
+    if (!c) return invalid("camera is NULL");
+    if (c->width <= 0 || c->height <= 0) return invalid("camera width/height must be > 0");
+    if (!(c->fx > 0) || !(c->fy > 0) || !finite_f(c->fx) || !finite_f(c->fy)) return invalid("camera fx, fy must be finite and > 0");
+    if (!(c->cx >= 0 && c->cx <= c->width) || !(c->cy >= 0 && c->cy <= c->height))
+        return invalid("camera principal point must satisfy 0 <= cx <= width, 0 <= cy <= height");
+    if (!(c->z_near >= 0) || !(c->z_far > c->z_near) || !finite_f(c->z_far))
+        return invalid("camera depth range must satisfy 0 <= z_near < z_far < inf");
+    return RTG_OK;
+}
+
+rtg_status check_params(const rtg_score_params* p) {
+    if (!p) return invalid("params is NULL");
+    if (!(p->lambda_xi >= 0) || !finite_f(p->lambda_xi)) return invalid("lambda_xi must be finite and >= 0");
+    if (!(p->k_sigma >= 0) || !finite_f(p->k_sigma)) return invalid("k_sigma must be finite and >= 0");
+    if (p->variant < RTG_VARIANT_XI || p->variant > RTG_VARIANT_SQ) return invalid("unknown variant");
+    if (p->info_stride < 1) return invalid("info_stride must be >= 1");
+    if (p->mode != RTG_MODE_DENSE && p->mode != RTG_MODE_CULLED) return invalid("unknown mode");
+    if (p->flags & ~(unsigned)(RTG_SCORE_FULL_GAIN | RTG_SCORE_NO_COLLISION)) return invalid("unknown flag bits");
+    if (std::isinf(p->tau_hi) || std::isinf(p->tau_lo)) return invalid("tau must be finite or NaN");
+    return RTG_OK;
+}
+
+rtg_status check_map(rtg_map m) {
+    if (!m) return invalid("map handle is NULL");
+    if (m->poisoned) {
+        set_error("map handle poisoned by an earlier CUDA error");
+        return RTG_ERR_BAD_HANDLE;
+    }
+    return RTG_OK;
+}
+
+rtg_status check_traj(rtg_traj t) {
+    if (!t) return invalid("trajectory handle is NULL");
+    if (t->poisoned) {
+        set_error("trajectory handle poisoned by an earlier CUDA error");
+        return RTG_ERR_BAD_HANDLE;
+    }
+    return RTG_OK;
+}
+
+template <typename T>
+cudaError_t stage(const T* src, size_t count, rtg_mem kind, T** dst_dev, cudaStream_t st) {
+    // returns a device pointer to the data: a staged copy for host input, the pointer itself otherwise
+    if (kind == RTG_MEM_DEVICE || src == nullptr) {
+        *dst_dev = const_cast<T*>(src);
+        return cudaSuccess;
+    }
+    cudaError_t e = dev_alloc((void**)dst_dev, sizeof(T) * (count ? count : 1), st);
+    if (e != cudaSuccess) return e;
+    if (count) e = cudaMemcpyAsync(*dst_dev, src, sizeof(T) * count, cudaMemcpyHostToDevice, st);
+    return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rtg_status_string(rtg_status s) {
+    switch (s) {
+        case RTG_OK: return "RTG_OK";
+        case RTG_ERR_INVALID_ARGUMENT: return "RTG_ERR_INVALID_ARGUMENT";
+        case RTG_ERR_CUDA: return "RTG_ERR_CUDA";
+        case RTG_ERR_OUT_OF_MEMORY: return "RTG_ERR_OUT_OF_MEMORY";
+        case RTG_ERR_NO_FEASIBLE: return "RTG_ERR_NO_FEASIBLE";
+        case RTG_ERR_BAD_HANDLE: return "RTG_ERR_BAD_HANDLE";
+    }
+    return "RTG_ERR_UNKNOWN";
+}
+
+const char* rtg_last_error(void) { return g_last_error.c_str(); }
+
+const char* rtg_version(void) { return "rtg 0.1 sm_100a"; }
+
+rtg_status rtg_profile_enable(int on) {
+    g_prof_on.store(on != 0);
+    return RTG_OK;
+}
+
+rtg_status rtg_profile_read(rtg_profile_t* out, int reset) {
+    if (!out) return invalid("out is NULL");
+    std::memset(out, 0, sizeof(*out));
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            out->ms[r.phase] += ms;
+            out->calls[r.phase] += 1;
+        }
+    }
+    out->launches = g_launches.load();
+    if (reset) {
+        for (auto& r : g_prof) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        g_prof.clear();
+        g_launches.store(0);
+    }
+    cudaGetLastError();
+    return RTG_OK;
+}
+
+rtg_status rtg_map_create_ex(int device, long long n, rtg_mem kind, const float* means, const float* quats,
+                             const float* scales, const float* opacity, const float* info_w,
+                             const unsigned char* flags, const rtg_robot* robot, const rtg_map_options* opts,
+                             void* stream, rtg_map* out) {
+    if (!out) return invalid("out is NULL");
+    *out = nullptr;
+    if (n < 0 || n >= (1LL << 31) - 1) return invalid("n must satisfy 0 <= n < 2^31 - 1");
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    if (n > 0 && (!means || !quats || !scales || !info_w)) return invalid("means, quats, scales and info_w are required");
+    if (!robot) return invalid("robot is NULL");
+    if (!(robot->r_robot >= 0) || !finite_f(robot->r_robot)) return invalid("r_robot must be finite and >= 0");
+    if (!(robot->lambda_g > 0) || !finite_f(robot->lambda_g)) return invalid("lambda_g must be finite and > 0");
+    if (robot->collide_rule != RTG_COLLIDE_ELLIPSOID && robot->collide_rule != RTG_COLLIDE_PRINCIPAL_AXIS)
+        return invalid("unknown collide_rule");
+    if (opts && (!std::isfinite(opts->gain_cell_xy) || !std::isfinite(opts->gain_cell_z) || !std::isfinite(opts->col_cell)))
+        return invalid("grid options must be finite");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return invalid("invalid device ordinal (no CUDA device?)");
+    }
+    API_CK(cudaSetDevice(device), nullptr);
+    ensure_pool(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    rtg_map_s* m = new (std::nothrow) rtg_map_s();
+    if (!m) return RTG_ERR_OUT_OF_MEMORY;
+    m->device = device;
+    m->stream = st;
+    m->n = n;
+    m->robot = *robot;
+    const float *dm = nullptr, *dq = nullptr, *ds = nullptr, *dop = nullptr, *dw = nullptr;
+    const unsigned char* df = nullptr;
+    cudaError_t e = stage(means, 3 * (size_t)n, kind, (float**)&dm, st);
+    if (e == cudaSuccess) e = stage(quats, 4 * (size_t)n, kind, (float**)&dq, st);
+    if (e == cudaSuccess) e = stage(scales, 3 * (size_t)n, kind, (float**)&ds, st);
+    if (e == cudaSuccess) e = stage(opacity, (size_t)n, kind, (float**)&dop, st);
+    if (e == cudaSuccess) e = stage(info_w, (size_t)n, kind, (float**)&dw, st);
+    if (e == cudaSuccess) e = stage(flags, (size_t)n, kind, (unsigned char**)&df, st);
+    rtg_status s;
+    if (e != cudaSuccess) {
+        s = cuda_fail(e, "rtg_map_create staging", nullptr);
+    } else {
+        prof_begin(PH_MAP, st);
+        s = build_map(m, dm, dq, ds, dop, dw, df, opts, st);
+        prof_end(PH_MAP, st);
+    }
+    if (kind == RTG_MEM_HOST) {
+        dev_free((void*)dm, st); dev_free((void*)dq, st); dev_free((void*)ds, st);
+        dev_free((void*)dop, st); dev_free((void*)dw, st); dev_free((void*)df, st);
+    }
+    if (s != RTG_OK) {
+        for (void* p : m->allocs) dev_free(p, st);
+        delete m;
+        return s;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        for (void* p : m->allocs) dev_free(p, st);
+        delete m;
+        return cuda_fail(e, "rtg_map_create", nullptr);
+    }
+    *out = m;
+    return RTG_OK;
+}
+
+rtg_status rtg_map_create(int device, long long n, rtg_mem kind, const float* means, const float* quats,
+                          const float* scales, const float* opacity, const float* info_w, const unsigned char* flags,
+                          const rtg_robot* robot, void* stream, rtg_map* out) {
+    return rtg_map_create_ex(device, n, kind, means, quats, scales, opacity, info_w, flags, robot, nullptr, stream,
+                             out);
+}
+
+rtg_status rtg_map_destroy(rtg_map m) {
+    if (!m) return invalid("map handle is NULL");
+    cudaSetDevice(m->device);
+    for (void* p : m->allocs) dev_free(p, m->stream);
+    delete m;
+    return RTG_OK;
+}
+
+rtg_status rtg_map_info(rtg_map m, rtg_map_info_t* out) {
+    rtg_status s = check_map(m);
+    if (s != RTG_OK) return s;
+    if (!out) return invalid("out is NULL");
+    cudaSetDevice(m->device);
+    ClassState cs;
+    cudaError_t e = cudaMemcpyAsync(&cs, m->cls, sizeof(cs), cudaMemcpyDeviceToHost, m->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "rtg_map_info", &m->poisoned);
+    out->n = m->n;
+    out->n_collide = m->n_col;
+    out->n_gain = m->n_gain;
+    out->tau_hi = cs.tau_hi;
+    out->tau_lo = cs.tau_lo;
+    out->u_mean = cs.mean;
+    out->u_std = cs.std;
+    out->fixed_point_shift = cs.shift;
+    out->gain_dims[0] = m->gg.nx; out->gain_dims[1] = m->gg.ny; out->gain_dims[2] = m->gg.nz;
+    out->col_dims[0] = m->cg.nx; out->col_dims[1] = m->cg.ny; out->col_dims[2] = m->cg.nz;
+    out->rb_max = m->rb_max;
+    out->device_bytes = m->bytes;
+    return RTG_OK;
+}
+
+static rtg_status traj_alloc(int device, int K, int T, cudaStream_t st, rtg_traj* out, rtg_traj_s** res) {
+    if (!out) return invalid("out is NULL");
+    *out = nullptr;
+    if (K < 1 || T < 1 || (long long)K * T >= (1LL << 31)) return invalid("need K >= 1, T >= 1, K*T < 2^31");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return invalid("invalid device ordinal (no CUDA device?)");
+    }
+    API_CK(cudaSetDevice(device), nullptr);
+    ensure_pool(device);
+    rtg_traj_s* t = new (std::nothrow) rtg_traj_s();
+    if (!t) return RTG_ERR_OUT_OF_MEMORY;
+    t->device = device;
+    t->stream = st;
+    t->K = K;
+    t->T = T;
+    size_t n = (size_t)K * T;
+    float* base = nullptr;
+    cudaError_t e = dev_alloc((void**)&base, sizeof(float) * 4 * n, st);
+    if (e != cudaSuccess) {
+        delete t;
+        return cuda_fail(e, "rtg_traj alloc", nullptr);
+    }
+    t->x = base;
+    t->y = base + n;
+    t->z = base + 2 * n;
+    t->yaw = base + 3 * n;
+    *res = t;
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_upload(int device, int K, int T, rtg_mem kind, const float* x, const float* y, const float* z,
+                           const float* yaw, void* stream, rtg_traj* out) {
+    if (!x || !y || !z || !yaw) return invalid("x, y, z and yaw are required");
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    cudaStream_t st = (cudaStream_t)stream;
+    rtg_traj_s* t = nullptr;
+    rtg_status s = traj_alloc(device, K, T, st, out, &t);
+    if (s != RTG_OK) return s;
+    size_t bytes = sizeof(float) * (size_t)K * T;
+    cudaMemcpyKind ck = kind == RTG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    cudaError_t e = cudaMemcpyAsync(t->x, x, bytes, ck, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(t->y, y, bytes, ck, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(t->z, z, bytes, ck, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(t->yaw, yaw, bytes, ck, st);
+    if (e != cudaSuccess) {
+        dev_free(t->x, st);
+        delete t;
+        return cuda_fail(e, "rtg_traj_upload", nullptr);
+    }
+    *out = t;
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_sample_unicycle(int device, int K, int T, float dt, const float start[4], const float* v,
+                                    const float* omega, rtg_mem kind, void* stream, rtg_traj* out) {
+    if (!start || !v || !omega) return invalid("start, v and omega are required");
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    if (!(dt >= 0) || !finite_f(dt)) return invalid("dt must be finite and >= 0");
+    for (int i = 0; i < 4; ++i)
+        if (!finite_f(start[i])) return invalid("start state must be finite");
+    cudaStream_t st = (cudaStream_t)stream;
+    rtg_traj_s* t = nullptr;
+    rtg_status s = traj_alloc(device, K, T, st, out, &t);
+    if (s != RTG_OK) return s;
+    float *dv = nullptr, *dw = nullptr;
+    cudaError_t e = stage(v, (size_t)K, kind, &dv, st);
+    if (e == cudaSuccess) e = stage(omega, (size_t)K, kind, &dw, st);
+    if (e == cudaSuccess) e = launch_sampler(K, T, (double)dt, start, dv, dw, t, st);
+    if (kind == RTG_MEM_HOST) {
+        dev_free(dv, st);
+        dev_free(dw, st);
+    }
+    if (e != cudaSuccess) {
+        dev_free(t->x, st);
+        delete t;
+        return cuda_fail(e, "rtg_traj_sample_unicycle", nullptr);
+    }
+    *out = t;
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_read(rtg_traj t, float* x, float* y, float* z, float* yaw, void* stream) {
+    rtg_status s = check_traj(t);
+    if (s != RTG_OK) return s;
+    if (!x || !y || !z || !yaw) return invalid("x, y, z and yaw are required");
+    cudaSetDevice(t->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t bytes = sizeof(float) * (size_t)t->K * t->T;
+    API_CK(cudaMemcpyAsync(x, t->x, bytes, cudaMemcpyDeviceToDevice, st), &t->poisoned);
+    API_CK(cudaMemcpyAsync(y, t->y, bytes, cudaMemcpyDeviceToDevice, st), &t->poisoned);
+    API_CK(cudaMemcpyAsync(z, t->z, bytes, cudaMemcpyDeviceToDevice, st), &t->poisoned);
+    API_CK(cudaMemcpyAsync(yaw, t->yaw, bytes, cudaMemcpyDeviceToDevice, st), &t->poisoned);
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_destroy(rtg_traj t) {
+    if (!t) return invalid("trajectory handle is NULL");
+    cudaSetDevice(t->device);
+    dev_free(t->x, t->stream);
+    delete t;
+    return RTG_OK;
+}
+
+// scratch of one scoring pass
+struct Scratch {
+    int* first_col = nullptr;
+    long long* wp_gq = nullptr;
+    int* wp_nh = nullptr;
+    int* wp_nl = nullptr;
+    int* list = nullptr;
+    int* ints = nullptr;                  // [0] list count, [1] phase-A counter, [2] phase-B counter
+    double* cam64 = nullptr;              // FP64 camera for the re-decision branch
+    unsigned long long* stats = nullptr;  // 4 counters
+    void* block = nullptr;
+};
+
+static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long list_max, const rtg_camera* cam,
+                                 cudaStream_t st) {
+    long long KT = K * T;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    size_t o_first = 0;
+    size_t o_gq = o_first + al(sizeof(int) * K);
+    size_t o_nh = o_gq + al(sizeof(long long) * KT);
+    size_t o_nl = o_nh + al(sizeof(int) * KT);
+    size_t o_list = o_nl + al(sizeof(int) * KT);
+    size_t o_ints = o_list + al(sizeof(int) * (list_max > 0 ? list_max : 1));
+    size_t o_stats = o_ints + al(sizeof(int) * 8);
+    size_t o_cam = o_stats + al(sizeof(unsigned long long) * 4);
+    size_t total = o_cam + al(sizeof(double) * 8);
+    cudaError_t e = dev_alloc(&s.block, total, st);
+    if (e != cudaSuccess) return e;
+    char* b = (char*)s.block;
+    s.first_col = (int*)(b + o_first);
+    s.wp_gq = (long long*)(b + o_gq);
+    s.wp_nh = (int*)(b + o_nh);
+    s.wp_nl = (int*)(b + o_nl);
+    s.list = (int*)(b + o_list);
+    s.ints = (int*)(b + o_ints);
+    s.stats = (unsigned long long*)(b + o_stats);
+    s.cam64 = (double*)(b + o_cam);
+    // the camera in FP64 travels by a tiny kernel-free copy: host values -> pinned-free memset path
+    double c64[8] = {(double)cam->width, (double)cam->height, cam->fx, cam->fy, cam->cx, cam->cy, cam->z_near, cam->z_far};
+    cudaError_t e2 = cudaMemcpyAsync(s.cam64, c64, sizeof(c64), cudaMemcpyHostToDevice, st);
+    if (e2 != cudaSuccess) return e2;
+    return cudaMemsetAsync(b + o_ints, 0, o_stats + al(sizeof(unsigned long long) * 4) - o_ints, st);
+}
+
+rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_score_params* p, int* first_col,
+                     unsigned char* feasible, double* gain, double* utility, void* stream) {
+    rtg_status s = check_map(m);
+    if (s == RTG_OK) s = check_traj(tr);
+    if (s == RTG_OK) s = check_camera(cam);
+    if (s == RTG_OK) s = check_params(p);
+    if (s != RTG_OK) return s;
+    if (m->device != tr->device) return invalid("map and trajectories live on different devices");
+    API_CK(cudaSetDevice(m->device), nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    prof_begin(PH_CLASSIFY, st);
+    s = classify_map(m, p->variant, p->k_sigma, p->tau_hi, p->tau_lo, st);
+    prof_end(PH_CLASSIFY, st);
+    if (s != RTG_OK) return s;
+    const long long K = tr->K, T = tr->T;
+    const long long per = T / p->info_stride;
+    const long long list_max = K * per;
+    Scratch sc;
+    prof_begin(PH_OTHER, st);
+    API_CK(scratch_alloc(sc, K, T, list_max, cam, st), &m->poisoned);
+    const CamK ck = make_cam(*cam, sc.cam64);
+    const int dense = p->mode == RTG_MODE_DENSE;
+    const int full_gain = (p->flags & RTG_SCORE_FULL_GAIN) ? 1 : 0;
+    note_launch(), k_fill_int<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(sc.first_col, K, (int)T);
+    if (dense) {
+        API_CK(cudaMemsetAsync(sc.wp_gq, 0, sizeof(long long) * K * T, st), &m->poisoned);
+        API_CK(cudaMemsetAsync(sc.wp_nh, 0, sizeof(int) * K * T, st), &m->poisoned);
+        API_CK(cudaMemsetAsync(sc.wp_nl, 0, sizeof(int) * K * T, st), &m->poisoned);
+    }
+    prof_end(PH_OTHER, st);
+    if (!(p->flags & RTG_SCORE_NO_COLLISION)) {
+        prof_begin(PH_COLLISION, st);
+        API_CK(launch_phase_a(m, tr, p->mode, sc.first_col, nullptr, 0, sc.ints + 1, nullptr, st), &m->poisoned);
+        prof_end(PH_COLLISION, st);
+    }
+    if (per > 0) {
+        prof_begin(PH_LIST, st);
+        API_CK(launch_list(sc.first_col, (int)K, (int)T, p->info_stride, full_gain, sc.list, sc.ints, st), &m->poisoned);
+        prof_end(PH_LIST, st);
+        prof_begin(PH_GAIN, st);
+        API_CK(launch_phase_b(m, tr, p->mode, ck, sc.list, sc.ints, list_max, sc.wp_gq, sc.wp_nh, sc.wp_nl,
+                              sc.ints + 2, nullptr, st),
+               &m->poisoned);
+        prof_end(PH_GAIN, st);
+    }
+    rtg_score_params pp = *p;
+    if (per == 0) pp.info_stride = (int)T + 1;   // no info waypoint: sums are empty
+    prof_begin(PH_REDUCE, st);
+    API_CK(launch_reduce(m, tr, pp, sc.first_col, sc.wp_gq, sc.wp_nh, sc.wp_nl, first_col, feasible, gain, utility, st),
+           &m->poisoned);
+    prof_end(PH_REDUCE, st);
+    dev_free(sc.block, st);
+    return RTG_OK;
+}
+
+rtg_status rtg_best(const double* utility, int K, long long index_base, void* stream, rtg_best_result* out) {
+    if (!out) return invalid("out is NULL");
+    out->score = -INFINITY;
+    out->index = -1;
+    if (!utility || K < 1) return invalid("utility must be a device array of K >= 1 values");
+    cudaStream_t st = (cudaStream_t)stream;
+    void* d = nullptr;
+    API_CK(dev_alloc(&d, 16, st), nullptr);
+    prof_begin(PH_BEST, st);
+    API_CK(launch_best(utility, K, index_base, d, st), nullptr);
+    prof_end(PH_BEST, st);
+    struct {
+        double score;
+        long long index;
+    } h;
+    API_CK(cudaMemcpyAsync(&h, d, 16, cudaMemcpyDeviceToHost, st), nullptr);
+    dev_free(d, st);
+    API_CK(cudaStreamSynchronize(st), nullptr);
+    out->score = h.score;
+    out->index = h.index;
+    if (h.index < 0) {
+        set_error("rtg_best: no feasible trajectory");
+        return RTG_ERR_NO_FEASIBLE;
+    }
+    return RTG_OK;
+}
+
+rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_score_params* p,
+                           unsigned char* wp_col, double* wp_gain, int* wp_nh, int* wp_nl, unsigned int* pair_mask,
+                           long long* stats, void* stream) {
+    rtg_status s = check_map(m);
+    if (s == RTG_OK) s = check_traj(tr);
+    if (s == RTG_OK) s = check_camera(cam);
+    if (s == RTG_OK) s = check_params(p);
+    if (s != RTG_OK) return s;
+    if (m->device != tr->device) return invalid("map and trajectories live on different devices");
+    if (!wp_col || !wp_gain || !wp_nh || !wp_nl) return invalid("wp_col, wp_gain, wp_nh, wp_nl are required");
+    const long long K = tr->K, T = tr->T, KT = K * T;
+    if (pair_mask && (double)KT * (double)m->n > 4294967296.0) return invalid("pair_mask needs K*T*N <= 2^32");
+    API_CK(cudaSetDevice(m->device), nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    s = classify_map(m, p->variant, p->k_sigma, p->tau_hi, p->tau_lo, st);
+    if (s != RTG_OK) return s;
+    Scratch sc;
+    API_CK(scratch_alloc(sc, K, T, KT, cam, st), &m->poisoned);
+    const CamK ck = make_cam(*cam, sc.cam64);
+    note_launch(), k_fill_int<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(sc.first_col, K, (int)T);
+    API_CK(cudaMemsetAsync(wp_col, 0, KT, st), &m->poisoned);
+    API_CK(cudaMemsetAsync(sc.wp_gq, 0, sizeof(long long) * KT, st), &m->poisoned);
+    API_CK(cudaMemsetAsync(wp_nh, 0, sizeof(int) * KT, st), &m->poisoned);
+    API_CK(cudaMemsetAsync(wp_nl, 0, sizeof(int) * KT, st), &m->poisoned);
+    if (!(p->flags & RTG_SCORE_NO_COLLISION))
+        API_CK(launch_phase_a(m, tr, p->mode, sc.first_col, wp_col, 1, sc.ints + 1, sc.stats, st), &m->poisoned);
+    API_CK(launch_iota(sc.list, KT, sc.ints, st), &m->poisoned);
+    API_CK(launch_phase_b(m, tr, p->mode, ck, sc.list, sc.ints, KT, sc.wp_gq, wp_nh, wp_nl, sc.ints + 2, sc.stats, st),
+           &m->poisoned);
+    API_CK(launch_debug_wp(KT, sc.wp_gq, m->cls, wp_gain, st), &m->poisoned);
+    if (pair_mask) {
+        size_t words = (size_t)((KT * m->n + 31) / 32);
+        API_CK(cudaMemsetAsync(pair_mask, 0, sizeof(unsigned) * (words ? words : 1), st), &m->poisoned);
+        API_CK(launch_pair_mask(m, tr, pair_mask, st), &m->poisoned);
+    }
+    unsigned long long hs[4] = {0, 0, 0, 0};
+    API_CK(cudaMemcpyAsync(hs, sc.stats, sizeof(hs), cudaMemcpyDeviceToHost, st), &m->poisoned);
+    dev_free(sc.block, st);
+    API_CK(cudaStreamSynchronize(st), &m->poisoned);
+    if (stats)
+        for (int i = 0; i < 4; ++i) stats[i] = (long long)hs[i];
+    return RTG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// rtg_internal.cuh -- shared device-side definitions of librtg (sm_100a).
+//
+// The pair tests live here ONCE and are used by both execution modes (dense and
+// culled) and the debug kernels, so every mode takes identical decisions.
+//
+// Numerics:
+//  * collision:  q32 = sum_i (M_i . d)^2 in FP32 with M = diag(1/a) R^T packed in FP64 and
+//    rounded once (SURVEY F2 / [A2], [A11]); pairs with |q32 - 1| < gq are re-decided in
+//    FP64 from the FP64-packed M (same formula as the oracle, O2).
+//  * visibility: min slack m32 of the folded frustum (|Z - zmid| <= zhalf,
+//    |X - kxc Z| <= kxh Z, |dz - kyc Z| <= kyh Z); pairs with |m32| < gam*Z + g0 are
+//    re-decided in FP64 with the six pinhole slacks (O3).  gam, g0 bound the FP32 error.
+//  * gains: u_q = round(u * 2^S) int64, summed exactly (associative -> order free).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rtg {
+
+constexpr int kTile = 512;           // dense-mode Gaussians per smem tile
+
+// ------------------------------------------------------------------ records
+// visibility record (sorted by visibility cell): mean + packed class increment
+//   inc = 1 (class H), 0x10000 (class L), 0 (O)  -- per-lane int32 partials flush often
+struct __align__(16) GRec { float x, y, z; int inc; };
+// collision record (sorted by collision cell): mean + inflated bounding radius^2
+struct __align__(16) CRec { float x, y, z, rb2; };
+// M rows (FP32): m[0..8] row-major, m[9] = original index (as int bits), pad
+struct __align__(16) CMat { float m[12]; };
+// FP64 M for the re-decision branch (9 used)
+struct CMat64 { double m[9]; };
+
+// ------------------------------------------------------------------ camera constants
+struct CamK {
+    float zmid, zhalf;   // depth  |Z - zmid| <= zhalf
+    float kxc, kxh;      // horiz  |X - kxc Z| <= kxh Z
+    float kyc, kyh;      // vert   |dz - kyc Z| <= kyh Z
+    float gam, g0;       // FP32 guard: FP64 re-decision iff |m32| < gam*Z + g0
+    const double* cam64; // device: {W, H, fx, fy, cx, cy, z_near, z_far} for the FP64 slacks
+};
+
+// per-waypoint constants (yaw kept for the rare FP64 re-decision)
+struct WpF { float px, py, pz, c, s, ax, bx, yaw; };
+
+__device__ __forceinline__ void wp_setup(float x, float y, float z, float yaw, const CamK& k, WpF& f) {
+    double sn, cs;
+    sincos((double)yaw, &sn, &cs);
+    f.px = x; f.py = y; f.pz = z; f.yaw = yaw;
+    f.c = (float)cs; f.s = (float)sn;
+    // X' = X - kxc Z with X = s dx - c dy, Z = c dx + s dy  (coefficients rounded once)
+    f.ax = (float)(sn - (double)k.kxc * cs);
+    f.bx = (float)(-cs - (double)k.kxc * sn);
+}
+
+// ------------------------------------------------------------------ visibility
+// FP32 margin: min over the three folded slack pairs (>= 0 <=> visible in FP32)
+__device__ __forceinline__ float vis_margin(const WpF& w, const CamK& k, float mx, float my,
+                                            float mz, float& Z) {
+    float dx = mx - w.px, dy = my - w.py, dz = mz - w.pz;
+    Z = fmaf(w.c, dx, w.s * dy);
+    float X = fmaf(w.ax, dx, w.bx * dy);
+    float Y = fmaf(-k.kyc, Z, dz);
+    float s1 = k.zhalf - fabsf(Z - k.zmid);
+    float s2 = fmaf(k.kxh, Z, -fabsf(X));
+    float s3 = fmaf(k.kyh, Z, -fabsf(Y));
+    return fminf(s1, fminf(s2, s3));
+}
+
+// FP64 decision with the six slacks of the pinhole test (visible <=> all >= 0); rare path
+static __device__ __noinline__ bool vis_decide64(float px, float py, float pz, float yaw, float mx, float my, float mz,
+                                          const double* __restrict__ k) {
+    const double W = k[0], H = k[1], fx = k[2], fy = k[3], cx = k[4], cy = k[5], zn = k[6], zf = k[7];
+    double sn, cs;
+    sincos((double)yaw, &sn, &cs);
+    double dx = (double)mx - px, dy = (double)my - py, dz = (double)mz - pz;
+    double Z = cs * dx + sn * dy;
+    double X = sn * dx - cs * dy;
+    double Y = -dz;
+    bool v = (Z - zn >= 0.0) & (zf - Z >= 0.0);
+    v &= (fx * X + cx * Z >= 0.0) & ((W - cx) * Z - fx * X >= 0.0);
+    v &= (fy * Y + cy * Z >= 0.0) & ((H - cy) * Z - fy * Y >= 0.0);
+    return v;
+}
+
+// exact-decision visibility of one pair; `nref` counts FP64 re-decisions
+__device__ __forceinline__ bool visible(const WpF& w, const CamK& k, float mx, float my, float mz,
+                                        unsigned& nref) {
+    float Z;
+    float m = vis_margin(w, k, mx, my, mz, Z);
+    bool v = m >= 0.0f;
+    if (fabsf(m) < fmaf(k.gam, Z, k.g0)) {
+        v = vis_decide64(w.px, w.py, w.pz, w.yaw, mx, my, mz, k.cam64);
+        ++nref;
+    }
+    return v;
+}
+
+// ------------------------------------------------------------------ collision
+static __device__ __noinline__ bool col_decide64(const CMat64* __restrict__ Mp, float px, float py, float pz,
+                                          float mx, float my, float mz) {
+    const double* M = Mp->m;
+    double dx = (double)px - (double)mx, dy = (double)py - (double)my, dz = (double)pz - (double)mz;
+    double e0 = M[0] * dx + M[1] * dy + M[2] * dz;
+    double e1 = M[3] * dx + M[4] * dy + M[5] * dz;
+    double e2 = M[6] * dx + M[7] * dy + M[8] * dz;
+    return e0 * e0 + e1 * e1 + e2 * e2 < 1.0;
+}
+
+// full quadratic form for a sphere-passing pair
+__device__ __forceinline__ bool collide_full(const float* m, float dx, float dy, float dz, float gq,
+                                             const CMat64* m64, float px, float py, float pz,
+                                             float mx, float my, float mz, unsigned& nref) {
+    float e0 = fmaf(m[0], dx, fmaf(m[1], dy, m[2] * dz));
+    float e1 = fmaf(m[3], dx, fmaf(m[4], dy, m[5] * dz));
+    float e2 = fmaf(m[6], dx, fmaf(m[7], dy, m[8] * dz));
+    float q = fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
+    bool c = q < 1.0f;
+    if (fabsf(q - 1.0f) < gq) {
+        c = col_decide64(m64, px, py, pz, mx, my, mz);
+        ++nref;
+    }
+    return c;
+}
+
+// ------------------------------------------------------------------ misc helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion tracked by an mbarrier (sm_90+; UBLKCP in SASS)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+}  // namespace rtg

@@ -1,0 +1,618 @@
+// rtg_map.cu -- map intake, packing, classification and grid construction.
+//
+//  a1  per Gaussian, in FP64: unit quaternion -> R, inflated semi-axes a_i = lambda_g s_i + r_robot
+//      (P:298-302), M = diag(1/a) R^T (rows: principal axes scaled by 1/a_i), bounding radius
+//      r_b = max_i a_i; stored as FP32 records (+ an FP64 copy of M for the re-decision branch).
+//      Records are placed by a counting sort into two uniform grids:
+//        * visibility grid: columns (hxy x hxy) of z-cells (hz), column-contiguous, gain-eligible
+//          Gaussians only;
+//        * collision grid: cubic cells (h), x fastest, collidable (non-ground) Gaussians only.
+//  a2  classification over the gain-eligible set in ORIGINAL input order (deterministic FP64
+//      two-pass mean / population std), class increments and exact fixed-point u per
+//      record, and the per-cell exclusive prefixes that let the culled kernel add whole cells.
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "rtg_host.hpp"
+
+namespace rtg {
+namespace {
+
+constexpr int kRedBlocks = 512;
+constexpr int kRedThreads = 256;
+
+__host__ __device__ inline int f2o(float f) {
+#ifdef __CUDA_ARCH__
+    int i = __float_as_int(f);
+#else
+    int i;
+    std::memcpy(&i, &f, 4);
+#endif
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+inline float o2f(int i) {
+    int b = i >= 0 ? i : i ^ 0x7fffffff;
+    float f;
+    std::memcpy(&f, &b, 4);
+    return f;
+}
+
+struct DevBounds {
+    int err;
+    int n_gain, n_col;
+    int gmin[3], gmax[3], cmin[3], cmax[3];
+    int rbmax, rhomax;
+};
+
+__global__ void k_bounds_init(DevBounds* b) {
+    b->err = 0;
+    b->n_gain = 0;
+    b->n_col = 0;
+    for (int i = 0; i < 3; ++i) {
+        b->gmin[i] = b->cmin[i] = f2o(FLT_MAX);
+        b->gmax[i] = b->cmax[i] = f2o(-FLT_MAX);
+    }
+    b->rbmax = f2o(0.f);
+    b->rhomax = f2o(1.f);
+}
+
+// inflated semi-axes in FP64
+__device__ __forceinline__ void semi_axes(const float* scales, long long n, long long i, const rtg_robot& rb,
+                                          double a[3]) {
+    double s0 = scales[i], s1 = scales[n + i], s2 = scales[2 * n + i];
+    if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
+        double sm = fmax(s0, fmax(s1, s2));
+        double r = (double)rb.lambda_g * sm + (double)rb.r_robot;
+        a[0] = a[1] = a[2] = r;
+    } else {
+        a[0] = (double)rb.lambda_g * s0 + (double)rb.r_robot;
+        a[1] = (double)rb.lambda_g * s1 + (double)rb.r_robot;
+        a[2] = (double)rb.lambda_g * s2 + (double)rb.r_robot;
+    }
+}
+
+__global__ void k_bounds(long long n, const float* __restrict__ means, const float* __restrict__ quats,
+                         const float* __restrict__ scales, const float* __restrict__ opacity,
+                         const float* __restrict__ w, const unsigned char* __restrict__ flags, rtg_robot rb,
+                         DevBounds* __restrict__ out) {
+    int err = 0, ng = 0, nc = 0;
+    int gmn[3] = {INT_MAX, INT_MAX, INT_MAX}, gmx[3] = {INT_MIN, INT_MIN, INT_MIN};
+    int cmn[3] = {INT_MAX, INT_MAX, INT_MAX}, cmx[3] = {INT_MIN, INT_MIN, INT_MIN};
+    int rbm = INT_MIN, rhm = INT_MIN;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        float p[3] = {means[i], means[n + i], means[2 * n + i]};
+        float q0 = quats[i], q1 = quats[n + i], q2 = quats[2 * n + i], q3 = quats[3 * n + i];
+        float s0 = scales[i], s1 = scales[n + i], s2 = scales[2 * n + i];
+        float wi = w[i];
+        float op = opacity ? opacity[i] : 0.5f;
+        if (!(isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]))) err |= 1;
+        double qn = (double)q0 * q0 + (double)q1 * q1 + (double)q2 * q2 + (double)q3 * q3;
+        if (!(qn >= 1e-24) || !isfinite(qn)) err |= 2;
+        if (!(s0 > 0.f && s1 > 0.f && s2 > 0.f) || !isfinite(s0) || !isfinite(s1) || !isfinite(s2)) err |= 4;
+        if (!(wi >= 0.f) || !isfinite(wi)) err |= 8;
+        if (!(op >= 0.f && op <= 1.f)) err |= 16;
+        unsigned f = flags ? flags[i] : 0u;
+        if (!(f & RTG_G_NO_GAIN)) {
+            ++ng;
+            for (int d = 0; d < 3; ++d) {
+                int o = f2o(p[d]);
+                gmn[d] = min(gmn[d], o);
+                gmx[d] = max(gmx[d], o);
+            }
+        }
+        if (!(f & RTG_G_NO_COLLIDE)) {
+            ++nc;
+            for (int d = 0; d < 3; ++d) {
+                int o = f2o(p[d]);
+                cmn[d] = min(cmn[d], o);
+                cmx[d] = max(cmx[d], o);
+            }
+            double a[3];
+            semi_axes(scales, n, i, rb, a);
+            double amax = fmax(a[0], fmax(a[1], a[2])), amin = fmin(a[0], fmin(a[1], a[2]));
+            if (isfinite(amax)) {
+                rbm = max(rbm, f2o(__double2float_ru(amax)));
+                rhm = max(rhm, f2o(__double2float_ru(amax / amin)));
+            }
+        }
+    }
+    // warp aggregate, one atomic per warp
+    unsigned full = 0xffffffffu;
+    err = __reduce_or_sync(full, err);
+    ng = __reduce_add_sync(full, ng);
+    nc = __reduce_add_sync(full, nc);
+    for (int d = 0; d < 3; ++d) {
+        gmn[d] = __reduce_min_sync(full, gmn[d]);
+        gmx[d] = __reduce_max_sync(full, gmx[d]);
+        cmn[d] = __reduce_min_sync(full, cmn[d]);
+        cmx[d] = __reduce_max_sync(full, cmx[d]);
+    }
+    rbm = __reduce_max_sync(full, rbm);
+    rhm = __reduce_max_sync(full, rhm);
+    if ((threadIdx.x & 31) == 0) {
+        if (err) atomicOr(&out->err, err);
+        if (ng) atomicAdd(&out->n_gain, ng);
+        if (nc) atomicAdd(&out->n_col, nc);
+        for (int d = 0; d < 3; ++d) {
+            atomicMin(&out->gmin[d], gmn[d]);
+            atomicMax(&out->gmax[d], gmx[d]);
+            atomicMin(&out->cmin[d], cmn[d]);
+            atomicMax(&out->cmax[d], cmx[d]);
+        }
+        atomicMax(&out->rbmax, rbm);
+        atomicMax(&out->rhomax, rhm);
+    }
+}
+
+__device__ __forceinline__ int cell_coord(float v, double o, double h, int nmax) {
+    int c = (int)floor(((double)v - o) / h);
+    return c < 0 ? 0 : (c >= nmax ? nmax - 1 : c);
+}
+
+__global__ void k_keys(long long n, const float* __restrict__ means, const unsigned char* __restrict__ flags,
+                       GainGrid gg, ColGrid cg, int* __restrict__ gkey, int* __restrict__ ckey,
+                       int* __restrict__ gcount, int* __restrict__ ccount) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        float x = means[i], y = means[n + i], z = means[2 * n + i];
+        unsigned f = flags ? flags[i] : 0u;
+        int gk = -1, ck = -1;
+        if (!(f & RTG_G_NO_GAIN)) {
+            int ix = cell_coord(x, gg.ox, gg.hxy, gg.nx);
+            int iy = cell_coord(y, gg.oy, gg.hxy, gg.ny);
+            int iz = cell_coord(z, gg.oz, gg.hz, gg.nz);
+            gk = (int)(((long long)iy * gg.nx + ix) * gg.nz + iz);
+            atomicAdd(&gcount[gk], 1);
+        }
+        if (!(f & RTG_G_NO_COLLIDE)) {
+            int ix = cell_coord(x, cg.ox, cg.h, cg.nx);
+            int iy = cell_coord(y, cg.oy, cg.h, cg.ny);
+            int iz = cell_coord(z, cg.oz, cg.h, cg.nz);
+            ck = (int)(((long long)iz * cg.ny + iy) * cg.nx + ix);
+            atomicAdd(&ccount[ck], 1);
+        }
+        gkey[i] = gk;
+        ckey[i] = ck;
+    }
+}
+
+__global__ void k_scatter_gain(long long n, const float* __restrict__ means, const int* __restrict__ gkey,
+                               int* __restrict__ cursor, GRec* __restrict__ grec, int* __restrict__ gidx) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int k = gkey[i];
+        if (k < 0) continue;
+        int slot = atomicAdd(&cursor[k], 1);
+        grec[slot] = GRec{means[i], means[n + i], means[2 * n + i], 0};
+        gidx[slot] = (int)i;
+    }
+}
+
+// FP64 packing of the collision record (a1)
+__global__ void k_scatter_col(long long n, const float* __restrict__ means, const float* __restrict__ quats,
+                              const float* __restrict__ scales, const int* __restrict__ ckey,
+                              int* __restrict__ cursor, rtg_robot rb, double guard, CRec* __restrict__ crec,
+                              CMat* __restrict__ cmat, CMat64* __restrict__ cmat64) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int k = ckey[i];
+        if (k < 0) continue;
+        int slot = atomicAdd(&cursor[k], 1);
+        double a[3];
+        semi_axes(scales, n, i, rb, a);
+        double M[9];
+        if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
+            for (int j = 0; j < 9; ++j) M[j] = 0.0;
+            M[0] = M[4] = M[8] = 1.0 / a[0];
+        } else {
+            double qw = quats[i], qx = quats[n + i], qy = quats[2 * n + i], qz = quats[3 * n + i];
+            double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+            qw /= nq; qx /= nq; qy /= nq; qz /= nq;
+            // Hamilton R (columns = local principal axes)
+            double R[3][3] = {
+                {1.0 - 2.0 * (qy * qy + qz * qz), 2.0 * (qx * qy - qw * qz), 2.0 * (qx * qz + qw * qy)},
+                {2.0 * (qx * qy + qw * qz), 1.0 - 2.0 * (qx * qx + qz * qz), 2.0 * (qy * qz - qw * qx)},
+                {2.0 * (qx * qz - qw * qy), 2.0 * (qy * qz + qw * qx), 1.0 - 2.0 * (qx * qx + qy * qy)}};
+            for (int r = 0; r < 3; ++r)         // row r of M = column r of R / a_r  (M = diag(1/a) R^T)
+                for (int c = 0; c < 3; ++c) M[3 * r + c] = R[c][r] / a[r];
+        }
+        double amax = fmax(a[0], fmax(a[1], a[2]));
+        float rb2 = __double2float_ru(amax * amax * (1.0 + guard) * (1.0 + 1.0e-6));
+        crec[slot] = CRec{means[i], means[n + i], means[2 * n + i], rb2};
+        CMat cm;
+        for (int j = 0; j < 9; ++j) cm.m[j] = (float)M[j];
+        cm.m[9] = __int_as_float((int)i);
+        cm.m[10] = 0.f;
+        cm.m[11] = 0.f;
+        cmat[slot] = cm;
+        CMat64 c64;
+        for (int j = 0; j < 9; ++j) c64.m[j] = M[j];
+        cmat64[slot] = c64;
+    }
+}
+
+__global__ void k_pad_gain(GRec* grec, long long* guq, int* gidx, long long from, long long to) {
+    long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < to) {
+        float nan = __int_as_float(0x7fc00000);
+        grec[i] = GRec{nan, nan, nan, 0};
+        guq[i] = 0;
+        gidx[i] = -1;
+    }
+}
+
+__global__ void k_pad_col(CRec* crec, CMat* cmat, CMat64* cm64, long long from, long long to) {
+    long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < to) {
+        float nan = __int_as_float(0x7fc00000);
+        crec[i] = CRec{nan, nan, nan, -1.f};
+        CMat z;
+        for (int j = 0; j < 12; ++j) z.m[j] = 0.f;
+        z.m[9] = __int_as_float(-1);
+        cmat[i] = z;
+        CMat64 z64;
+        for (int j = 0; j < 9; ++j) z64.m[j] = 0.0;
+        cm64[i] = z64;
+    }
+}
+
+// ------------------------------------------------------------------ classification (a2)
+
+__device__ __forceinline__ double u_of(float w, int variant) {
+    double u = (double)w;
+    return variant == RTG_VARIANT_SQ ? u * u : u;
+}
+
+// deterministic block tree over a fixed contiguous chunk
+__device__ double block_sum(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// pass 1: partial sums of u, counts and max u over eligible Gaussians, original order
+__global__ void k_red1(long long n, const float* __restrict__ w, const unsigned char* __restrict__ flags,
+                       int variant, double* __restrict__ part) {
+    __shared__ double sh[kRedThreads];
+    long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double s = 0.0, c = 0.0, mx = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        if (flags && (flags[i] & RTG_G_NO_GAIN)) continue;
+        double u = u_of(w[i], variant);
+        s += u;
+        c += 1.0;
+        mx = fmax(mx, u);
+    }
+    double S = block_sum(s, sh);
+    double C = block_sum(c, sh);
+    sh[threadIdx.x] = mx;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + st]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[3 * blockIdx.x + 0] = S;
+        part[3 * blockIdx.x + 1] = C;
+        part[3 * blockIdx.x + 2] = sh[0];
+    }
+}
+
+__global__ void k_red1_final(const double* __restrict__ part, int nparts, ClassState* cs) {
+    __shared__ double sh[kRedThreads];
+    double s = 0.0, c = 0.0, mx = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+        s += part[3 * i];
+        c += part[3 * i + 1];
+        mx = fmax(mx, part[3 * i + 2]);
+    }
+    double S = block_sum(s, sh);
+    double C = block_sum(c, sh);
+    sh[threadIdx.x] = mx;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + st]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        cs->n_eligible = (int)C;
+        cs->mean = C > 0 ? S / C : 0.0;
+        cs->std = sh[0];   // temporarily holds max u (consumed by k_red2_final)
+    }
+}
+
+// pass 2: partial sums of (u - mean)^2
+__global__ void k_red2(long long n, const float* __restrict__ w, const unsigned char* __restrict__ flags,
+                       int variant, const ClassState* __restrict__ cs, double* __restrict__ part) {
+    __shared__ double sh[kRedThreads];
+    double m = cs->mean;
+    long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double s = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        if (flags && (flags[i] & RTG_G_NO_GAIN)) continue;
+        double d = u_of(w[i], variant) - m;
+        s += d * d;
+    }
+    double S = block_sum(s, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = S;
+}
+
+__global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassState* cs, double k_sigma,
+                             double tau_hi, double tau_lo, int has_hi, int has_lo) {
+    __shared__ double sh[kRedThreads];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
+    double S = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+        double umax = cs->std;
+        double cnt = (double)cs->n_eligible;
+        double sd = cnt > 0 ? sqrt(S / cnt) : 0.0;
+        cs->std = sd;
+        cs->tau_hi = has_hi ? tau_hi : cs->mean + k_sigma * sd;
+        cs->tau_lo = has_lo ? tau_lo : cs->mean - k_sigma * sd;
+        int shift = 0;
+        double tot = cnt * umax;
+        if (tot > 0.0) {
+            shift = (int)floor(61.0 - log2(tot));
+            shift = shift > 1000 ? 1000 : (shift < -1000 ? -1000 : shift);
+        }
+        cs->shift = shift;
+        cs->scale = ldexp(1.0, shift);
+        cs->inv_scale = ldexp(1.0, -shift);
+    }
+}
+
+// class increments and fixed-point u per visibility record
+__global__ void k_class_records(long long n_gain, GRec* __restrict__ grec, long long* __restrict__ guq,
+                                long long* __restrict__ ghl, const int* __restrict__ gidx,
+                                const float* __restrict__ w, int variant, const ClassState* __restrict__ cs) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_gain) return;
+    double u = u_of(w[gidx[i]], variant);
+    int inc = 0;
+    long long hl = 0;
+    if (u > cs->tau_hi) {
+        inc = 1;
+        hl = 1;
+    } else if (u < cs->tau_lo) {
+        inc = 0x10000;
+        hl = 1LL << 32;
+    }
+    grec[i].inc = inc;
+    long long q = llrint(u * cs->scale);
+    guq[i] = q;
+    ghl[i] = hl;
+}
+
+__global__ void k_gather_cells(long long ncells1, const int* __restrict__ gstart, const long long* __restrict__ pq,
+                               const long long* __restrict__ phl, long long* __restrict__ aq,
+                               long long* __restrict__ ahl) {
+    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= ncells1) return;
+    int s = gstart[c];
+    aq[c] = pq[s];
+    ahl[c] = phl[s];
+}
+
+inline unsigned nblocks(long long n, int t) {
+    long long b = (n + t - 1) / t;
+    return (unsigned)(b < 1 ? 1 : (b > 65535LL * 32 ? 65535LL * 32 : b));
+}
+
+}  // namespace
+
+rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi, double tau_lo,
+                        cudaStream_t st) {
+    bool has_hi = !std::isnan(tau_hi), has_lo = !std::isnan(tau_lo);
+    if (m->cls_variant == variant && m->cls_k == k_sigma && m->cls_th_nan == !has_hi &&
+        m->cls_tl_nan == !has_lo && (!has_hi || m->cls_th == tau_hi) && (!has_lo || m->cls_tl == tau_lo))
+        return RTG_OK;
+    int nparts = kRedBlocks;
+    note_launch(), k_red1<<<nparts, kRedThreads, 0, st>>>(m->n, m->w_orig, m->flags, variant, m->red_scratch);
+    note_launch(), k_red1_final<<<1, kRedThreads, 0, st>>>(m->red_scratch, nparts, m->cls);
+    note_launch(), k_red2<<<nparts, kRedThreads, 0, st>>>(m->n, m->w_orig, m->flags, variant, m->cls, m->red_scratch);
+    note_launch(), k_red2_final<<<1, kRedThreads, 0, st>>>(m->red_scratch, nparts, m->cls, k_sigma, tau_hi, tau_lo, has_hi,
+                                            has_lo);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("classify: %s", cudaGetErrorString(e));
+        return RTG_ERR_CUDA;
+    }
+    long long ng = m->n_gain;
+    long long *ghl = nullptr, *pq = nullptr, *phl = nullptr;
+    if (dev_alloc((void**)&ghl, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
+        dev_alloc((void**)&pq, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
+        dev_alloc((void**)&phl, sizeof(long long) * (ng + 1), st) != cudaSuccess) {
+        set_error("classify: out of device memory");
+        return RTG_ERR_OUT_OF_MEMORY;
+    }
+    if (ng > 0)
+        note_launch(), k_class_records<<<nblocks(ng, 256), 256, 0, st>>>(ng, m->grec, m->guq, ghl, m->gidx, m->w_orig, variant,
+                                                          m->cls);
+    e = exclusive_scan_i64(m->guq, pq, ng, st);
+    if (e == cudaSuccess) e = exclusive_scan_i64(ghl, phl, ng, st);
+    if (e == cudaSuccess) {
+        long long nc1 = m->gg.ncells + 1;
+        note_launch(), k_gather_cells<<<nblocks(nc1, 256), 256, 0, st>>>(nc1, m->gstart, pq, phl, m->gaggq, m->gagghl);
+        e = cudaGetLastError();
+    }
+    dev_free(ghl, st);
+    dev_free(pq, st);
+    dev_free(phl, st);
+    if (e != cudaSuccess) {
+        set_error("classify: %s", cudaGetErrorString(e));
+        return RTG_ERR_CUDA;
+    }
+    m->cls_variant = variant;
+    m->cls_k = k_sigma;
+    m->cls_th_nan = !has_hi;
+    m->cls_tl_nan = !has_lo;
+    m->cls_th = tau_hi;
+    m->cls_tl = tau_lo;
+    return RTG_OK;
+}
+
+#define MAP_CK(expr)                                                              \
+    do {                                                                          \
+        cudaError_t e_ = (expr);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            set_error("%s: %s", #expr, cudaGetErrorString(e_));                   \
+            return e_ == cudaErrorMemoryAllocation ? RTG_ERR_OUT_OF_MEMORY : RTG_ERR_CUDA; \
+        }                                                                         \
+    } while (0)
+
+template <typename T>
+static cudaError_t map_alloc(rtg_map_s* m, T** p, size_t count, cudaStream_t st) {
+    size_t bytes = sizeof(T) * (count > 0 ? count : 1);
+    cudaError_t e = dev_alloc((void**)p, bytes, st);
+    if (e == cudaSuccess) {
+        m->allocs.push_back(*p);
+        m->bytes += (long long)bytes;
+    }
+    return e;
+}
+
+static void pick_dims(float lo, float hi, double h, int& n) {
+    double span = (double)hi - (double)lo;
+    n = (int)floor(span / h) + 1;
+    if (n < 1) n = 1;
+}
+
+// Builds everything of rtg_map_create from device-resident inputs.
+rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const float* scales,
+                     const float* opacity, const float* w, const unsigned char* flags, const rtg_map_options* opt,
+                     cudaStream_t st) {
+    long long n = m->n;
+    const rtg_robot rb = m->robot;
+    // --- bounds + validation (one sync)
+    DevBounds* db = nullptr;
+    MAP_CK(dev_alloc((void**)&db, sizeof(DevBounds), st));
+    note_launch(), k_bounds_init<<<1, 1, 0, st>>>(db);
+    if (n > 0) note_launch(), k_bounds<<<nblocks(n, 256) > 4096 ? 4096 : nblocks(n, 256), 256, 0, st>>>(n, means, quats, scales, opacity, w, flags, rb, db);
+    DevBounds hb;
+    MAP_CK(cudaMemcpyAsync(&hb, db, sizeof(DevBounds), cudaMemcpyDeviceToHost, st));
+    MAP_CK(cudaStreamSynchronize(st));
+    dev_free(db, st);
+    if (hb.err) {
+        set_error("rtg_map_create: invalid element(s):%s%s%s%s%s", (hb.err & 1) ? " non-finite mean" : "",
+                  (hb.err & 2) ? " quaternion norm < 1e-12" : "", (hb.err & 4) ? " scale <= 0 or non-finite" : "",
+                  (hb.err & 8) ? " info_w < 0 or non-finite" : "", (hb.err & 16) ? " opacity outside [0,1]" : "");
+        return RTG_ERR_INVALID_ARGUMENT;
+    }
+    m->n_gain = hb.n_gain;
+    m->n_col = hb.n_col;
+    m->rb_max = m->n_col > 0 ? o2f(hb.rbmax) : 0.f;
+    double rho = m->n_col > 0 ? (double)o2f(hb.rhomax) : 1.0;
+    const double u32 = ldexp(1.0, -24);
+    double gq = (104.0 * rho + 6.0) * u32;   // FP32 error bound of q near 1, x2
+    m->gq = (float)gq;
+    // --- grid geometry
+    double hxy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.5;
+    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 0.5;
+    GainGrid& gg = m->gg;
+    if (m->n_gain > 0) {
+        float lo[3], hi[3];
+        for (int d = 0; d < 3; ++d) { lo[d] = o2f(hb.gmin[d]); hi[d] = o2f(hb.gmax[d]); }
+        for (;;) {
+            pick_dims(lo[0], hi[0], hxy, gg.nx);
+            pick_dims(lo[1], hi[1], hxy, gg.ny);
+            pick_dims(lo[2], hi[2], hz, gg.nz);
+            if ((double)gg.nx * gg.ny * gg.nz <= 64.0e6) break;
+            hxy *= 2.0;
+            hz *= 2.0;
+        }
+        gg.ox = lo[0]; gg.oy = lo[1]; gg.oz = lo[2];
+    } else {
+        gg.nx = gg.ny = gg.nz = 1;
+        gg.ox = gg.oy = gg.oz = 0.f;
+    }
+    gg.hxy = (float)hxy;
+    gg.hz = (float)hz;
+    gg.ncells = (long long)gg.nx * gg.ny * gg.nz;
+    ColGrid& cg = m->cg;
+    double hc = (opt && opt->col_cell > 0) ? opt->col_cell : fmax(0.5, 0.5 * (double)m->rb_max);
+    if (m->n_col > 0) {
+        float lo[3], hi[3];
+        for (int d = 0; d < 3; ++d) { lo[d] = o2f(hb.cmin[d]); hi[d] = o2f(hb.cmax[d]); }
+        for (;;) {
+            pick_dims(lo[0], hi[0], hc, cg.nx);
+            pick_dims(lo[1], hi[1], hc, cg.ny);
+            pick_dims(lo[2], hi[2], hc, cg.nz);
+            if ((double)cg.nx * cg.ny * cg.nz <= 64.0e6) break;
+            hc *= 2.0;
+        }
+        cg.ox = lo[0]; cg.oy = lo[1]; cg.oz = lo[2];
+    } else {
+        cg.nx = cg.ny = cg.nz = 1;
+        cg.ox = cg.oy = cg.oz = 0.f;
+    }
+    cg.h = (float)hc;
+    cg.ncells = (long long)cg.nx * cg.ny * cg.nz;
+    // --- allocations
+    m->n_gain_pad = ((m->n_gain + kTile - 1) / kTile) * kTile;
+    m->n_col_pad = ((m->n_col + kTile - 1) / kTile) * kTile;
+    MAP_CK(map_alloc(m, &m->w_orig, n, st));
+    if (flags) MAP_CK(map_alloc(m, &m->flags, n, st));
+    MAP_CK(map_alloc(m, &m->grec, m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->guq, m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->gidx, m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->gstart, gg.ncells + 1, st));
+    MAP_CK(map_alloc(m, &m->gaggq, gg.ncells + 1, st));
+    MAP_CK(map_alloc(m, &m->gagghl, gg.ncells + 1, st));
+    MAP_CK(map_alloc(m, &m->crec, m->n_col_pad, st));
+    MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
+    MAP_CK(map_alloc(m, &m->cmat64, m->n_col_pad, st));
+    MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
+    MAP_CK(map_alloc(m, &m->cls, 1, st));
+    MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
+    if (n > 0) MAP_CK(cudaMemcpyAsync(m->w_orig, w, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+    if (flags && n > 0) MAP_CK(cudaMemcpyAsync(m->flags, flags, n, cudaMemcpyDeviceToDevice, st));
+    // --- counting sort into both grids
+    int *gkey = nullptr, *ckey = nullptr, *gcount = nullptr, *ccount = nullptr;
+    MAP_CK(dev_alloc((void**)&gkey, sizeof(int) * (n > 0 ? n : 1), st));
+    MAP_CK(dev_alloc((void**)&ckey, sizeof(int) * (n > 0 ? n : 1), st));
+    MAP_CK(dev_alloc((void**)&gcount, sizeof(int) * (gg.ncells + 1), st));
+    MAP_CK(dev_alloc((void**)&ccount, sizeof(int) * (cg.ncells + 1), st));
+    MAP_CK(cudaMemsetAsync(gcount, 0, sizeof(int) * (gg.ncells + 1), st));
+    MAP_CK(cudaMemsetAsync(ccount, 0, sizeof(int) * (cg.ncells + 1), st));
+    unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
+    if (n > 0) note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, gcount, ccount);
+    MAP_CK(cudaGetLastError());
+    MAP_CK(exclusive_scan_i32(gcount, m->gstart, gg.ncells, st));
+    MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
+    // cursors (reuse the count arrays)
+    MAP_CK(cudaMemcpyAsync(gcount, m->gstart, sizeof(int) * gg.ncells, cudaMemcpyDeviceToDevice, st));
+    MAP_CK(cudaMemcpyAsync(ccount, m->cstart, sizeof(int) * cg.ncells, cudaMemcpyDeviceToDevice, st));
+    if (n > 0) {
+        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, gkey, gcount, m->grec, m->gidx);
+        note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, ccount, rb, gq, m->crec, m->cmat,
+                                          m->cmat64);
+    }
+    if (m->n_gain_pad > m->n_gain)
+        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(m->grec, m->guq, m->gidx, m->n_gain,
+                                                                            m->n_gain_pad);
+    if (m->n_col_pad > m->n_col)
+        note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->cmat64, m->n_col,
+                                                                         m->n_col_pad);
+    MAP_CK(cudaGetLastError());
+    dev_free(gkey, st);
+    dev_free(ckey, st);
+    dev_free(gcount, st);
+    dev_free(ccount, st);
+    // --- default classification (k = 1/2, derived thresholds)
+    m->cls_variant = -1;
+    return classify_map(m, RTG_VARIANT_XI, 0.5, NAN, NAN, st);
+}
+
+}  // namespace rtg

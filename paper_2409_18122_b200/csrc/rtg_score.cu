@@ -1,0 +1,869 @@
+// rtg_score.cu -- scoring kernels.
+//
+// Phase A (collision, a4): first colliding waypoint per trajectory.
+//   dense : every waypoint x every collidable Gaussian, TMA-bulk-staged record tiles in smem,
+//           split over the Gaussian axis (integer atomicMin / flag stores: order-free).
+//   culled: one warp per trajectory walks t = 0..T-1 and stops at the first collision
+//           (early exit); each waypoint tests only the collision-grid cells within the
+//           largest bounding radius, lanes load-balanced over the union of cell rows.
+// Phase B (visibility + gain, a5) over the info waypoints of feasible trajectories
+//   (two-phase; or of all trajectories with RTG_SCORE_FULL_GAIN):
+//   dense : waypoints in registers (4 per thread) x TMA-staged Gaussian tiles.
+//   culled: one warp per waypoint enumerates the visibility-grid columns under the frustum's
+//           footprint; whole z-cell runs strictly inside the frustum are added from exact
+//           fixed-point prefix sums, the straddling cells' Gaussians are tested one by one.
+// Reduction (a6) per trajectory and argmax (a7).
+#include <cfloat>
+#include <cmath>
+
+#include "rtg_host.hpp"
+
+namespace rtg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ===================================================================== dense phase A
+// Each thread owns 2 waypoints of the flattened K*T index; blockIdx.y splits the Gaussians.
+constexpr int kDenseColThreads = 256;
+constexpr int kDenseColWpt = 2;
+
+__global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
+    const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
+    const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CMat64* __restrict__ cm64,
+    long long n_col_pad, int tiles_per_split, float gq, int* __restrict__ first_col,
+    unsigned char* __restrict__ wp_col, int all_waypoints, unsigned long long* __restrict__ stats) {
+    __shared__ __align__(128) CRec s_tile[2][kTile];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const long long KT = (long long)K * T;
+    const long long tile0 = (long long)blockIdx.y * tiles_per_split;
+    const long long ntiles_all = n_col_pad / kTile;
+    long long ntiles = ntiles_all - tile0;
+    if (ntiles > tiles_per_split) ntiles = tiles_per_split;
+    if (ntiles <= 0) return;
+
+    float px[kDenseColWpt], py[kDenseColWpt], pz[kDenseColWpt];
+    int kk[kDenseColWpt], tt[kDenseColWpt];
+    bool act[kDenseColWpt], hit[kDenseColWpt];
+#pragma unroll
+    for (int j = 0; j < kDenseColWpt; ++j) {
+        long long i = (long long)blockIdx.x * (kDenseColThreads * kDenseColWpt) + j * kDenseColThreads + threadIdx.x;
+        act[j] = i < KT;
+        hit[j] = false;
+        long long ii = act[j] ? i : 0;
+        px[j] = X[ii]; py[j] = Y[ii]; pz[j] = Zw[ii];
+        act[j] = act[j] && isfinite(px[j]) && isfinite(py[j]) && isfinite(pz[j]);
+        kk[j] = (int)(ii / T);
+        tt[j] = (int)(ii % T);
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t tile_bytes = kTile * sizeof(CRec);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2 && s < ntiles; ++s) {
+            mbar_expect_tx(&s_bar[s], tile_bytes);
+            bulk_g2s(s_tile[s], crec + (tile0 + s) * kTile, tile_bytes, &s_bar[s]);
+        }
+    }
+    unsigned nref = 0;
+    for (long long it = 0; it < ntiles; ++it) {
+        const int s = (int)(it & 1);
+        // opportunistic skip: a waypoint after a known collision cannot change first_col
+        bool live = false;
+#pragma unroll
+        for (int j = 0; j < kDenseColWpt; ++j) {
+            if (act[j] && !hit[j] && !all_waypoints) {
+                int fc = *((volatile int*)&first_col[kk[j]]);
+                if (fc < tt[j]) act[j] = false;
+            }
+            live |= act[j] && !hit[j];
+        }
+        mbar_wait(&s_bar[s], (uint32_t)((it >> 1) & 1));
+        if (__syncthreads_or(live)) {
+            const CRec* tile = s_tile[s];
+#pragma unroll 4
+            for (int g = 0; g < kTile; ++g) {
+                const CRec A = tile[g];
+#pragma unroll
+                for (int j = 0; j < kDenseColWpt; ++j) {
+                    float dx = px[j] - A.x, dy = py[j] - A.y, dz = pz[j] - A.z;
+                    float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (d2 < A.rb2 && act[j] && !hit[j]) {
+                        long long gi = (tile0 + it) * kTile + g;
+                        hit[j] = collide_full(cmat[gi].m, dx, dy, dz, gq, &cm64[gi], px[j], py[j],
+                                              pz[j], A.x, A.y, A.z, nref);
+                    }
+                }
+            }
+        } else {
+            // nothing left to test in this block: drain the in-flight copies and stop
+            __syncthreads();
+            if (threadIdx.x == 0 && it + 1 < ntiles) mbar_wait(&s_bar[s ^ 1], (uint32_t)(((it + 1) >> 1) & 1));
+            break;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && it + 2 < ntiles) {
+            mbar_expect_tx(&s_bar[s], tile_bytes);
+            bulk_g2s(s_tile[s], crec + (tile0 + it + 2) * kTile, tile_bytes, &s_bar[s]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kDenseColWpt; ++j) {
+        if (hit[j]) {
+            long long i = (long long)kk[j] * T + tt[j];
+            if (wp_col) wp_col[i] = 1;
+            atomicMin(&first_col[kk[j]], tt[j]);
+        }
+    }
+    if (stats && nref) atomicAdd(&stats[0], (unsigned long long)nref);
+}
+
+// ===================================================================== culled phase A
+struct ColGridK {
+    float ox, oy, oz, h, R;
+    int nx, ny, nz;
+};
+
+__device__ __forceinline__ int clamp_cell(float v, int lo, int hi) {
+    v = fminf(fmaxf(v, (float)lo - 1.0f), (float)hi + 1.0f);
+    int c = (int)floorf(v);
+    return c;
+}
+
+constexpr int kWarps = 8;   // warps per block of the persistent culled kernels
+
+__global__ void __launch_bounds__(kWarps * 32) k_col_culled(
+    const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
+    const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CMat64* __restrict__ cm64,
+    const int* __restrict__ cstart, ColGridK g, float gq, int* __restrict__ first_col,
+    unsigned char* __restrict__ wp_col, int all_waypoints, int* __restrict__ counter,
+    unsigned long long* __restrict__ stats) {
+    __shared__ int s_incl[kWarps][32];
+    __shared__ int s_off[kWarps][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned nref = 0;
+    unsigned long long ntest = 0;
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(counter, 1);
+        k = __shfl_sync(kFull, k, 0);
+        if (k >= K) break;
+        int first = T;
+        for (int t = 0; t < T; ++t) {
+            const long long i = (long long)k * T + t;
+            const float px = X[i], py = Y[i], pz = Zw[i];
+            bool hit = false;
+            if (isfinite(px) && isfinite(py) && isfinite(pz)) {
+                int ix0 = max(0, clamp_cell((px - g.R - g.ox) / g.h, 0, g.nx));
+                int ix1 = min(g.nx - 1, clamp_cell((px + g.R - g.ox) / g.h, 0, g.nx));
+                int iy0 = max(0, clamp_cell((py - g.R - g.oy) / g.h, 0, g.ny));
+                int iy1 = min(g.ny - 1, clamp_cell((py + g.R - g.oy) / g.h, 0, g.ny));
+                int iz0 = max(0, clamp_cell((pz - g.R - g.oz) / g.h, 0, g.nz));
+                int iz1 = min(g.nz - 1, clamp_cell((pz + g.R - g.oz) / g.h, 0, g.nz));
+                if (ix0 <= ix1 && iy0 <= iy1 && iz0 <= iz1) {
+                    const int nyr = iy1 - iy0 + 1;
+                    const int nrows = nyr * (iz1 - iz0 + 1);
+                    for (int r0 = 0; r0 < nrows && !hit; r0 += 32) {
+                        const int r = r0 + lane;
+                        int beg = 0, len = 0;
+                        if (r < nrows) {
+                            int iz = iz0 + r / nyr, iy = iy0 + r % nyr;
+                            long long base = ((long long)iz * g.ny + iy) * g.nx;
+                            beg = cstart[base + ix0];
+                            len = cstart[base + ix1 + 1] - beg;
+                        }
+                        int incl = len;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            int v = __shfl_up_sync(kFull, incl, o);
+                            if (lane >= o) incl += v;
+                        }
+                        const int total = __shfl_sync(kFull, incl, 31);
+                        s_incl[wid][lane] = incl;
+                        s_off[wid][lane] = beg - (incl - len);
+                        __syncwarp();
+                        int owner = 0;
+                        for (int b0 = 0; b0 < total; b0 += 32) {
+                            const int pos = b0 + lane;
+                            bool h = false;
+                            if (pos < total) {
+                                while (s_incl[wid][owner] <= pos) ++owner;
+                                const int gi = pos + s_off[wid][owner];
+                                const CRec A = crec[gi];
+                                float dx = px - A.x, dy = py - A.y, dz = pz - A.z;
+                                float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                                if (d2 < A.rb2)
+                                    h = collide_full(cmat[gi].m, dx, dy, dz, gq, &cm64[gi], px, py,
+                                                     pz, A.x, A.y, A.z, nref);
+                            }
+                            ntest += (unsigned long long)min(32, total - b0);
+                            if (__any_sync(kFull, h)) {
+                                hit = true;
+                                break;
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            if (all_waypoints && lane == 0) wp_col[i] = hit ? 1 : 0;
+            if (hit) {
+                first = min(first, t);
+                if (!all_waypoints) break;
+            }
+        }
+        if (lane == 0) first_col[k] = first;
+    }
+    if (stats) {
+        nref = __reduce_add_sync(kFull, nref);
+        if (lane == 0) {
+            if (nref) atomicAdd(&stats[0], (unsigned long long)nref);
+            atomicAdd(&stats[2], ntest);
+        }
+    }
+}
+
+// ===================================================================== info-waypoint list
+// list = { k*T + t : trajectory k computed, (t+1) % stride == 0 }, k ascending, t ascending
+__global__ void k_build_list(const int* __restrict__ first_col, int K, int T, int stride, int full_gain,
+                             int* __restrict__ list, int* __restrict__ count) {
+    __shared__ int s_warp[32];
+    __shared__ int s_carry;
+    const int per = T / stride;   // number of info waypoints per trajectory
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int k0 = 0; k0 < K; k0 += blockDim.x) {
+        int k = k0 + threadIdx.x;
+        int inc = (k < K && (full_gain || first_col[k] == T)) ? 1 : 0;
+        // block exclusive scan of inc
+        int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int x = inc;
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += v;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(kFull, w, o);
+                if (lane >= o) w += v;
+            }
+            s_warp[lane] = w;
+        }
+        __syncthreads();
+        int rank = s_carry + (wid > 0 ? s_warp[wid - 1] : 0) + x - inc;
+        if (inc) {
+            for (int j = 0; j < per; ++j) list[(long long)rank * per + j] = k * T + (j + 1) * stride - 1;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += s_warp[(blockDim.x >> 5) - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = s_carry * per;
+}
+
+// identity list (debug: every waypoint)
+__global__ void k_iota(int* __restrict__ list, long long n, int* __restrict__ count) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) list[i] = (int)i;
+    if (i == 0) *count = (int)n;
+}
+
+// ===================================================================== dense phase B
+constexpr int kDenseGainThreads = 256;
+constexpr int kDenseGainWpt = 4;
+
+__global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
+    const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
+    const float* __restrict__ Yaw, const int* __restrict__ list, int list_n, const GRec* __restrict__ grec,
+    const long long* __restrict__ guq, long long n_gain_pad, int tiles_per_split, CamK cam,
+    unsigned long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
+    unsigned long long* __restrict__ stats) {
+    __shared__ __align__(128) GRec s_rec[2][kTile];
+    __shared__ __align__(128) long long s_uq[2][kTile];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const long long tile0 = (long long)blockIdx.y * tiles_per_split;
+    long long ntiles = n_gain_pad / kTile - tile0;
+    if (ntiles > tiles_per_split) ntiles = tiles_per_split;
+    if (ntiles <= 0) return;
+
+    WpF wf[kDenseGainWpt];
+    int wid[kDenseGainWpt];
+    bool act[kDenseGainWpt];
+    long long accq[kDenseGainWpt];
+    int nh[kDenseGainWpt], nl[kDenseGainWpt];
+#pragma unroll
+    for (int j = 0; j < kDenseGainWpt; ++j) {
+        int e = blockIdx.x * (kDenseGainThreads * kDenseGainWpt) + j * kDenseGainThreads + threadIdx.x;
+        act[j] = e < list_n;
+        int i = act[j] ? list[e] : list[0];
+        wid[j] = i;
+        float x = X[i], y = Y[i], z = Zw[i], yw = Yaw[i];
+        act[j] = act[j] && isfinite(x) && isfinite(y) && isfinite(z) && isfinite(yw);
+        if (!act[j]) { x = __int_as_float(0x7fc00000); y = x; z = x; yw = 0.f; }   // NaN pose: sees nothing
+        wp_setup(x, y, z, yw, cam, wf[j]);
+        accq[j] = 0;
+        nh[j] = 0;
+        nl[j] = 0;
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t rb = kTile * sizeof(GRec), qb = kTile * sizeof(long long);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2 && s < ntiles; ++s) {
+            mbar_expect_tx(&s_bar[s], rb + qb);
+            bulk_g2s(s_rec[s], grec + (tile0 + s) * kTile, rb, &s_bar[s]);
+            bulk_g2s(s_uq[s], guq + (tile0 + s) * kTile, qb, &s_bar[s]);
+        }
+    }
+    unsigned nref = 0;
+    for (long long it = 0; it < ntiles; ++it) {
+        const int s = (int)(it & 1);
+        mbar_wait(&s_bar[s], (uint32_t)((it >> 1) & 1));
+        int pc[kDenseGainWpt];
+#pragma unroll
+        for (int j = 0; j < kDenseGainWpt; ++j) pc[j] = 0;
+        const GRec* rec = s_rec[s];
+        const long long* uq = s_uq[s];
+#pragma unroll 2
+        for (int g = 0; g < kTile; ++g) {
+            const GRec G = rec[g];
+            const long long q = uq[g];
+#pragma unroll
+            for (int j = 0; j < kDenseGainWpt; ++j) {
+                if (visible(wf[j], cam, G.x, G.y, G.z, nref)) {
+                    accq[j] += q;
+                    pc[j] += G.inc;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kDenseGainWpt; ++j) {
+            nh[j] += pc[j] & 0xffff;
+            nl[j] += pc[j] >> 16;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && it + 2 < ntiles) {
+            mbar_expect_tx(&s_bar[s], rb + qb);
+            bulk_g2s(s_rec[s], grec + (tile0 + it + 2) * kTile, rb, &s_bar[s]);
+            bulk_g2s(s_uq[s], guq + (tile0 + it + 2) * kTile, qb, &s_bar[s]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kDenseGainWpt; ++j) {
+        if (act[j]) {
+            if (accq[j]) atomicAdd(&wp_gq[wid[j]], (unsigned long long)accq[j]);
+            if (nh[j]) atomicAdd(&wp_nh[wid[j]], nh[j]);
+            if (nl[j]) atomicAdd(&wp_nl[wid[j]], nl[j]);
+        }
+    }
+    if (stats && nref) atomicAdd(&stats[1], (unsigned long long)nref);
+}
+
+// ===================================================================== culled phase B
+struct GainGridK {
+    float ox, oy, oz, h, hz, eps;
+    int nx, ny, nz;
+};
+
+__global__ void __launch_bounds__(kWarps * 32) k_gain_culled(
+    const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
+    const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
+    const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
+    const long long* __restrict__ aggq, const long long* __restrict__ agghl, GainGridK g, CamK cam,
+    long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl, int* __restrict__ counter,
+    unsigned long long* __restrict__ stats) {
+    __shared__ int s_rincl[kWarps][32];
+    __shared__ int s_roff[kWarps][32];
+    __shared__ int s_iincl[kWarps][64];
+    __shared__ int s_ioff[kWarps][64];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int L = *list_count;
+    unsigned nref = 0;
+    unsigned long long ntest = 0, nagg = 0;
+    const float zn = cam.zmid - cam.zhalf, zf = cam.zmid + cam.zhalf;
+    const float kxl = cam.kxh - cam.kxc, kxr = cam.kxh + cam.kxc;
+    const float kyu = cam.kyh + cam.kyc, kyd = cam.kyh - cam.kyc;
+    const float eps = g.eps, hh = 0.5f * g.h;
+    for (;;) {
+        int e = 0;
+        if (lane == 0) e = atomicAdd(counter, 1);
+        e = __shfl_sync(kFull, e, 0);
+        if (e >= L) break;
+        const int i = list[e];
+        const float px = X[i], py = Y[i], pz = Zw[i], yw = Yaw[i];
+        long long accq = 0;
+        int acch = 0, accl = 0;
+        if (isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(yw)) {
+            WpF f;
+            wp_setup(px, py, pz, yw, cam, f);
+            // footprint trapezoid of the frustum in the xy plane (grid-relative coordinates)
+            const float qx = px - g.ox, qy = py - g.oy;
+            const float Fx = f.c, Fy = f.s, Rx = f.s, Ry = -f.c;
+            float vx[4], vy[4];
+            vx[0] = qx + zn * Fx - kxl * zn * Rx; vy[0] = qy + zn * Fy - kxl * zn * Ry;
+            vx[1] = qx + zn * Fx + kxr * zn * Rx; vy[1] = qy + zn * Fy + kxr * zn * Ry;
+            vx[2] = qx + zf * Fx + kxr * zf * Rx; vy[2] = qy + zf * Fy + kxr * zf * Ry;
+            vx[3] = qx + zf * Fx - kxl * zf * Rx; vy[3] = qy + zf * Fy - kxl * zf * Ry;
+            const float ymn = fminf(fminf(vy[0], vy[1]), fminf(vy[2], vy[3])) - eps;
+            const float ymx = fmaxf(fmaxf(vy[0], vy[1]), fmaxf(vy[2], vy[3])) + eps;
+            const int iy0 = max(0, clamp_cell(ymn / g.h, 0, g.ny));
+            const int iy1 = min(g.ny - 1, clamp_cell(ymx / g.h, 0, g.ny));
+            // per-waypoint column-test constants (linear functions over an h x h column)
+            const float Zr = (fabsf(f.c) + fabsf(f.s)) * hh;
+            const float f1r = (fabsf(cam.kxh * f.c - f.ax) + fabsf(cam.kxh * f.s - f.bx)) * hh;
+            const float f2r = (fabsf(cam.kxh * f.c + f.ax) + fabsf(cam.kxh * f.s + f.bx)) * hh;
+            const float zrel = pz - g.oz;
+            for (int rbase = iy0; rbase <= iy1; rbase += 32) {
+                const int iy = rbase + lane;
+                int ixlo = 0, len = 0;
+                if (iy <= iy1) {
+                    const float yb0 = iy * g.h - eps, yb1 = (iy + 1) * g.h + eps;
+                    float xlo = FLT_MAX, xhi = -FLT_MAX;
+#pragma unroll
+                    for (int ed = 0; ed < 4; ++ed) {
+                        const float ax = vx[ed], ay = vy[ed], bx = vx[(ed + 1) & 3], by = vy[(ed + 1) & 3];
+                        const float elo = fminf(ay, by), ehi = fmaxf(ay, by);
+                        if (ehi < yb0 || elo > yb1) continue;
+                        float xa, xb;
+                        if (ehi - elo <= 1e-12f) {
+                            xa = ax; xb = bx;
+                        } else {
+                            const float inv = 1.0f / (by - ay);
+                            const float t0 = (fmaxf(yb0, elo) - ay) * inv, t1 = (fminf(yb1, ehi) - ay) * inv;
+                            xa = fmaf(t0, bx - ax, ax);
+                            xb = fmaf(t1, bx - ax, ax);
+                        }
+                        xlo = fminf(xlo, fminf(xa, xb));
+                        xhi = fmaxf(xhi, fmaxf(xa, xb));
+                    }
+                    if (xlo <= xhi) {
+                        const int ix0 = max(0, clamp_cell((xlo - eps) / g.h, 0, g.nx));
+                        const int ix1 = min(g.nx - 1, clamp_cell((xhi + eps) / g.h, 0, g.nx));
+                        if (ix0 <= ix1) {
+                            ixlo = ix0;
+                            len = ix1 - ix0 + 1;
+                        }
+                    }
+                }
+                int incl = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int v = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int total = __shfl_sync(kFull, incl, 31);
+                s_rincl[wid][lane] = incl;
+                s_roff[wid][lane] = ixlo - (incl - len);
+                __syncwarp();
+                int owner = 0;
+                for (int cb = 0; cb < total; cb += 32) {
+                    const int pos = cb + lane;
+                    int b0 = 0, l0 = 0, b1 = 0, l1 = 0;
+                    if (pos < total) {
+                        while (s_rincl[wid][owner] <= pos) ++owner;
+                        const int ix = pos + s_roff[wid][owner];
+                        const int cy = rbase + owner;
+                        // column centre relative to the camera
+                        const float xc = fmaf((float)ix + 0.5f, g.h, -qx);
+                        const float yc = fmaf((float)cy + 0.5f, g.h, -qy);
+                        const float Zc = fmaf(f.c, xc, f.s * yc);
+                        const float Xc = fmaf(f.ax, xc, f.bx * yc);
+                        const float f1c = fmaf(cam.kxh, Zc, -Xc), f2c = fmaf(cam.kxh, Zc, Xc);
+                        const float Zmin = Zc - Zr, Zmax = Zc + Zr;
+                        const bool out = (Zmax < zn - eps) | (Zmin > zf + eps) | (f1c + f1r < -eps) |
+                                         (f2c + f2r < -eps);
+                        if (!out) {
+                            const bool in_h = (Zmin >= zn + eps) & (Zmax <= zf - eps) & (f1c - f1r >= eps) &
+                                              (f2c - f2r >= eps);
+                            const float Zhi = fmaxf(fminf(Zmax, zf), 0.0f);
+                            int c = clamp_cell((zrel - kyd * Zhi - eps) / g.hz, 0, g.nz);
+                            int dd = clamp_cell((zrel + kyu * Zhi + eps) / g.hz, 0, g.nz) + 1;
+                            c = min(max(c, 0), g.nz);
+                            dd = min(max(dd, c), g.nz);
+                            int a = c, b = c;
+                            if (in_h) {
+                                float za = (zrel - kyd * Zmin + eps) / g.hz;
+                                float zb = (zrel + kyu * Zmin - eps) / g.hz;
+                                za = fminf(fmaxf(za, -1.0f), (float)g.nz + 1.0f);
+                                zb = fminf(fmaxf(zb, -1.0f), (float)g.nz + 1.0f);
+                                a = min(max((int)ceilf(za), c), dd);
+                                b = min(max((int)floorf(zb), a), dd);
+                            }
+                            const long long base = ((long long)cy * g.nx + ix) * g.nz;
+                            const int sc = gstart[base + c], sa = gstart[base + a];
+                            const int sb = gstart[base + b], sd = gstart[base + dd];
+                            if (b > a) {
+                                accq += aggq[base + b] - aggq[base + a];
+                                const long long hl = agghl[base + b] - agghl[base + a];
+                                acch += (int)(hl & 0xffffffffLL);
+                                accl += (int)(hl >> 32);
+                                nagg += (unsigned long long)(b - a);
+                            }
+                            b0 = sc; l0 = sa - sc;
+                            b1 = sb; l1 = sd - sb;
+                        }
+                    }
+                    // load-balanced individual tests over this chunk's partial cell runs
+                    const int sl = l0 + l1;
+                    int ic = sl;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int v = __shfl_up_sync(kFull, ic, o);
+                        if (lane >= o) ic += v;
+                    }
+                    const int tot = __shfl_sync(kFull, ic, 31);
+                    const int ex = ic - sl;
+                    s_iincl[wid][2 * lane] = ex + l0;
+                    s_ioff[wid][2 * lane] = b0 - ex;
+                    s_iincl[wid][2 * lane + 1] = ic;
+                    s_ioff[wid][2 * lane + 1] = b1 - (ex + l0);
+                    __syncwarp();
+                    int own = 0, pc = 0;
+                    for (int gb = 0; gb < tot; gb += 32) {
+                        const int gp = gb + lane;
+                        if (gp < tot) {
+                            while (s_iincl[wid][own] <= gp) ++own;
+                            const int gi = gp + s_ioff[wid][own];
+                            const GRec G = grec[gi];
+                            const long long q = guq[gi];
+                            if (visible(f, cam, G.x, G.y, G.z, nref)) {
+                                accq += q;
+                                pc += G.inc;
+                            }
+                        }
+                    }
+                    ntest += (unsigned long long)tot;
+                    acch += pc & 0xffff;
+                    accl += pc >> 16;
+                    __syncwarp();
+                }
+            }
+        }
+        // warp totals (integers: exact, order-free)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            accq += __shfl_xor_sync(kFull, accq, o);
+            acch += __shfl_xor_sync(kFull, acch, o);
+            accl += __shfl_xor_sync(kFull, accl, o);
+        }
+        if (lane == 0) {
+            wp_gq[i] = accq;
+            wp_nh[i] = acch;
+            wp_nl[i] = accl;
+        }
+    }
+    if (stats) {
+        nref = __reduce_add_sync(kFull, nref);
+        if (lane == 0) {
+            if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
+            atomicAdd(&stats[2], ntest);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nagg += __shfl_xor_sync(kFull, nagg, o);
+        if (lane == 0) atomicAdd(&stats[3], nagg);
+    }
+}
+
+// ===================================================================== a6 reduction
+__global__ void k_reduce(int K, int T, int stride, int variant, float lambda_xi, int full_gain,
+                         const int* __restrict__ first_col, const long long* __restrict__ wp_gq,
+                         const int* __restrict__ wp_nh, const int* __restrict__ wp_nl,
+                         const ClassState* __restrict__ cs, int* __restrict__ out_first,
+                         unsigned char* __restrict__ out_feasible, double* __restrict__ out_gain,
+                         double* __restrict__ out_util) {
+    const int lane = threadIdx.x & 31;
+    const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (k >= K) return;
+    const int fc = first_col[k];
+    const bool feasible = fc >= T;
+    const bool computed = feasible || full_gain;
+    long long q = 0, h = 0, l = 0;
+    if (computed) {
+        for (int t = stride - 1 + lane * stride; t < T; t += 32 * stride) {
+            long long i = (long long)k * T + t;
+            q += wp_gq[i];
+            h += wp_nh[i];
+            l += wp_nl[i];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        q += __shfl_xor_sync(kFull, q, o);
+        h += __shfl_xor_sync(kFull, h, o);
+        l += __shfl_xor_sync(kFull, l, o);
+    }
+    if (lane == 0) {
+        const double nan = __longlong_as_double(0x7ff8000000000000LL);
+        double gain = computed ? (double)q * cs->inv_scale : nan;
+        double xi = (double)h - (double)lambda_xi * (double)l;
+        double util = feasible ? (variant == RTG_VARIANT_SUM ? gain : xi) : -INFINITY;
+        if (out_first) out_first[k] = feasible ? T : fc;
+        if (out_feasible) out_feasible[k] = feasible ? 1 : 0;
+        if (out_gain) out_gain[k] = gain;
+        if (out_util) out_util[k] = util;
+    }
+}
+
+// per-waypoint debug outputs
+__global__ void k_debug_wp(long long n, const long long* __restrict__ wp_gq, const ClassState* __restrict__ cs,
+                           double* __restrict__ out_gain) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) out_gain[i] = (double)wp_gq[i] * cs->inv_scale;
+}
+
+// ===================================================================== a7 argmax
+struct BestDev {
+    double score;
+    long long index;
+};
+
+__global__ void k_best(const double* __restrict__ u, int K, long long base, BestDev* __restrict__ out) {
+    __shared__ double sv[1024];
+    __shared__ int si[1024];
+    double bv = -INFINITY;
+    int bi = -1;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        double v = u[k];
+        if (v > bv) {   // strict: keeps the lowest index among equal values (k ascending per thread)
+            bv = v;
+            bi = k;
+        }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            double ov = sv[threadIdx.x + s];
+            int oi = si[threadIdx.x + s];
+            double mv = sv[threadIdx.x];
+            int mi = si[threadIdx.x];
+            if (oi >= 0 && (mi < 0 || ov > mv || (ov == mv && oi < mi))) {
+                sv[threadIdx.x] = ov;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out->score = si[0] >= 0 ? sv[0] : -INFINITY;
+        out->index = si[0] >= 0 ? base + si[0] : -1;
+    }
+}
+
+// ===================================================================== debug pair mask
+__global__ void k_pair_mask(const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
+                            long long KT, long long N, const CRec* __restrict__ crec, const CMat* __restrict__ cmat,
+                            const CMat64* __restrict__ cm64, long long n_col, float gq,
+                            unsigned int* __restrict__ mask) {
+    long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= KT * n_col) return;
+    long long i = idx / n_col, g = idx % n_col;
+    float px = X[i], py = Y[i], pz = Zw[i];
+    const CRec A = crec[g];
+    float dx = px - A.x, dy = py - A.y, dz = pz - A.z;
+    float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    unsigned nref = 0;
+    if (d2 < A.rb2 &&
+        collide_full(cmat[g].m, dx, dy, dz, gq, &cm64[g], px, py, pz, A.x, A.y, A.z, nref)) {
+        long long orig = __float_as_int(cmat[g].m[9]);
+        unsigned long long bit = (unsigned long long)(i * N + orig);
+        atomicOr(&mask[bit >> 5], 1u << (bit & 31));
+    }
+}
+
+// ===================================================================== sampler (a3)
+__global__ void k_sample_unicycle(int K, int T, double dt, double x0, double y0, double z0, double th0,
+                                  const float* __restrict__ v, const float* __restrict__ om, float* __restrict__ X,
+                                  float* __restrict__ Y, float* __restrict__ Zw, float* __restrict__ Yaw) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= (long long)K * T) return;
+    int k = (int)(i / T), l = (int)(i % T);
+    double vv = v[k], ww = om[k];
+    double t = (l + 1) * dt;
+    double th = th0 + ww * t;
+    double x, y;
+    if (fabs(ww) < 1e-12) {
+        x = x0 + vv * t * cos(th0);
+        y = y0 + vv * t * sin(th0);
+    } else {
+        x = x0 + (vv / ww) * (sin(th) - sin(th0));
+        y = y0 + (vv / ww) * (cos(th0) - cos(th));
+    }
+    double wr = remainder(th, 2.0 * M_PI);   // in [-pi, pi]
+    if (wr <= -M_PI) wr += 2.0 * M_PI;
+    X[i] = (float)x;
+    Y[i] = (float)y;
+    Zw[i] = (float)z0;
+    Yaw[i] = (float)wr;
+}
+
+// ===================================================================== host launchers
+namespace {
+int g_occ_col = 0, g_occ_gain = 0, g_sms = 0;
+void occupancy(int dev) {
+    if (g_sms) return;
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_col, k_col_culled, kWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_gain, k_gain_culled, kWarps * 32, 0);
+    if (g_occ_col < 1) g_occ_col = 1;
+    if (g_occ_gain < 1) g_occ_gain = 1;
+}
+}  // namespace
+
+CamK make_cam(const rtg_camera& c, const double* cam64_dev) {
+    CamK k;
+    double W = c.width, H = c.height, fx = c.fx, fy = c.fy, cx = c.cx, cy = c.cy, zn = c.z_near, zf = c.z_far;
+    double kxl = cx / fx, kxr = (W - cx) / fx, kyu = cy / fy, kyd = (H - cy) / fy;
+    k.zmid = (float)(0.5 * (zn + zf));
+    k.zhalf = (float)(0.5 * (zf - zn));
+    k.kxc = (float)(0.5 * (kxr - kxl));
+    k.kxh = (float)(0.5 * (kxr + kxl));
+    k.kyc = (float)(0.5 * (kyu - kyd));
+    k.kyh = (float)(0.5 * (kyu + kyd));
+    // FP32 error bound of the min slack, doubled
+    const double u = ldexp(1.0, -24);
+    double kxm = fabs(k.kxc) + k.kxh, kym = fabs(k.kyc) + k.kyh;
+    k.gam = (float)(24.0 * u * (1.0 + kxm) * (1.0 + kym) * sqrt(1.0 + kxm * kxm) * 2.0);
+    k.g0 = (float)(8.0 * u * (fabs(k.zmid) + k.zhalf + 1.0));
+    k.cam64 = cam64_dev;
+    return k;
+}
+
+cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_col, unsigned char* wp_col,
+                           int all_wp, int* counter, unsigned long long* stats, cudaStream_t st) {
+    occupancy(m->device);
+    const int K = tr->K, T = tr->T;
+    if (mode == RTG_MODE_DENSE) {
+        long long KT = (long long)K * T;
+        int wblocks = (int)((KT + kDenseColThreads * kDenseColWpt - 1) / (kDenseColThreads * kDenseColWpt));
+        long long ntiles = m->n_col_pad / kTile;
+        if (ntiles == 0) return cudaGetLastError();
+        long long want = (long long)g_sms * 8;
+        long long splits = (want + wblocks - 1) / wblocks;
+        if (splits > ntiles) splits = ntiles;
+        if (splits < 1) splits = 1;
+        int tps = (int)((ntiles + splits - 1) / splits);
+        splits = (ntiles + tps - 1) / tps;
+        dim3 grid(wblocks, (unsigned)splits);
+        note_launch(), k_col_dense<<<grid, kDenseColThreads, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->cmat64,
+                                                       m->n_col_pad, tps, m->gq, first_col, wp_col, all_wp, stats);
+    } else {
+        if (m->n_col == 0) return cudaGetLastError();
+        ColGridK g;
+        g.ox = m->cg.ox; g.oy = m->cg.oy; g.oz = m->cg.oz; g.h = m->cg.h;
+        g.R = m->rb_max * (1.0f + 2e-5f) + 1e-4f;
+        g.nx = m->cg.nx; g.ny = m->cg.ny; g.nz = m->cg.nz;
+        int blocks = (K + kWarps - 1) / kWarps;
+        int cap = g_sms * g_occ_col;
+        if (blocks > cap) blocks = cap;
+        note_launch(), k_col_culled<<<blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->cmat64,
+                                                     m->cstart, g, m->gq, first_col, wp_col, all_wp, counter, stats);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_list(const int* first_col, int K, int T, int stride, int full_gain, int* list, int* count,
+                        cudaStream_t st) {
+    note_launch(), k_build_list<<<1, 1024, 0, st>>>(first_col, K, T, stride, full_gain, list, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_iota(int* list, long long n, int* count, cudaStream_t st) {
+    note_launch(), k_iota<<<(unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1), 256, 0, st>>>(list, n, count);
+    return cudaGetLastError();
+}
+
+// dense phase B needs the list length on the host (one sync; dense mode is the brute-force path)
+cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& cam, const int* list,
+                           const int* count, long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl,
+                           int* counter, unsigned long long* stats, cudaStream_t st) {
+    occupancy(m->device);
+    if (mode == RTG_MODE_DENSE) {
+        int n = 0;
+        cudaError_t e = cudaMemcpyAsync(&n, count, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        long long ntiles = m->n_gain_pad / kTile;
+        if (n == 0 || ntiles == 0) return cudaGetLastError();
+        int per_block = kDenseGainThreads * kDenseGainWpt;
+        int wblocks = (n + per_block - 1) / per_block;
+        long long want = (long long)g_sms * 8;
+        long long splits = (want + wblocks - 1) / wblocks;
+        if (splits > ntiles) splits = ntiles;
+        if (splits < 1) splits = 1;
+        int tps = (int)((ntiles + splits - 1) / splits);
+        splits = (ntiles + tps - 1) / tps;
+        dim3 grid(wblocks, (unsigned)splits);
+        note_launch(), k_gain_dense<<<grid, kDenseGainThreads, 0, st>>>(tr->x, tr->y, tr->z, tr->yaw, list, n, m->grec, m->guq,
+                                                         m->n_gain_pad, tps, cam, (unsigned long long*)wp_gq, wp_nh,
+                                                         wp_nl, stats);
+    } else {
+        GainGridK g;
+        g.ox = m->gg.ox; g.oy = m->gg.oy; g.oz = m->gg.oz; g.h = m->gg.hxy; g.hz = m->gg.hz;
+        double ext = fmax(fmax(fabs(g.ox), fabs(g.oy)), fabs(g.oz)) + (double)(m->gg.nx + m->gg.ny + m->gg.nz) *
+                     fmax(m->gg.hxy, m->gg.hz) + cam.zmid + cam.zhalf;
+        g.eps = (float)(1e-3 + 256.0 * ldexp(1.0, -24) * ext);
+        g.nx = m->gg.nx; g.ny = m->gg.ny; g.nz = m->gg.nz;
+        long long blocks = (list_max + kWarps - 1) / kWarps;
+        long long cap = (long long)g_sms * g_occ_gain;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        note_launch(), k_gain_culled<<<(unsigned)blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec,
+                                                                m->guq, m->gstart, m->gaggq, m->gagghl, g, cam,
+                                                                wp_gq, wp_nh, wp_nl, counter, stats);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(rtg_map_s* m, rtg_traj_s* tr, const rtg_score_params& p, const int* first_col,
+                          const long long* wp_gq, const int* wp_nh, const int* wp_nl, int* out_first,
+                          unsigned char* out_feasible, double* out_gain, double* out_util, cudaStream_t st) {
+    int K = tr->K;
+    int threads = 256;
+    int blocks = (int)(((long long)K * 32 + threads - 1) / threads);
+    note_launch(), k_reduce<<<blocks, threads, 0, st>>>(K, tr->T, p.info_stride, p.variant, p.lambda_xi,
+                                         (p.flags & RTG_SCORE_FULL_GAIN) ? 1 : 0, first_col, wp_gq, wp_nh, wp_nl,
+                                         m->cls, out_first, out_feasible, out_gain, out_util);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_wp(long long n, const long long* wp_gq, const ClassState* cs, double* out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    note_launch(), k_debug_wp<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, wp_gq, cs, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaStream_t st) {
+    long long KT = (long long)tr->K * tr->T;
+    long long tot = KT * m->n_col;
+    if (tot == 0) return cudaSuccess;
+    note_launch(), k_pair_mask<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tr->x, tr->y, tr->z, KT, m->n, m->crec, m->cmat,
+                                                                m->cmat64, m->n_col, m->gq, mask);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st) {
+    note_launch(), k_best<<<1, 1024, 0, st>>>(u, K, base, (BestDev*)out_dev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sampler(int K, int T, double dt, const float* start, const float* v, const float* om,
+                           rtg_traj_s* tr, cudaStream_t st) {
+    long long n = (long long)K * T;
+    note_launch(), k_sample_unicycle<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(K, T, dt, start[0], start[1], start[2], start[3],
+                                                                   v, om, tr->x, tr->y, tr->z, tr->yaw);
+    return cudaGetLastError();
+}
+
+}  // namespace rtg

@@ -1,0 +1,355 @@
+"""Thin Python binding of librtg (include/rtg.h) -- argument marshalling only.
+
+Every step of the scoring path runs in the library's CUDA kernels; this module only
+turns torch tensors / numpy arrays into pointers, sizes and streams and raises on a
+non-OK status.  There is no CPU fallback: importing this module fails loudly when
+librtg.so is missing, and every call that needs a GPU fails loudly without one.
+
+Names follow the C ABI: ``map_create`` -> rtg_map_create, ``traj_upload`` ->
+rtg_traj_upload, ``traj_sample_unicycle``, ``score`` -> rtg_score, ``best`` -> rtg_best,
+``score_debug`` -> rtg_score_debug.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtg.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"librtg.so not found at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc, sm_100a). There is no CPU fallback.")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ ABI mirror
+OK, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_NO_FEASIBLE, ERR_BAD_HANDLE = range(6)
+MEM_HOST, MEM_DEVICE = 0, 1
+G_NO_COLLIDE, G_NO_GAIN = 1, 2
+COLLIDE_ELLIPSOID, COLLIDE_PRINCIPAL_AXIS = 0, 1
+VARIANT_XI, VARIANT_SUM, VARIANT_SQ = 0, 1, 2
+MODE_DENSE, MODE_CULLED = 0, 1
+SCORE_FULL_GAIN, SCORE_NO_COLLISION = 1, 2
+
+
+class Robot(ctypes.Structure):
+    _fields_ = [("r_robot", ctypes.c_float), ("lambda_g", ctypes.c_float), ("collide_rule", ctypes.c_int)]
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int), ("height", ctypes.c_int), ("fx", ctypes.c_float), ("fy", ctypes.c_float),
+                ("cx", ctypes.c_float), ("cy", ctypes.c_float), ("z_near", ctypes.c_float), ("z_far", ctypes.c_float)]
+
+
+class ScoreParams(ctypes.Structure):
+    _fields_ = [("lambda_xi", ctypes.c_float), ("k_sigma", ctypes.c_float), ("variant", ctypes.c_int),
+                ("info_stride", ctypes.c_int), ("mode", ctypes.c_int), ("flags", ctypes.c_uint),
+                ("tau_hi", ctypes.c_double), ("tau_lo", ctypes.c_double)]
+
+
+class BestResult(ctypes.Structure):
+    _fields_ = [("score", ctypes.c_double), ("index", ctypes.c_longlong)]
+
+
+class MapOptions(ctypes.Structure):
+    _fields_ = [("gain_cell_xy", ctypes.c_float), ("gain_cell_z", ctypes.c_float), ("col_cell", ctypes.c_float)]
+
+
+class MapInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_longlong), ("n_collide", ctypes.c_longlong), ("n_gain", ctypes.c_longlong),
+                ("tau_hi", ctypes.c_double), ("tau_lo", ctypes.c_double), ("u_mean", ctypes.c_double),
+                ("u_std", ctypes.c_double), ("fixed_point_shift", ctypes.c_int),
+                ("gain_dims", ctypes.c_int * 3), ("col_dims", ctypes.c_int * 3), ("rb_max", ctypes.c_float),
+                ("device_bytes", ctypes.c_longlong)]
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 8), ("calls", ctypes.c_longlong * 8), ("launches", ctypes.c_longlong)]
+
+
+PHASES = ("map_build", "classify", "collision", "info_list", "visibility_gain", "reduce", "argmax", "other")
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_LL = ctypes.c_longlong
+_S = ctypes.c_int  # rtg_status
+
+_SIGS = {
+    "rtg_map_create": (_S, [_I, _LL, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Robot), _P, ctypes.POINTER(_P)]),
+    "rtg_map_create_ex": (_S, [_I, _LL, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Robot),
+                               ctypes.POINTER(MapOptions), _P, ctypes.POINTER(_P)]),
+    "rtg_map_destroy": (_S, [_P]),
+    "rtg_map_info": (_S, [_P, ctypes.POINTER(MapInfo)]),
+    "rtg_traj_upload": (_S, [_I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.POINTER(_P)]),
+    "rtg_traj_sample_unicycle": (_S, [_I, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_float), _P, _P, _I, _P,
+                                      ctypes.POINTER(_P)]),
+    "rtg_traj_read": (_S, [_P, _P, _P, _P, _P, _P]),
+    "rtg_traj_destroy": (_S, [_P]),
+    "rtg_score": (_S, [_P, _P, ctypes.POINTER(Camera), ctypes.POINTER(ScoreParams), _P, _P, _P, _P, _P]),
+    "rtg_best": (_S, [_P, _I, _LL, _P, ctypes.POINTER(BestResult)]),
+    "rtg_score_debug": (_S, [_P, _P, ctypes.POINTER(Camera), ctypes.POINTER(ScoreParams), _P, _P, _P, _P, _P,
+                             _P, _P]),
+    "rtg_profile_enable": (_S, [_I]),
+    "rtg_profile_read": (_S, [ctypes.POINTER(Profile), _I]),
+    "rtg_status_string": (ctypes.c_char_p, [_I]),
+    "rtg_last_error": (ctypes.c_char_p, []),
+    "rtg_version": (ctypes.c_char_p, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+class RTGError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.rtg_last_error().decode()
+        super().__init__(f"{where}: {_lib.rtg_status_string(status).decode()}: {msg}")
+
+
+def _check(status: int, where: str, allow=()):
+    if status != OK and status not in allow:
+        raise RTGError(status, where)
+    return status
+
+
+def version() -> str:
+    return _lib.rtg_version().decode()
+
+
+def profile_enable(on: bool = True) -> None:
+    _check(_lib.rtg_profile_enable(1 if on else 0), "rtg_profile_enable")
+
+
+def profile_read(reset: bool = True) -> dict:
+    """Accumulated device ms / calls per phase (CUDA events on the launch streams) + kernel launches."""
+    p = Profile()
+    _check(_lib.rtg_profile_read(ctypes.byref(p), 1 if reset else 0), "rtg_profile_read")
+    return dict(ms={n: p.ms[i] for i, n in enumerate(PHASES)}, calls={n: p.calls[i] for i, n in enumerate(PHASES)},
+                launches=p.launches)
+
+
+# ------------------------------------------------------------------ helpers
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(a) -> Optional[int]:
+    """Pointer of a contiguous torch tensor or numpy array (None passes NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("numpy array must be C-contiguous")
+        return a.ctypes.data
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return a.data_ptr()
+
+
+def _kind(a) -> int:
+    if isinstance(a, np.ndarray):
+        return MEM_HOST
+    return MEM_DEVICE if a.is_cuda else MEM_HOST
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        torch = _torch()
+        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def make_camera(cam) -> Camera:
+    return Camera(int(cam.width), int(cam.height), float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy),
+                  float(cam.z_near), float(cam.z_far))
+
+
+def make_params(lambda_xi=1.0, k_sigma=0.5, variant=VARIANT_XI, info_stride=1, mode=MODE_CULLED, flags=0,
+                tau_hi=float("nan"), tau_lo=float("nan")) -> ScoreParams:
+    return ScoreParams(lambda_xi, k_sigma, variant, info_stride, mode, flags, tau_hi, tau_lo)
+
+
+# ------------------------------------------------------------------ handles
+class Map:
+    """rtg_map handle; arrays are planar SoA (means [3,N], quats [4,N], scales [3,N], ...).
+    Host (numpy / CPU tensor) inputs are copied to the device inside the call; CUDA tensors are
+    read in place."""
+
+    def __init__(self, means, quats, scales, opacity, info_w, flags=None, r_robot=0.3, lambda_g=3.0,
+                 collide_rule=COLLIDE_ELLIPSOID, device=0, stream=None, options=None):
+        n = int(means.shape[-1])
+        kind = _kind(means)
+        for a in (quats, scales, opacity, info_w, flags):
+            if a is not None and _kind(a) != kind:
+                raise ValueError("all map arrays must live in the same memory (host or device)")
+        self._robot = Robot(float(r_robot), float(lambda_g), int(collide_rule))
+        self.handle = _P()
+        self.n = n
+        self._keep = (means, quats, scales, opacity, info_w, flags)
+        st = _stream(stream)
+        if options is not None:
+            opt = MapOptions(*[float(x) for x in options])
+            s = _lib.rtg_map_create_ex(device, n, kind, _ptr(means), _ptr(quats), _ptr(scales), _ptr(opacity),
+                                       _ptr(info_w), _ptr(flags), ctypes.byref(self._robot), ctypes.byref(opt), st,
+                                       ctypes.byref(self.handle))
+        else:
+            s = _lib.rtg_map_create(device, n, kind, _ptr(means), _ptr(quats), _ptr(scales), _ptr(opacity),
+                                    _ptr(info_w), _ptr(flags), ctypes.byref(self._robot), st,
+                                    ctypes.byref(self.handle))
+        _check(s, "rtg_map_create")
+
+    def info(self) -> MapInfo:
+        out = MapInfo()
+        _check(_lib.rtg_map_info(self.handle, ctypes.byref(out)), "rtg_map_info")
+        return out
+
+    def close(self):
+        if self.handle:
+            _check(_lib.rtg_map_destroy(self.handle), "rtg_map_destroy")
+            self.handle = _P()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Traj:
+    """rtg_traj handle: x, y, z, yaw each [K, T] (trajectory-major)."""
+
+    def __init__(self, handle: _P, K: int, T: int):
+        self.handle = handle
+        self.K = K
+        self.T = T
+
+    @classmethod
+    def upload(cls, x, y, z, yaw, device=0, stream=None) -> "Traj":
+        K, T = (int(s) for s in x.shape)
+        kind = _kind(x)
+        h = _P()
+        _check(_lib.rtg_traj_upload(device, K, T, kind, _ptr(x), _ptr(y), _ptr(z), _ptr(yaw), _stream(stream),
+                                    ctypes.byref(h)), "rtg_traj_upload")
+        return cls(h, K, T)
+
+    @classmethod
+    def sample_unicycle(cls, v, omega, T: int, dt: float, start, device=0, stream=None) -> "Traj":
+        K = int(v.shape[0])
+        st4 = (ctypes.c_float * 4)(*[float(s) for s in start])
+        h = _P()
+        _check(_lib.rtg_traj_sample_unicycle(device, K, int(T), float(dt), st4, _ptr(v), _ptr(omega), _kind(v),
+                                             _stream(stream), ctypes.byref(h)), "rtg_traj_sample_unicycle")
+        return cls(h, K, int(T))
+
+    def read(self, stream=None):
+        torch = _torch()
+        out = [torch.empty((self.K, self.T), dtype=torch.float32, device="cuda") for _ in range(4)]
+        _check(_lib.rtg_traj_read(self.handle, *[_ptr(o) for o in out], _stream(stream)), "rtg_traj_read")
+        return out
+
+    def close(self):
+        if self.handle:
+            _check(_lib.rtg_traj_destroy(self.handle), "rtg_traj_destroy")
+            self.handle = _P()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ calls
+def score(m: Map, tr: Traj, camera, params: ScoreParams, first_col=None, feasible=None, gain=None, utility=None,
+          stream=None):
+    """rtg_score into caller-owned CUDA tensors (allocated here when None). Returns them."""
+    torch = _torch()
+    K = tr.K
+    dev = torch.device("cuda")
+    first_col = torch.empty(K, dtype=torch.int32, device=dev) if first_col is None else first_col
+    feasible = torch.empty(K, dtype=torch.uint8, device=dev) if feasible is None else feasible
+    gain = torch.empty(K, dtype=torch.float64, device=dev) if gain is None else gain
+    utility = torch.empty(K, dtype=torch.float64, device=dev) if utility is None else utility
+    cam = camera if isinstance(camera, Camera) else make_camera(camera)
+    _check(_lib.rtg_score(m.handle, tr.handle, ctypes.byref(cam), ctypes.byref(params), _ptr(first_col),
+                          _ptr(feasible), _ptr(gain), _ptr(utility), _stream(stream)), "rtg_score")
+    return first_col, feasible, gain, utility
+
+
+def best(utility, index_base: int = 0, stream=None):
+    """rtg_best -> (score, global index); index -1 / score -inf when nothing is feasible."""
+    out = BestResult()
+    _check(_lib.rtg_best(_ptr(utility), int(utility.numel()), int(index_base), _stream(stream), ctypes.byref(out)),
+           "rtg_best", allow=(ERR_NO_FEASIBLE,))
+    return out.score, out.index
+
+
+def score_debug(m: Map, tr: Traj, camera, params: ScoreParams, pair_mask: bool = False, stream=None):
+    """rtg_score_debug: per-waypoint arrays for every waypoint (+ optional pair mask, stats)."""
+    torch = _torch()
+    KT = tr.K * tr.T
+    dev = torch.device("cuda")
+    wp_col = torch.empty(KT, dtype=torch.uint8, device=dev)
+    wp_gain = torch.empty(KT, dtype=torch.float64, device=dev)
+    wp_nh = torch.empty(KT, dtype=torch.int32, device=dev)
+    wp_nl = torch.empty(KT, dtype=torch.int32, device=dev)
+    mask = None
+    if pair_mask:
+        words = (KT * m.n + 31) // 32
+        mask = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
+    stats = (ctypes.c_longlong * 4)()
+    cam = camera if isinstance(camera, Camera) else make_camera(camera)
+    _check(_lib.rtg_score_debug(m.handle, tr.handle, ctypes.byref(cam), ctypes.byref(params), _ptr(wp_col),
+                                _ptr(wp_gain), _ptr(wp_nh), _ptr(wp_nl), _ptr(mask), stats, _stream(stream)),
+           "rtg_score_debug")
+    return dict(wp_col=wp_col, wp_gain=wp_gain, wp_nh=wp_nh, wp_nl=wp_nl, pair_mask=mask,
+                stats=dict(col_refined=stats[0], vis_refined=stats[1], tested=stats[2], cells_aggregated=stats[3]))
+
+
+def unpack_pair_mask(mask, KT: int, N: int) -> np.ndarray:
+    words = mask.cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: KT * N]
+    return bits.reshape(KT, N).astype(bool)
+
+
+def map_from_workload(wl, device=0, stream=None, on_device=True, options=None) -> Map:
+    """Convenience: build a Map from a workloads.Workload (arrays moved to CUDA when on_device)."""
+    arrs = [wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags]
+    if on_device:
+        torch = _torch()
+        arrs = [None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{device}") for a in arrs]
+    return Map(*arrs, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
+               device=device, stream=stream, options=options)
+
+
+def traj_from_workload(wl, device=0, stream=None, on_device=True, x=None, y=None, z=None, yaw=None) -> Traj:
+    arrs = [wl.x if x is None else x, wl.y if y is None else y, wl.z if z is None else z,
+            wl.yaw if yaw is None else yaw]
+    if on_device:
+        torch = _torch()
+        arrs = [torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{device}") for a in arrs]
+        t = Traj.upload(*arrs, device=device, stream=stream)
+        t._keep = arrs
+        return t
+    return Traj.upload(*[np.ascontiguousarray(a, dtype=np.float32) for a in arrs], device=device, stream=stream)

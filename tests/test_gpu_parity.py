@@ -1,0 +1,366 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  * collision bits: equal to the oracle's FP64 decision; a mismatch is tolerated only on a
+    waypoint whose oracle record holds a pair within 1e-6 of the threshold (reported);
+  * visible counts n_H, n_L and xi: inside the oracle's [lo, hi] band bounds, and equal to the
+    nominal FP64 decision when the waypoint has no band pair;
+  * gains: inside [lo, hi] +- (1e-5 relative + fixed-point quantum n_vis * 2^-(S+1));
+  * first_col in the oracle's allowed set, feasibility, utility, argmax in the acceptable set.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2409_18122_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+MODES = ("dense", "culled")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2409_18122_b200 import build
+    build.build()
+    from paper_2409_18122_b200 import rtg
+    return rtg
+
+
+def _mode(R, name):
+    return R.MODE_DENSE if name == "dense" else R.MODE_CULLED
+
+
+def gpu_run(R, wl, mode, flags=None, stride=1, variant=0, lambda_xi=1.0, tau=(float("nan"), float("nan")),
+            pair_mask=False, x=None, y=None, z=None, yaw=None, debug=True):
+    flags = R.SCORE_FULL_GAIN if flags is None else flags
+    m = R.map_from_workload(wl)
+    tr = R.traj_from_workload(wl, x=x, y=y, z=z, yaw=yaw)
+    p = R.make_params(lambda_xi=lambda_xi, variant=variant, info_stride=stride, mode=_mode(R, mode), flags=flags,
+                      tau_hi=tau[0], tau_lo=tau[1])
+    fc, fe, g, u = R.score(m, tr, wl.camera, p)
+    out = dict(first_col=fc.cpu().numpy(), feasible=fe.cpu().numpy(), gain=g.cpu().numpy(),
+               utility=u.cpu().numpy())
+    out["best"] = R.best(u)
+    if debug:
+        d = R.score_debug(m, tr, wl.camera, p, pair_mask=pair_mask)
+        out.update({k: v.cpu().numpy() for k, v in d.items() if k not in ("pair_mask", "stats")})
+        out["stats"] = d["stats"]
+        if pair_mask:
+            out["pair_mask"] = R.unpack_pair_mask(d["pair_mask"], tr.K * tr.T, m.n)
+    out["info"] = m.info()
+    torch.cuda.synchronize()
+    m.close()
+    tr.close()
+    return out
+
+
+def check_waypoints(gpu, orc, shift):
+    wp = orc["wp"]
+    quantum = np.maximum(wp["nh_hi"] + wp["nl_hi"] + 1, 1) * 2.0 ** -(shift + 1)
+    # collision
+    col_mis = gpu["wp_col"].astype(bool) != wp["col"]
+    assert not np.any(col_mis & (wp["amb_col"] == 0)), np.nonzero(col_mis & (wp["amb_col"] == 0))[0][:10]
+    # counts
+    for key in ("nh", "nl"):
+        g = gpu["wp_" + key]
+        assert np.all((g >= wp[key + "_lo"]) & (g <= wp[key + "_hi"])), key
+        clean = wp["amb_vis"] == 0
+        assert np.array_equal(g[clean], wp[key][clean]), key
+    # gains
+    g = gpu["wp_gain"]
+    tol = 1e-5 * np.abs(wp["gain_hi"]) + quantum
+    assert np.all(g >= wp["gain_lo"] - tol) and np.all(g <= wp["gain_hi"] + tol)
+    clean = wp["amb_vis"] == 0
+    assert np.all(np.abs(g[clean] - wp["gain"][clean]) <= tol[clean])
+    return dict(col_mismatch=int(col_mis.sum()), band_col=int((wp["amb_col"] > 0).sum()),
+                band_vis=int((wp["amb_vis"] > 0).sum()))
+
+
+def check_trajectories(gpu, orc, T, full_gain=True):
+    K = orc["first_col"].shape[0]
+    allowed = orc["first_col_allowed"]
+    fc = gpu["first_col"]
+    assert np.all(allowed[np.arange(K), np.clip(fc, 0, T)]), "first_col outside the allowed set"
+    assert np.array_equal(gpu["feasible"].astype(bool), fc == T)
+    feas = gpu["feasible"].astype(bool)
+    tol = 1e-5 * np.abs(orc["gain_hi"]) + 1e-9
+    sel = np.ones(K, bool) if full_gain else feas
+    assert np.all(gpu["gain"][sel] >= orc["gain_lo"][sel] - tol[sel])
+    assert np.all(gpu["gain"][sel] <= orc["gain_hi"][sel] + tol[sel])
+    if not full_gain:
+        assert np.all(np.isnan(gpu["gain"][~feas]))
+    assert np.all(np.isneginf(gpu["utility"][~feas]))
+    u = gpu["utility"][feas]
+    tu = 1e-5 * np.abs(orc["utility_hi"][feas]) + 1e-9
+    assert np.all(u >= orc["utility_lo"][feas] - tu) or not np.any(feas)
+    assert np.all(u <= np.where(np.isfinite(orc["utility_hi"][feas]), orc["utility_hi"][feas], np.inf) + tu)
+    b = gpu["best"][1]
+    assert b in set(int(v) for v in orc["acceptable"]), (b, orc["acceptable"][:10])
+
+
+# ----------------------------------------------------------------- tiny (configs[0])
+
+@pytest.mark.parametrize("mode", MODES)
+def test_tiny_full_parity(R, mode):
+    wl = W.tiny()
+    gpu = gpu_run(R, wl, mode, pair_mask=True)
+    orc = O.score(wl)
+    mask, band = O.pair_mask(wl.means, wl.quats, wl.scales, wl.flags, wl.robot, wl.x, wl.y, wl.z)
+    mis = gpu["pair_mask"] != mask
+    assert not np.any(mis & ~band), int((mis & ~band).sum())
+    assert mask.sum() > 1000
+    rep = check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
+    check_trajectories(gpu, orc, wl.T)
+    assert gpu["best"] == (-math.inf, -1)     # tiny is degenerate, nothing feasible
+    print("tiny", mode, rep, gpu["stats"])
+
+
+# ----------------------------------------------------------------- room (configs[1]), trajectory subset
+
+@pytest.fixture(scope="module")
+def room():
+    return W.room()
+
+
+@pytest.fixture(scope="module")
+def room_orc(room):
+    idx = np.arange(0, room.K, 16)          # 64 trajectories x 50 waypoints x 100k Gaussians
+    return idx, O.score(room, traj_idx=idx)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_room_subset_parity(R, room, room_orc, mode):
+    idx, orc = room_orc
+    gpu = gpu_run(R, room, mode, x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx])
+    rep = check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
+    check_trajectories(gpu, orc, room.T)
+    assert 0 < gpu["feasible"].sum() < len(idx)
+    print("room", mode, rep, gpu["stats"])
+
+
+def test_dense_equals_culled_bitwise(R, room):
+    idx = np.arange(0, room.K, 8)
+    a = gpu_run(R, room, "dense", x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx])
+    b = gpu_run(R, room, "culled", x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx])
+    for k in ("first_col", "feasible", "wp_col", "wp_nh", "wp_nl"):
+        assert np.array_equal(a[k], b[k]), k
+    # exact fixed-point sums: bit-identical doubles
+    assert np.array_equal(a["gain"].view(np.int64), b["gain"].view(np.int64))
+    assert np.array_equal(a["wp_gain"].view(np.int64), b["wp_gain"].view(np.int64))
+    assert a["best"] == b["best"]
+    assert b["stats"]["cells_aggregated"] > 0
+
+
+@pytest.mark.parametrize("variant,stride,lam,tau,rule", [
+    (1, 1, 1.0, None, 0),        # RTGuIDE-sum
+    (2, 1, 1.0, None, 0),        # RTGuIDE-sq
+    (0, 10, 1.0, None, 0),       # paper-faithful 1 s segments at dt = 0.1
+    (0, 1, 0.5, None, 0),        # lambda_xi != 1
+    (0, 1, 1.0, (0.7, 0.3), 0),  # caller thresholds
+    (0, 1, 1.0, None, 1),        # principal-axis collision rule
+])
+def test_room_variants(R, room, variant, stride, lam, tau, rule):
+    import dataclasses
+    wl = dataclasses.replace(room, robot=W.Robot(room.robot.r_robot, room.robot.lambda_g, rule))
+    idx = np.arange(3, room.K, 32)
+    t = tau if tau else (float("nan"), float("nan"))
+    orc = O.score(wl, traj_idx=idx, variant=variant, info_stride=stride, lambda_xi=lam, tau_hi=t[0], tau_lo=t[1])
+    for mode in MODES:
+        gpu = gpu_run(R, wl, mode, x=wl.x[idx], y=wl.y[idx], z=wl.z[idx], yaw=wl.yaw[idx], variant=variant,
+                      stride=stride, lambda_xi=lam, tau=t)
+        check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
+        check_trajectories(gpu, orc, wl.T)
+
+
+# ----------------------------------------------------------------- multi-room (configs[2]), sample
+
+def test_multi_room_sample_parity(R):
+    wl = W.multi_room()
+    idx = np.array([0, 511, 1024, 2047, 3000, 4095])
+    orc = O.score(wl, traj_idx=idx)
+    gpu = gpu_run(R, wl, "culled", x=wl.x[idx], y=wl.y[idx], z=wl.z[idx], yaw=wl.yaw[idx])
+    check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
+    check_trajectories(gpu, orc, wl.T)
+
+
+# ----------------------------------------------------------------- outdoor (configs[3]) at full size
+
+def test_outdoor_full_size_sampled(R):
+    """Full map (2M) and full K=16384 x T=100 in the bench launch configuration (culled, early
+    exit); outputs of sampled trajectories compared with the oracle one by one."""
+    wl = W.outdoor()
+    gpu = gpu_run(R, wl, "culled", flags=0, debug=False)
+    rng = np.random.default_rng(5)
+    feas = np.nonzero(gpu["feasible"])[0]
+    infeas = np.nonzero(gpu["feasible"] == 0)[0]
+    assert len(feas) > 1000 and len(infeas) > 1000
+    idx = np.sort(np.concatenate([rng.choice(feas, 2, replace=False), rng.choice(infeas, 2, replace=False)]))
+    orc = O.score(wl, traj_idx=idx)
+    sub = {k: gpu[k][idx] for k in ("first_col", "feasible", "gain", "utility")}
+    sub["best"] = (None, -2)
+    K = len(idx)
+    allowed = orc["first_col_allowed"]
+    assert np.all(allowed[np.arange(K), sub["first_col"]])
+    f = sub["feasible"].astype(bool)
+    assert np.all(np.isnan(sub["gain"][~f])) and np.all(np.isneginf(sub["utility"][~f]))
+    tol = 1e-5 * np.abs(orc["gain_hi"][f]) + 1e-9
+    assert np.all((sub["gain"][f] >= orc["gain_lo"][f] - tol) & (sub["gain"][f] <= orc["gain_hi"][f] + tol))
+    assert np.all((sub["utility"][f] >= orc["xi_lo"][f]) & (sub["utility"][f] <= orc["xi_hi"][f]))
+    # the argmax is a property of all K: its utility is the maximum and ties go to the lowest index
+    u = gpu["utility"]
+    b = gpu["best"][1]
+    assert u[b] == np.max(u) and np.all(u[:b] < u[b])
+
+
+# ----------------------------------------------------------------- hand cases (golden fixtures)
+
+def _one_gaussian_wl(mu, quat, s, r_robot, lam, pose, cam, w=0.9):
+    means = np.array(mu, np.float32).reshape(3, 1)
+    quats = np.array(quat, np.float32).reshape(4, 1)
+    scales = np.array(s, np.float32).reshape(3, 1)
+    one = lambda v: np.array([[v]], np.float32)
+    return W.Workload("hand", means, quats, scales, np.ones(1, np.float32), np.array([w], np.float32), None,
+                      one(pose[0]), one(pose[1]), one(pose[2]), one(pose[3]), W.Robot(r_robot, lam), cam, 0.1)
+
+
+def test_golden_collision_cases_on_gpu(R):
+    import json, os
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "collision_cases.json")))["cases"]
+    cam = W.Camera(64, 48, 50.0, 50.0, 32.0, 24.0, 0.1, 5.0)
+    for c in cases:
+        wl = _one_gaussian_wl(c["mu"], c["quat"], c["s"], c["r_robot"], c["lambda_g"], list(c["p"]) + [0.0], cam)
+        for mode in MODES:
+            gpu = gpu_run(R, wl, mode)
+            assert bool(gpu["wp_col"][0]) == c["collide"], (c["name"], mode)
+            assert gpu["first_col"][0] == (0 if c["collide"] else 1)
+
+
+def test_golden_visibility_cases_on_gpu(R):
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "visibility_cases.json")))
+    for c in g["cases"]:
+        cd = dict(g["camera"])
+        if "z_far" in c:
+            cd["z_far"] = c["z_far"]
+        cam = W.Camera(**cd)
+        # tiny Gaussian far from the robot radius so only visibility matters
+        wl = _one_gaussian_wl(c["mu"], [1, 0, 0, 0], [0.001] * 3, 0.0, 1.0, c["pose"], cam)
+        for mode in MODES:
+            gpu = gpu_run(R, wl, mode, tau=(0.5, 0.2))
+            assert gpu["wp_nh"][0] == int(c["visible"]), (c["name"], mode)
+            assert gpu["wp_gain"][0] == (float(np.float32(0.9)) if c["visible"] else 0.0)
+
+
+# ----------------------------------------------------------------- edge cases
+
+def test_empty_map_all_feasible(R):
+    wl = W.tiny(K=5, T=7)
+    import dataclasses
+    e = np.zeros((3, 0), np.float32)
+    wl0 = dataclasses.replace(wl, means=e, quats=np.zeros((4, 0), np.float32), scales=e,
+                              opacity=np.zeros(0, np.float32), info_w=np.zeros(0, np.float32))
+    for mode in MODES:
+        gpu = gpu_run(R, wl0, mode)
+        assert np.all(gpu["first_col"] == 7) and np.all(gpu["feasible"] == 1)
+        assert np.all(gpu["gain"] == 0) and np.all(gpu["utility"] == 0)
+        assert gpu["best"] == (0.0, 0)
+
+
+def test_degenerate_shapes_and_flags(R, room):
+    # K=1, T=1; info_stride > T (no info waypoint); all NO_GAIN; NaN waypoint; gain-only views
+    import dataclasses
+    idx = np.array([5])
+    sub = dict(x=room.x[idx, :1], y=room.y[idx, :1], z=room.z[idx, :1], yaw=room.yaw[idx, :1])
+    for mode in MODES:
+        a = gpu_run(R, room, mode, **sub)
+        o = O.score(room, x=sub["x"], y=sub["y"], z=sub["z"], yaw=sub["yaw"])
+        check_waypoints(a, o, a["info"].fixed_point_shift)
+        check_trajectories(a, o, 1)
+        b = gpu_run(R, room, mode, stride=99, **sub)
+        assert b["feasible"][0] == 0 or b["utility"][0] == 0.0
+    ng = dataclasses.replace(room, flags=(room.flags | W.FLAG_NO_GAIN).astype(np.uint8))
+    idx = np.arange(0, room.K, 128)
+    c = gpu_run(R, ng, "culled", x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx])
+    assert np.all(c["wp_gain"] == 0) and np.all(c["wp_nh"] == 0)
+    xs = room.x[idx].copy()
+    xs[0, 3] = np.nan
+    d = gpu_run(R, room, "culled", x=xs, y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx])
+    assert d["wp_col"][3] == 0 and d["wp_gain"][3] == 0
+    v = gpu_run(R, room, "culled", flags=R.SCORE_NO_COLLISION, x=room.x[idx], y=room.y[idx], z=room.z[idx],
+                yaw=room.yaw[idx])
+    assert np.all(v["feasible"] == 1) and np.all(v["first_col"] == room.T)
+
+
+def test_invalid_map_elements(R):
+    wl = W.tiny(N=50, K=2, T=2)
+    import dataclasses
+    bad = [
+        dataclasses.replace(wl, means=np.where(np.arange(50) == 7, np.nan, wl.means).astype(np.float32)),
+        dataclasses.replace(wl, quats=np.zeros_like(wl.quats)),
+        dataclasses.replace(wl, scales=-wl.scales),
+        dataclasses.replace(wl, info_w=-wl.info_w - 1),
+    ]
+    for b in bad:
+        with pytest.raises(R.RTGError) as e:
+            R.map_from_workload(b)
+        assert e.value.status == R.ERR_INVALID_ARGUMENT
+
+
+# ----------------------------------------------------------------- sampler, argmax, determinism, shards
+
+def test_unicycle_sampler_matches_oracle(R):
+    wl = W.tiny()
+    c = wl.controls
+    v = torch.from_numpy(c["v"]).cuda()
+    w = torch.from_numpy(c["w"]).cuda()
+    tr = R.Traj.sample_unicycle(v, w, wl.T, wl.dt, c["start"])
+    X, Y, Z, YW = (a.cpu().numpy() for a in tr.read())
+    for k in range(wl.K):
+        ox, oy, oz, oyaw = O.unicycle(c["start"], c["v"][k], c["w"][k], wl.dt, wl.T)
+        assert np.all(np.abs(X[k] - ox) <= 2 * np.spacing(np.float32(np.abs(ox) + 1)))
+        assert np.all(np.abs(Y[k] - oy) <= 2 * np.spacing(np.float32(np.abs(oy) + 1)))
+        assert np.all(Z[k] == np.float32(oz))
+        assert np.all(np.abs(np.angle(np.exp(1j * (YW[k] - oyaw)))) < 1e-6)
+    tr.close()
+
+
+def test_best_ties_and_index_base(R):
+    u = torch.tensor([1.0, 5.0, 5.0, -math.inf, 2.0], dtype=torch.float64, device="cuda")
+    assert R.best(u) == (5.0, 1)
+    assert R.best(u, index_base=100) == (5.0, 101)
+    n = torch.full((7,), -math.inf, dtype=torch.float64, device="cuda")
+    assert R.best(n) == (-math.inf, -1)
+    big = torch.zeros(70000, dtype=torch.float64, device="cuda")
+    big[69999] = 3.0
+    big[12345] = 3.0
+    assert R.best(big) == (3.0, 12345)
+
+
+def test_determinism_and_shard_emulation(R, room):
+    idx = np.arange(0, room.K, 4)
+    full = gpu_run(R, room, "culled", flags=0, x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx],
+                   debug=False)
+    again = gpu_run(R, room, "culled", flags=0, x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx],
+                    debug=False)
+    for k in ("first_col", "feasible", "gain", "utility"):
+        assert np.array_equal(full[k].view(np.uint8), again[k].view(np.uint8)), k
+    K = len(idx)
+    for G in (2, 4):
+        best = []
+        for r in range(G):
+            sel = np.arange(r, K, G)
+            part = gpu_run(R, room, "culled", flags=0, x=room.x[idx][sel], y=room.y[idx][sel],
+                           z=room.z[idx][sel], yaw=room.yaw[idx][sel], debug=False)
+            for k in ("first_col", "feasible", "gain", "utility"):
+                assert np.array_equal(part[k].view(np.uint8), full[k][sel].view(np.uint8)), (G, r, k)
+            s, i = part["best"]
+            best.append((s, int(sel[i]) if i >= 0 else -1))
+        top = max(b[0] for b in best)
+        g_best = min(b[1] for b in best if b[0] == top)
+        assert (top, g_best) == full["best"]
