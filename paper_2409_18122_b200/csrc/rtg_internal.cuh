@@ -42,6 +42,15 @@ struct CamK {
 // per-waypoint constants (yaw kept for the rare FP64 re-decision)
 struct WpF { float px, py, pz, c, s, ax, bx, yaw; };
 
+__device__ __forceinline__ void wp_setup_cs(float x, float y, float z, float yaw, const CamK& k, WpF& f,
+                                            double& cs, double& sn) {
+    sincos((double)yaw, &sn, &cs);
+    f.px = x; f.py = y; f.pz = z; f.yaw = yaw;
+    f.c = (float)cs; f.s = (float)sn;
+    f.ax = (float)(sn - (double)k.kxc * cs);
+    f.bx = (float)(-cs - (double)k.kxc * sn);
+}
+
 __device__ __forceinline__ void wp_setup(float x, float y, float z, float yaw, const CamK& k, WpF& f) {
     double sn, cs;
     sincos((double)yaw, &sn, &cs);
@@ -66,20 +75,28 @@ __device__ __forceinline__ float vis_margin(const WpF& w, const CamK& k, float m
     return fminf(s1, fminf(s2, s3));
 }
 
-// FP64 decision with the six slacks of the pinhole test (visible <=> all >= 0); rare path
+// FP64 decision with the six slacks of the pinhole test (visible <=> all >= 0), cos/sin of the
+// yaw given in FP64.  Every product is an explicit fma/mul so all kernels round identically.
+__device__ __forceinline__ bool vis_decide64_cs(float px, float py, float pz, double cs, double sn, float mx,
+                                                float my, float mz, const double* __restrict__ k) {
+    const double W = __ldg(k + 0), H = __ldg(k + 1), fx = __ldg(k + 2), fy = __ldg(k + 3);
+    const double cx = __ldg(k + 4), cy = __ldg(k + 5), zn = __ldg(k + 6), zf = __ldg(k + 7);
+    const double dx = (double)mx - (double)px, dy = (double)my - (double)py, dz = (double)mz - (double)pz;
+    const double Z = fma(cs, dx, sn * dy);
+    const double X = fma(sn, dx, -(cs * dy));
+    const double Y = -dz;
+    bool v = (Z - zn >= 0.0) & (zf - Z >= 0.0);
+    v &= (fma(fx, X, cx * Z) >= 0.0) & (fma(W - cx, Z, -(fx * X)) >= 0.0);
+    v &= (fma(fy, Y, cy * Z) >= 0.0) & (fma(H - cy, Z, -(fy * Y)) >= 0.0);
+    return v;
+}
+
+// same decision recomputing cos/sin (dense kernels keep no FP64 registers per waypoint); rare path
 static __device__ __noinline__ bool vis_decide64(float px, float py, float pz, float yaw, float mx, float my, float mz,
-                                          const double* __restrict__ k) {
-    const double W = k[0], H = k[1], fx = k[2], fy = k[3], cx = k[4], cy = k[5], zn = k[6], zf = k[7];
+                                                 const double* __restrict__ k) {
     double sn, cs;
     sincos((double)yaw, &sn, &cs);
-    double dx = (double)mx - px, dy = (double)my - py, dz = (double)mz - pz;
-    double Z = cs * dx + sn * dy;
-    double X = sn * dx - cs * dy;
-    double Y = -dz;
-    bool v = (Z - zn >= 0.0) & (zf - Z >= 0.0);
-    v &= (fx * X + cx * Z >= 0.0) & ((W - cx) * Z - fx * X >= 0.0);
-    v &= (fy * Y + cy * Z >= 0.0) & ((H - cy) * Z - fy * Y >= 0.0);
-    return v;
+    return vis_decide64_cs(px, py, pz, cs, sn, mx, my, mz, k);
 }
 
 // exact-decision visibility of one pair; `nref` counts FP64 re-decisions
@@ -90,6 +107,19 @@ __device__ __forceinline__ bool visible(const WpF& w, const CamK& k, float mx, f
     bool v = m >= 0.0f;
     if (fabsf(m) < fmaf(k.gam, Z, k.g0)) {
         v = vis_decide64(w.px, w.py, w.pz, w.yaw, mx, my, mz, k.cam64);
+        ++nref;
+    }
+    return v;
+}
+
+// same, with the waypoint's FP64 cos/sin at hand (culled kernel: kept in shared memory)
+__device__ __forceinline__ bool visible_cs(const WpF& w, const CamK& k, float mx, float my, float mz,
+                                           const double* cs_sn, unsigned& nref) {
+    float Z;
+    float m = vis_margin(w, k, mx, my, mz, Z);
+    bool v = m >= 0.0f;
+    if (fabsf(m) < fmaf(k.gam, Z, k.g0)) {
+        v = vis_decide64_cs(w.px, w.py, w.pz, cs_sn[0], cs_sn[1], mx, my, mz, k.cam64);
         ++nref;
     }
     return v;

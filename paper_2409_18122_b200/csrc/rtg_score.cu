@@ -369,211 +369,6 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
     if (stats && nref) atomicAdd(&stats[1], (unsigned long long)nref);
 }
 
-// ===================================================================== culled phase B
-struct GainGridK {
-    float ox, oy, oz, h, hz, eps;
-    int nx, ny, nz;
-};
-
-__global__ void __launch_bounds__(kWarps * 32) k_gain_culled(
-    const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
-    const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
-    const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
-    const long long* __restrict__ aggq, const long long* __restrict__ agghl, GainGridK g, CamK cam,
-    long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl, int* __restrict__ counter,
-    unsigned long long* __restrict__ stats) {
-    __shared__ int s_rincl[kWarps][32];
-    __shared__ int s_roff[kWarps][32];
-    __shared__ int s_iincl[kWarps][64];
-    __shared__ int s_ioff[kWarps][64];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int L = *list_count;
-    unsigned nref = 0;
-    unsigned long long ntest = 0, nagg = 0;
-    const float zn = cam.zmid - cam.zhalf, zf = cam.zmid + cam.zhalf;
-    const float kxl = cam.kxh - cam.kxc, kxr = cam.kxh + cam.kxc;
-    const float kyu = cam.kyh + cam.kyc, kyd = cam.kyh - cam.kyc;
-    const float eps = g.eps, hh = 0.5f * g.h;
-    for (;;) {
-        int e = 0;
-        if (lane == 0) e = atomicAdd(counter, 1);
-        e = __shfl_sync(kFull, e, 0);
-        if (e >= L) break;
-        const int i = list[e];
-        const float px = X[i], py = Y[i], pz = Zw[i], yw = Yaw[i];
-        long long accq = 0;
-        int acch = 0, accl = 0;
-        if (isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(yw)) {
-            WpF f;
-            wp_setup(px, py, pz, yw, cam, f);
-            // footprint trapezoid of the frustum in the xy plane (grid-relative coordinates)
-            const float qx = px - g.ox, qy = py - g.oy;
-            const float Fx = f.c, Fy = f.s, Rx = f.s, Ry = -f.c;
-            float vx[4], vy[4];
-            vx[0] = qx + zn * Fx - kxl * zn * Rx; vy[0] = qy + zn * Fy - kxl * zn * Ry;
-            vx[1] = qx + zn * Fx + kxr * zn * Rx; vy[1] = qy + zn * Fy + kxr * zn * Ry;
-            vx[2] = qx + zf * Fx + kxr * zf * Rx; vy[2] = qy + zf * Fy + kxr * zf * Ry;
-            vx[3] = qx + zf * Fx - kxl * zf * Rx; vy[3] = qy + zf * Fy - kxl * zf * Ry;
-            const float ymn = fminf(fminf(vy[0], vy[1]), fminf(vy[2], vy[3])) - eps;
-            const float ymx = fmaxf(fmaxf(vy[0], vy[1]), fmaxf(vy[2], vy[3])) + eps;
-            const int iy0 = max(0, clamp_cell(ymn / g.h, 0, g.ny));
-            const int iy1 = min(g.ny - 1, clamp_cell(ymx / g.h, 0, g.ny));
-            // per-waypoint column-test constants (linear functions over an h x h column)
-            const float Zr = (fabsf(f.c) + fabsf(f.s)) * hh;
-            const float f1r = (fabsf(cam.kxh * f.c - f.ax) + fabsf(cam.kxh * f.s - f.bx)) * hh;
-            const float f2r = (fabsf(cam.kxh * f.c + f.ax) + fabsf(cam.kxh * f.s + f.bx)) * hh;
-            const float zrel = pz - g.oz;
-            for (int rbase = iy0; rbase <= iy1; rbase += 32) {
-                const int iy = rbase + lane;
-                int ixlo = 0, len = 0;
-                if (iy <= iy1) {
-                    const float yb0 = iy * g.h - eps, yb1 = (iy + 1) * g.h + eps;
-                    float xlo = FLT_MAX, xhi = -FLT_MAX;
-#pragma unroll
-                    for (int ed = 0; ed < 4; ++ed) {
-                        const float ax = vx[ed], ay = vy[ed], bx = vx[(ed + 1) & 3], by = vy[(ed + 1) & 3];
-                        const float elo = fminf(ay, by), ehi = fmaxf(ay, by);
-                        if (ehi < yb0 || elo > yb1) continue;
-                        float xa, xb;
-                        if (ehi - elo <= 1e-12f) {
-                            xa = ax; xb = bx;
-                        } else {
-                            const float inv = 1.0f / (by - ay);
-                            const float t0 = (fmaxf(yb0, elo) - ay) * inv, t1 = (fminf(yb1, ehi) - ay) * inv;
-                            xa = fmaf(t0, bx - ax, ax);
-                            xb = fmaf(t1, bx - ax, ax);
-                        }
-                        xlo = fminf(xlo, fminf(xa, xb));
-                        xhi = fmaxf(xhi, fmaxf(xa, xb));
-                    }
-                    if (xlo <= xhi) {
-                        const int ix0 = max(0, clamp_cell((xlo - eps) / g.h, 0, g.nx));
-                        const int ix1 = min(g.nx - 1, clamp_cell((xhi + eps) / g.h, 0, g.nx));
-                        if (ix0 <= ix1) {
-                            ixlo = ix0;
-                            len = ix1 - ix0 + 1;
-                        }
-                    }
-                }
-                int incl = len;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int v = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const int total = __shfl_sync(kFull, incl, 31);
-                s_rincl[wid][lane] = incl;
-                s_roff[wid][lane] = ixlo - (incl - len);
-                __syncwarp();
-                int owner = 0;
-                for (int cb = 0; cb < total; cb += 32) {
-                    const int pos = cb + lane;
-                    int b0 = 0, l0 = 0, b1 = 0, l1 = 0;
-                    if (pos < total) {
-                        while (s_rincl[wid][owner] <= pos) ++owner;
-                        const int ix = pos + s_roff[wid][owner];
-                        const int cy = rbase + owner;
-                        // column centre relative to the camera
-                        const float xc = fmaf((float)ix + 0.5f, g.h, -qx);
-                        const float yc = fmaf((float)cy + 0.5f, g.h, -qy);
-                        const float Zc = fmaf(f.c, xc, f.s * yc);
-                        const float Xc = fmaf(f.ax, xc, f.bx * yc);
-                        const float f1c = fmaf(cam.kxh, Zc, -Xc), f2c = fmaf(cam.kxh, Zc, Xc);
-                        const float Zmin = Zc - Zr, Zmax = Zc + Zr;
-                        const bool out = (Zmax < zn - eps) | (Zmin > zf + eps) | (f1c + f1r < -eps) |
-                                         (f2c + f2r < -eps);
-                        if (!out) {
-                            const bool in_h = (Zmin >= zn + eps) & (Zmax <= zf - eps) & (f1c - f1r >= eps) &
-                                              (f2c - f2r >= eps);
-                            const float Zhi = fmaxf(fminf(Zmax, zf), 0.0f);
-                            int c = clamp_cell((zrel - kyd * Zhi - eps) / g.hz, 0, g.nz);
-                            int dd = clamp_cell((zrel + kyu * Zhi + eps) / g.hz, 0, g.nz) + 1;
-                            c = min(max(c, 0), g.nz);
-                            dd = min(max(dd, c), g.nz);
-                            int a = c, b = c;
-                            if (in_h) {
-                                float za = (zrel - kyd * Zmin + eps) / g.hz;
-                                float zb = (zrel + kyu * Zmin - eps) / g.hz;
-                                za = fminf(fmaxf(za, -1.0f), (float)g.nz + 1.0f);
-                                zb = fminf(fmaxf(zb, -1.0f), (float)g.nz + 1.0f);
-                                a = min(max((int)ceilf(za), c), dd);
-                                b = min(max((int)floorf(zb), a), dd);
-                            }
-                            const long long base = ((long long)cy * g.nx + ix) * g.nz;
-                            const int sc = gstart[base + c], sa = gstart[base + a];
-                            const int sb = gstart[base + b], sd = gstart[base + dd];
-                            if (b > a) {
-                                accq += aggq[base + b] - aggq[base + a];
-                                const long long hl = agghl[base + b] - agghl[base + a];
-                                acch += (int)(hl & 0xffffffffLL);
-                                accl += (int)(hl >> 32);
-                                nagg += (unsigned long long)(b - a);
-                            }
-                            b0 = sc; l0 = sa - sc;
-                            b1 = sb; l1 = sd - sb;
-                        }
-                    }
-                    // load-balanced individual tests over this chunk's partial cell runs
-                    const int sl = l0 + l1;
-                    int ic = sl;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        int v = __shfl_up_sync(kFull, ic, o);
-                        if (lane >= o) ic += v;
-                    }
-                    const int tot = __shfl_sync(kFull, ic, 31);
-                    const int ex = ic - sl;
-                    s_iincl[wid][2 * lane] = ex + l0;
-                    s_ioff[wid][2 * lane] = b0 - ex;
-                    s_iincl[wid][2 * lane + 1] = ic;
-                    s_ioff[wid][2 * lane + 1] = b1 - (ex + l0);
-                    __syncwarp();
-                    int own = 0, pc = 0;
-                    for (int gb = 0; gb < tot; gb += 32) {
-                        const int gp = gb + lane;
-                        if (gp < tot) {
-                            while (s_iincl[wid][own] <= gp) ++own;
-                            const int gi = gp + s_ioff[wid][own];
-                            const GRec G = grec[gi];
-                            const long long q = guq[gi];
-                            if (visible(f, cam, G.x, G.y, G.z, nref)) {
-                                accq += q;
-                                pc += G.inc;
-                            }
-                        }
-                    }
-                    ntest += (unsigned long long)tot;
-                    acch += pc & 0xffff;
-                    accl += pc >> 16;
-                    __syncwarp();
-                }
-            }
-        }
-        // warp totals (integers: exact, order-free)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            accq += __shfl_xor_sync(kFull, accq, o);
-            acch += __shfl_xor_sync(kFull, acch, o);
-            accl += __shfl_xor_sync(kFull, accl, o);
-        }
-        if (lane == 0) {
-            wp_gq[i] = accq;
-            wp_nh[i] = acch;
-            wp_nl[i] = accl;
-        }
-    }
-    if (stats) {
-        nref = __reduce_add_sync(kFull, nref);
-        if (lane == 0) {
-            if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
-            atomicAdd(&stats[2], ntest);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nagg += __shfl_xor_sync(kFull, nagg, o);
-        if (lane == 0) atomicAdd(&stats[3], nagg);
-    }
-}
-
 // ===================================================================== a6 reduction
 __global__ void k_reduce(int K, int T, int stride, int variant, float lambda_xi, int full_gain,
                          const int* __restrict__ first_col, const long long* __restrict__ wp_gq,
@@ -709,15 +504,16 @@ __global__ void k_sample_unicycle(int K, int T, double dt, double x0, double y0,
 }
 
 // ===================================================================== host launchers
+cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, const int* list, const int* count,
+                               long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl, int* counter,
+                               unsigned long long* stats, cudaStream_t st);
 namespace {
-int g_occ_col = 0, g_occ_gain = 0, g_sms = 0;
+int g_occ_col = 0, g_sms = 0;
 void occupancy(int dev) {
     if (g_sms) return;
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_col, k_col_culled, kWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_gain, k_gain_culled, kWarps * 32, 0);
     if (g_occ_col < 1) g_occ_col = 1;
-    if (g_occ_gain < 1) g_occ_gain = 1;
 }
 }  // namespace
 
@@ -809,19 +605,7 @@ cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& c
                                                          m->n_gain_pad, tps, cam, (unsigned long long*)wp_gq, wp_nh,
                                                          wp_nl, stats);
     } else {
-        GainGridK g;
-        g.ox = m->gg.ox; g.oy = m->gg.oy; g.oz = m->gg.oz; g.h = m->gg.hxy; g.hz = m->gg.hz;
-        double ext = fmax(fmax(fabs(g.ox), fabs(g.oy)), fabs(g.oz)) + (double)(m->gg.nx + m->gg.ny + m->gg.nz) *
-                     fmax(m->gg.hxy, m->gg.hz) + cam.zmid + cam.zhalf;
-        g.eps = (float)(1e-3 + 256.0 * ldexp(1.0, -24) * ext);
-        g.nx = m->gg.nx; g.ny = m->gg.ny; g.nz = m->gg.nz;
-        long long blocks = (list_max + kWarps - 1) / kWarps;
-        long long cap = (long long)g_sms * g_occ_gain;
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        note_launch(), k_gain_culled<<<(unsigned)blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec,
-                                                                m->guq, m->gstart, m->gaggq, m->gagghl, g, cam,
-                                                                wp_gq, wp_nh, wp_nl, counter, stats);
+        return launch_gain_culled(m, tr, cam, list, count, list_max, wp_gq, wp_nh, wp_nl, counter, stats, st);
     }
     return cudaGetLastError();
 }
