@@ -88,7 +88,7 @@ CamK make_cam(const rtg_camera& c, const double* cam64_dev);
 cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_col, unsigned char* wp_col, int all_wp,
                            int* counter, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_list(const int* first_col, int K, int T, int stride, int full_gain, int* list, int* count,
-                        cudaStream_t st);
+                        int* ranked, cudaStream_t st);
 cudaError_t launch_iota(int* list, long long n, int* count, cudaStream_t st);
 cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& cam, const int* list,
                            const int* count, long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl,
@@ -461,6 +461,7 @@ struct Scratch {
     int* list = nullptr;
     int* ints = nullptr;                  // [0] list count, [1] phase-A counter, [2] phase-B counter
     double* cam64 = nullptr;              // FP64 camera for the re-decision branch
+    int* ranked = nullptr;                // computed trajectories in order (info list build)
     unsigned long long* stats = nullptr;  // 4 counters
     void* block = nullptr;
 };
@@ -477,7 +478,8 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     size_t o_ints = o_list + al(sizeof(int) * (list_max > 0 ? list_max : 1));
     size_t o_stats = o_ints + al(sizeof(int) * 8);
     size_t o_cam = o_stats + al(sizeof(unsigned long long) * 4);
-    size_t total = o_cam + al(sizeof(double) * 8);
+    size_t o_ranked = o_cam + al(sizeof(double) * 8);
+    size_t total = o_ranked + al(sizeof(int) * K);
     cudaError_t e = dev_alloc(&s.block, total, st);
     if (e != cudaSuccess) return e;
     char* b = (char*)s.block;
@@ -489,7 +491,8 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     s.ints = (int*)(b + o_ints);
     s.stats = (unsigned long long*)(b + o_stats);
     s.cam64 = (double*)(b + o_cam);
-    // the camera in FP64 travels by a tiny kernel-free copy: host values -> pinned-free memset path
+    s.ranked = (int*)(b + o_ranked);
+    // the FP64 camera (8 doubles) for the re-decision branch: pageable copy, stream-ordered
     double c64[8] = {(double)cam->width, (double)cam->height, cam->fx, cam->fy, cam->cx, cam->cy, cam->z_near, cam->z_far};
     cudaError_t e2 = cudaMemcpyAsync(s.cam64, c64, sizeof(c64), cudaMemcpyHostToDevice, st);
     if (e2 != cudaSuccess) return e2;
@@ -533,7 +536,8 @@ rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_sc
     }
     if (per > 0) {
         prof_begin(PH_LIST, st);
-        API_CK(launch_list(sc.first_col, (int)K, (int)T, p->info_stride, full_gain, sc.list, sc.ints, st), &m->poisoned);
+        API_CK(launch_list(sc.first_col, (int)K, (int)T, p->info_stride, full_gain, sc.list, sc.ints, sc.ranked, st),
+               &m->poisoned);
         prof_end(PH_LIST, st);
         prof_begin(PH_GAIN, st);
         API_CK(launch_phase_b(m, tr, p->mode, ck, sc.list, sc.ints, list_max, sc.wp_gq, sc.wp_nh, sc.wp_nl,

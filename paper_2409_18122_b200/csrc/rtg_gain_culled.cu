@@ -46,10 +46,6 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
     __shared__ double s_cs[kWarpsG][2];     // FP64 cos, sin of the waypoint's yaw (re-decisions)
     __shared__ float s_k[kWarpsG][8];       // per-waypoint column-test constants
     __shared__ float s_v[kWarpsG][8];       // footprint vertices (x0..x3, y0..y3)
-    __shared__ int s_rincl[kWarpsG][32];    // rows: inclusive prefix of column counts
-    __shared__ int s_roff[kWarpsG][32];     // rows: ix = position + offset
-    __shared__ int s_at[kWarpsG][32];       // test window: item starting at each position
-    __shared__ int s_ioff[kWarpsG][64];     // items: record index = position + offset
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int L = *list_count;
     unsigned nref = 0;
@@ -129,16 +125,19 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                     if (lane >= o) incl += v;
                 }
                 const int total = __shfl_sync(kFullG, incl, 31);
-                s_rincl[wid][lane] = incl;
-                s_roff[wid][lane] = ixlo - (incl - len);
-                __syncwarp();
-                int owner = 0;
+                const int roff = ixlo - (incl - len);
                 for (int cb = 0; cb < total; cb += 32) {
                     const int pos = cb + lane;
+                    // row owning column position pos: first lane whose inclusive prefix exceeds it
+                    int owner = 0;
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int v = __shfl_sync(kFullG, incl, owner + st - 1);
+                        if (v <= pos) owner += st;
+                    }
+                    const int ix = pos + __shfl_sync(kFullG, roff, owner);
                     int b0 = 0, l0 = 0, b1 = 0, l1 = 0;
                     if (pos < total) {
-                        while (s_rincl[wid][owner] <= pos) ++owner;
-                        const int ix = pos + s_roff[wid][owner];
                         const int cy = rbase + owner;
                         const float Zr = s_k[wid][0], f1r = s_k[wid][1], f2r = s_k[wid][2];
                         const float zrel = s_k[wid][5];
@@ -189,56 +188,30 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                     }
                     const int tot = __shfl_sync(kFullG, ic, 31);
                     const int ex = ic - sl;
-                    s_ioff[wid][2 * lane] = b0 - ex;
-                    s_ioff[wid][2 * lane + 1] = b1 - (ex + l0);
-                    // owner of position gb+lane = last non-empty run starting at or before it:
-                    // run starts inside the 32-wide window are OR-ed into one word; the owner is
-                    // read at the highest start bit <= lane, else carried from the last window
-                    int carry = 0;
-                    auto locate = [&](int gb) -> int {
-                        unsigned bits = 0;
-                        const int e0 = ex - gb, e1 = ex + l0 - gb;
-                        if (l0 > 0 && (unsigned)e0 < 32u) {
-                            bits |= 1u << e0;
-                            s_at[wid][e0] = 2 * lane;
-                        }
-                        if (l1 > 0 && (unsigned)e1 < 32u) {
-                            bits |= 1u << e1;
-                            s_at[wid][e1] = 2 * lane + 1;
-                        }
-                        const unsigned word = __reduce_or_sync(kFullG, bits);
-                        __syncwarp();
-                        const unsigned mk = word & (0xffffffffu >> (31 - lane));
-                        const int own = mk ? s_at[wid][31 - __clz(mk)] : carry;
-                        carry = __shfl_sync(kFullG, own, 31);
-                        const int gi = gb + lane + s_ioff[wid][own];
-                        __syncwarp();
-                        return gi;
-                    };
+                    // owner lane of position gp = first lane whose inclusive prefix exceeds gp
+                    // (warp binary search over the prefixes held in registers); then the lane's
+                    // first or second run and the record index inside it
                     int pc = 0;
-                    GRec Gn = GRec{0.f, 0.f, 0.f, 0};
-                    long long qn = 0;
-                    if (tot > 0) {
-                        const int gi = locate(0);
-                        if (lane < tot) {
-                            Gn = grec[gi];
-                            qn = guq[gi];
-                        }
-                    }
                     for (int gb = 0; gb < tot; gb += 32) {
-                        const GRec G = Gn;
-                        const long long q = qn;
-                        const bool act = gb + lane < tot;
-                        if (gb + 32 < tot) {      // prefetch the next window's records
-                            const int gi = locate(gb + 32);
-                            if (gb + 32 + lane < tot) {
-                                Gn = grec[gi];
-                                qn = guq[gi];
-                            }
+                        const int gp = gb + lane;
+                        int lo = 0;
+#pragma unroll
+                        for (int st = 16; st > 0; st >>= 1) {
+                            const int v = __shfl_sync(kFullG, ic, lo + st - 1);
+                            if (v <= gp) lo += st;
                         }
-                        if (act && visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref)) {
-                            accq += q;
-                            pc += G.inc;
+                        const int eo = gp - __shfl_sync(kFullG, ex, lo);
+                        const int lo0 = __shfl_sync(kFullG, l0, lo);
+                        const int bo0 = __shfl_sync(kFullG, b0, lo);
+                        const int bo1 = __shfl_sync(kFullG, b1, lo);
+                        const int gi = eo < lo0 ? bo0 + eo : bo1 + (eo - lo0);
+                        if (gp < tot) {
+                            const GRec G = grec[gi];
+                            const long long q = guq[gi];
+                            if (visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref)) {
+                                accq += q;
+                                pc += G.inc;
+                            }
                         }
                     }
                     if (kStats) ntest += (unsigned long long)tot;

@@ -141,9 +141,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
     const int* __restrict__ cstart, ColGridK g, float gq, int* __restrict__ first_col,
     unsigned char* __restrict__ wp_col, int all_waypoints, int* __restrict__ counter,
     unsigned long long* __restrict__ stats) {
-    __shared__ int s_incl[kWarps][32];
-    __shared__ int s_off[kWarps][32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     unsigned nref = 0;
     unsigned long long ntest = 0;
     for (;;) {
@@ -182,16 +180,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
                             if (lane >= o) incl += v;
                         }
                         const int total = __shfl_sync(kFull, incl, 31);
-                        s_incl[wid][lane] = incl;
-                        s_off[wid][lane] = beg - (incl - len);
-                        __syncwarp();
-                        int owner = 0;
+                        const int roff = beg - (incl - len);
                         for (int b0 = 0; b0 < total; b0 += 32) {
                             const int pos = b0 + lane;
+                            // row owning candidate pos: first lane whose inclusive prefix exceeds it
+                            int owner = 0;
+#pragma unroll
+                            for (int st = 16; st > 0; st >>= 1) {
+                                const int v = __shfl_sync(kFull, incl, owner + st - 1);
+                                if (v <= pos) owner += st;
+                            }
+                            const int gi = pos + __shfl_sync(kFull, roff, owner);
                             bool h = false;
                             if (pos < total) {
-                                while (s_incl[wid][owner] <= pos) ++owner;
-                                const int gi = pos + s_off[wid][owner];
                                 const CRec A = crec[gi];
                                 float dx = px - A.x, dy = py - A.y, dz = pz - A.z;
                                 float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
@@ -257,14 +258,21 @@ __global__ void k_build_list(const int* __restrict__ first_col, int K, int T, in
         }
         __syncthreads();
         int rank = s_carry + (wid > 0 ? s_warp[wid - 1] : 0) + x - inc;
-        if (inc) {
-            for (int j = 0; j < per; ++j) list[(long long)rank * per + j] = k * T + (j + 1) * stride - 1;
-        }
+        if (inc) list[rank] = k;      // ranked trajectories; expanded by k_fill_list
         __syncthreads();
         if (threadIdx.x == 0) s_carry += s_warp[(blockDim.x >> 5) - 1];
         __syncthreads();
     }
     if (threadIdx.x == 0) *count = s_carry * per;
+}
+
+// list[e] = ranked[e / per] * T + (e % per + 1) * stride - 1 for e < count (= ranked count * per)
+__global__ void k_fill_list(const int* __restrict__ ranked, const int* __restrict__ count, int per, int T, int stride,
+                            int* __restrict__ list) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= *count) return;
+    const int r = (int)(e / per), j = (int)(e - (long long)r * per);
+    list[e] = ranked[r] * T + (j + 1) * stride - 1;
 }
 
 // identity list (debug: every waypoint)
@@ -570,8 +578,12 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
 }
 
 cudaError_t launch_list(const int* first_col, int K, int T, int stride, int full_gain, int* list, int* count,
-                        cudaStream_t st) {
-    note_launch(), k_build_list<<<1, 1024, 0, st>>>(first_col, K, T, stride, full_gain, list, count);
+                        int* ranked, cudaStream_t st) {
+    note_launch(), k_build_list<<<1, 1024, 0, st>>>(first_col, K, T, stride, full_gain, ranked, count);
+    const long long per = T / stride, n = (long long)K * per;
+    if (n > 0)
+        note_launch(), k_fill_list<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ranked, count, (int)per, T, stride,
+                                                                                  list);
     return cudaGetLastError();
 }
 
