@@ -229,10 +229,13 @@ def main():
         tr.close()
         return res
 
-    def timed(host: bool, steps: int, warmup: int):
+    def timed(host: bool, steps: int, warmup: int, profile: bool = False):
         for _ in range(warmup):
             step(host)
         torch.cuda.synchronize()
+        if profile:                      # per-phase CUDA events over the timed steps only
+            R.profile_read(reset=True)
+            R.profile_enable(True)
         total_ms = 0.0
         res = None
         for _ in range(steps):
@@ -247,21 +250,19 @@ def main():
             b.record(stream)
             torch.cuda.synchronize()
             total_ms += a.elapsed_time(b)
+        if profile:
+            R.profile_enable(False)
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()) / steps, res
 
     # ---- device-resident timing (value), with clocks and per-phase events
-    R.profile_read(reset=True)
-    R.profile_enable(True)
     with ClockSampler(local) as clocks:
-        ms, res = timed(False, args.steps, args.warmup)
-    R.profile_enable(False)
+        ms, res = timed(False, args.steps, args.warmup, profile=True)
     prof = R.profile_read(reset=True)
-    # the warm-up steps ran with profiling on as well: per-step phase times use all profiled calls
-    nprof = max(1, prof["calls"]["collision"] or prof["calls"]["visibility_gain"] or 1)
-    launches_per_step = prof["launches"] / (args.steps + args.warmup)
+    nprof = args.steps
+    launches_per_step = prof["launches"] / args.steps
     clock = clocks.summary()
     pairs = float(K) * T * N * world
     value = pairs / (ms / 1000.0)

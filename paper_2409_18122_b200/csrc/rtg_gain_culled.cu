@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
     const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
-    const long long* __restrict__ aggq, const long long* __restrict__ agghl, const GainK g, const CamK cam,
+    const CellAgg* __restrict__ agg, const GainK g, const CamK cam,
     long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl, int* __restrict__ counter,
     unsigned long long* __restrict__ stats) {
     __shared__ double s_cs[kWarpsG][2];     // FP64 cos, sin of the waypoint's yaw (re-decisions)
@@ -164,12 +164,14 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                                 a = min(max((int)ceilf(za), c), dd);
                                 b = min(max((int)floorf(zb), a), dd);
                             }
-                            const int base = (cy * g.nx + ix) * g.nz;
-                            const int sc = gstart[base + c], sa = gstart[base + a];
-                            const int sb = gstart[base + b], sd = gstart[base + dd];
+                            // x-fastest tables: entry (cy, iz, ix) at (cy*(nz+1) + iz)*nx + ix
+                            const int base = cy * (g.nz + 1) * g.nx + ix;
+                            const int sc = gstart[base + c * g.nx], sa = gstart[base + a * g.nx];
+                            const int sb = gstart[base + b * g.nx], sd = gstart[base + dd * g.nx];
                             if (b > a) {
-                                accq += aggq[base + b] - aggq[base + a];
-                                const long long hl = agghl[base + b] - agghl[base + a];
+                                const CellAgg hi = agg[base + b * g.nx], lo = agg[base + a * g.nx];
+                                accq += hi.q - lo.q;
+                                const long long hl = hi.hl - lo.hl;
                                 acch += (int)(hl & 0xffffffffLL);
                                 accl += (int)(hl >> 32);
                                 if (kStats) nagg += (unsigned long long)(b - a);
@@ -275,11 +277,11 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     if (blocks < 1) blocks = 1;
     if (stats)
         note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstart, m->gaggq, m->gagghl, g, cam,
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
             wp_gq, wp_nh, wp_nl, counter, stats);
     else
         note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstart, m->gaggq, m->gagghl, g, cam,
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
             wp_gq, wp_nh, wp_nl, counter, stats);
     return cudaGetLastError();
 }

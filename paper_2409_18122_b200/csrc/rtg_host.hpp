@@ -69,9 +69,12 @@ struct rtg_map_s {
     rtg::GRec* grec = nullptr;
     long long* guq = nullptr;            // fixed-point u per record
     int* gidx = nullptr;                 // original index per record
-    int* gstart = nullptr;               // [ncells+1] first record of each gain cell
-    long long* gaggq = nullptr;          // [ncells+1] exclusive prefix of u_q at cell start
-    long long* gagghl = nullptr;         // [ncells+1] exclusive prefix of (nH | nL<<32)
+    int* gstart = nullptr;               // [ncells+1] first record of each gain cell, (iy, ix, iz) order
+    // culled-kernel tables in x-fastest layout [iy][iz][ix], iz = 0..nz (iz = nz: column end), so
+    // the lanes of a warp, which take neighbouring columns of a row, load neighbouring words
+    long long ntab = 0;                  // ny * (nz + 1) * nx
+    int* gstartT = nullptr;              // [ntab] first record of the cell (end of column at iz = nz)
+    rtg::CellAgg* gaggT = nullptr;       // [ntab] exclusive prefixes (u_q, nH | nL << 32) there
     rtg::GainGrid gg{};
     // collision records (sorted by collision cell), padded likewise
     long long n_col_pad = 0;

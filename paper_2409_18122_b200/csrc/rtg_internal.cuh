@@ -27,6 +27,8 @@ struct __align__(16) GRec { float x, y, z; int inc; };
 struct __align__(16) CRec { float x, y, z, rb2; };
 // M rows (FP32): m[0..8] row-major, m[9] = original index (as int bits), pad
 struct __align__(16) CMat { float m[12]; };
+// exact exclusive prefixes at a visibility-cell boundary: sum of u_q and packed (nH | nL << 32)
+struct __align__(16) CellAgg { long long q; long long hl; };
 // FP64 M for the re-decision branch (9 used)
 struct CMat64 { double m[9]; };
 

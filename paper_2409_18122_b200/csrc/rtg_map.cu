@@ -395,14 +395,20 @@ __global__ void k_class_records(long long n_gain, GRec* __restrict__ grec, long 
     ghl[i] = hl;
 }
 
-__global__ void k_gather_cells(long long ncells1, const int* __restrict__ gstart, const long long* __restrict__ pq,
-                               const long long* __restrict__ phl, long long* __restrict__ aq,
-                               long long* __restrict__ ahl) {
-    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (c >= ncells1) return;
-    int s = gstart[c];
-    aq[c] = pq[s];
-    ahl[c] = phl[s];
+// culled-kernel tables, x-fastest [iy][iz][ix] with iz = 0..nz: entry (iy, iz, ix) describes the
+// boundary before z-cell iz of column (ix, iy); in the (iy, ix, iz) record order the boundary at
+// iz = nz is the start of the next column, i.e. sorted cell index (iy*nx + ix)*nz + iz for all iz
+__global__ void k_gather_cells(GainGrid gg, const int* __restrict__ gstart, const long long* __restrict__ pq,
+                               const long long* __restrict__ phl, int* __restrict__ startT,
+                               CellAgg* __restrict__ aggT) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long nz1 = gg.nz + 1;
+    if (e >= (long long)gg.ny * nz1 * gg.nx) return;
+    const long long ix = e % gg.nx, r = e / gg.nx;
+    const long long iz = r % nz1, iy = r / nz1;
+    const int s = gstart[(iy * gg.nx + ix) * gg.nz + iz];
+    startT[e] = s;
+    aggT[e] = CellAgg{pq[s], phl[s]};
 }
 
 inline unsigned nblocks(long long n, int t) {
@@ -443,8 +449,8 @@ rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi
     e = exclusive_scan_i64(m->guq, pq, ng, st);
     if (e == cudaSuccess) e = exclusive_scan_i64(ghl, phl, ng, st);
     if (e == cudaSuccess) {
-        long long nc1 = m->gg.ncells + 1;
-        note_launch(), k_gather_cells<<<nblocks(nc1, 256), 256, 0, st>>>(nc1, m->gstart, pq, phl, m->gaggq, m->gagghl);
+        note_launch(), k_gather_cells<<<nblocks(m->ntab, 256), 256, 0, st>>>(m->gg, m->gstart, pq, phl, m->gstartT,
+                                                                             m->gaggT);
         e = cudaGetLastError();
     }
     dev_free(ghl, st);
@@ -568,8 +574,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->guq, m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gidx, m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gstart, gg.ncells + 1, st));
-    MAP_CK(map_alloc(m, &m->gaggq, gg.ncells + 1, st));
-    MAP_CK(map_alloc(m, &m->gagghl, gg.ncells + 1, st));
+    m->ntab = (long long)gg.ny * (gg.nz + 1) * gg.nx;
+    MAP_CK(map_alloc(m, &m->gstartT, m->ntab, st));
+    MAP_CK(map_alloc(m, &m->gaggT, m->ntab, st));
     MAP_CK(map_alloc(m, &m->crec, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cmat64, m->n_col_pad, st));
