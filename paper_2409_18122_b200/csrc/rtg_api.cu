@@ -462,7 +462,7 @@ struct Scratch {
     int* ints = nullptr;                  // [0] list count, [1] phase-A counter, [2] phase-B counter
     double* cam64 = nullptr;              // FP64 camera for the re-decision branch
     int* ranked = nullptr;                // computed trajectories in order (info list build)
-    unsigned long long* stats = nullptr;  // 4 counters
+    unsigned long long* stats = nullptr;  // 8 counters (rtg_score_debug)
     void* block = nullptr;
 };
 
@@ -477,7 +477,7 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     size_t o_list = o_nl + al(sizeof(int) * KT);
     size_t o_ints = o_list + al(sizeof(int) * (list_max > 0 ? list_max : 1));
     size_t o_stats = o_ints + al(sizeof(int) * 8);
-    size_t o_cam = o_stats + al(sizeof(unsigned long long) * 4);
+    size_t o_cam = o_stats + al(sizeof(unsigned long long) * 8);
     size_t o_ranked = o_cam + al(sizeof(double) * 8);
     size_t total = o_ranked + al(sizeof(int) * K);
     cudaError_t e = dev_alloc(&s.block, total, st);
@@ -496,7 +496,7 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     double c64[8] = {(double)cam->width, (double)cam->height, cam->fx, cam->fy, cam->cx, cam->cy, cam->z_near, cam->z_far};
     cudaError_t e2 = cudaMemcpyAsync(s.cam64, c64, sizeof(c64), cudaMemcpyHostToDevice, st);
     if (e2 != cudaSuccess) return e2;
-    return cudaMemsetAsync(b + o_ints, 0, o_stats + al(sizeof(unsigned long long) * 4) - o_ints, st);
+    return cudaMemsetAsync(b + o_ints, 0, o_stats + al(sizeof(unsigned long long) * 8) - o_ints, st);
 }
 
 rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_score_params* p, int* first_col,
@@ -617,12 +617,12 @@ rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const 
         API_CK(cudaMemsetAsync(pair_mask, 0, sizeof(unsigned) * (words ? words : 1), st), &m->poisoned);
         API_CK(launch_pair_mask(m, tr, pair_mask, st), &m->poisoned);
     }
-    unsigned long long hs[4] = {0, 0, 0, 0};
+    unsigned long long hs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     API_CK(cudaMemcpyAsync(hs, sc.stats, sizeof(hs), cudaMemcpyDeviceToHost, st), &m->poisoned);
     dev_free(sc.block, st);
     API_CK(cudaStreamSynchronize(st), &m->poisoned);
     if (stats)
-        for (int i = 0; i < 4; ++i) stats[i] = (long long)hs[i];
+        for (int i = 0; i < 8; ++i) stats[i] = (long long)hs[i];
     return RTG_OK;
 }
 

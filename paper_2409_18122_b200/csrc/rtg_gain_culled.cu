@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int L = *list_count;
     unsigned nref = 0;
-    unsigned long long ntest = 0, nagg = 0;
+    unsigned long long ntest = 0, nagg = 0, ncol = 0, nstr = 0, nvis = 0;
     for (;;) {
         int e = 0;
         if (lane == 0) e = atomicAdd(counter, 1);
@@ -178,6 +178,10 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                             }
                             b0 = sc; l0 = sa - sc;
                             b1 = sb; l1 = sd - sb;
+                            if (kStats) {
+                                ncol += 1;
+                                if (!in_h) nstr += (unsigned long long)(l0 + l1);
+                            }
                         }
                     }
                     // individual tests over this chunk's runs, lanes load-balanced
@@ -213,6 +217,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                             if (visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref)) {
                                 accq += q;
                                 pc += G.inc;
+                                if (kStats) nvis += 1;
                             }
                         }
                     }
@@ -239,11 +244,19 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
     if (kStats) {
         nref = __reduce_add_sync(kFullG, nref);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nagg += __shfl_xor_sync(kFullG, nagg, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            nagg += __shfl_xor_sync(kFullG, nagg, o);
+            ncol += __shfl_xor_sync(kFullG, ncol, o);
+            nstr += __shfl_xor_sync(kFullG, nstr, o);
+            nvis += __shfl_xor_sync(kFullG, nvis, o);
+        }
         if (lane == 0) {
             if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
             atomicAdd(&stats[2], ntest);
             atomicAdd(&stats[3], nagg);
+            atomicAdd(&stats[5], nstr);
+            atomicAdd(&stats[6], ncol);
+            atomicAdd(&stats[7], nvis);
         }
     }
 }

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
         nref = __reduce_add_sync(kFull, nref);
         if (lane == 0) {
             if (nref) atomicAdd(&stats[0], (unsigned long long)nref);
-            atomicAdd(&stats[2], ntest);
+            atomicAdd(&stats[4], ntest);
         }
     }
 }

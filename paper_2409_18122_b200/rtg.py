@@ -318,13 +318,14 @@ def score_debug(m: Map, tr: Traj, camera, params: ScoreParams, pair_mask: bool =
     if pair_mask:
         words = (KT * m.n + 31) // 32
         mask = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
-    stats = (ctypes.c_longlong * 4)()
+    stats = (ctypes.c_longlong * 8)()
     cam = camera if isinstance(camera, Camera) else make_camera(camera)
     _check(_lib.rtg_score_debug(m.handle, tr.handle, ctypes.byref(cam), ctypes.byref(params), _ptr(wp_col),
                                 _ptr(wp_gain), _ptr(wp_nh), _ptr(wp_nl), _ptr(mask), stats, _stream(stream)),
            "rtg_score_debug")
     return dict(wp_col=wp_col, wp_gain=wp_gain, wp_nh=wp_nh, wp_nl=wp_nl, pair_mask=mask,
-                stats=dict(col_refined=stats[0], vis_refined=stats[1], tested=stats[2], cells_aggregated=stats[3]))
+                stats=dict(col_refined=stats[0], vis_refined=stats[1], tested=stats[2], cells_aggregated=stats[3],
+                           col_tested=stats[4], tested_straddle=stats[5], columns=stats[6], tested_visible=stats[7]))
 
 
 def unpack_pair_mask(mask, KT: int, N: int) -> np.ndarray:
