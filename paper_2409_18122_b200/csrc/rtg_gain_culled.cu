@@ -30,6 +30,15 @@ struct GainK {
     float zn, zf, kxl, kxr, kyu, kyd, kxh;
 };
 
+constexpr int kLongRun = 16;   // runs at least this long are tested run by run, whole warp
+
+// acc += q and pc += inc when p (predicated adds, no selects)
+__device__ __forceinline__ void add_if(bool p, long long& acc, long long q, int& pc, int inc) {
+    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.s64 %0, %0, %2;\n\t@pp add.s32 %1, %1, %3;\n\t}"
+        : "+l"(acc), "+r"(pc)
+        : "l"(q), "r"(inc), "r"((int)p));
+}
+
 __device__ __forceinline__ int fcell(float v, int hi) {   // floor of v clamped to [-1, hi + 1]
     v = fminf(fmaxf(v, -1.0f), (float)hi + 1.0f);
     return (int)floorf(v);
@@ -184,7 +193,39 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                             }
                         }
                     }
-                    // individual tests over this chunk's runs, lanes load-balanced
+                    // individual tests over this chunk's runs
+                    if (kStats) ntest += (unsigned long long)(l0 + l1);
+                    int pc = 0;
+                    auto test = [&](int gi) {
+                        const GRec G = grec[gi];
+                        const long long q = guq[gi];
+                        const bool v = visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref);
+                        add_if(v, accq, q, pc, G.inc);
+                        if (kStats) nvis += v;
+                    };
+                    // (1) long runs (straddling columns, mostly): one run at a time across the
+                    //     whole warp, consecutive records per lane, no per-position search
+                    {
+                        const unsigned lm0 = __ballot_sync(kFullG, l0 >= kLongRun);
+                        const unsigned lm1 = __ballot_sync(kFullG, l1 >= kLongRun);
+#pragma unroll
+                        for (int pass = 0; pass < 2; ++pass) {
+                            unsigned lm = pass ? lm1 : lm0;
+                            const int bb = pass ? b1 : b0, ll = pass ? l1 : l0;
+                            while (lm) {
+                                const int j = __ffs(lm) - 1;
+                                lm &= lm - 1;
+                                const int start = __shfl_sync(kFullG, bb, j);
+                                const int len = __shfl_sync(kFullG, ll, j);
+                                for (int o = lane; o < len; o += 32) test(start + o);
+                            }
+                        }
+                        if (l0 >= kLongRun) l0 = 0;
+                        if (l1 >= kLongRun) l1 = 0;
+                    }
+                    // (2) short runs packed into full windows: the owner lane of position gp is
+                    //     the first lane whose inclusive prefix exceeds gp (warp binary search over
+                    //     the prefixes held in registers), then its first or second run
                     const int sl = l0 + l1;
                     int ic = sl;
 #pragma unroll
@@ -194,10 +235,6 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                     }
                     const int tot = __shfl_sync(kFullG, ic, 31);
                     const int ex = ic - sl;
-                    // owner lane of position gp = first lane whose inclusive prefix exceeds gp
-                    // (warp binary search over the prefixes held in registers); then the lane's
-                    // first or second run and the record index inside it
-                    int pc = 0;
                     for (int gb = 0; gb < tot; gb += 32) {
                         const int gp = gb + lane;
                         int lo = 0;
@@ -211,17 +248,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                         const int bo0 = __shfl_sync(kFullG, b0, lo);
                         const int bo1 = __shfl_sync(kFullG, b1, lo);
                         const int gi = eo < lo0 ? bo0 + eo : bo1 + (eo - lo0);
-                        if (gp < tot) {
-                            const GRec G = grec[gi];
-                            const long long q = guq[gi];
-                            if (visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref)) {
-                                accq += q;
-                                pc += G.inc;
-                                if (kStats) nvis += 1;
-                            }
-                        }
+                        if (gp < tot) test(gi);
                     }
-                    if (kStats) ntest += (unsigned long long)tot;
                     acch += pc & 0xffff;
                     accl += pc >> 16;
                     __syncwarp();
@@ -245,6 +273,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
         nref = __reduce_add_sync(kFullG, nref);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
+            ntest += __shfl_xor_sync(kFullG, ntest, o);
             nagg += __shfl_xor_sync(kFullG, nagg, o);
             ncol += __shfl_xor_sync(kFullG, ncol, o);
             nstr += __shfl_xor_sync(kFullG, nstr, o);
