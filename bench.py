@@ -167,6 +167,7 @@ def main():
     import torch.distributed as dist
     from paper_2409_18122_b200 import build as B
     B.build()
+    from paper_2409_18122_b200 import dist as D
     from paper_2409_18122_b200 import rtg as R
     from paper_2409_18122_b200 import workloads as W
 
@@ -203,19 +204,11 @@ def main():
     outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
             torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    gather = torch.zeros(2 * world, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
     def global_best(score, idx):
-        gidx = rank + idx * world if idx >= 0 else -1
-        if world == 1:
-            return score, gidx
-        mine = torch.tensor([score, float(gidx)], dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(gather, mine)
-        g = gather.view(world, 2).cpu().numpy()
-        top = g[:, 0].max()
-        cands = [int(i) for s, i in g if s == top and i >= 0]
-        return float(top), (min(cands) if cands else -1)
+        # one NCCL all_gather of (score, global index) per step (paper_2409_18122_b200/dist.py)
+        return D.global_best(score, idx, rank, world, device=dev)
 
     def step(host: bool):
         src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
@@ -284,12 +277,24 @@ def main():
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    roof = roofline(dom, phase_ms[dom], wl, outs, clock, hbm_peak, R, dev)
+    feasible = outs[1].cpu().numpy().astype(bool)
+    work = None
+    if args.mode == "culled":
+        m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
+                  device=local)
+        work = work_sample(R, m, wl, cam, params, feasible)
+        m.close()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"{args.config}/{args.mode}/stride{args.stride}")
+    roof = roofline(dom, phase_ms[dom], wl, int(feasible.sum()), args.stride, args.mode, clock,
+                    hbm_peak, work, traffic)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cores = oracle_threads()
-        n_traj = max(1, min(K, cores))
+        n_traj = max(1, min(K, 4 * cores))
         v, dt, nt = oracle_sample(wl, n_traj)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{nt} random trajectories x T={T} x N={N} of this workload ({dt:.1f} s)"}
@@ -312,32 +317,52 @@ def main():
     return 0
 
 
-def roofline(phase, ms, wl, outs, clock, hbm_peak, R, dev):
-    """Roofline object for the dominant phase; algorithmic work per unit as in DESIGN.md."""
+# Algorithmic work per unit:
+I_TEST = 20.0     # FP32/ALU lane instructions of one exact visibility pair test + accumulate
+I_COLUMN = 25.0   # lane instructions to classify one visibility-grid column (SURVEY [A5]: ~25 per cell)
+I_SPHERE = 8.0    # collision sphere reject per candidate pair (3 FADD, 3 FMA, compare, branch)
+KERNEL = {"visibility_gain": "k_gain_culled", "collision": "k_col_culled", "map_build": "k_scatter_col"}
+
+
+def work_sample(R, m, wl, cam, params, feasible, n=96):
+    """Per-waypoint work units of the culled kernels, measured with rtg_score_debug on a sample of
+    feasible trajectories (untimed)."""
+    import numpy as np
+    f = np.nonzero(feasible)[0]
+    if len(f) == 0:
+        return None
+    idx = f[np.linspace(0, len(f) - 1, min(n, len(f))).astype(int)]
+    tr = R.traj_from_workload(wl, x=wl.x[idx], y=wl.y[idx], z=wl.z[idx], yaw=wl.yaw[idx])
+    p = R.make_params(mode=params.mode, info_stride=1, flags=R.SCORE_FULL_GAIN)
+    d = R.score_debug(m, tr, cam, p)
+    tr.close()
+    nwp = len(idx) * wl.T
+    return {k: v / nwp for k, v in d["stats"].items()}
+
+
+def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, traffic):
+    """Roofline object of the dominant phase (achieved = algorithmic work per launch / launch time)."""
     sm_mhz = (clock.get("sm_mhz") or 1965.0)
+    peak_ti = 148 * 128 * sm_mhz * 1e6 / 1e12          # lane-instruction issue peak, T/s (guide unit counts)
+    tr = traffic.get(KERNEL.get(phase, ""), None) if traffic else None
     if phase == "map_build":
-        # read 49 B/G raw input, write the packed records; bound: HBM
         n = wl.N
-        alg_bytes = n * 49 + n * (16 + 8 + 4) + (n // 2) * (16 + 48 + 72)
+        alg_bytes = n * 49 + n * (16 + 8 + 4) * 2 + (n // 2) * (16 + 48 + 72)
         gbs = alg_bytes / (ms / 1e3) / 1e9
         return {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                "traffic": None, "phase": phase, "ms": ms}
-    # FP32-pipe issue roofline: nominal pairs x the kernel's FP32 instruction budget per pair
-    # would exceed the peak for the culled kernels (they skip pairs), so report pair tests
-    # actually executed is impossible live; we report nominal-pair rate against the dense-kernel
-    # budget as "equivalent" and say so in DESIGN.md.
-    K, T, N = wl.K, wl.T, wl.N
-    feas = float(outs[1].float().mean().item())
-    if phase == "collision":
-        instr_per_pair = 8.0
-        pairs = K * T * wl.flags.astype(bool).__invert__().sum() if wl.flags is not None else K * T * N
+                "traffic": tr, "phase": phase, "kernel_ms": ms}
+    n_info = n_feasible * (wl.T // stride)
+    if phase == "visibility_gain":
+        if mode == "dense":
+            lane_instr = n_info * float(wl.N) * I_TEST
+        else:
+            lane_instr = n_info * (I_TEST * work["tested"] + I_COLUMN * work["columns"])
     else:
-        instr_per_pair = 21.0
-        pairs = K * feas * T * N
-    peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # T lane-instr/s
-    ach = pairs * instr_per_pair / (ms / 1e3) / 1e12
-    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "T FP32-lane-instr/s (dense-equivalent)",
-            "frac": ach / peak, "traffic": None, "phase": phase, "ms": ms}
+        lane_instr = wl.K * wl.T * (work["col_tested"] if work else 0.0) * I_SPHERE
+    ach = lane_instr / (ms / 1e3) / 1e12
+    return {"bound": "alu", "achieved": ach, "peak": peak_ti, "unit": "T lane-instr/s", "frac": ach / peak_ti,
+            "traffic": tr, "phase": phase, "kernel": KERNEL.get(phase), "kernel_ms": ms,
+            "work_per_waypoint": work}
 
 
 if __name__ == "__main__":

@@ -1,0 +1,82 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): sharding and the global argmax exchange."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2409_18122_b200 import dist as D
+
+
+def test_shards_partition_all_trajectories():
+    for K, W in ((10, 3), (16384, 8), (5, 8), (1, 1)):
+        parts = [D.shard_indices(K, r, W) for r in range(W)]
+        allk = np.sort(np.concatenate(parts))
+        assert np.array_equal(allk, np.arange(K))
+        for r, p in enumerate(parts):
+            assert all(D.local_to_global(j, r, W) == k for j, k in enumerate(p))
+
+
+def test_reduce_best_ties_and_none():
+    assert D.reduce_best(np.array([[3.0, 7], [5.0, 9], [5.0, 2]])) == (5.0, 2)
+    assert D.reduce_best(np.array([[-math.inf, -1], [-math.inf, -1]])) == (-math.inf, -1)
+    assert D.reduce_best(np.array([[-math.inf, -1], [-2.0, 4]])) == (-2.0, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, utility, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        idx = D.shard_indices(len(utility), rank, world)
+        local = utility[idx]
+        # local argmax exactly as rtg_best computes it: max, ties -> lowest local index
+        if np.all(np.isneginf(local)):
+            s, j = -math.inf, -1
+        else:
+            j = int(np.argmax(local))
+            s = float(local[j])
+        q.put((rank, D.global_best(s, j, rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["random", "ties_across_ranks", "none_feasible"])
+def test_global_best_gloo_world2(case):
+    rng = np.random.default_rng(3)
+    u = rng.normal(size=101)
+    u[rng.random(101) < 0.4] = -np.inf
+    if case == "ties_across_ranks":
+        u[:] = -np.inf
+        u[[7, 4, 10]] = 2.5            # 4 -> rank 0, 7 -> rank 1, 10 -> rank 0
+    if case == "none_feasible":
+        u[:] = -np.inf
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, u, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if np.all(np.isneginf(u)):
+        expect = (-math.inf, -1)
+    else:
+        k = int(np.argmax(u))
+        expect = (float(u[k]), k)
+    assert res[0] == res[1] == expect
