@@ -294,7 +294,7 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cores = oracle_threads()
-        n_traj = max(1, min(K, 4 * cores))
+        n_traj = max(1, min(K, 2 * cores))
         v, dt, nt = oracle_sample(wl, n_traj)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{nt} random trajectories x T={T} x N={N} of this workload ({dt:.1f} s)"}
@@ -321,7 +321,9 @@ def main():
 I_TEST = 20.0     # FP32/ALU lane instructions of one exact visibility pair test + accumulate
 I_COLUMN = 25.0   # lane instructions to classify one visibility-grid column (SURVEY [A5]: ~25 per cell)
 I_SPHERE = 8.0    # collision sphere reject per candidate pair (3 FADD, 3 FMA, compare, branch)
-KERNEL = {"visibility_gain": "k_gain_culled", "collision": "k_col_culled", "map_build": "k_scatter_col"}
+KERNEL = {("visibility_gain", "culled"): "k_gain_culled", ("collision", "culled"): "k_col_culled",
+          ("visibility_gain", "dense"): "k_gain_dense", ("collision", "dense"): "k_col_dense",
+          ("map_build", "culled"): "k_scatter_col", ("map_build", "dense"): "k_scatter_col"}
 
 
 def work_sample(R, m, wl, cam, params, feasible, n=96):
@@ -344,7 +346,8 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, tra
     """Roofline object of the dominant phase (achieved = algorithmic work per launch / launch time)."""
     sm_mhz = (clock.get("sm_mhz") or 1965.0)
     peak_ti = 148 * 128 * sm_mhz * 1e6 / 1e12          # lane-instruction issue peak, T/s (guide unit counts)
-    tr = traffic.get(KERNEL.get(phase, ""), None) if traffic else None
+    kname = KERNEL.get((phase, mode), "")
+    tr = traffic.get(kname, None) if traffic else None
     if phase == "map_build":
         n = wl.N
         alg_bytes = n * 49 + n * (16 + 8 + 4) * 2 + (n // 2) * (16 + 48 + 72)
@@ -361,7 +364,7 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, tra
         lane_instr = wl.K * wl.T * (work["col_tested"] if work else 0.0) * I_SPHERE
     ach = lane_instr / (ms / 1e3) / 1e12
     return {"bound": "alu", "achieved": ach, "peak": peak_ti, "unit": "T lane-instr/s", "frac": ach / peak_ti,
-            "traffic": tr, "phase": phase, "kernel": KERNEL.get(phase), "kernel_ms": ms,
+            "traffic": tr, "phase": phase, "kernel": kname, "kernel_ms": ms,
             "work_per_waypoint": work}
 
 

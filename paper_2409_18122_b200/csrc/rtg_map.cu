@@ -132,7 +132,29 @@ __global__ void k_bounds(long long n, const float* __restrict__ means, const flo
     }
     rbm = __reduce_max_sync(full, rbm);
     rhm = __reduce_max_sync(full, rhm);
+    // block aggregate through shared memory: one set of atomics per block
+    __shared__ int sh[8][17];
+    const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
+        int* s = sh[wid];
+        s[0] = err; s[1] = ng; s[2] = nc;
+        for (int d = 0; d < 3; ++d) {
+            s[3 + d] = gmn[d]; s[6 + d] = gmx[d]; s[9 + d] = cmn[d]; s[12 + d] = cmx[d];
+        }
+        s[15] = rbm; s[16] = rhm;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < nw; ++w) {
+        const int* s = sh[w];
+        err |= s[0]; ng += s[1]; nc += s[2];
+        for (int d = 0; d < 3; ++d) {
+            gmn[d] = min(gmn[d], s[3 + d]); gmx[d] = max(gmx[d], s[6 + d]);
+            cmn[d] = min(cmn[d], s[9 + d]); cmx[d] = max(cmx[d], s[12 + d]);
+        }
+        rbm = max(rbm, s[15]); rhm = max(rhm, s[16]);
+    }
+    {
         if (err) atomicOr(&out->err, err);
         if (ng) atomicAdd(&out->n_gain, ng);
         if (nc) atomicAdd(&out->n_col, nc);
@@ -505,7 +527,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     DevBounds* db = nullptr;
     MAP_CK(dev_alloc((void**)&db, sizeof(DevBounds), st));
     note_launch(), k_bounds_init<<<1, 1, 0, st>>>(db);
-    if (n > 0) note_launch(), k_bounds<<<nblocks(n, 256) > 4096 ? 4096 : nblocks(n, 256), 256, 0, st>>>(n, means, quats, scales, opacity, w, flags, rb, db);
+    if (n > 0)
+        note_launch(), k_bounds<<<nblocks(n, 256) > 592 ? 592 : nblocks(n, 256), 256, 0, st>>>(
+                           n, means, quats, scales, opacity, w, flags, rb, db);
     DevBounds hb;
     MAP_CK(cudaMemcpyAsync(&hb, db, sizeof(DevBounds), cudaMemcpyDeviceToHost, st));
     MAP_CK(cudaStreamSynchronize(st));

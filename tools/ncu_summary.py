@@ -1,0 +1,93 @@
+"""Summarise ncu outputs into profiles/ (committed evidence).
+
+usage:
+  python tools/ncu_summary.py launches <launches.csv> <out.txt>
+  python tools/ncu_summary.py full <report.ncu-rep> <out.txt> [traffic_key]
+The `full` mode also records dram bytes per launch of the captured kernel into
+profiles/traffic.json under traffic_key (e.g. outdoor/culled/stride1), which bench.py reports
+as roofline.traffic.
+"""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCALE = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3}
+
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+    "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "smsp__sass_inst_executed_op_global_ld.sum",
+]
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.OrderedDict()
+    for r in data:
+        if len(r) <= iv:
+            continue
+        name = r[ik].split("(")[0].replace("void ", "")
+        ms = float(r[iv].replace(",", "")) * SCALE.get(r[iu], 1e-6)
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += ms
+    tot = sum(a[1] for a in agg.values())
+    lines = [f"# ncu launch list ({os.path.basename(path)}): gpu__time_duration per kernel, cold-cache, serialised",
+             f"# {sum(a[0] for a in agg.values())} launches, {tot:.3f} ms total", ""]
+    for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"{k[:72]:72s} launches={n:3d} ms={ms:9.4f} share={ms / tot * 100:5.1f}%")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines[:12]))
+
+
+def full(rep, out, key=None):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    hdr, units = r[0], r[1]
+    lines = [f"# ncu --set full summary of {os.path.basename(rep)}"]
+    traffic = {}
+    for vals in r[2:]:
+        name = vals[hdr.index("Kernel Name")].split("(")[0]
+        lines.append(f"\n## {name}")
+        got = {}
+        for w in METRICS:
+            if w in hdr:
+                i = hdr.index(w)
+                lines.append(f"{w:60s} {units[i]:10s} {vals[i]}")
+                got[w] = (units[i], vals[i])
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        b = 0.0
+        for w in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if w in got:
+                u, v = got[w]
+                b += float(v.replace(",", "")) * mult.get(u, 1)
+        short = name.split("::")[-1].split("<")[0]
+        traffic[short] = b
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if key:
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        t = json.load(open(tpath)) if os.path.exists(tpath) else {}
+        t.setdefault(key, {}).update(traffic)
+        json.dump(t, open(tpath, "w"), indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
