@@ -45,7 +45,7 @@ __device__ __forceinline__ int fcell(float v, int hi) {   // floor of v clamped 
 }
 
 template <bool kStats>
-__global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
+__global__ void __launch_bounds__(kWarpsG * 32, 3) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
     const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
@@ -196,15 +196,26 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                     // individual tests over this chunk's runs
                     if (kStats) ntest += (unsigned long long)(l0 + l1);
                     int pc = 0;
-                    auto test = [&](int gi) {
-                        const GRec G = grec[gi];
-                        const long long q = guq[gi];
-                        const bool v = visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref);
+                    // exact test of one record per lane, all lanes together (act = lane has one);
+                    // the rare FP64 re-decision runs behind a warp-uniform branch
+                    auto decide = [&](const GRec& G, long long q, bool act) {
+                        float Z;
+                        const float m = vis_margin(f, cam, G.x, G.y, G.z, Z);
+                        bool v = act & (m >= 0.0f);
+                        const bool band = act & (fabsf(m) < fmaf(cam.gam, Z, cam.g0));
+                        if (__any_sync(kFullG, band)) {
+                            if (band) {
+                                v = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], G.x, G.y, G.z,
+                                                    cam.cam64);
+                                ++nref;
+                            }
+                        }
                         add_if(v, accq, q, pc, G.inc);
                         if (kStats) nvis += v;
                     };
+                    const GRec kNone = GRec{0.f, 0.f, 0.f, 0};
                     // (1) long runs (straddling columns, mostly): one run at a time across the
-                    //     whole warp, consecutive records per lane, no per-position search
+                    //     whole warp, consecutive records per lane, two windows in flight
                     {
                         const unsigned lm0 = __ballot_sync(kFullG, l0 >= kLongRun);
                         const unsigned lm1 = __ballot_sync(kFullG, l1 >= kLongRun);
@@ -217,7 +228,16 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                                 lm &= lm - 1;
                                 const int start = __shfl_sync(kFullG, bb, j);
                                 const int len = __shfl_sync(kFullG, ll, j);
-                                for (int o = lane; o < len; o += 32) test(start + o);
+                                for (int base = 0; base < len; base += 64) {
+                                    const int o0 = base + lane, o1 = o0 + 32;
+                                    const bool a0 = o0 < len, a1 = o1 < len;
+                                    const GRec G0 = a0 ? grec[start + o0] : kNone;
+                                    const GRec G1 = a1 ? grec[start + o1] : kNone;
+                                    const long long q0 = a0 ? guq[start + o0] : 0;
+                                    const long long q1 = a1 ? guq[start + o1] : 0;
+                                    decide(G0, q0, a0);
+                                    if (__any_sync(kFullG, a1)) decide(G1, q1, a1);
+                                }
                             }
                         }
                         if (l0 >= kLongRun) l0 = 0;
@@ -248,7 +268,10 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                         const int bo0 = __shfl_sync(kFullG, b0, lo);
                         const int bo1 = __shfl_sync(kFullG, b1, lo);
                         const int gi = eo < lo0 ? bo0 + eo : bo1 + (eo - lo0);
-                        if (gp < tot) test(gi);
+                        const bool act = gp < tot;
+                        const GRec G = act ? grec[gi] : kNone;
+                        const long long q = act ? guq[gi] : 0;
+                        decide(G, q, act);
                     }
                     acch += pc & 0xffff;
                     accl += pc >> 16;
