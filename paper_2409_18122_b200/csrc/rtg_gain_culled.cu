@@ -44,8 +44,8 @@ __device__ __forceinline__ int fcell(float v, int hi) {   // floor of v clamped 
     return (int)floorf(v);
 }
 
-template <bool kStats>
-__global__ void __launch_bounds__(kWarpsG * 32, 3) k_gain_culled(
+template <bool kStats, int kMinBlocks>
+__global__ void __launch_bounds__(kWarpsG * 32, kMinBlocks) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
     const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
@@ -320,9 +320,17 @@ int g_sms_g = 0, g_occ_g = 0;
 cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, const int* list, const int* count,
                                long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl, int* counter,
                                unsigned long long* stats, cudaStream_t st) {
+    // RTG_GAIN_OCC (3 or 4): resident blocks per SM the kernel is compiled for (tuning knob)
+    static const int occ_sel = [] {
+        const char* e = getenv("RTG_GAIN_OCC");
+        return (e && atoi(e) == 4) ? 4 : 3;
+    }();
     if (!g_sms_g) {
         cudaDeviceGetAttribute(&g_sms_g, cudaDevAttrMultiProcessorCount, m->device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false>, kWarpsG * 32, 0);
+        if (occ_sel == 4)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false, 4>, kWarpsG * 32, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false, 3>, kWarpsG * 32, 0);
         if (g_occ_g < 1) g_occ_g = 1;
     }
     GainK g;
@@ -340,14 +348,17 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     long long cap = (long long)g_sms_g * g_occ_g;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+#define RTG_GAIN_ARGS                                                                                         \
+    tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam, wp_gq, wp_nh, wp_nl, \
+        counter, stats
+    const unsigned nb = (unsigned)blocks, nt = kWarpsG * 32;
     if (stats)
-        note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
-            wp_gq, wp_nh, wp_nl, counter, stats);
+        note_launch(), k_gain_culled<true, 3><<<nb, nt, 0, st>>>(RTG_GAIN_ARGS);
+    else if (occ_sel == 4)
+        note_launch(), k_gain_culled<false, 4><<<nb, nt, 0, st>>>(RTG_GAIN_ARGS);
     else
-        note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
-            wp_gq, wp_nh, wp_nl, counter, stats);
+        note_launch(), k_gain_culled<false, 3><<<nb, nt, 0, st>>>(RTG_GAIN_ARGS);
+#undef RTG_GAIN_ARGS
     return cudaGetLastError();
 }
 
