@@ -44,8 +44,8 @@ __device__ __forceinline__ int fcell(float v, int hi) {   // floor of v clamped 
     return (int)floorf(v);
 }
 
-template <bool kStats, int kMinBlocks>
-__global__ void __launch_bounds__(kWarpsG * 32, kMinBlocks) k_gain_culled(
+template <bool kStats>
+__global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
     const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
@@ -196,26 +196,15 @@ __global__ void __launch_bounds__(kWarpsG * 32, kMinBlocks) k_gain_culled(
                     // individual tests over this chunk's runs
                     if (kStats) ntest += (unsigned long long)(l0 + l1);
                     int pc = 0;
-                    // exact test of one record per lane, all lanes together (act = lane has one);
-                    // the rare FP64 re-decision runs behind a warp-uniform branch
-                    auto decide = [&](const GRec& G, long long q, bool act) {
-                        float Z;
-                        const float m = vis_margin(f, cam, G.x, G.y, G.z, Z);
-                        bool v = act & (m >= 0.0f);
-                        const bool band = act & (fabsf(m) < fmaf(cam.gam, Z, cam.g0));
-                        if (__any_sync(kFullG, band)) {
-                            if (band) {
-                                v = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], G.x, G.y, G.z,
-                                                    cam.cam64);
-                                ++nref;
-                            }
-                        }
+                    auto test = [&](int gi) {
+                        const GRec G = grec[gi];
+                        const long long q = guq[gi];
+                        const bool v = visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref);
                         add_if(v, accq, q, pc, G.inc);
                         if (kStats) nvis += v;
                     };
-                    const GRec kNone = GRec{0.f, 0.f, 0.f, 0};
                     // (1) long runs (straddling columns, mostly): one run at a time across the
-                    //     whole warp, consecutive records per lane, two windows in flight
+                    //     whole warp, consecutive records per lane, no per-position search
                     {
                         const unsigned lm0 = __ballot_sync(kFullG, l0 >= kLongRun);
                         const unsigned lm1 = __ballot_sync(kFullG, l1 >= kLongRun);
@@ -228,16 +217,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, kMinBlocks) k_gain_culled(
                                 lm &= lm - 1;
                                 const int start = __shfl_sync(kFullG, bb, j);
                                 const int len = __shfl_sync(kFullG, ll, j);
-                                for (int base = 0; base < len; base += 64) {
-                                    const int o0 = base + lane, o1 = o0 + 32;
-                                    const bool a0 = o0 < len, a1 = o1 < len;
-                                    const GRec G0 = a0 ? grec[start + o0] : kNone;
-                                    const GRec G1 = a1 ? grec[start + o1] : kNone;
-                                    const long long q0 = a0 ? guq[start + o0] : 0;
-                                    const long long q1 = a1 ? guq[start + o1] : 0;
-                                    decide(G0, q0, a0);
-                                    if (__any_sync(kFullG, a1)) decide(G1, q1, a1);
-                                }
+                                for (int o = lane; o < len; o += 32) test(start + o);
                             }
                         }
                         if (l0 >= kLongRun) l0 = 0;
@@ -268,10 +248,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, kMinBlocks) k_gain_culled(
                         const int bo0 = __shfl_sync(kFullG, b0, lo);
                         const int bo1 = __shfl_sync(kFullG, b1, lo);
                         const int gi = eo < lo0 ? bo0 + eo : bo1 + (eo - lo0);
-                        const bool act = gp < tot;
-                        const GRec G = act ? grec[gi] : kNone;
-                        const long long q = act ? guq[gi] : 0;
-                        decide(G, q, act);
+                        if (gp < tot) test(gi);
                     }
                     acch += pc & 0xffff;
                     accl += pc >> 16;
@@ -320,17 +297,9 @@ int g_sms_g = 0, g_occ_g = 0;
 cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, const int* list, const int* count,
                                long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl, int* counter,
                                unsigned long long* stats, cudaStream_t st) {
-    // RTG_GAIN_OCC (3 or 4): resident blocks per SM the kernel is compiled for (tuning knob)
-    static const int occ_sel = [] {
-        const char* e = getenv("RTG_GAIN_OCC");
-        return (e && atoi(e) == 4) ? 4 : 3;
-    }();
     if (!g_sms_g) {
         cudaDeviceGetAttribute(&g_sms_g, cudaDevAttrMultiProcessorCount, m->device);
-        if (occ_sel == 4)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false, 4>, kWarpsG * 32, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false, 3>, kWarpsG * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false>, kWarpsG * 32, 0);
         if (g_occ_g < 1) g_occ_g = 1;
     }
     GainK g;
@@ -348,17 +317,14 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     long long cap = (long long)g_sms_g * g_occ_g;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-#define RTG_GAIN_ARGS                                                                                         \
-    tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam, wp_gq, wp_nh, wp_nl, \
-        counter, stats
-    const unsigned nb = (unsigned)blocks, nt = kWarpsG * 32;
     if (stats)
-        note_launch(), k_gain_culled<true, 3><<<nb, nt, 0, st>>>(RTG_GAIN_ARGS);
-    else if (occ_sel == 4)
-        note_launch(), k_gain_culled<false, 4><<<nb, nt, 0, st>>>(RTG_GAIN_ARGS);
+        note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
+            wp_gq, wp_nh, wp_nl, counter, stats);
     else
-        note_launch(), k_gain_culled<false, 3><<<nb, nt, 0, st>>>(RTG_GAIN_ARGS);
-#undef RTG_GAIN_ARGS
+        note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
+            wp_gq, wp_nh, wp_nl, counter, stats);
     return cudaGetLastError();
 }
 
