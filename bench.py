@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=-1, help="steps timed per phase (default: all)")
+    ap.add_argument("--cells", default=None,
+                    help="visibility grid cells 'hy,hx,hz' [m] (rtg_map_options; default: library defaults)")
     return ap.parse_args()
 
 
@@ -210,10 +212,15 @@ def main():
         # one NCCL all_gather of (score, global index) per step (paper_2409_18122_b200/dist.py)
         return D.global_best(score, idx, rank, world, device=dev)
 
+    map_opts = None
+    if args.cells:
+        hy, hx, hz = (float(v) for v in args.cells.split(","))
+        map_opts = (hy, hz, 0.0, hx)
+
     def step(host: bool):
         src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
         m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
-                  device=local)
+                  device=local, options=map_opts)
         tr = R.Traj.upload(*src_traj, device=local)
         R.score(m, tr, cam, params, *outs)
         s, i = R.best(outs[3])
@@ -281,7 +288,7 @@ def main():
     work = None
     if args.mode == "culled":
         m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
-                  device=local)
+                  device=local, options=map_opts)
         work = work_sample(R, m, wl, cam, params, feasible)
         m.close()
     traffic = None
@@ -319,7 +326,7 @@ def main():
 
 # Algorithmic work per unit:
 I_TEST = 20.0     # FP32/ALU lane instructions of one exact visibility pair test + accumulate
-I_COLUMN = 25.0   # lane instructions to classify one visibility-grid column (SURVEY [A5]: ~25 per cell)
+I_UNIT = 25.0     # lane instructions to cut one (row, z-cell) unit of inside columns (2 vertical cuts, 4 loads)
 I_SPHERE = 8.0    # collision sphere reject per candidate pair (3 FADD, 3 FMA, compare, branch)
 KERNEL = {("visibility_gain", "culled"): "k_gain_culled", ("collision", "culled"): "k_col_culled",
           ("visibility_gain", "dense"): "k_gain_dense", ("collision", "dense"): "k_col_dense",
@@ -359,7 +366,7 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, tra
         if mode == "dense":
             lane_instr = n_info * float(wl.N) * I_TEST
         else:
-            lane_instr = n_info * (I_TEST * work["tested"] + I_COLUMN * work["columns"])
+            lane_instr = n_info * (I_TEST * work["tested"] + I_UNIT * work["units"])
     else:
         lane_instr = wl.K * wl.T * (work["col_tested"] if work else 0.0) * I_SPHERE
     ach = lane_instr / (ms / 1e3) / 1e12

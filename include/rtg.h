@@ -126,11 +126,15 @@ typedef struct {
     long long index;     /* index_base + local index, -1 when none   */
 } rtg_best_result;
 
-/* Grid options for rtg_map_create_ex; any field <= 0 selects the default. */
+/* Grid options for rtg_map_create_ex; any field <= 0 selects the default.  The visibility
+ * grid has rows of height gain_cell_xy along y, cells of width gain_cell_x along x and
+ * z-cells of height gain_cell_z (the culled gain kernel tests individually only Gaussians of
+ * cells that straddle the frustum, so thinner rows mean fewer tests but more rows). */
 typedef struct {
-    float gain_cell_xy;  /* visibility grid column width [m]   (default 0.5)               */
-    float gain_cell_z;   /* visibility grid cell height [m]    (default 0.5)               */
-    float col_cell;      /* collision grid cell edge [m]       (default max(0.5, r_b/2))   */
+    float gain_cell_xy;  /* visibility grid row height (y) [m]    (default 0.25)           */
+    float gain_cell_z;   /* visibility grid cell height (z) [m]   (default 1.0)            */
+    float col_cell;      /* collision grid cell edge [m]          (default max(0.5, r_b/2)) */
+    float gain_cell_x;   /* visibility grid cell width (x) [m]    (default gain_cell_xy/2) */
 } rtg_map_options;
 
 /* Read-only facts about a built map (rtg_map_info). */
@@ -221,8 +225,9 @@ rtg_status rtg_best(const double* utility, int K, long long index_base, void* st
  * pair_mask (or NULL): ceil(K*T*N/32) words, bit (i*N + g) = waypoint i collides with
  * Gaussian g (original index), only when K*T*N <= 2^32.  stats (host, or NULL): 8 counters
  * {collision pairs FP64-redecided, visibility pairs FP64-redecided, visibility pairs tested
- * individually, z-cells added whole, collision candidates tested, visibility pairs tested in
- * horizontally straddling columns, columns classified, individually tested pairs visible}
+ * individually, (row, z-cell) x-runs added whole, collision candidates tested, visibility pairs
+ * tested in the horizontally straddling flanks of rows, (row, z-cell) units cut, individually
+ * tested pairs visible}
  * (culled mode; dense mode fills the first two).  Synchronises the stream.
  */
 rtg_status rtg_score_debug(rtg_map map, rtg_traj traj, const rtg_camera* cam,

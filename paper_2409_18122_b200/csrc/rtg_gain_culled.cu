@@ -1,20 +1,30 @@
 // rtg_gain_culled.cu -- exact culled visibility + information gain.
 //
 // One warp per info waypoint (persistent warps pull waypoints from an atomic counter in
-// (k, t) order, so neighbouring warps share frusta and L1/L2 lines).  Per waypoint:
-//   1. the frustum's xy footprint is the trapezoid {z_near <= Z <= z_far, -kxl Z <= X <= kxr Z};
-//      lanes take the visibility-grid rows it covers and clip the trapezoid to each row band;
-//   2. lanes take the covered columns (load-balanced over rows).  A column's square is tested
-//      against the linear horizontal constraints (centre +- radius); for a column entirely
-//      inside, the z-cells whose whole height is inside the vertical wedge at the column's
-//      smallest depth are summed from the exact fixed-point prefix records (two loads), the
-//      z-cells the wedge may cut form at most two contiguous record runs; a straddling column
-//      contributes one run (its candidate z-range);
-//   3. the runs' Gaussians are tested one by one with the shared exact pair test (FP32 +
-//      FP64 re-decision), lanes load-balanced over the union of the runs.
-// All sums are integers (fixed-point u, packed class counts): exact and order free, so the
-// result is bit-identical to the dense kernel.
+// (k, t) order, so neighbouring warps share frusta and L1/L2 lines).  The frustum is six linear
+// constraints f_j(p) = a_j dx + b_j dy + g_j dz + d_j >= 0 (the pinhole slacks of O3: near, far,
+// two side planes through the camera centre, top and bottom); over a grid cell (box) the
+// minimum / maximum of each is its centre value -/+ a radius, and along a grid row the centre
+// value is linear in the x-cell index, so the cells of a row that are possibly visible / fully
+// inside form index intervals found with one division per constraint.  Per waypoint:
+//   1. lanes take the grid rows (y bands) the frustum's footprint covers; per row the four
+//      horizontal constraints give the x-interval P of possibly visible columns and its
+//      sub-interval I of columns whose whole column box is horizontally inside;
+//   2. the flanks P \ I are tested Gaussian by Gaussian from record copy A (sorted by
+//      (row, x-cell)): each flank is ONE contiguous record run (all z);
+//   3. the inside columns I are walked z-cell by z-cell from copy B (sorted by (row, z-cell,
+//      x-cell), so a row's z-slab is x-contiguous): per (row, z-cell) unit the two vertical
+//      constraints cut I into an x-run fully inside (added from exact per-record prefixes: two
+//      loads) and at most two straddling x-runs (tested); the z-cells a row can see come from
+//      the vertical wedge at the row's largest depth and the row's occupied z-range;
+//   4. tested runs go to a per-warp queue and are tested 32 Gaussians per warp instruction
+//      regardless of run lengths (run owner of each lane from a ballot-OR of run heads), with
+//      the shared exact pair test (FP32 + FP64 re-decision inside the proven guard band).
+// Sums are exact integers (u_q in FP64 below 2^53; packed class counts): order free, so the
+// result is bit-identical to the dense kernel.  eps (>> FP32 error of the cell tests) keeps
+// "inside" strictly inside and "possible" a superset.
 #include <cfloat>
+#include <climits>
 
 #include "rtg_host.hpp"
 
@@ -23,42 +33,69 @@ namespace {
 
 constexpr unsigned kFullG = 0xffffffffu;
 constexpr int kWarpsG = 8;
+constexpr int kQCap = 256;    // queued runs per warp
+constexpr int kQFlush = 192;  // test the queue once more runs than this are waiting (an append adds <= 64)
 
 struct GainK {
-    float ox, oy, oz, h, hz, hh, eps, inv_h, inv_hz;
-    int nx, ny, nz;
+    float ox, oy, oz, hx, hy, hz, inv_hz, eps;
+    int nx, ny, nz, nxb, offB;
     float zn, zf, kxl, kxr, kyu, kyd, kxh;
 };
 
-constexpr int kLongRun = 16;   // runs at least this long are tested run by run, whole warp
-
-// acc += q and pc += inc when p (predicated adds, no selects)
-__device__ __forceinline__ void add_if(bool p, long long& acc, long long q, int& pc, int inc) {
-    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.s64 %0, %0, %2;\n\t@pp add.s32 %1, %1, %3;\n\t}"
-        : "+l"(acc), "+r"(pc)
-        : "l"(q), "r"(inc), "r"((int)p));
-}
+#ifndef RTG_GAIN_MINB
+#define RTG_GAIN_MINB 4
+#endif
 
 __device__ __forceinline__ int fcell(float v, int hi) {   // floor of v clamped to [-1, hi + 1]
     v = fminf(fmaxf(v, -1.0f), (float)hi + 1.0f);
     return (int)floorf(v);
 }
 
+// constraint j seen by grid cell (ix, iy, iz): centre value = A ix + B iy + G iz + K, box radius r;
+// stored as {K, B, inv = 1/A, e = eps + r} (G = 0 for the horizontal ones, -+hz for top / bottom).
+// cut() tightens [plo, phi] (possibly visible: A ix >= -e - Cj) and [ilo, ihi] (inside:
+// A ix >= e - Cj) with Cj the centre value at ix = 0.
+__device__ __forceinline__ void cut(const float4& C, float Cj, float& plo, float& phi, float& ilo, float& ihi) {
+    const float tp = (-C.w - Cj) * C.z, ti = (C.w - Cj) * C.z;
+    if (C.z > 0.f) {
+        plo = fmaxf(plo, ceilf(tp));
+        ilo = fmaxf(ilo, ceilf(ti));
+    } else {
+        phi = fminf(phi, floorf(tp));
+        ihi = fminf(ihi, floorf(ti));
+    }
+}
+
+// acc += q, pc += inc when p (predicated: no selects in the hot loop)
+__device__ __forceinline__ void add_if(bool p, double& acc, double q, int& pc, int inc) {
+    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.f64 %0, %0, %2;\n\t@pp add.s32 %1, %1, %3;\n\t}"
+        : "+d"(acc), "+r"(pc)
+        : "d"(q), "r"(inc), "r"((int)p));
+}
+
 template <bool kStats>
-__global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
+__global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
-    const GRec* __restrict__ grec, const long long* __restrict__ guq, const int* __restrict__ gstart,
-    const CellAgg* __restrict__ agg, const GainK g, const CamK cam,
-    long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl, int* __restrict__ counter,
-    unsigned long long* __restrict__ stats) {
-    __shared__ double s_cs[kWarpsG][2];     // FP64 cos, sin of the waypoint's yaw (re-decisions)
-    __shared__ float s_k[kWarpsG][8];       // per-waypoint column-test constants
-    __shared__ float s_v[kWarpsG][8];       // footprint vertices (x0..x3, y0..y3)
+    const GRec* __restrict__ grec, const double* __restrict__ guq, const int* __restrict__ gstartA,
+    const int* __restrict__ gtabB, const int2* __restrict__ zocc, const TabP* __restrict__ gtabP, const GainK g,
+    const CamK cam, long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
+    int* __restrict__ counter, unsigned long long* __restrict__ stats) {
+    __shared__ double s_cs[kWarpsG][2];      // FP64 cos, sin of the waypoint's yaw (re-decisions)
+    __shared__ float4 s_con[kWarpsG][6];     // the frustum's constraints on grid cells
+    __shared__ float s_v[kWarpsG][8];        // footprint vertices (x0..x3, y0..y3), grid-relative
+    // queued test runs: first record -> (first record - items before the run); length -> items before
+    // the run.  64 entries of padding hold INT_MAX while the queue is tested.
+    __shared__ __align__(16) int s_st[kWarpsG][kQCap + 64];
+    __shared__ __align__(16) int s_ex[kWarpsG][kQCap + 64];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lanes_lt = (1u << lane) - 1u;
+    const unsigned lanes_le = (2u << lane) - 1u;
+    int* const qs = s_st[wid];
+    int* const qe = s_ex[wid];
     const int L = *list_count;
     unsigned nref = 0;
-    unsigned long long ntest = 0, nagg = 0, ncol = 0, nstr = 0, nvis = 0;
+    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0;
     for (;;) {
         int e = 0;
         if (lane == 0) e = atomicAdd(counter, 1);
@@ -66,8 +103,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
         if (e >= L) break;
         const int i = list[e];
         const float px = X[i], py = Y[i], pz = Zw[i], yw = Yaw[i];
-        long long accq = 0;
-        int acch = 0, accl = 0;
+        double acc = 0.0;            // sum of u_q over visible Gaussians (exact integer)
+        int acch = 0, accl = 0, pc = 0;
         if (isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(yw)) {
             WpF f;
             {
@@ -80,191 +117,276 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
                     s_v[wid][lane] = fmaf(zz, fmaf(kk, f.s, f.c), qx);
                     s_v[wid][4 + lane] = fmaf(zz, fmaf(-kk, f.c, f.s), qy);
                 }
+                if (lane < 6) {
+                    // Z = c dx + s dy, X' = ax dx + bx dy (X - kxc Z), constraint j:
+                    //   0: Z - zn  1: zf - Z  2: kxh Z - X'  3: kxh Z + X'  4: kyu Z - dz  5: kyd Z + dz
+                    float a, b, gz = 0.f, d = 0.f;
+                    if (lane == 0) { a = f.c; b = f.s; d = -g.zn; }
+                    else if (lane == 1) { a = -f.c; b = -f.s; d = g.zf; }
+                    else if (lane == 2) { a = fmaf(g.kxh, f.c, -f.ax); b = fmaf(g.kxh, f.s, -f.bx); }
+                    else if (lane == 3) { a = fmaf(g.kxh, f.c, f.ax); b = fmaf(g.kxh, f.s, f.bx); }
+                    else if (lane == 4) { a = g.kyu * f.c; b = g.kyu * f.s; gz = -1.f; }
+                    else { a = g.kyd * f.c; b = g.kyd * f.s; gz = 1.f; }
+                    // cell-centre offsets from the waypoint at index 0
+                    const float X0 = fmaf(0.5f, g.hx, -qx), Y0 = fmaf(0.5f, g.hy, -qy);
+                    const float Z0 = fmaf(0.5f, g.hz, g.oz - pz);
+                    const float A = a * g.hx, B = b * g.hy;
+                    s_con[wid][lane] = make_float4(fmaf(a, X0, fmaf(b, Y0, fmaf(gz, Z0, d))), B,
+                                                   fabsf(A) > 1e-30f ? 1.0f / A : 1e30f,
+                                                   g.eps + 0.5f * (fabsf(A) + fabsf(B) + fabsf(gz) * g.hz));
+                }
                 if (lane == 0) {
                     s_cs[wid][0] = cs;
                     s_cs[wid][1] = sn;
-                    // column-test radii of the linear functions Z, kxh Z -+ X' over an h x h square
-                    s_k[wid][0] = (fabsf(f.c) + fabsf(f.s)) * g.hh;
-                    s_k[wid][1] = (fabsf(fmaf(g.kxh, f.c, -f.ax)) + fabsf(fmaf(g.kxh, f.s, -f.bx))) * g.hh;
-                    s_k[wid][2] = (fabsf(fmaf(g.kxh, f.c, f.ax)) + fabsf(fmaf(g.kxh, f.s, f.bx))) * g.hh;
-                    s_k[wid][3] = qx;
-                    s_k[wid][4] = qy;
-                    s_k[wid][5] = pz - g.oz;
                 }
                 __syncwarp();
             }
             const float ymn = fminf(fminf(s_v[wid][4], s_v[wid][5]), fminf(s_v[wid][6], s_v[wid][7])) - g.eps;
             const float ymx = fmaxf(fmaxf(s_v[wid][4], s_v[wid][5]), fmaxf(s_v[wid][6], s_v[wid][7])) + g.eps;
-            const int iy0 = max(0, fcell(ymn * g.inv_h, g.ny));
-            const int iy1 = min(g.ny - 1, fcell(ymx * g.inv_h, g.ny));
-            for (int rbase = iy0; rbase <= iy1; rbase += 32) {
-                const int iy = rbase + lane;
-                int ixlo = 0, len = 0;
-                if (iy <= iy1) {
-                    const float yb0 = iy * g.h - g.eps, yb1 = (iy + 1) * g.h + g.eps;
-                    float xlo = FLT_MAX, xhi = -FLT_MAX;
-#pragma unroll
-                    for (int ed = 0; ed < 4; ++ed) {
-                        const float ax = s_v[wid][ed], ay = s_v[wid][4 + ed];
-                        const float bx = s_v[wid][(ed + 1) & 3], by = s_v[wid][4 + ((ed + 1) & 3)];
-                        const float elo = fminf(ay, by), ehi = fmaxf(ay, by);
-                        if (ehi < yb0 || elo > yb1) continue;
-                        float xa = ax, xb = bx;
-                        if (ehi - elo > 1e-12f) {
-                            const float inv = __fdividef(1.0f, by - ay);
-                            xa = fmaf((fmaxf(yb0, elo) - ay) * inv, bx - ax, ax);
-                            xb = fmaf((fminf(yb1, ehi) - ay) * inv, bx - ax, ax);
-                        }
-                        xlo = fminf(xlo, fminf(xa, xb));
-                        xhi = fmaxf(xhi, fmaxf(xa, xb));
-                    }
-                    if (xlo <= xhi) {
-                        const int ix0 = max(0, fcell((xlo - g.eps) * g.inv_h, g.nx));
-                        const int ix1 = min(g.nx - 1, fcell((xhi + g.eps) * g.inv_h, g.nx));
-                        if (ix0 <= ix1) {
-                            ixlo = ix0;
-                            len = ix1 - ix0 + 1;
-                        }
-                    }
-                }
-                int incl = len;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(kFullG, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const int total = __shfl_sync(kFullG, incl, 31);
-                const int roff = ixlo - (incl - len);
-                for (int cb = 0; cb < total; cb += 32) {
-                    const int pos = cb + lane;
-                    // row owning column position pos: first lane whose inclusive prefix exceeds it
-                    int owner = 0;
+            const float inv_hy = 1.0f / g.hy;
+            const int iy0 = max(0, fcell(ymn * inv_hy, g.ny));
+            const int iy1 = min(g.ny - 1, fcell(ymx * inv_hy, g.ny));
+            const float zrel = pz - g.oz;
+            // producer / consumer loop: each pass produces one row chunk (32 rows: flank runs) or
+            // one window of 32 (row, z-cell) units (aggregates + straddling runs), queues the
+            // runs, and tests the queue once it holds more than kQFlush runs (all of it at the end)
+            int nq = 0;                      // queued runs (warp-uniform)
+            int rnext = iy0, rcur = 0;       // next / current row chunk
+            int U = 0, ub = 0;               // units of the current chunk, next unit window
+            int incl = 0, zoff = 0, ri0 = 0, ri1 = 0;   // lane's row of the current chunk
+            for (;;) {
+                int s0 = 0, l0 = 0, s1 = 0, l1 = 0;
+                bool done = false;
+                if (ub < U) {
+                    // ---- unit window: (row, z-cell) units ub .. ub + 31 of the current chunk
+                    const int pos = ub + lane;
+                    int owner = 0;   // first lane whose inclusive prefix exceeds pos
 #pragma unroll
                     for (int st = 16; st > 0; st >>= 1) {
                         const int v = __shfl_sync(kFullG, incl, owner + st - 1);
                         if (v <= pos) owner += st;
                     }
-                    const int ix = pos + __shfl_sync(kFullG, roff, owner);
-                    int b0 = 0, l0 = 0, b1 = 0, l1 = 0;
-                    if (pos < total) {
-                        const int cy = rbase + owner;
-                        const float Zr = s_k[wid][0], f1r = s_k[wid][1], f2r = s_k[wid][2];
-                        const float zrel = s_k[wid][5];
-                        const float xc = fmaf((float)ix + 0.5f, g.h, -s_k[wid][3]);
-                        const float yc = fmaf((float)cy + 0.5f, g.h, -s_k[wid][4]);
-                        const float Zc = fmaf(f.c, xc, f.s * yc);
-                        const float Xc = fmaf(f.ax, xc, f.bx * yc);
-                        const float f1c = fmaf(g.kxh, Zc, -Xc), f2c = fmaf(g.kxh, Zc, Xc);
-                        const float Zmin = Zc - Zr, Zmax = Zc + Zr;
-                        const bool out = (Zmax < g.zn - g.eps) | (Zmin > g.zf + g.eps) | (f1c + f1r < -g.eps) |
-                                         (f2c + f2r < -g.eps);
-                        if (!out) {
-                            const bool in_h = (Zmin >= g.zn + g.eps) & (Zmax <= g.zf - g.eps) &
-                                              (f1c - f1r >= g.eps) & (f2c - f2r >= g.eps);
-                            const float Zhi = fmaxf(fminf(Zmax, g.zf), 0.0f);
-                            int c = fcell((zrel - g.kyd * Zhi - g.eps) * g.inv_hz, g.nz);
-                            int dd = fcell((zrel + g.kyu * Zhi + g.eps) * g.inv_hz, g.nz) + 1;
-                            c = min(max(c, 0), g.nz);
-                            dd = min(max(dd, c), g.nz);
-                            int a = c, b = c;
-                            if (in_h) {
-                                const float za = fminf(fmaxf((zrel - g.kyd * Zmin + g.eps) * g.inv_hz, -1.0f), g.nz + 1.0f);
-                                const float zb = fminf(fmaxf((zrel + g.kyu * Zmin - g.eps) * g.inv_hz, -1.0f), g.nz + 1.0f);
-                                a = min(max((int)ceilf(za), c), dd);
-                                b = min(max((int)floorf(zb), a), dd);
-                            }
-                            // x-fastest tables: entry (cy, iz, ix) at (cy*(nz+1) + iz)*nx + ix
-                            const int base = cy * (g.nz + 1) * g.nx + ix;
-                            const int sc = gstart[base + c * g.nx], sa = gstart[base + a * g.nx];
-                            const int sb = gstart[base + b * g.nx], sd = gstart[base + dd * g.nx];
-                            if (b > a) {
-                                const CellAgg hi = agg[base + b * g.nx], lo = agg[base + a * g.nx];
-                                accq += hi.q - lo.q;
-                                const long long hl = hi.hl - lo.hl;
-                                acch += (int)(hl & 0xffffffffLL);
-                                accl += (int)(hl >> 32);
-                                if (kStats) nagg += (unsigned long long)(b - a);
-                            }
-                            b0 = sc; l0 = sa - sc;
-                            b1 = sb; l1 = sd - sb;
-                            if (kStats) {
-                                ncol += 1;
-                                if (!in_h) nstr += (unsigned long long)(l0 + l1);
-                            }
-                        }
-                    }
-                    // individual tests over this chunk's runs
-                    if (kStats) ntest += (unsigned long long)(l0 + l1);
-                    int pc = 0;
-                    auto test = [&](int gi) {
-                        const GRec G = grec[gi];
-                        const long long q = guq[gi];
-                        const bool v = visible_cs(f, cam, G.x, G.y, G.z, s_cs[wid], nref);
-                        add_if(v, accq, q, pc, G.inc);
-                        if (kStats) nvis += v;
-                    };
-                    // (1) long runs (straddling columns, mostly): one run at a time across the
-                    //     whole warp, consecutive records per lane, no per-position search
+                    const int iz = pos + __shfl_sync(kFullG, zoff, owner);
+                    const int ui0 = __shfl_sync(kFullG, ri0, owner), ui1 = __shfl_sync(kFullG, ri1, owner);
+                    const int uy = rcur + owner;
+                    const float fuy = (float)uy, fiz = (float)iz;
+                    float vplo = (float)ui0, vphi = (float)ui1, vilo = vplo, vihi = vphi;
                     {
-                        const unsigned lm0 = __ballot_sync(kFullG, l0 >= kLongRun);
-                        const unsigned lm1 = __ballot_sync(kFullG, l1 >= kLongRun);
-#pragma unroll
-                        for (int pass = 0; pass < 2; ++pass) {
-                            unsigned lm = pass ? lm1 : lm0;
-                            const int bb = pass ? b1 : b0, ll = pass ? l1 : l0;
-                            while (lm) {
-                                const int j = __ffs(lm) - 1;
-                                lm &= lm - 1;
-                                const int start = __shfl_sync(kFullG, bb, j);
-                                const int len = __shfl_sync(kFullG, ll, j);
-                                for (int o = lane; o < len; o += 32) test(start + o);
-                            }
-                        }
-                        if (l0 >= kLongRun) l0 = 0;
-                        if (l1 >= kLongRun) l1 = 0;
+                        const float4 Ct = s_con[wid][4], Cb = s_con[wid][5];
+                        cut(Ct, fmaf(Ct.y, fuy, fmaf(-g.hz, fiz, Ct.x)), vplo, vphi, vilo, vihi);
+                        cut(Cb, fmaf(Cb.y, fuy, fmaf(g.hz, fiz, Cb.x)), vplo, vphi, vilo, vihi);
                     }
-                    // (2) short runs packed into full windows: the owner lane of position gp is
-                    //     the first lane whose inclusive prefix exceeds gp (warp binary search over
-                    //     the prefixes held in registers), then its first or second run
-                    const int sl = l0 + l1;
-                    int ic = sl;
+                    const int q0 = (int)fminf(vplo, (float)g.nx), q1 = pos < U ? (int)vphi : -1;
+                    const int j0 = max((int)fminf(vilo, (float)g.nx), q0), j1 = min((int)vihi, q1);
+                    if (q0 <= q1) {
+                        // z-fastest table: entry (uy, x, iz) at (uy * (nx + 1) + x) * nz + iz
+                        // all lookups independent: one memory round trip per unit
+                        const int ub0 = uy * (g.nx + 1) * g.nz + iz;
+                        const int* sb = gtabB + ub0;
+                        const bool in = j0 <= j1;
+                        const int a0 = __ldg(sb + q0 * g.nz), a3 = __ldg(sb + (q1 + 1) * g.nz);
+                        const int a1 = !in ? a3 : (j0 == q0 ? a0 : __ldg(sb + j0 * g.nz));
+                        const int a2 = !in ? a3 : (j1 == q1 ? a3 : __ldg(sb + (j1 + 1) * g.nz));
+                        if (in) {
+                            const TabP hi = gtabP[ub0 + (j1 + 1) * g.nz], lo = gtabP[ub0 + j0 * g.nz];
+                            acc += hi.q - lo.q;
+                            acch += hi.nh - lo.nh;
+                            accl += hi.nl - lo.nl;
+                            if (kStats) nagg += 1;
+                        }
+                        s0 = g.offB + a0;
+                        l0 = a1 - a0;
+                        s1 = g.offB + a2;
+                        l1 = a3 - a2;
+                    }
+                    if (kStats) nunit += pos < U;
+                    ub += 32;
+                } else if (rnext <= iy1) {
+                    // ---- row chunk: rows rnext .. rnext + 31, horizontal intervals
+                    rcur = rnext;
+                    rnext += 32;
+                    const int iy = rcur + lane;
+                    const float fiy = (float)iy;
+                    float plo = 0.f, phi = (float)(g.nx - 1), ilo = 0.f, ihi = phi;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float4 C = s_con[wid][j];
+                        cut(C, fmaf(C.y, fiy, C.x), plo, phi, ilo, ihi);
+                    }
+                    const int p0 = (int)fminf(plo, (float)g.nx);
+                    const int p1 = iy <= iy1 ? (int)phi : -1;
+                    ri0 = max((int)fminf(ilo, (float)g.nx), p0);
+                    ri1 = min((int)ihi, p1);
+                    int nu = 0, izlo = 0;
+                    if (p0 <= p1) {
+                        // flanks P \ I of copy A (one run when I is empty)
+                        const int* sa = gstartA + iy * g.nx;
+                        const bool in = ri0 <= ri1;
+                        s0 = __ldg(sa + p0);
+                        l0 = __ldg(sa + (in ? ri0 : p1 + 1)) - s0;
+                        if (in) {
+                            s1 = __ldg(sa + ri1 + 1);
+                            l1 = __ldg(sa + p1 + 1) - s1;
+                            // z-cells the inside columns can see: vertical wedge at their largest
+                            // depth, cut to the occupied z-range of the x-blocks they span
+                            const float4 Cn = s_con[wid][0];
+                            const float F0 = fmaf(Cn.y, fiy, Cn.x);
+                            const float An = 1.0f / Cn.z;
+                            const float Zmax =
+                                fminf(fmaxf(fmaf(An, (float)ri0, F0), fmaf(An, (float)ri1, F0)) + Cn.w + g.zn,
+                                      g.zf + g.eps);
+                            const int zlo = fcell((zrel - g.kyd * Zmax - g.eps) * g.inv_hz, g.nz);
+                            const int zhi = fcell((zrel + g.kyu * Zmax + g.eps) * g.inv_hz, g.nz);
+                            int olo = INT_MAX, ohi = -1;
+                            const int2* zo = zocc + iy * g.nxb;
+                            for (int b = ri0 / kZoccX; b <= ri1 / kZoccX; ++b) {
+                                const int2 o = __ldg(zo + b);
+                                olo = min(olo, o.x);
+                                ohi = max(ohi, o.y);
+                            }
+                            izlo = max(zlo, olo);
+                            nu = max(0, min(zhi, ohi) - izlo + 1);
+                        }
+                        if (kStats) nflank += (unsigned long long)(l0 + l1);
+                    }
+                    incl = nu;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
-                        const int v = __shfl_up_sync(kFullG, ic, o);
-                        if (lane >= o) ic += v;
+                        const int v = __shfl_up_sync(kFullG, incl, o);
+                        if (lane >= o) incl += v;
                     }
-                    const int tot = __shfl_sync(kFullG, ic, 31);
-                    const int ex = ic - sl;
-                    for (int gb = 0; gb < tot; gb += 32) {
-                        const int gp = gb + lane;
-                        int lo = 0;
+                    U = __shfl_sync(kFullG, incl, 31);
+                    zoff = izlo - (incl - nu);
+                    ub = 0;
+                } else {
+                    done = true;
+                }
+                // ---- queue this lane's (<= 2) runs
+                {
+                    const bool c0 = l0 > 0, c1 = l1 > 0;
+                    const unsigned b0 = __ballot_sync(kFullG, c0), b1 = __ballot_sync(kFullG, c1);
+                    int slot = nq + __popc(b0 & lanes_lt) + __popc(b1 & lanes_lt);
+                    if (c0) {
+                        qs[slot] = s0;
+                        qe[slot] = l0;
+                        ++slot;
+                    }
+                    if (c1) {
+                        qs[slot] = s1;
+                        qe[slot] = l1;
+                    }
+                    nq += __popc(b0) + __popc(b1);
+                }
+                if (nq > kQFlush || (done && nq > 0)) {
+                    // ---- test every queued item, 64 per pass (two per lane)
+                    __syncwarp();
+                    int tot;
+                    {
+                        // items before each run (lane j: runs 8j .. 8j+7, then a warp scan); the
+                        // start becomes start - items before, so item p of run r is record p + qs[r]
+                        int4 la = *reinterpret_cast<const int4*>(qe + 8 * lane);
+                        int4 lb = *reinterpret_cast<const int4*>(qe + 8 * lane + 4);
+                        int4 sa = *reinterpret_cast<const int4*>(qs + 8 * lane);
+                        int4 sb = *reinterpret_cast<const int4*>(qs + 8 * lane + 4);
+                        const int r8 = nq - 8 * lane;   // runs of this lane that exist: min(8, max(0, r8))
+                        if (r8 < 1) la.x = 0;
+                        if (r8 < 2) la.y = 0;
+                        if (r8 < 3) la.z = 0;
+                        if (r8 < 4) la.w = 0;
+                        if (r8 < 5) lb.x = 0;
+                        if (r8 < 6) lb.y = 0;
+                        if (r8 < 7) lb.z = 0;
+                        if (r8 < 8) lb.w = 0;
+                        const int sum = la.x + la.y + la.z + la.w + lb.x + lb.y + lb.z + lb.w;
+                        int sc = sum;
 #pragma unroll
-                        for (int st = 16; st > 0; st >>= 1) {
-                            const int v = __shfl_sync(kFullG, ic, lo + st - 1);
-                            if (v <= gp) lo += st;
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int v = __shfl_up_sync(kFullG, sc, o);
+                            if (lane >= o) sc += v;
                         }
-                        const int eo = gp - __shfl_sync(kFullG, ex, lo);
-                        const int lo0 = __shfl_sync(kFullG, l0, lo);
-                        const int bo0 = __shfl_sync(kFullG, b0, lo);
-                        const int bo1 = __shfl_sync(kFullG, b1, lo);
-                        const int gi = eo < lo0 ? bo0 + eo : bo1 + (eo - lo0);
-                        if (gp < tot) test(gi);
+                        tot = __shfl_sync(kFullG, sc, 31);
+                        int4 ea, eb;
+                        ea.x = sc - sum;
+                        ea.y = ea.x + la.x;
+                        ea.z = ea.y + la.y;
+                        ea.w = ea.z + la.z;
+                        eb.x = ea.w + la.w;
+                        eb.y = eb.x + lb.x;
+                        eb.z = eb.y + lb.y;
+                        eb.w = eb.z + lb.z;
+                        sa.x -= ea.x; sa.y -= ea.y; sa.z -= ea.z; sa.w -= ea.w;
+                        sb.x -= eb.x; sb.y -= eb.y; sb.z -= eb.z; sb.w -= eb.w;
+                        *reinterpret_cast<int4*>(qe + 8 * lane) = ea;
+                        *reinterpret_cast<int4*>(qe + 8 * lane + 4) = eb;
+                        *reinterpret_cast<int4*>(qs + 8 * lane) = sa;
+                        *reinterpret_cast<int4*>(qs + 8 * lane + 4) = sb;
+                        __syncwarp();
+                        qe[nq + lane] = INT_MAX;
+                        qe[nq + 32 + lane] = INT_MAX;
+                        __syncwarp();
                     }
-                    acch += pc & 0xffff;
-                    accl += pc >> 16;
+                    int r0 = 0;   // run holding item gb
+                    for (int gb0 = 0; gb0 < tot; gb0 += 64 * 16384) {   // class counts: flushed every 16384 passes
+                        const int gend = min(tot, gb0 + 64 * 16384);
+                        for (int gb = gb0; gb < gend; gb += 64) {
+                            // runs r0+1 .. r0+64 start at positions pa, pb (relative to gb) >= 1
+                            const int ra = r0 + 1 + lane;
+                            const int pa = qe[ra] - gb, pb = qe[ra + 32] - gb;
+                            const unsigned hlo = __reduce_or_sync(kFullG, pa < 32 ? 1u << pa : 0u);
+                            const unsigned ua = (unsigned)(pa - 32), ubb = (unsigned)(pb - 32);
+                            const unsigned hhi = __reduce_or_sync(
+                                kFullG, (ua < 32u ? 1u << ua : 0u) | (ubb < 32u ? 1u << ubb : 0u));
+                            const int na = __popc(hlo);
+                            const int gpa = gb + lane, gpb = gpa + 32;
+                            const int gia = gpa + qs[r0 + __popc(hlo & lanes_le)];
+                            const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_le)];
+                            const GRec Ga = grec[gia], Gb = grec[gib];
+                            const double qa = guq[gia], qb = guq[gib];
+                            float Za, Zb;
+                            const float ma = vis_margin(f, cam, Ga.x, Ga.y, Ga.z, Za);
+                            const float mb = vis_margin(f, cam, Gb.x, Gb.y, Gb.z, Zb);
+                            bool visa = ma >= 0.0f, visb = mb >= 0.0f;
+                            const bool amba = fabsf(ma) < fmaf(cam.gam, Za, cam.g0);
+                            const bool ambb = fabsf(mb) < fmaf(cam.gam, Zb, cam.g0);
+                            if (__any_sync(kFullG, amba || ambb)) {
+                                if (amba) {
+                                    visa = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], Ga.x, Ga.y,
+                                                           Ga.z, cam.cam64);
+                                    ++nref;
+                                }
+                                if (ambb) {
+                                    visb = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], Gb.x, Gb.y,
+                                                           Gb.z, cam.cam64);
+                                    ++nref;
+                                }
+                            }
+                            visa = visa && gpa < tot;
+                            visb = visb && gpb < tot;
+                            add_if(visa, acc, qa, pc, Ga.inc);
+                            add_if(visb, acc, qb, pc, Gb.inc);
+                            if (kStats) nvis += (unsigned)visa + (unsigned)visb;
+                            r0 += na + __popc(hhi) + (__any_sync(kFullG, pa == 64 || pb == 64) ? 1 : 0);
+                        }
+                        acch += pc & 0xffff;
+                        accl += pc >> 16;
+                        pc = 0;
+                    }
+                    if (kStats) ntest += (unsigned long long)tot;
+                    nq = 0;
                     __syncwarp();
                 }
+                if (done) break;
             }
         }
-        // warp totals (integers: exact, order-free)
+        // warp totals (exact: integers below 2^53)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            accq += __shfl_xor_sync(kFullG, accq, o);
+            acc += __shfl_xor_sync(kFullG, acc, o);
             acch += __shfl_xor_sync(kFullG, acch, o);
             accl += __shfl_xor_sync(kFullG, accl, o);
         }
         if (lane == 0) {
-            wp_gq[i] = accq;
+            wp_gq[i] = (long long)acc;
             wp_nh[i] = acch;
             wp_nl[i] = accl;
         }
@@ -275,16 +397,16 @@ __global__ void __launch_bounds__(kWarpsG * 32, 4) k_gain_culled(
         for (int o = 16; o > 0; o >>= 1) {
             ntest += __shfl_xor_sync(kFullG, ntest, o);
             nagg += __shfl_xor_sync(kFullG, nagg, o);
-            ncol += __shfl_xor_sync(kFullG, ncol, o);
-            nstr += __shfl_xor_sync(kFullG, nstr, o);
+            nunit += __shfl_xor_sync(kFullG, nunit, o);
+            nflank += __shfl_xor_sync(kFullG, nflank, o);
             nvis += __shfl_xor_sync(kFullG, nvis, o);
         }
         if (lane == 0) {
             if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
-            atomicAdd(&stats[2], ntest);
+            atomicAdd(&stats[2], ntest / 32);   // every lane counted the warp's items
             atomicAdd(&stats[3], nagg);
-            atomicAdd(&stats[5], nstr);
-            atomicAdd(&stats[6], ncol);
+            atomicAdd(&stats[5], nflank);
+            atomicAdd(&stats[6], nunit);
             atomicAdd(&stats[7], nvis);
         }
     }
@@ -297,18 +419,28 @@ int g_sms_g = 0, g_occ_g = 0;
 cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, const int* list, const int* count,
                                long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl, int* counter,
                                unsigned long long* stats, cudaStream_t st) {
+    if (m->n_gain == 0) {   // nothing is visible: zero sums
+        cudaError_t e = cudaMemsetAsync(wp_gq, 0, sizeof(long long) * (size_t)tr->K * tr->T, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(wp_nh, 0, sizeof(int) * (size_t)tr->K * tr->T, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(wp_nl, 0, sizeof(int) * (size_t)tr->K * tr->T, st);
+        return e;
+    }
     if (!g_sms_g) {
         cudaDeviceGetAttribute(&g_sms_g, cudaDevAttrMultiProcessorCount, m->device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false>, kWarpsG * 32, 0);
         if (g_occ_g < 1) g_occ_g = 1;
     }
+    const GainGrid& gg = m->gg;
     GainK g;
-    g.ox = m->gg.ox; g.oy = m->gg.oy; g.oz = m->gg.oz; g.h = m->gg.hxy; g.hz = m->gg.hz; g.hh = 0.5f * m->gg.hxy;
-    g.inv_h = 1.0f / m->gg.hxy; g.inv_hz = 1.0f / m->gg.hz;
-    double ext = fmax(fmax(fabs(g.ox), fabs(g.oy)), fabs(g.oz)) +
-                 (double)(m->gg.nx + m->gg.ny + m->gg.nz) * fmax(m->gg.hxy, m->gg.hz) + cam.zmid + cam.zhalf;
-    g.eps = (float)(1e-3 + 256.0 * ldexp(1.0, -24) * ext);   // >> FP32 error of the cell tests
-    g.nx = m->gg.nx; g.ny = m->gg.ny; g.nz = m->gg.nz;
+    g.ox = gg.ox; g.oy = gg.oy; g.oz = gg.oz; g.hx = gg.hx; g.hy = gg.hy; g.hz = gg.hz;
+    g.inv_hz = 1.0f / gg.hz;
+    g.nx = gg.nx; g.ny = gg.ny; g.nz = gg.nz; g.nxb = gg.nxb;
+    g.offB = (int)m->n_gain_pad;
+    // eps >> the FP32 error of a cell's centre value (a few ulps of the largest term: offsets of
+    // at most the grid extent plus the distance of any waypoint to the grid origin)
+    double ext = fabs(gg.ox) + fabs(gg.oy) + fabs(gg.oz) + gg.nx * (double)gg.hx + gg.ny * (double)gg.hy +
+                 gg.nz * (double)gg.hz + cam.zmid + cam.zhalf;
+    g.eps = (float)(1e-3 + 64.0 * ldexp(1.0, -24) * 2.0 * ext);
     g.zn = cam.zmid - cam.zhalf; g.zf = cam.zmid + cam.zhalf;
     g.kxl = cam.kxh - cam.kxc; g.kxr = cam.kxh + cam.kxc;
     g.kyu = cam.kyh + cam.kyc; g.kyd = cam.kyh - cam.kyc;
@@ -319,12 +451,12 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     if (blocks < 1) blocks = 1;
     if (stats)
         note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
-            wp_gq, wp_nh, wp_nl, counter, stats);
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
+            cam, wp_gq, wp_nh, wp_nl, counter, stats);
     else
         note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartT, m->gaggT, g, cam,
-            wp_gq, wp_nh, wp_nl, counter, stats);
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
+            cam, wp_gq, wp_nh, wp_nl, counter, stats);
     return cudaGetLastError();
 }
 

@@ -30,10 +30,16 @@ struct ClassState {
     int n_eligible;
 };
 
+// visibility grid: rows (hy) x x-cells (hx) x z-cells (hz) over the bounding box of the
+// gain-eligible means.  Two record copies are sorted by it: copy A by (iy, ix) (whole columns,
+// used for the horizontally straddling flanks of a row), copy B by (iy, iz, ix) (a row's z-slab
+// is x-contiguous, used for the horizontally inside part of a row, z-cell by z-cell).
 struct GainGrid {
-    float ox, oy, oz, hxy, hz;
+    float ox, oy, oz, hx, hy, hz;
     int nx, ny, nz;
-    long long ncells;
+    int nxb;             // x-blocks of kZoccX cells (z-occupancy table)
+    long long ncellsA;   // ny * nx
+    long long ncellsB;   // ny * nz * nx
 };
 
 struct ColGrid {
@@ -64,17 +70,19 @@ struct rtg_map_s {
     // original-order inputs kept for (re)classification
     float* w_orig = nullptr;             // [n]
     unsigned char* flags = nullptr;      // [n] or null
-    // visibility records (sorted by gain cell), padded to a multiple of kTile with NaN means
+    // visibility records: copy A at [0, n_gain) (sorted by (iy, ix)), padded to n_gain_pad (a
+    // multiple of kTile) with NaN means, then copy B at [n_gain_pad, n_gain_pad + n_gain) (sorted
+    // by (iy, iz, ix)), padded likewise.  guq / gidx are parallel to grec.
     long long n_gain_pad = 0;
-    rtg::GRec* grec = nullptr;
-    long long* guq = nullptr;            // fixed-point u per record
+    rtg::GRec* grec = nullptr;           // [2 * n_gain_pad]
+    double* guq = nullptr;               // fixed-point u per record (an exact integer < 2^53)
     int* gidx = nullptr;                 // original index per record
-    int* gstart = nullptr;               // [ncells+1] first record of each gain cell, (iy, ix, iz) order
-    // culled-kernel tables in x-fastest layout [iy][iz][ix], iz = 0..nz (iz = nz: column end), so
-    // the lanes of a warp, which take neighbouring columns of a row, load neighbouring words
-    long long ntab = 0;                  // ny * (nz + 1) * nx
-    int* gstartT = nullptr;              // [ntab] first record of the cell (end of column at iz = nz)
-    rtg::CellAgg* gaggT = nullptr;       // [ntab] exclusive prefixes (u_q, nH | nL << 32) there
+    int* gstartA = nullptr;              // [ncellsA + 1] first copy-A record of column (iy, ix)
+    int* gtabB = nullptr;                // [ny][nx + 1][nz] first copy-B record (relative to n_gain_pad) of
+                                         // cell (iy, iz, ix); ix = nx: end of the z-slab (iy, iz)
+    int2* zocc = nullptr;                // [ny][nxb] occupied z-cell range {lo, hi} of each row block of
+                                         // kZoccX x-cells (lo > hi: empty)
+    rtg::TabP* gtabP = nullptr;          // [ny][nx + 1][nz] exact exclusive prefixes at the gtabB entries
     rtg::GainGrid gg{};
     // collision records (sorted by collision cell), padded likewise
     long long n_col_pad = 0;

@@ -10,7 +10,8 @@
 //  * visibility: min slack m32 of the folded frustum (|Z - zmid| <= zhalf,
 //    |X - kxc Z| <= kxh Z, |dz - kyc Z| <= kyh Z); pairs with |m32| < gam*Z + g0 are
 //    re-decided in FP64 with the six pinhole slacks (O3).  gam, g0 bound the FP32 error.
-//  * gains: u_q = round(u * 2^S) int64, summed exactly (associative -> order free).
+//  * gains: u_q = round(u * 2^S) with S chosen so that the sum over ALL eligible Gaussians is
+//    < 2^53: every partial sum is an exact integer in FP64 (associative -> order free).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -18,6 +19,7 @@
 namespace rtg {
 
 constexpr int kTile = 512;           // dense-mode Gaussians per smem tile
+constexpr int kZoccX = 64;           // x-cells per block of the visibility grid's z-occupancy table
 
 // ------------------------------------------------------------------ records
 // visibility record (sorted by visibility cell): mean + packed class increment
@@ -27,8 +29,9 @@ struct __align__(16) GRec { float x, y, z; int inc; };
 struct __align__(16) CRec { float x, y, z, rb2; };
 // M rows (FP32): m[0..8] row-major, m[9] = original index (as int bits), pad
 struct __align__(16) CMat { float m[12]; };
-// exact exclusive prefixes at a visibility-cell boundary: sum of u_q and packed (nH | nL << 32)
-struct __align__(16) CellAgg { long long q; long long hl; };
+// exact exclusive prefixes at a copy-B cell boundary (z-fastest table entry): sum of u_q (an
+// integer < 2^53, exact in FP64) and the class counts nH, nL
+struct __align__(16) TabP { double q; int nh, nl; };
 // FP64 M for the re-decision branch (9 used)
 struct CMat64 { double m[9]; };
 

@@ -4,12 +4,13 @@
 //      (P:298-302), M = diag(1/a) R^T (rows: principal axes scaled by 1/a_i), bounding radius
 //      r_b = max_i a_i; stored as FP32 records (+ an FP64 copy of M for the re-decision branch).
 //      Records are placed by a counting sort into two uniform grids:
-//        * visibility grid: columns (hxy x hxy) of z-cells (hz), column-contiguous, gain-eligible
-//          Gaussians only;
+//        * visibility grid: rows (hy) x x-cells (hx) x z-cells (hz), gain-eligible Gaussians only,
+//          two copies: A sorted by (row, x-cell) (whole columns), B by (row, z-cell, x-cell)
+//          (x-contiguous z-slabs) with exact per-record prefixes of u_q and the class counts;
 //        * collision grid: cubic cells (h), x fastest, collidable (non-ground) Gaussians only.
 //  a2  classification over the gain-eligible set in ORIGINAL input order (deterministic FP64
 //      two-pass mean / population std), class increments and exact fixed-point u per
-//      record, and the per-cell exclusive prefixes that let the culled kernel add whole cells.
+//      record, and the exclusive prefixes over copy B that let the culled kernel add whole x-runs.
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -174,20 +175,32 @@ __device__ __forceinline__ int cell_coord(float v, double o, double h, int nmax)
     return c < 0 ? 0 : (c >= nmax ? nmax - 1 : c);
 }
 
+__global__ void k_zocc_init(int2* zocc, long long n) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) zocc[i] = make_int2(INT_MAX, -1);
+}
+
+// cell keys: visibility copy B key (iy, iz, ix) (copy A's (iy, ix) follows from it), collision key
+// (iz, iy, ix); per-cell counts and the occupied z-range of every visibility row
 __global__ void k_keys(long long n, const float* __restrict__ means, const unsigned char* __restrict__ flags,
                        GainGrid gg, ColGrid cg, int* __restrict__ gkey, int* __restrict__ ckey,
-                       int* __restrict__ gcount, int* __restrict__ ccount) {
+                       int* __restrict__ gcountA, int* __restrict__ gcountB, int2* __restrict__ zocc,
+                       int* __restrict__ ccount) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         float x = means[i], y = means[n + i], z = means[2 * n + i];
         unsigned f = flags ? flags[i] : 0u;
         int gk = -1, ck = -1;
         if (!(f & RTG_G_NO_GAIN)) {
-            int ix = cell_coord(x, gg.ox, gg.hxy, gg.nx);
-            int iy = cell_coord(y, gg.oy, gg.hxy, gg.ny);
+            int ix = cell_coord(x, gg.ox, gg.hx, gg.nx);
+            int iy = cell_coord(y, gg.oy, gg.hy, gg.ny);
             int iz = cell_coord(z, gg.oz, gg.hz, gg.nz);
-            gk = (int)(((long long)iy * gg.nx + ix) * gg.nz + iz);
-            atomicAdd(&gcount[gk], 1);
+            gk = (int)(((long long)iy * gg.nz + iz) * gg.nx + ix);
+            atomicAdd(&gcountB[gk], 1);
+            atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);
+            int2* zo = zocc + (long long)iy * gg.nxb + ix / kZoccX;
+            if (iz < zo->x) atomicMin(&zo->x, iz);
+            if (iz > zo->y) atomicMax(&zo->y, iz);
         }
         if (!(f & RTG_G_NO_COLLIDE)) {
             int ix = cell_coord(x, cg.ox, cg.h, cg.nx);
@@ -201,15 +214,23 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
     }
 }
 
+// both visibility copies: A at cursorA (relative to 0), B at offB + cursorB
 __global__ void k_scatter_gain(long long n, const float* __restrict__ means, const int* __restrict__ gkey,
-                               int* __restrict__ cursor, GRec* __restrict__ grec, int* __restrict__ gidx) {
+                               GainGrid gg, int* __restrict__ cursorA, int* __restrict__ cursorB, long long offB,
+                               GRec* __restrict__ grec, int* __restrict__ gidx) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int k = gkey[i];
         if (k < 0) continue;
-        int slot = atomicAdd(&cursor[k], 1);
-        grec[slot] = GRec{means[i], means[n + i], means[2 * n + i], 0};
-        gidx[slot] = (int)i;
+        const long long nzx = (long long)gg.nz * gg.nx;
+        const long long iy = k / nzx, ix = k % gg.nx;
+        const GRec r{means[i], means[n + i], means[2 * n + i], 0};
+        int sa = atomicAdd(&cursorA[iy * gg.nx + ix], 1);
+        int sb = atomicAdd(&cursorB[k], 1);
+        grec[sa] = r;
+        gidx[sa] = (int)i;
+        grec[offB + sb] = r;
+        gidx[offB + sb] = (int)i;
     }
 }
 
@@ -256,13 +277,17 @@ __global__ void k_scatter_col(long long n, const float* __restrict__ means, cons
     }
 }
 
-__global__ void k_pad_gain(GRec* grec, long long* guq, int* gidx, long long from, long long to) {
+// NaN padding of both copies: [from, to) and [offB + from, offB + to)
+__global__ void k_pad_gain(GRec* grec, double* guq, int* gidx, long long from, long long to, long long offB) {
     long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < to) {
         float nan = __int_as_float(0x7fc00000);
-        grec[i] = GRec{nan, nan, nan, 0};
-        guq[i] = 0;
-        gidx[i] = -1;
+        for (int c = 0; c < 2; ++c) {
+            long long j = i + c * offB;
+            grec[j] = GRec{nan, nan, nan, 0};
+            guq[j] = 0.0;
+            gidx[j] = -1;
+        }
     }
 }
 
@@ -386,7 +411,7 @@ __global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassS
         int shift = 0;
         double tot = cnt * umax;
         if (tot > 0.0) {
-            shift = (int)floor(61.0 - log2(tot));
+            shift = (int)floor(52.0 - log2(tot));   // sum of all u_q < 2^53: exact in FP64
             shift = shift > 1000 ? 1000 : (shift < -1000 ? -1000 : shift);
         }
         cs->shift = shift;
@@ -395,13 +420,16 @@ __global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassS
     }
 }
 
-// class increments and fixed-point u per visibility record
-__global__ void k_class_records(long long n_gain, GRec* __restrict__ grec, long long* __restrict__ guq,
-                                long long* __restrict__ ghl, const int* __restrict__ gidx,
+// class increments and fixed-point u per visibility record (both copies); copy B also
+// writes u_q and the packed class count for its exact prefixes
+__global__ void k_class_records(long long n_rec, long long offB, GRec* __restrict__ grec, double* __restrict__ guq,
+                                long long* __restrict__ qB, long long* __restrict__ hlB, const int* __restrict__ gidx,
                                 const float* __restrict__ w, int variant, const ClassState* __restrict__ cs) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i >= n_gain) return;
-    double u = u_of(w[gidx[i]], variant);
+    if (i >= n_rec) return;
+    const int g = gidx[i];
+    if (g < 0) return;
+    double u = u_of(w[g], variant);
     int inc = 0;
     long long hl = 0;
     if (u > cs->tau_hi) {
@@ -413,24 +441,32 @@ __global__ void k_class_records(long long n_gain, GRec* __restrict__ grec, long 
     }
     grec[i].inc = inc;
     long long q = llrint(u * cs->scale);
-    guq[i] = q;
-    ghl[i] = hl;
+    guq[i] = (double)q;   // exact: q < 2^53
+    if (i >= offB) {
+        qB[i - offB] = q;
+        hlB[i - offB] = hl;
+    }
 }
 
-// culled-kernel tables, x-fastest [iy][iz][ix] with iz = 0..nz: entry (iy, iz, ix) describes the
-// boundary before z-cell iz of column (ix, iy); in the (iy, ix, iz) record order the boundary at
-// iz = nz is the start of the next column, i.e. sorted cell index (iy*nx + ix)*nz + iz for all iz
-__global__ void k_gather_cells(GainGrid gg, const int* __restrict__ gstart, const long long* __restrict__ pq,
-                               const long long* __restrict__ phl, int* __restrict__ startT,
-                               CellAgg* __restrict__ aggT) {
+// copy-B start table in z-fastest layout [iy][ix][iz], ix = 0..nx (ix = nx: end of the z-slab):
+// the culled kernel's lanes take consecutive z-cells of a row, so their lookups share lines
+__global__ void k_gather_tabB(GainGrid gg, const int* __restrict__ startB, int* __restrict__ tabB) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long nz1 = gg.nz + 1;
-    if (e >= (long long)gg.ny * nz1 * gg.nx) return;
-    const long long ix = e % gg.nx, r = e / gg.nx;
-    const long long iz = r % nz1, iy = r / nz1;
-    const int s = gstart[(iy * gg.nx + ix) * gg.nz + iz];
-    startT[e] = s;
-    aggT[e] = CellAgg{pq[s], phl[s]};
+    const long long nx1 = gg.nx + 1;
+    if (e >= (long long)gg.ny * nx1 * gg.nz) return;
+    const long long iz = e % gg.nz, r = e / gg.nz;
+    const long long ix = r % nx1, iy = r / nx1;
+    tabB[e] = startB[(iy * gg.nz + iz) * gg.nx + ix];
+}
+
+// prefixes at every copy-B table entry (same z-fastest layout as gtabB): one lookup per x-run end
+__global__ void k_pack_tabP(long long nt, const int* __restrict__ tabB, const long long* __restrict__ pq,
+                            const long long* __restrict__ phl, TabP* __restrict__ tabP) {
+    long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= nt) return;
+    const int s = tabB[e];
+    const long long hl = phl[s];
+    tabP[e] = TabP{(double)pq[s], (int)(hl & 0xffffffffLL), (int)(hl >> 32)};
 }
 
 inline unsigned nblocks(long long n, int t) {
@@ -458,24 +494,27 @@ rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi
         return RTG_ERR_CUDA;
     }
     long long ng = m->n_gain;
-    long long *ghl = nullptr, *pq = nullptr, *phl = nullptr;
-    if (dev_alloc((void**)&ghl, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
+    long long *qB = nullptr, *hlB = nullptr, *pq = nullptr, *phl = nullptr;
+    if (dev_alloc((void**)&qB, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
+        dev_alloc((void**)&hlB, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
         dev_alloc((void**)&pq, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
         dev_alloc((void**)&phl, sizeof(long long) * (ng + 1), st) != cudaSuccess) {
         set_error("classify: out of device memory");
         return RTG_ERR_OUT_OF_MEMORY;
     }
+    const long long nrec = 2 * m->n_gain_pad;
     if (ng > 0)
-        note_launch(), k_class_records<<<nblocks(ng, 256), 256, 0, st>>>(ng, m->grec, m->guq, ghl, m->gidx, m->w_orig, variant,
-                                                          m->cls);
-    e = exclusive_scan_i64(m->guq, pq, ng, st);
-    if (e == cudaSuccess) e = exclusive_scan_i64(ghl, phl, ng, st);
+        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->n_gain_pad, m->grec, m->guq, qB,
+                                                                           hlB, m->gidx, m->w_orig, variant, m->cls);
+    e = exclusive_scan_i64(qB, pq, ng, st);
+    if (e == cudaSuccess) e = exclusive_scan_i64(hlB, phl, ng, st);
     if (e == cudaSuccess) {
-        note_launch(), k_gather_cells<<<nblocks(m->ntab, 256), 256, 0, st>>>(m->gg, m->gstart, pq, phl, m->gstartT,
-                                                                             m->gaggT);
+        const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
+        note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, pq, phl, m->gtabP);
         e = cudaGetLastError();
     }
-    dev_free(ghl, st);
+    dev_free(qB, st);
+    dev_free(hlB, st);
     dev_free(pq, st);
     dev_free(phl, st);
     if (e != cudaSuccess) {
@@ -548,18 +587,21 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     double gq = (104.0 * rho + 6.0) * u32;   // FP32 error bound of q near 1, x2
     m->gq = (float)gq;
     // --- grid geometry
-    double hxy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.5;
-    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 0.5;
+    double hy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.25;
+    double hx = (opt && opt->gain_cell_x > 0) ? opt->gain_cell_x : 0.5 * hy;
+    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 1.0;
     GainGrid& gg = m->gg;
     if (m->n_gain > 0) {
         float lo[3], hi[3];
         for (int d = 0; d < 3; ++d) { lo[d] = o2f(hb.gmin[d]); hi[d] = o2f(hb.gmax[d]); }
         for (;;) {
-            pick_dims(lo[0], hi[0], hxy, gg.nx);
-            pick_dims(lo[1], hi[1], hxy, gg.ny);
+            pick_dims(lo[0], hi[0], hx, gg.nx);
+            pick_dims(lo[1], hi[1], hy, gg.ny);
             pick_dims(lo[2], hi[2], hz, gg.nz);
-            if ((double)gg.nx * gg.ny * gg.nz <= 64.0e6) break;
-            hxy *= 2.0;
+            // (the culled kernel packs cell indices in 16 bits)
+            if ((double)gg.nx * gg.ny * gg.nz <= 96.0e6 && gg.nx < 65535 && gg.ny < 65535 && gg.nz < 65535) break;
+            hx *= 2.0;
+            hy *= 2.0;
             hz *= 2.0;
         }
         gg.ox = lo[0]; gg.oy = lo[1]; gg.oz = lo[2];
@@ -567,9 +609,12 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
         gg.nx = gg.ny = gg.nz = 1;
         gg.ox = gg.oy = gg.oz = 0.f;
     }
-    gg.hxy = (float)hxy;
+    gg.hx = (float)hx;
+    gg.hy = (float)hy;
     gg.hz = (float)hz;
-    gg.ncells = (long long)gg.nx * gg.ny * gg.nz;
+    gg.ncellsA = (long long)gg.nx * gg.ny;
+    gg.nxb = (gg.nx + kZoccX - 1) / kZoccX;
+    gg.ncellsB = (long long)gg.nx * gg.ny * gg.nz;
     ColGrid& cg = m->cg;
     double hc = (opt && opt->col_cell > 0) ? opt->col_cell : fmax(0.5, 0.5 * (double)m->rb_max);
     if (m->n_col > 0) {
@@ -590,17 +635,18 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     cg.h = (float)hc;
     cg.ncells = (long long)cg.nx * cg.ny * cg.nz;
     // --- allocations
-    m->n_gain_pad = ((m->n_gain + kTile - 1) / kTile) * kTile;
+    // >= 64 NaN records after each copy: the culled kernel's idle lanes read past a run's end
+    m->n_gain_pad = m->n_gain > 0 ? ((m->n_gain + 64 + kTile - 1) / kTile) * kTile : 0;
     m->n_col_pad = ((m->n_col + kTile - 1) / kTile) * kTile;
     MAP_CK(map_alloc(m, &m->w_orig, n, st));
     if (flags) MAP_CK(map_alloc(m, &m->flags, n, st));
-    MAP_CK(map_alloc(m, &m->grec, m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->guq, m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->gidx, m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->gstart, gg.ncells + 1, st));
-    m->ntab = (long long)gg.ny * (gg.nz + 1) * gg.nx;
-    MAP_CK(map_alloc(m, &m->gstartT, m->ntab, st));
-    MAP_CK(map_alloc(m, &m->gaggT, m->ntab, st));
+    MAP_CK(map_alloc(m, &m->grec, 2 * m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->guq, 2 * m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->gidx, 2 * m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->gstartA, gg.ncellsA + 1, st));
+    MAP_CK(map_alloc(m, &m->gtabB, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
+    MAP_CK(map_alloc(m, &m->zocc, (size_t)gg.ny * gg.nxb, st));
+    MAP_CK(map_alloc(m, &m->gtabP, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
     MAP_CK(map_alloc(m, &m->crec, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cmat64, m->n_col_pad, st));
@@ -610,36 +656,51 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     if (n > 0) MAP_CK(cudaMemcpyAsync(m->w_orig, w, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
     if (flags && n > 0) MAP_CK(cudaMemcpyAsync(m->flags, flags, n, cudaMemcpyDeviceToDevice, st));
     // --- counting sort into both grids
-    int *gkey = nullptr, *ckey = nullptr, *gcount = nullptr, *ccount = nullptr;
+    int *gkey = nullptr, *ckey = nullptr, *gcountA = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
     MAP_CK(dev_alloc((void**)&gkey, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&ckey, sizeof(int) * (n > 0 ? n : 1), st));
-    MAP_CK(dev_alloc((void**)&gcount, sizeof(int) * (gg.ncells + 1), st));
+    MAP_CK(dev_alloc((void**)&gcountA, sizeof(int) * (gg.ncellsA + 1), st));
+    MAP_CK(dev_alloc((void**)&gcountB, sizeof(int) * (gg.ncellsB + 1), st));
+    MAP_CK(dev_alloc((void**)&gstartB, sizeof(int) * (gg.ncellsB + 1), st));
     MAP_CK(dev_alloc((void**)&ccount, sizeof(int) * (cg.ncells + 1), st));
-    MAP_CK(cudaMemsetAsync(gcount, 0, sizeof(int) * (gg.ncells + 1), st));
+    MAP_CK(cudaMemsetAsync(gcountA, 0, sizeof(int) * (gg.ncellsA + 1), st));
+    MAP_CK(cudaMemsetAsync(gcountB, 0, sizeof(int) * (gg.ncellsB + 1), st));
     MAP_CK(cudaMemsetAsync(ccount, 0, sizeof(int) * (cg.ncells + 1), st));
+    note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc, (long long)gg.ny * gg.nxb);
     unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
-    if (n > 0) note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, gcount, ccount);
+    if (n > 0)
+        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, gcountA, gcountB, m->zocc,
+                                                  ccount);
     MAP_CK(cudaGetLastError());
-    MAP_CK(exclusive_scan_i32(gcount, m->gstart, gg.ncells, st));
+    MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));
+    MAP_CK(exclusive_scan_i32(gcountB, gstartB, gg.ncellsB, st));
     MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
     // cursors (reuse the count arrays)
-    MAP_CK(cudaMemcpyAsync(gcount, m->gstart, sizeof(int) * gg.ncells, cudaMemcpyDeviceToDevice, st));
+    MAP_CK(cudaMemcpyAsync(gcountA, m->gstartA, sizeof(int) * gg.ncellsA, cudaMemcpyDeviceToDevice, st));
+    MAP_CK(cudaMemcpyAsync(gcountB, gstartB, sizeof(int) * gg.ncellsB, cudaMemcpyDeviceToDevice, st));
+    {
+        const long long nt = (long long)gg.ny * (gg.nx + 1) * gg.nz;
+        note_launch(), k_gather_tabB<<<nblocks(nt, 256), 256, 0, st>>>(gg, gstartB, m->gtabB);
+    }
     MAP_CK(cudaMemcpyAsync(ccount, m->cstart, sizeof(int) * cg.ncells, cudaMemcpyDeviceToDevice, st));
     if (n > 0) {
-        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, gkey, gcount, m->grec, m->gidx);
+        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, gkey, gg, gcountA, gcountB, m->n_gain_pad, m->grec,
+                                                          m->gidx);
         note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, ccount, rb, gq, m->crec, m->cmat,
                                           m->cmat64);
     }
     if (m->n_gain_pad > m->n_gain)
-        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(m->grec, m->guq, m->gidx, m->n_gain,
-                                                                            m->n_gain_pad);
+        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
+                           m->grec, m->guq, m->gidx, m->n_gain, m->n_gain_pad, m->n_gain_pad);
     if (m->n_col_pad > m->n_col)
         note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->cmat64, m->n_col,
                                                                          m->n_col_pad);
     MAP_CK(cudaGetLastError());
     dev_free(gkey, st);
     dev_free(ckey, st);
-    dev_free(gcount, st);
+    dev_free(gcountA, st);
+    dev_free(gcountB, st);
+    dev_free(gstartB, st);
     dev_free(ccount, st);
     // --- default classification (k = 1/2, derived thresholds)
     m->cls_variant = -1;

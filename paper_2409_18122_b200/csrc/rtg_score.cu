@@ -289,11 +289,11 @@ constexpr int kDenseGainWpt = 4;
 __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, int list_n, const GRec* __restrict__ grec,
-    const long long* __restrict__ guq, long long n_gain_pad, int tiles_per_split, CamK cam,
+    const double* __restrict__ guq, long long n_gain_pad, int tiles_per_split, CamK cam,
     unsigned long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
     unsigned long long* __restrict__ stats) {
     __shared__ __align__(128) GRec s_rec[2][kTile];
-    __shared__ __align__(128) long long s_uq[2][kTile];
+    __shared__ __align__(128) double s_uq[2][kTile];
     __shared__ __align__(8) uint64_t s_bar[2];
     const long long tile0 = (long long)blockIdx.y * tiles_per_split;
     long long ntiles = n_gain_pad / kTile - tile0;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
     WpF wf[kDenseGainWpt];
     int wid[kDenseGainWpt];
     bool act[kDenseGainWpt];
-    long long accq[kDenseGainWpt];
+    double accq[kDenseGainWpt];   // exact: integers below 2^53
     int nh[kDenseGainWpt], nl[kDenseGainWpt];
 #pragma unroll
     for (int j = 0; j < kDenseGainWpt; ++j) {
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
         act[j] = act[j] && isfinite(x) && isfinite(y) && isfinite(z) && isfinite(yw);
         if (!act[j]) { x = __int_as_float(0x7fc00000); y = x; z = x; yw = 0.f; }   // NaN pose: sees nothing
         wp_setup(x, y, z, yw, cam, wf[j]);
-        accq[j] = 0;
+        accq[j] = 0.0;
         nh[j] = 0;
         nl[j] = 0;
     }
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
         fence_mbar_init();
     }
     __syncthreads();
-    const uint32_t rb = kTile * sizeof(GRec), qb = kTile * sizeof(long long);
+    const uint32_t rb = kTile * sizeof(GRec), qb = kTile * sizeof(double);
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2 && s < ntiles; ++s) {
             mbar_expect_tx(&s_bar[s], rb + qb);
@@ -341,11 +341,11 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
 #pragma unroll
         for (int j = 0; j < kDenseGainWpt; ++j) pc[j] = 0;
         const GRec* rec = s_rec[s];
-        const long long* uq = s_uq[s];
+        const double* uq = s_uq[s];
 #pragma unroll 2
         for (int g = 0; g < kTile; ++g) {
             const GRec G = rec[g];
-            const long long q = uq[g];
+            const double q = uq[g];
 #pragma unroll
             for (int j = 0; j < kDenseGainWpt; ++j) {
                 if (visible(wf[j], cam, G.x, G.y, G.z, nref)) {
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
 #pragma unroll
     for (int j = 0; j < kDenseGainWpt; ++j) {
         if (act[j]) {
-            if (accq[j]) atomicAdd(&wp_gq[wid[j]], (unsigned long long)accq[j]);
+            if (accq[j] != 0.0) atomicAdd(&wp_gq[wid[j]], (unsigned long long)(long long)accq[j]);
             if (nh[j]) atomicAdd(&wp_nh[wid[j]], nh[j]);
             if (nl[j]) atomicAdd(&wp_nl[wid[j]], nl[j]);
         }

@@ -56,7 +56,8 @@ class BestResult(ctypes.Structure):
 
 
 class MapOptions(ctypes.Structure):
-    _fields_ = [("gain_cell_xy", ctypes.c_float), ("gain_cell_z", ctypes.c_float), ("col_cell", ctypes.c_float)]
+    _fields_ = [("gain_cell_xy", ctypes.c_float), ("gain_cell_z", ctypes.c_float), ("col_cell", ctypes.c_float),
+                ("gain_cell_x", ctypes.c_float)]
 
 
 class MapInfo(ctypes.Structure):
@@ -325,7 +326,7 @@ def score_debug(m: Map, tr: Traj, camera, params: ScoreParams, pair_mask: bool =
            "rtg_score_debug")
     return dict(wp_col=wp_col, wp_gain=wp_gain, wp_nh=wp_nh, wp_nl=wp_nl, pair_mask=mask,
                 stats=dict(col_refined=stats[0], vis_refined=stats[1], tested=stats[2], cells_aggregated=stats[3],
-                           col_tested=stats[4], tested_straddle=stats[5], columns=stats[6], tested_visible=stats[7]))
+                           col_tested=stats[4], tested_flank=stats[5], units=stats[6], tested_visible=stats[7]))
 
 
 def unpack_pair_mask(mask, KT: int, N: int) -> np.ndarray:

@@ -154,7 +154,7 @@ def test_dense_equals_culled_bitwise(R, room):
     assert np.array_equal(a["gain"].view(np.int64), b["gain"].view(np.int64))
     assert np.array_equal(a["wp_gain"].view(np.int64), b["wp_gain"].view(np.int64))
     assert a["best"] == b["best"]
-    assert b["stats"]["cells_aggregated"] > 0
+    assert b["stats"]["cells_aggregated"] > 0 and b["stats"]["units"] > 0
 
 
 @pytest.mark.parametrize("variant,stride,lam,tau,rule", [
