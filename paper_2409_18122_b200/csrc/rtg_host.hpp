@@ -52,6 +52,8 @@ struct ColGrid {
 // scans (rtg_scan.cu): exclusive prefix of n values into out[0..n] (out[n] = total)
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_t st);
 cudaError_t exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t st);
+// n pairs (in[2i], in[2i+1]) scanned together into out[0 .. 2n+1]
+cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st);
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
@@ -88,7 +90,7 @@ struct rtg_map_s {
     long long n_col_pad = 0;
     rtg::CRec* crec = nullptr;
     rtg::CMat* cmat = nullptr;
-    rtg::CMat64* cmat64 = nullptr;
+    rtg::CSrc* csrc = nullptr;           // the fp32 inputs of each collision record (FP64 re-decisions)
     int* cstart = nullptr;               // [ncells+1]
     rtg::ColGrid cg{};
     float rb_max = 0.f;

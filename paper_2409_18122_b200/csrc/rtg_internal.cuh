@@ -16,6 +16,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/rtg.h"
+
 namespace rtg {
 
 constexpr int kTile = 512;           // dense-mode Gaussians per smem tile
@@ -32,8 +34,35 @@ struct __align__(16) CMat { float m[12]; };
 // exact exclusive prefixes at a copy-B cell boundary (z-fastest table entry): sum of u_q (an
 // integer < 2^53, exact in FP64) and the class counts nH, nL
 struct __align__(16) TabP { double q; int nh, nl; };
-// FP64 M for the re-decision branch (9 used)
-struct CMat64 { double m[9]; };
+// the fp32 inputs M is packed from (sorted like the collision records): the rare FP64
+// re-decision recomputes M from them with the same code as the packing (pack_m64)
+struct __align__(32) CSrc { float q[4]; float s[3]; float pad; };
+
+// a1 in FP64: inflated semi-axes a_i = lambda_g s_i + r_robot (PRINCIPAL_AXIS: every
+// a_i = lambda_g max s + r_robot) and M = diag(1/a) R^T with R the Hamilton rotation of
+// the normalised quaternion (w, x, y, z).  Used for packing and for every FP64 re-decision.
+__device__ __forceinline__ void pack_m64(double qw, double qx, double qy, double qz, double s0, double s1, double s2,
+                                         const rtg_robot& rb, double M[9], double a[3]) {
+    if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
+        const double r = (double)rb.lambda_g * fmax(s0, fmax(s1, s2)) + (double)rb.r_robot;
+        a[0] = a[1] = a[2] = r;
+        for (int j = 0; j < 9; ++j) M[j] = 0.0;
+        M[0] = M[4] = M[8] = 1.0 / r;
+        return;
+    }
+    a[0] = (double)rb.lambda_g * s0 + (double)rb.r_robot;
+    a[1] = (double)rb.lambda_g * s1 + (double)rb.r_robot;
+    a[2] = (double)rb.lambda_g * s2 + (double)rb.r_robot;
+    const double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw /= nq; qx /= nq; qy /= nq; qz /= nq;
+    // Hamilton R (columns = local principal axes)
+    const double R[3][3] = {
+        {1.0 - 2.0 * (qy * qy + qz * qz), 2.0 * (qx * qy - qw * qz), 2.0 * (qx * qz + qw * qy)},
+        {2.0 * (qx * qy + qw * qz), 1.0 - 2.0 * (qx * qx + qz * qz), 2.0 * (qy * qz - qw * qx)},
+        {2.0 * (qx * qz - qw * qy), 2.0 * (qy * qz + qw * qx), 1.0 - 2.0 * (qx * qx + qy * qy)}};
+    for (int r = 0; r < 3; ++r)         // row r of M = column r of R / a_r  (M = diag(1/a) R^T)
+        for (int c = 0; c < 3; ++c) M[3 * r + c] = R[c][r] / a[r];
+}
 
 // ------------------------------------------------------------------ camera constants
 struct CamK {
@@ -131,9 +160,11 @@ __device__ __forceinline__ bool visible_cs(const WpF& w, const CamK& k, float mx
 }
 
 // ------------------------------------------------------------------ collision
-static __device__ __noinline__ bool col_decide64(const CMat64* __restrict__ Mp, float px, float py, float pz,
-                                          float mx, float my, float mz) {
-    const double* M = Mp->m;
+static __device__ __noinline__ bool col_decide64(const CSrc* __restrict__ src, const rtg_robot rb, float px, float py,
+                                                 float pz, float mx, float my, float mz) {
+    const CSrc c = *src;
+    double M[9], a[3];
+    pack_m64(c.q[0], c.q[1], c.q[2], c.q[3], c.s[0], c.s[1], c.s[2], rb, M, a);
     double dx = (double)px - (double)mx, dy = (double)py - (double)my, dz = (double)pz - (double)mz;
     double e0 = M[0] * dx + M[1] * dy + M[2] * dz;
     double e1 = M[3] * dx + M[4] * dy + M[5] * dz;
@@ -143,7 +174,7 @@ static __device__ __noinline__ bool col_decide64(const CMat64* __restrict__ Mp, 
 
 // full quadratic form for a sphere-passing pair
 __device__ __forceinline__ bool collide_full(const float* m, float dx, float dy, float dz, float gq,
-                                             const CMat64* m64, float px, float py, float pz,
+                                             const CSrc* src, const rtg_robot& rb, float px, float py, float pz,
                                              float mx, float my, float mz, unsigned& nref) {
     float e0 = fmaf(m[0], dx, fmaf(m[1], dy, m[2] * dz));
     float e1 = fmaf(m[3], dx, fmaf(m[4], dy, m[5] * dz));
@@ -151,7 +182,7 @@ __device__ __forceinline__ bool collide_full(const float* m, float dx, float dy,
     float q = fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
     bool c = q < 1.0f;
     if (fabsf(q - 1.0f) < gq) {
-        c = col_decide64(m64, px, py, pz, mx, my, mz);
+        c = col_decide64(src, rb, px, py, pz, mx, my, mz);
         ++nref;
     }
     return c;

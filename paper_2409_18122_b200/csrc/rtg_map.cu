@@ -238,30 +238,18 @@ __global__ void k_scatter_gain(long long n, const float* __restrict__ means, con
 __global__ void k_scatter_col(long long n, const float* __restrict__ means, const float* __restrict__ quats,
                               const float* __restrict__ scales, const int* __restrict__ ckey,
                               int* __restrict__ cursor, rtg_robot rb, double guard, CRec* __restrict__ crec,
-                              CMat* __restrict__ cmat, CMat64* __restrict__ cmat64) {
+                              CMat* __restrict__ cmat, CSrc* __restrict__ csrc) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int k = ckey[i];
         if (k < 0) continue;
         int slot = atomicAdd(&cursor[k], 1);
-        double a[3];
-        semi_axes(scales, n, i, rb, a);
-        double M[9];
-        if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
-            for (int j = 0; j < 9; ++j) M[j] = 0.0;
-            M[0] = M[4] = M[8] = 1.0 / a[0];
-        } else {
-            double qw = quats[i], qx = quats[n + i], qy = quats[2 * n + i], qz = quats[3 * n + i];
-            double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-            qw /= nq; qx /= nq; qy /= nq; qz /= nq;
-            // Hamilton R (columns = local principal axes)
-            double R[3][3] = {
-                {1.0 - 2.0 * (qy * qy + qz * qz), 2.0 * (qx * qy - qw * qz), 2.0 * (qx * qz + qw * qy)},
-                {2.0 * (qx * qy + qw * qz), 1.0 - 2.0 * (qx * qx + qz * qz), 2.0 * (qy * qz - qw * qx)},
-                {2.0 * (qx * qz - qw * qy), 2.0 * (qy * qz + qw * qx), 1.0 - 2.0 * (qx * qx + qy * qy)}};
-            for (int r = 0; r < 3; ++r)         // row r of M = column r of R / a_r  (M = diag(1/a) R^T)
-                for (int c = 0; c < 3; ++c) M[3 * r + c] = R[c][r] / a[r];
-        }
+        CSrc src;
+        src.q[0] = quats[i]; src.q[1] = quats[n + i]; src.q[2] = quats[2 * n + i]; src.q[3] = quats[3 * n + i];
+        src.s[0] = scales[i]; src.s[1] = scales[n + i]; src.s[2] = scales[2 * n + i];
+        src.pad = 0.f;
+        double a[3], M[9];
+        pack_m64(src.q[0], src.q[1], src.q[2], src.q[3], src.s[0], src.s[1], src.s[2], rb, M, a);
         double amax = fmax(a[0], fmax(a[1], a[2]));
         float rb2 = __double2float_ru(amax * amax * (1.0 + guard) * (1.0 + 1.0e-6));
         crec[slot] = CRec{means[i], means[n + i], means[2 * n + i], rb2};
@@ -271,9 +259,7 @@ __global__ void k_scatter_col(long long n, const float* __restrict__ means, cons
         cm.m[10] = 0.f;
         cm.m[11] = 0.f;
         cmat[slot] = cm;
-        CMat64 c64;
-        for (int j = 0; j < 9; ++j) c64.m[j] = M[j];
-        cmat64[slot] = c64;
+        csrc[slot] = src;
     }
 }
 
@@ -291,7 +277,7 @@ __global__ void k_pad_gain(GRec* grec, double* guq, int* gidx, long long from, l
     }
 }
 
-__global__ void k_pad_col(CRec* crec, CMat* cmat, CMat64* cm64, long long from, long long to) {
+__global__ void k_pad_col(CRec* crec, CMat* cmat, CSrc* csrc, long long from, long long to) {
     long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < to) {
         float nan = __int_as_float(0x7fc00000);
@@ -300,9 +286,12 @@ __global__ void k_pad_col(CRec* crec, CMat* cmat, CMat64* cm64, long long from, 
         for (int j = 0; j < 12; ++j) z.m[j] = 0.f;
         z.m[9] = __int_as_float(-1);
         cmat[i] = z;
-        CMat64 z64;
-        for (int j = 0; j < 9; ++j) z64.m[j] = 0.0;
-        cm64[i] = z64;
+        CSrc zs;
+        for (int j = 0; j < 4; ++j) zs.q[j] = 0.f;
+        zs.q[0] = 1.f;
+        for (int j = 0; j < 3; ++j) zs.s[j] = 1.f;
+        zs.pad = 0.f;
+        csrc[i] = zs;
     }
 }
 
@@ -423,7 +412,7 @@ __global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassS
 // class increments and fixed-point u per visibility record (both copies); copy B also
 // writes u_q and the packed class count for its exact prefixes
 __global__ void k_class_records(long long n_rec, long long offB, GRec* __restrict__ grec, double* __restrict__ guq,
-                                long long* __restrict__ qB, long long* __restrict__ hlB, const int* __restrict__ gidx,
+                                long long* __restrict__ qhlB, const int* __restrict__ gidx,
                                 const float* __restrict__ w, int variant, const ClassState* __restrict__ cs) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n_rec) return;
@@ -443,8 +432,8 @@ __global__ void k_class_records(long long n_rec, long long offB, GRec* __restric
     long long q = llrint(u * cs->scale);
     guq[i] = (double)q;   // exact: q < 2^53
     if (i >= offB) {
-        qB[i - offB] = q;
-        hlB[i - offB] = hl;
+        qhlB[2 * (i - offB)] = q;
+        qhlB[2 * (i - offB) + 1] = hl;
     }
 }
 
@@ -460,13 +449,12 @@ __global__ void k_gather_tabB(GainGrid gg, const int* __restrict__ startB, int* 
 }
 
 // prefixes at every copy-B table entry (same z-fastest layout as gtabB): one lookup per x-run end
-__global__ void k_pack_tabP(long long nt, const int* __restrict__ tabB, const long long* __restrict__ pq,
-                            const long long* __restrict__ phl, TabP* __restrict__ tabP) {
+__global__ void k_pack_tabP(long long nt, const int* __restrict__ tabB, const longlong2* __restrict__ pqhl,
+                            TabP* __restrict__ tabP) {
     long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= nt) return;
-    const int s = tabB[e];
-    const long long hl = phl[s];
-    tabP[e] = TabP{(double)pq[s], (int)(hl & 0xffffffffLL), (int)(hl >> 32)};
+    const longlong2 v = pqhl[tabB[e]];
+    tabP[e] = TabP{(double)v.x, (int)(v.y & 0xffffffffLL), (int)(v.y >> 32)};
 }
 
 inline unsigned nblocks(long long n, int t) {
@@ -494,29 +482,24 @@ rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi
         return RTG_ERR_CUDA;
     }
     long long ng = m->n_gain;
-    long long *qB = nullptr, *hlB = nullptr, *pq = nullptr, *phl = nullptr;
-    if (dev_alloc((void**)&qB, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
-        dev_alloc((void**)&hlB, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
-        dev_alloc((void**)&pq, sizeof(long long) * (ng + 1), st) != cudaSuccess ||
-        dev_alloc((void**)&phl, sizeof(long long) * (ng + 1), st) != cudaSuccess) {
+    long long *qhlB = nullptr, *pqhl = nullptr;
+    if (dev_alloc((void**)&qhlB, 2 * sizeof(long long) * (ng + 1), st) != cudaSuccess ||
+        dev_alloc((void**)&pqhl, 2 * sizeof(long long) * (ng + 1), st) != cudaSuccess) {
         set_error("classify: out of device memory");
         return RTG_ERR_OUT_OF_MEMORY;
     }
     const long long nrec = 2 * m->n_gain_pad;
     if (ng > 0)
-        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->n_gain_pad, m->grec, m->guq, qB,
-                                                                           hlB, m->gidx, m->w_orig, variant, m->cls);
-    e = exclusive_scan_i64(qB, pq, ng, st);
-    if (e == cudaSuccess) e = exclusive_scan_i64(hlB, phl, ng, st);
+        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->n_gain_pad, m->grec, m->guq, qhlB,
+                                                                           m->gidx, m->w_orig, variant, m->cls);
+    e = exclusive_scan_i64x2(qhlB, pqhl, ng, st);
     if (e == cudaSuccess) {
         const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
-        note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, pq, phl, m->gtabP);
+        note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, (const longlong2*)pqhl, m->gtabP);
         e = cudaGetLastError();
     }
-    dev_free(qB, st);
-    dev_free(hlB, st);
-    dev_free(pq, st);
-    dev_free(phl, st);
+    dev_free(qhlB, st);
+    dev_free(pqhl, st);
     if (e != cudaSuccess) {
         set_error("classify: %s", cudaGetErrorString(e));
         return RTG_ERR_CUDA;
@@ -649,7 +632,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->gtabP, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
     MAP_CK(map_alloc(m, &m->crec, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
-    MAP_CK(map_alloc(m, &m->cmat64, m->n_col_pad, st));
+    MAP_CK(map_alloc(m, &m->csrc, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
     MAP_CK(map_alloc(m, &m->cls, 1, st));
     MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
@@ -687,13 +670,13 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
         note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, gkey, gg, gcountA, gcountB, m->n_gain_pad, m->grec,
                                                           m->gidx);
         note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, ccount, rb, gq, m->crec, m->cmat,
-                                          m->cmat64);
+                                          m->csrc);
     }
     if (m->n_gain_pad > m->n_gain)
         note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
                            m->grec, m->guq, m->gidx, m->n_gain, m->n_gain_pad, m->n_gain_pad);
     if (m->n_col_pad > m->n_col)
-        note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->cmat64, m->n_col,
+        note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, m->n_col,
                                                                          m->n_col_pad);
     MAP_CK(cudaGetLastError());
     dev_free(gkey, st);

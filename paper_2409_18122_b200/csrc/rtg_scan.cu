@@ -1,5 +1,8 @@
 // rtg_scan.cu -- exclusive prefix sums used to build the cell grids (counting sort) and the
-// exact fixed-point cell aggregates.  Three-phase block scan, recursive over block totals.
+// exact fixed-point prefixes.  Single pass, decoupled look-back: tiles take ids in launch order
+// from an atomic counter, publish their aggregate, then look back over their predecessors' published
+// aggregates / inclusive prefixes (a warp examines 32 predecessors at a time) until an inclusive
+// prefix closes the sum.  Integer sums are exact, so the result does not depend on the order.
 #include "rtg_host.hpp"
 
 namespace rtg {
@@ -7,16 +10,44 @@ namespace {
 
 constexpr int kScanThreads = 512;
 constexpr int kScanPer = 8;
-constexpr int kScanBlock = kScanThreads * kScanPer;   // elements per block
+constexpr int kScanTile = kScanThreads * kScanPer;   // elements per tile
+
+// a pair of 64-bit sums (u_q prefix, packed class counts) scanned together
+struct I64x2 {
+    long long a, b;
+    I64x2() = default;
+    __host__ __device__ I64x2(long long x) : a(x), b(x) {}
+    __host__ __device__ I64x2(long long x, long long y) : a(x), b(y) {}
+    __host__ __device__ I64x2& operator+=(const I64x2& o) { a += o.a; b += o.b; return *this; }
+    __host__ __device__ I64x2 operator+(const I64x2& o) const { return I64x2(a + o.a, b + o.b); }
+    __host__ __device__ I64x2 operator-(const I64x2& o) const { return I64x2(a - o.a, b - o.b); }
+};
+__device__ __forceinline__ int shfl_up(int v, int o) { return __shfl_up_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ long long shfl_up(long long v, int o) { return __shfl_up_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ I64x2 shfl_up(I64x2 v, int o) {
+    return I64x2(__shfl_up_sync(0xffffffffu, v.a, o), __shfl_up_sync(0xffffffffu, v.b, o));
+}
+__device__ __forceinline__ int shfl_down(int v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ long long shfl_down(long long v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ I64x2 shfl_down(I64x2 v, int o) {
+    return I64x2(__shfl_down_sync(0xffffffffu, v.a, o), __shfl_down_sync(0xffffffffu, v.b, o));
+}
+
+// L2 loads of other tiles' published values (never a stale L1 line)
+__device__ __forceinline__ int load_cg(const int* p) { return __ldcg(p); }
+__device__ __forceinline__ long long load_cg(const long long* p) { return __ldcg(p); }
+__device__ __forceinline__ I64x2 load_cg(const I64x2* p) {
+    const long long* q = reinterpret_cast<const long long*>(p);
+    return I64x2(__ldcg(q), __ldcg(q + 1));
+}
 
 template <typename T>
 __device__ T block_exclusive_scan(T v, T* sh, T& total) {
-    // warp inclusive scan
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        T y = __shfl_up_sync(0xffffffffu, x, o);
+        T y = shfl_up(x, o);
         if (lane >= o) x += y;
     }
     if (lane == 31) sh[wid] = x;
@@ -25,7 +56,7 @@ __device__ T block_exclusive_scan(T v, T* sh, T& total) {
         T w = lane < (kScanThreads / 32) ? sh[lane] : T(0);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            T y = __shfl_up_sync(0xffffffffu, w, o);
+            T y = shfl_up(w, o);
             if (lane >= o) w += y;
         }
         if (lane < (kScanThreads / 32)) sh[lane] = w;
@@ -33,78 +64,111 @@ __device__ T block_exclusive_scan(T v, T* sh, T& total) {
     __syncthreads();
     T warp_prefix = wid > 0 ? sh[wid - 1] : T(0);
     total = sh[kScanThreads / 32 - 1];
-    __syncthreads();
     return warp_prefix + x - v;
 }
 
-// out[i] = sum_{j<i} in[j] within the block; block_sums[b] = block total
+// status of tile t: flag[t] = 0 (nothing yet), 1 (aggregate published), 2 (inclusive prefix
+// published); the value is written before the flag, separated by a fence
 template <typename T>
-__global__ void k_scan_local(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ block_sums,
-                             long long n) {
+__global__ void __launch_bounds__(kScanThreads) k_scan(const T* __restrict__ in, T* __restrict__ out, long long n,
+                                                        int* __restrict__ ticket, volatile int* flag, T* agg, T* inc) {
     __shared__ T sh[kScanThreads / 32];
-    long long base = (long long)blockIdx.x * kScanBlock + (long long)threadIdx.x * kScanPer;
+    __shared__ T s_prefix;
+    __shared__ int s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const long long base = (long long)tile * kScanTile + (long long)threadIdx.x * kScanPer;
     T loc[kScanPer];
-    T s = 0;
+    T s = T(0);
 #pragma unroll
     for (int i = 0; i < kScanPer; ++i) {
-        long long j = base + i;
+        const long long j = base + i;
         loc[i] = j < n ? in[j] : T(0);
         s += loc[i];
     }
     T total;
     T pre = block_exclusive_scan<T>(s, sh, total);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (tile == 0) {
+            if (lane == 0) {
+                inc[0] = total;
+                __threadfence();
+                flag[0] = 2;
+                s_prefix = T(0);
+            }
+        } else {
+            if (lane == 0) {
+                agg[tile] = total;
+                __threadfence();
+                flag[tile] = 1;
+            }
+            // look back over predecessors tile-1-lane, 32 at a time
+            T run = T(0);
+            int look = tile - 1;
+            for (;;) {
+                const int p = look - lane;
+                int f = 2;
+                if (p >= 0) {
+                    do { f = flag[p]; } while (f == 0);
+                }
+                __threadfence();
+                const unsigned closed = __ballot_sync(0xffffffffu, f == 2);   // lanes at an inclusive prefix
+                const int stop = closed ? __ffs(closed) - 1 : 31;           // nearest one (p >= 0 has one by tile 0)
+                T v = T(0);
+                if (p >= 0 && lane <= stop) v = (f == 2) ? load_cg(inc + p) : load_cg(agg + p);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += shfl_down(v, o);
+                run += v;   // lane 0 holds the warp sum
+                if (closed) break;
+                look -= 32;
+            }
+            if (lane == 0) {
+                inc[tile] = run + total;
+                __threadfence();
+                flag[tile] = 2;
+                s_prefix = run;
+            }
+        }
+    }
+    __syncthreads();
+    pre += s_prefix;
 #pragma unroll
     for (int i = 0; i < kScanPer; ++i) {
-        long long j = base + i;
+        const long long j = base + i;
         if (j < n) out[j] = pre;
         pre += loc[i];
-    }
-    if (threadIdx.x == 0 && block_sums) block_sums[blockIdx.x] = total;
-}
-
-template <typename T>
-__global__ void k_scan_add(T* __restrict__ out, const T* __restrict__ offs, long long n) {
-    long long base = (long long)blockIdx.x * kScanBlock + (long long)threadIdx.x * kScanPer;
-    T o = offs[blockIdx.x];
-#pragma unroll
-    for (int i = 0; i < kScanPer; ++i) {
-        long long j = base + i;
-        if (j < n) out[j] += o;
+        if (j == n - 1) out[n] = pre;   // total
     }
 }
 
-// out[n] = out[n-1] + in[n-1]
 template <typename T>
-__global__ void k_scan_tail(const T* __restrict__ in, T* __restrict__ out, long long n) {
-    if (threadIdx.x == 0) out[n] = n > 0 ? out[n - 1] + in[n - 1] : T(0);
-}
+__global__ void k_scan_empty(T* out) { out[0] = T(0); }
 
 template <typename T>
 cudaError_t scan_impl(const T* in, T* out, long long n, cudaStream_t st) {
     if (n <= 0) {
-        note_launch(), k_scan_tail<T><<<1, 32, 0, st>>>(in, out, 0);
+        note_launch(), k_scan_empty<T><<<1, 1, 0, st>>>(out);
         return cudaGetLastError();
     }
-    long long nb = (n + kScanBlock - 1) / kScanBlock;
-    if (nb == 1) {
-        note_launch(), k_scan_local<T><<<1, kScanThreads, 0, st>>>(in, out, nullptr, n);
-    } else {
-        T* sums = nullptr;
-        cudaError_t e = dev_alloc((void**)&sums, sizeof(T) * (nb + 1), st);
-        if (e != cudaSuccess) return e;
-        note_launch(), k_scan_local<T><<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, sums, n);
-        // scan block totals in place (exclusive), recursively
-        T* sums_scan = nullptr;
-        e = dev_alloc((void**)&sums_scan, sizeof(T) * (nb + 1), st);
-        if (e != cudaSuccess) return e;
-        e = scan_impl<T>(sums, sums_scan, nb, st);
-        if (e != cudaSuccess) return e;
-        note_launch(), k_scan_add<T><<<(unsigned)nb, kScanThreads, 0, st>>>(out, sums_scan, n);
-        dev_free(sums, st);
-        dev_free(sums_scan, st);
-    }
-    note_launch(), k_scan_tail<T><<<1, 32, 0, st>>>(in, out, n);
-    return cudaGetLastError();
+    const long long nt = (n + kScanTile - 1) / kScanTile;
+    if (nt >= (1LL << 31)) return cudaErrorInvalidValue;
+    // scratch: ticket + flags (zeroed), aggregates, inclusive prefixes
+    const size_t fb = sizeof(int) * (size_t)(nt + 1), vb = sizeof(T) * (size_t)nt;
+    char* mem = nullptr;
+    cudaError_t e = dev_alloc((void**)&mem, ((fb + 255) & ~(size_t)255) + 2 * vb + 64, st);
+    if (e != cudaSuccess) return e;
+    int* ticket = (int*)mem;
+    int* flags = ticket + 1;
+    T* agg = (T*)(mem + ((fb + 255) & ~(size_t)255));
+    T* inc = agg + nt;
+    e = cudaMemsetAsync(mem, 0, fb, st);
+    if (e != cudaSuccess) return e;
+    note_launch(), k_scan<T><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, ticket, flags, agg, inc);
+    e = cudaGetLastError();
+    dev_free(mem, st);
+    return e;
 }
 
 }  // namespace
@@ -114,6 +178,10 @@ cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_
 }
 cudaError_t exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t st) {
     return scan_impl<long long>(in, out, n, st);
+}
+// pairs of int64 (in[2i], in[2i+1]) scanned together
+cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st) {
+    return scan_impl<I64x2>(reinterpret_cast<const I64x2*>(in), reinterpret_cast<I64x2*>(out), n, st);
 }
 
 }  // namespace rtg

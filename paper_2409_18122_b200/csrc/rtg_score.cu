@@ -29,7 +29,7 @@ constexpr int kDenseColWpt = 2;
 
 __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
-    const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CMat64* __restrict__ cm64,
+    const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CSrc* __restrict__ csrc, const rtg_robot rb,
     long long n_col_pad, int tiles_per_split, float gq, int* __restrict__ first_col,
     unsigned char* __restrict__ wp_col, int all_waypoints, unsigned long long* __restrict__ stats) {
     __shared__ __align__(128) CRec s_tile[2][kTile];
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
                     float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                     if (d2 < A.rb2 && act[j] && !hit[j]) {
                         long long gi = (tile0 + it) * kTile + g;
-                        hit[j] = collide_full(cmat[gi].m, dx, dy, dz, gq, &cm64[gi], px[j], py[j],
+                        hit[j] = collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, px[j], py[j],
                                               pz[j], A.x, A.y, A.z, nref);
                     }
                 }
@@ -137,7 +137,7 @@ constexpr int kWarps = 8;   // warps per block of the persistent culled kernels
 
 __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
-    const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CMat64* __restrict__ cm64,
+    const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CSrc* __restrict__ csrc, const rtg_robot rb,
     const int* __restrict__ cstart, ColGridK g, float gq, int* __restrict__ first_col,
     unsigned char* __restrict__ wp_col, int all_waypoints, int* __restrict__ counter,
     unsigned long long* __restrict__ stats) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
                                 float dx = px - A.x, dy = py - A.y, dz = pz - A.z;
                                 float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                                 if (d2 < A.rb2)
-                                    h = collide_full(cmat[gi].m, dx, dy, dz, gq, &cm64[gi], px, py,
+                                    h = collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, px, py,
                                                      pz, A.x, A.y, A.z, nref);
                             }
                             ntest += (unsigned long long)min(32, total - b0);
@@ -467,7 +467,7 @@ __global__ void k_best(const double* __restrict__ u, int K, long long base, Best
 // ===================================================================== debug pair mask
 __global__ void k_pair_mask(const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
                             long long KT, long long N, const CRec* __restrict__ crec, const CMat* __restrict__ cmat,
-                            const CMat64* __restrict__ cm64, long long n_col, float gq,
+                            const CSrc* __restrict__ csrc, const rtg_robot rb, long long n_col, float gq,
                             unsigned int* __restrict__ mask) {
     long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (idx >= KT * n_col) return;
@@ -478,7 +478,7 @@ __global__ void k_pair_mask(const float* __restrict__ X, const float* __restrict
     float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     unsigned nref = 0;
     if (d2 < A.rb2 &&
-        collide_full(cmat[g].m, dx, dy, dz, gq, &cm64[g], px, py, pz, A.x, A.y, A.z, nref)) {
+        collide_full(cmat[g].m, dx, dy, dz, gq, &csrc[g], rb, px, py, pz, A.x, A.y, A.z, nref)) {
         long long orig = __float_as_int(cmat[g].m[9]);
         unsigned long long bit = (unsigned long long)(i * N + orig);
         atomicOr(&mask[bit >> 5], 1u << (bit & 31));
@@ -560,7 +560,7 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
         int tps = (int)((ntiles + splits - 1) / splits);
         splits = (ntiles + tps - 1) / tps;
         dim3 grid(wblocks, (unsigned)splits);
-        note_launch(), k_col_dense<<<grid, kDenseColThreads, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->cmat64,
+        note_launch(), k_col_dense<<<grid, kDenseColThreads, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->csrc, m->robot,
                                                        m->n_col_pad, tps, m->gq, first_col, wp_col, all_wp, stats);
     } else {
         if (m->n_col == 0) return cudaGetLastError();
@@ -571,7 +571,7 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
         int blocks = (K + kWarps - 1) / kWarps;
         int cap = g_sms * g_occ_col;
         if (blocks > cap) blocks = cap;
-        note_launch(), k_col_culled<<<blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->cmat64,
+        note_launch(), k_col_culled<<<blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->csrc, m->robot,
                                                      m->cstart, g, m->gq, first_col, wp_col, all_wp, counter, stats);
     }
     return cudaGetLastError();
@@ -645,7 +645,7 @@ cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaS
     long long tot = KT * m->n_col;
     if (tot == 0) return cudaSuccess;
     note_launch(), k_pair_mask<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tr->x, tr->y, tr->z, KT, m->n, m->crec, m->cmat,
-                                                                m->cmat64, m->n_col, m->gq, mask);
+                                                                m->csrc, m->robot, m->n_col, m->gq, mask);
     return cudaGetLastError();
 }
 
