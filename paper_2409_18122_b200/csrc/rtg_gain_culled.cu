@@ -66,18 +66,21 @@ __device__ __forceinline__ void cut(const float4& C, float Cj, float& plo, float
     }
 }
 
-// acc += q, pc += inc when p (predicated: no selects in the hot loop)
-__device__ __forceinline__ void add_if(bool p, double& acc, double q, int& pc, int inc) {
-    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.f64 %0, %0, %2;\n\t@pp add.s32 %1, %1, %3;\n\t}"
-        : "+d"(acc), "+r"(pc)
-        : "d"(q), "r"(inc), "r"((int)p));
+// acc += u_q and pc += class increment of record word uc when p (64-bit exact integer sum)
+__device__ __forceinline__ void add_if(bool p, unsigned long long& acc, unsigned uc, int& pc) {
+    unsigned lo = (unsigned)acc, hi = (unsigned)(acc >> 32);
+    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.cc.u32 %0, %0, %3;\n\t@pp addc.u32 %1, %1, 0;\n\t}"
+        : "+r"(lo), "+r"(hi)
+        : "r"(0), "r"(uc & kUqMask), "r"((int)p));
+    acc = ((unsigned long long)hi << 32) | lo;
+    if (p) pc += uc_inc(uc);
 }
 
 template <bool kStats>
 __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
-    const GRec* __restrict__ grec, const double* __restrict__ guq, const int* __restrict__ gstartA,
+    const GRec* __restrict__ grec, const int* __restrict__ gstartA,
     const int* __restrict__ gtabB, const int2* __restrict__ zocc, const TabP* __restrict__ gtabP, const GainK g,
     const CamK cam, long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
     int* __restrict__ counter, unsigned long long* __restrict__ stats) {
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
         if (e >= L) break;
         const int i = list[e];
         const float px = X[i], py = Y[i], pz = Zw[i], yw = Yaw[i];
-        double acc = 0.0;            // sum of u_q over visible Gaussians (exact integer)
+        unsigned long long acc = 0;  // sum of u_q over visible Gaussians (exact integer)
         int acch = 0, accl = 0, pc = 0;
         if (isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(yw)) {
             WpF f;
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         const int a2 = !in ? a3 : (j1 == q1 ? a3 : __ldg(sb + (j1 + 1) * g.nz));
                         if (in) {
                             const TabP hi = gtabP[ub0 + (j1 + 1) * g.nz], lo = gtabP[ub0 + j0 * g.nz];
-                            acc += hi.q - lo.q;
+                            acc += (unsigned long long)__double2ll_rn(hi.q - lo.q);
                             acch += hi.nh - lo.nh;
                             accl += hi.nl - lo.nl;
                             if (kStats) nagg += 1;
@@ -341,7 +344,6 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_le)];
                             const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_le)];
                             const GRec Ga = grec[gia], Gb = grec[gib];
-                            const double qa = guq[gia], qb = guq[gib];
                             float Za, Zb;
                             const float ma = vis_margin(f, cam, Ga.x, Ga.y, Ga.z, Za);
                             const float mb = vis_margin(f, cam, Gb.x, Gb.y, Gb.z, Zb);
@@ -362,8 +364,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             }
                             visa = visa && gpa < tot;
                             visb = visb && gpb < tot;
-                            add_if(visa, acc, qa, pc, Ga.inc);
-                            add_if(visb, acc, qb, pc, Gb.inc);
+                            add_if(visa, acc, Ga.uc, pc);
+                            add_if(visb, acc, Gb.uc, pc);
                             if (kStats) nvis += (unsigned)visa + (unsigned)visb;
                             r0 += na + __popc(hhi) + (__any_sync(kFullG, pa == 64 || pb == 64) ? 1 : 0);
                         }
@@ -451,11 +453,11 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     if (blocks < 1) blocks = 1;
     if (stats)
         note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
             cam, wp_gq, wp_nh, wp_nl, counter, stats);
     else
         note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->guq, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
+            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
             cam, wp_gq, wp_nh, wp_nl, counter, stats);
     return cudaGetLastError();
 }

@@ -54,6 +54,8 @@ cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_
 cudaError_t exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t st);
 // n pairs (in[2i], in[2i+1]) scanned together into out[0 .. 2n+1]
 cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st);
+// copy-B records' (u_q, nH | nL << 32) pairs (from GRec::uc) scanned into out[0 .. 2n+1]
+cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st);
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
@@ -74,10 +76,9 @@ struct rtg_map_s {
     unsigned char* flags = nullptr;      // [n] or null
     // visibility records: copy A at [0, n_gain) (sorted by (iy, ix)), padded to n_gain_pad (a
     // multiple of kTile) with NaN means, then copy B at [n_gain_pad, n_gain_pad + n_gain) (sorted
-    // by (iy, iz, ix)), padded likewise.  guq / gidx are parallel to grec.
+    // by (iy, iz, ix)), padded likewise.  gidx is parallel to grec.
     long long n_gain_pad = 0;
     rtg::GRec* grec = nullptr;           // [2 * n_gain_pad]
-    double* guq = nullptr;               // fixed-point u per record (an exact integer < 2^53)
     int* gidx = nullptr;                 // original index per record
     int* gstartA = nullptr;              // [ncellsA + 1] first copy-A record of column (iy, ix)
     int* gtabB = nullptr;                // [ny][nx + 1][nz] first copy-B record (relative to n_gain_pad) of

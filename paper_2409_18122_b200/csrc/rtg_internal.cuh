@@ -10,8 +10,8 @@
 //  * visibility: min slack m32 of the folded frustum (|Z - zmid| <= zhalf,
 //    |X - kxc Z| <= kxh Z, |dz - kyc Z| <= kyh Z); pairs with |m32| < gam*Z + g0 are
 //    re-decided in FP64 with the six pinhole slacks (O3).  gam, g0 bound the FP32 error.
-//  * gains: u_q = round(u * 2^S) with S chosen so that the sum over ALL eligible Gaussians is
-//    < 2^53: every partial sum is an exact integer in FP64 (associative -> order free).
+//  * gains: u_q = round(u * 2^S) < 2^30 with S chosen so that the sum over ALL eligible Gaussians
+//    is < 2^53: every partial sum is an exact integer in FP64 (associative -> order free).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,9 +24,15 @@ constexpr int kTile = 512;           // dense-mode Gaussians per smem tile
 constexpr int kZoccX = 64;           // x-cells per block of the visibility grid's z-occupancy table
 
 // ------------------------------------------------------------------ records
-// visibility record (sorted by visibility cell): mean + packed class increment
-//   inc = 1 (class H), 0x10000 (class L), 0 (O)  -- per-lane int32 partials flush often
-struct __align__(16) GRec { float x, y, z; int inc; };
+// visibility record (sorted by visibility cell): mean + uc = u_q | class << 30 with u_q the
+// fixed-point u (< 2^30, exact integer) and class 1 (H), 2 (L), 0 (O)
+struct __align__(16) GRec { float x, y, z; unsigned uc; };
+constexpr unsigned kUqMask = 0x3fffffffu;
+// per-lane packed class counter increment of uc: 1 (H), 0x10000 (L), 0 (O)
+__device__ __forceinline__ int uc_inc(unsigned uc) {
+    const int c = (int)(uc >> 30);
+    return c + (c >> 1) * 0xfffe;
+}
 // collision record (sorted by collision cell): mean + inflated bounding radius^2
 struct __align__(16) CRec { float x, y, z, rb2; };
 // M rows (FP32): m[0..8] row-major, m[9] = original index (as int bits), pad

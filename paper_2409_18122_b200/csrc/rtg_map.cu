@@ -170,8 +170,10 @@ __global__ void k_bounds(long long n, const float* __restrict__ means, const flo
     }
 }
 
-__device__ __forceinline__ int cell_coord(float v, double o, double h, int nmax) {
-    int c = (int)floor(((double)v - o) / h);
+// cell of coordinate v on a grid with origin o and inverse cell size ih (FP64; the culled kernels
+// allow for eps around the cell boundaries, so ih may be rounded)
+__device__ __forceinline__ int cell_coord(float v, double o, double ih, int nmax) {
+    int c = (int)floor(((double)v - o) * ih);
     return c < 0 ? 0 : (c >= nmax ? nmax - 1 : c);
 }
 
@@ -186,15 +188,16 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
                        GainGrid gg, ColGrid cg, int* __restrict__ gkey, int* __restrict__ ckey,
                        int* __restrict__ gcountA, int* __restrict__ gcountB, int2* __restrict__ zocc,
                        int* __restrict__ ccount) {
+    const double igx = 1.0 / gg.hx, igy = 1.0 / gg.hy, igz = 1.0 / gg.hz, icg = 1.0 / cg.h;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         float x = means[i], y = means[n + i], z = means[2 * n + i];
         unsigned f = flags ? flags[i] : 0u;
         int gk = -1, ck = -1;
         if (!(f & RTG_G_NO_GAIN)) {
-            int ix = cell_coord(x, gg.ox, gg.hx, gg.nx);
-            int iy = cell_coord(y, gg.oy, gg.hy, gg.ny);
-            int iz = cell_coord(z, gg.oz, gg.hz, gg.nz);
+            int ix = cell_coord(x, gg.ox, igx, gg.nx);
+            int iy = cell_coord(y, gg.oy, igy, gg.ny);
+            int iz = cell_coord(z, gg.oz, igz, gg.nz);
             gk = (int)(((long long)iy * gg.nz + iz) * gg.nx + ix);
             atomicAdd(&gcountB[gk], 1);
             atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);
@@ -203,9 +206,9 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
             if (iz > zo->y) atomicMax(&zo->y, iz);
         }
         if (!(f & RTG_G_NO_COLLIDE)) {
-            int ix = cell_coord(x, cg.ox, cg.h, cg.nx);
-            int iy = cell_coord(y, cg.oy, cg.h, cg.ny);
-            int iz = cell_coord(z, cg.oz, cg.h, cg.nz);
+            int ix = cell_coord(x, cg.ox, icg, cg.nx);
+            int iy = cell_coord(y, cg.oy, icg, cg.ny);
+            int iz = cell_coord(z, cg.oz, icg, cg.nz);
             ck = (int)(((long long)iz * cg.ny + iy) * cg.nx + ix);
             atomicAdd(&ccount[ck], 1);
         }
@@ -214,17 +217,32 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
     }
 }
 
-// both visibility copies: A at cursorA (relative to 0), B at offB + cursorB
-__global__ void k_scatter_gain(long long n, const float* __restrict__ means, const int* __restrict__ gkey,
-                               GainGrid gg, int* __restrict__ cursorA, int* __restrict__ cursorB, long long offB,
-                               GRec* __restrict__ grec, int* __restrict__ gidx) {
+__device__ __forceinline__ double u_of(float w, int variant) {
+    double u = (double)w;
+    return variant == RTG_VARIANT_SQ ? u * u : u;
+}
+
+// packed record word uc = u_q | class << 30 of a Gaussian with weight w (a2): class 1 (H,
+// u > tau_hi), 2 (L, u < tau_lo), 0 (O); u_q = round(u 2^S) < 2^30
+__device__ __forceinline__ unsigned class_of(float w, int variant, const ClassState* __restrict__ cs) {
+    const double u = u_of(w, variant);
+    const unsigned c = u > cs->tau_hi ? 1u : (u < cs->tau_lo ? 2u : 0u);
+    return (unsigned)llrint(u * cs->scale) | (c << 30);
+}
+
+// both visibility copies: A at cursorA (relative to 0), B at offB + cursorB, with their packed
+// class and fixed-point u (the classification statistics are computed before the scatter)
+__global__ void k_scatter_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
+                               const int* __restrict__ gkey, GainGrid gg, int* __restrict__ cursorA,
+                               int* __restrict__ cursorB, long long offB, GRec* __restrict__ grec,
+                               int* __restrict__ gidx, int variant, const ClassState* __restrict__ cs) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int k = gkey[i];
         if (k < 0) continue;
         const long long nzx = (long long)gg.nz * gg.nx;
         const long long iy = k / nzx, ix = k % gg.nx;
-        const GRec r{means[i], means[n + i], means[2 * n + i], 0};
+        const GRec r{means[i], means[n + i], means[2 * n + i], class_of(w[i], variant, cs)};
         int sa = atomicAdd(&cursorA[iy * gg.nx + ix], 1);
         int sb = atomicAdd(&cursorB[k], 1);
         grec[sa] = r;
@@ -264,14 +282,13 @@ __global__ void k_scatter_col(long long n, const float* __restrict__ means, cons
 }
 
 // NaN padding of both copies: [from, to) and [offB + from, offB + to)
-__global__ void k_pad_gain(GRec* grec, double* guq, int* gidx, long long from, long long to, long long offB) {
+__global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to, long long offB) {
     long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < to) {
         float nan = __int_as_float(0x7fc00000);
         for (int c = 0; c < 2; ++c) {
             long long j = i + c * offB;
-            grec[j] = GRec{nan, nan, nan, 0};
-            guq[j] = 0.0;
+            grec[j] = GRec{nan, nan, nan, 0u};
             gidx[j] = -1;
         }
     }
@@ -297,10 +314,6 @@ __global__ void k_pad_col(CRec* crec, CMat* cmat, CSrc* csrc, long long from, lo
 
 // ------------------------------------------------------------------ classification (a2)
 
-__device__ __forceinline__ double u_of(float w, int variant) {
-    double u = (double)w;
-    return variant == RTG_VARIANT_SQ ? u * u : u;
-}
 
 // deterministic block tree over a fixed contiguous chunk
 __device__ double block_sum(double v, double* sh) {
@@ -400,7 +413,8 @@ __global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassS
         int shift = 0;
         double tot = cnt * umax;
         if (tot > 0.0) {
-            shift = (int)floor(52.0 - log2(tot));   // sum of all u_q < 2^53: exact in FP64
+            // sum of all u_q < 2^53 (exact in FP64) and every u_q < 2^30 (packed with the class)
+            shift = (int)floor(fmin(52.0 - log2(tot), 29.0 - log2(umax)));
             shift = shift > 1000 ? 1000 : (shift < -1000 ? -1000 : shift);
         }
         cs->shift = shift;
@@ -411,30 +425,13 @@ __global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassS
 
 // class increments and fixed-point u per visibility record (both copies); copy B also
 // writes u_q and the packed class count for its exact prefixes
-__global__ void k_class_records(long long n_rec, long long offB, GRec* __restrict__ grec, double* __restrict__ guq,
-                                long long* __restrict__ qhlB, const int* __restrict__ gidx,
+__global__ void k_class_records(long long n_rec, GRec* __restrict__ grec, const int* __restrict__ gidx,
                                 const float* __restrict__ w, int variant, const ClassState* __restrict__ cs) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n_rec) return;
     const int g = gidx[i];
     if (g < 0) return;
-    double u = u_of(w[g], variant);
-    int inc = 0;
-    long long hl = 0;
-    if (u > cs->tau_hi) {
-        inc = 1;
-        hl = 1;
-    } else if (u < cs->tau_lo) {
-        inc = 0x10000;
-        hl = 1LL << 32;
-    }
-    grec[i].inc = inc;
-    long long q = llrint(u * cs->scale);
-    guq[i] = (double)q;   // exact: q < 2^53
-    if (i >= offB) {
-        qhlB[2 * (i - offB)] = q;
-        qhlB[2 * (i - offB) + 1] = hl;
-    }
+    grec[i].uc = class_of(w[g], variant, cs);
 }
 
 // copy-B start table in z-fastest layout [iy][ix][iz], ix = 0..nx (ix = nx: end of the z-slab):
@@ -464,52 +461,63 @@ inline unsigned nblocks(long long n, int t) {
 
 }  // namespace
 
+// a2 statistics over the gain-eligible Gaussians in input order (deterministic FP64 two-pass
+// mean / population std) -> thresholds and fixed-point scale in cls
+static cudaError_t class_stats(long long n, const float* w, const unsigned char* flags, int variant, double k_sigma,
+                               double tau_hi, double tau_lo, ClassState* cls, double* scratch, cudaStream_t st) {
+    const bool has_hi = !std::isnan(tau_hi), has_lo = !std::isnan(tau_lo);
+    const int nparts = kRedBlocks;
+    note_launch(), k_red1<<<nparts, kRedThreads, 0, st>>>(n, w, flags, variant, scratch);
+    note_launch(), k_red1_final<<<1, kRedThreads, 0, st>>>(scratch, nparts, cls);
+    note_launch(), k_red2<<<nparts, kRedThreads, 0, st>>>(n, w, flags, variant, cls, scratch);
+    note_launch(), k_red2_final<<<1, kRedThreads, 0, st>>>(scratch, nparts, cls, k_sigma, tau_hi, tau_lo, has_hi, has_lo);
+    return cudaGetLastError();
+}
+
+// exact prefixes of copy B's (u_q, packed class count) pairs, gathered at the table entries
+static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st) {
+    const long long ng = m->n_gain;
+    long long* pqhl = nullptr;
+    cudaError_t e = dev_alloc((void**)&pqhl, 2 * sizeof(long long) * (ng + 1), st);
+    if (e != cudaSuccess) return e;
+    e = exclusive_scan_grec_uc(m->grec + m->n_gain_pad, pqhl, ng, st);
+    if (e == cudaSuccess) {
+        const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
+        note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, (const longlong2*)pqhl, m->gtabP);
+        e = cudaGetLastError();
+    }
+    dev_free(pqhl, st);
+    return e;
+}
+
+static void set_class_params(rtg_map_s* m, int variant, double k_sigma, double tau_hi, double tau_lo) {
+    m->cls_variant = variant;
+    m->cls_k = k_sigma;
+    m->cls_th_nan = std::isnan(tau_hi);
+    m->cls_tl_nan = std::isnan(tau_lo);
+    m->cls_th = tau_hi;
+    m->cls_tl = tau_lo;
+}
+
 rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi, double tau_lo,
                         cudaStream_t st) {
     bool has_hi = !std::isnan(tau_hi), has_lo = !std::isnan(tau_lo);
     if (m->cls_variant == variant && m->cls_k == k_sigma && m->cls_th_nan == !has_hi &&
         m->cls_tl_nan == !has_lo && (!has_hi || m->cls_th == tau_hi) && (!has_lo || m->cls_tl == tau_lo))
         return RTG_OK;
-    int nparts = kRedBlocks;
-    note_launch(), k_red1<<<nparts, kRedThreads, 0, st>>>(m->n, m->w_orig, m->flags, variant, m->red_scratch);
-    note_launch(), k_red1_final<<<1, kRedThreads, 0, st>>>(m->red_scratch, nparts, m->cls);
-    note_launch(), k_red2<<<nparts, kRedThreads, 0, st>>>(m->n, m->w_orig, m->flags, variant, m->cls, m->red_scratch);
-    note_launch(), k_red2_final<<<1, kRedThreads, 0, st>>>(m->red_scratch, nparts, m->cls, k_sigma, tau_hi, tau_lo, has_hi,
-                                            has_lo);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        set_error("classify: %s", cudaGetErrorString(e));
-        return RTG_ERR_CUDA;
-    }
-    long long ng = m->n_gain;
-    long long *qhlB = nullptr, *pqhl = nullptr;
-    if (dev_alloc((void**)&qhlB, 2 * sizeof(long long) * (ng + 1), st) != cudaSuccess ||
-        dev_alloc((void**)&pqhl, 2 * sizeof(long long) * (ng + 1), st) != cudaSuccess) {
-        set_error("classify: out of device memory");
-        return RTG_ERR_OUT_OF_MEMORY;
-    }
+    cudaError_t e = class_stats(m->n, m->w_orig, m->flags, variant, k_sigma, tau_hi, tau_lo, m->cls, m->red_scratch, st);
     const long long nrec = 2 * m->n_gain_pad;
-    if (ng > 0)
-        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->n_gain_pad, m->grec, m->guq, qhlB,
-                                                                           m->gidx, m->w_orig, variant, m->cls);
-    e = exclusive_scan_i64x2(qhlB, pqhl, ng, st);
-    if (e == cudaSuccess) {
-        const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
-        note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, (const longlong2*)pqhl, m->gtabP);
+    if (e == cudaSuccess && m->n_gain > 0) {
+        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->grec, m->gidx, m->w_orig, variant,
+                                                                           m->cls);
         e = cudaGetLastError();
     }
-    dev_free(qhlB, st);
-    dev_free(pqhl, st);
+    if (e == cudaSuccess) e = class_prefix(m, st);
     if (e != cudaSuccess) {
         set_error("classify: %s", cudaGetErrorString(e));
-        return RTG_ERR_CUDA;
+        return e == cudaErrorMemoryAllocation ? RTG_ERR_OUT_OF_MEMORY : RTG_ERR_CUDA;
     }
-    m->cls_variant = variant;
-    m->cls_k = k_sigma;
-    m->cls_th_nan = !has_hi;
-    m->cls_tl_nan = !has_lo;
-    m->cls_th = tau_hi;
-    m->cls_tl = tau_lo;
+    set_class_params(m, variant, k_sigma, tau_hi, tau_lo);
     return RTG_OK;
 }
 
@@ -548,13 +556,26 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     // --- bounds + validation (one sync)
     DevBounds* db = nullptr;
     MAP_CK(dev_alloc((void**)&db, sizeof(DevBounds), st));
+    // the default classification's statistics (k = 1/2, derived thresholds) depend only on
+    // the inputs: they run while the host reads the bounds back, and the scatter then writes final
+    // records (class increments, fixed-point u)
+    MAP_CK(map_alloc(m, &m->cls, 1, st));
+    MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
     note_launch(), k_bounds_init<<<1, 1, 0, st>>>(db);
     if (n > 0)
         note_launch(), k_bounds<<<nblocks(n, 256) > 592 ? 592 : nblocks(n, 256), 256, 0, st>>>(
                            n, means, quats, scales, opacity, w, flags, rb, db);
     DevBounds hb;
     MAP_CK(cudaMemcpyAsync(&hb, db, sizeof(DevBounds), cudaMemcpyDeviceToHost, st));
-    MAP_CK(cudaStreamSynchronize(st));
+    cudaEvent_t ev;
+    MAP_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    MAP_CK(cudaEventRecord(ev, st));
+    MAP_CK(class_stats(n, w, flags, RTG_VARIANT_XI, 0.5, NAN, NAN, m->cls, m->red_scratch, st));
+    {
+        cudaError_t es = cudaEventSynchronize(ev);
+        cudaEventDestroy(ev);
+        MAP_CK(es);
+    }
     dev_free(db, st);
     if (hb.err) {
         set_error("rtg_map_create: invalid element(s):%s%s%s%s%s", (hb.err & 1) ? " non-finite mean" : "",
@@ -624,7 +645,6 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->w_orig, n, st));
     if (flags) MAP_CK(map_alloc(m, &m->flags, n, st));
     MAP_CK(map_alloc(m, &m->grec, 2 * m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->guq, 2 * m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gidx, 2 * m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gstartA, gg.ncellsA + 1, st));
     MAP_CK(map_alloc(m, &m->gtabB, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
@@ -634,8 +654,6 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->csrc, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
-    MAP_CK(map_alloc(m, &m->cls, 1, st));
-    MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
     if (n > 0) MAP_CK(cudaMemcpyAsync(m->w_orig, w, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
     if (flags && n > 0) MAP_CK(cudaMemcpyAsync(m->flags, flags, n, cudaMemcpyDeviceToDevice, st));
     // --- counting sort into both grids
@@ -667,14 +685,14 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     }
     MAP_CK(cudaMemcpyAsync(ccount, m->cstart, sizeof(int) * cg.ncells, cudaMemcpyDeviceToDevice, st));
     if (n > 0) {
-        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, gkey, gg, gcountA, gcountB, m->n_gain_pad, m->grec,
-                                                          m->gidx);
+        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, gg, gcountA, gcountB, m->n_gain_pad,
+                                                          m->grec, m->gidx, RTG_VARIANT_XI, m->cls);
         note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, ccount, rb, gq, m->crec, m->cmat,
                                           m->csrc);
     }
     if (m->n_gain_pad > m->n_gain)
         note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
-                           m->grec, m->guq, m->gidx, m->n_gain, m->n_gain_pad, m->n_gain_pad);
+                           m->grec, m->gidx, m->n_gain, m->n_gain_pad, m->n_gain_pad);
     if (m->n_col_pad > m->n_col)
         note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, m->n_col,
                                                                          m->n_col_pad);
@@ -686,8 +704,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     dev_free(gstartB, st);
     dev_free(ccount, st);
     // --- default classification (k = 1/2, derived thresholds)
-    m->cls_variant = -1;
-    return classify_map(m, RTG_VARIANT_XI, 0.5, NAN, NAN, st);
+    MAP_CK(class_prefix(m, st));
+    set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
+    return RTG_OK;
 }
 
 }  // namespace rtg

@@ -69,8 +69,24 @@ __device__ T block_exclusive_scan(T v, T* sh, T& total) {
 
 // status of tile t: flag[t] = 0 (nothing yet), 1 (aggregate published), 2 (inclusive prefix
 // published); the value is written before the flag, separated by a fence
+// input loaders
 template <typename T>
-__global__ void __launch_bounds__(kScanThreads) k_scan(const T* __restrict__ in, T* __restrict__ out, long long n,
+struct LoadArr {
+    const T* __restrict__ p;
+    __device__ T operator()(long long j) const { return p[j]; }
+};
+// copy-B record -> (u_q, packed class count nH | nL << 32)
+struct LoadUc {
+    const GRec* __restrict__ p;
+    __device__ I64x2 operator()(long long j) const {
+        const unsigned uc = p[j].uc;
+        const unsigned c = uc >> 30;
+        return I64x2((long long)(uc & kUqMask), c == 1u ? 1LL : (c == 2u ? (1LL << 32) : 0LL));
+    }
+};
+
+template <typename T, typename Load>
+__global__ void __launch_bounds__(kScanThreads) k_scan(Load in, T* __restrict__ out, long long n,
                                                         int* __restrict__ ticket, volatile int* flag, T* agg, T* inc) {
     __shared__ T sh[kScanThreads / 32];
     __shared__ T s_prefix;
@@ -84,7 +100,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const T* __restrict__ in,
 #pragma unroll
     for (int i = 0; i < kScanPer; ++i) {
         const long long j = base + i;
-        loc[i] = j < n ? in[j] : T(0);
+        loc[i] = j < n ? in(j) : T(0);
         s += loc[i];
     }
     T total;
@@ -146,8 +162,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const T* __restrict__ in,
 template <typename T>
 __global__ void k_scan_empty(T* out) { out[0] = T(0); }
 
-template <typename T>
-cudaError_t scan_impl(const T* in, T* out, long long n, cudaStream_t st) {
+template <typename T, typename Load>
+cudaError_t scan_impl(Load in, T* out, long long n, cudaStream_t st) {
     if (n <= 0) {
         note_launch(), k_scan_empty<T><<<1, 1, 0, st>>>(out);
         return cudaGetLastError();
@@ -165,7 +181,7 @@ cudaError_t scan_impl(const T* in, T* out, long long n, cudaStream_t st) {
     T* inc = agg + nt;
     e = cudaMemsetAsync(mem, 0, fb, st);
     if (e != cudaSuccess) return e;
-    note_launch(), k_scan<T><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, ticket, flags, agg, inc);
+    note_launch(), k_scan<T, Load><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, ticket, flags, agg, inc);
     e = cudaGetLastError();
     dev_free(mem, st);
     return e;
@@ -174,14 +190,17 @@ cudaError_t scan_impl(const T* in, T* out, long long n, cudaStream_t st) {
 }  // namespace
 
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_t st) {
-    return scan_impl<int>(in, out, n, st);
+    return scan_impl<int>(LoadArr<int>{in}, out, n, st);
 }
 cudaError_t exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t st) {
-    return scan_impl<long long>(in, out, n, st);
+    return scan_impl<long long>(LoadArr<long long>{in}, out, n, st);
 }
 // pairs of int64 (in[2i], in[2i+1]) scanned together
 cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st) {
-    return scan_impl<I64x2>(reinterpret_cast<const I64x2*>(in), reinterpret_cast<I64x2*>(out), n, st);
+    return scan_impl<I64x2>(LoadArr<I64x2>{reinterpret_cast<const I64x2*>(in)}, reinterpret_cast<I64x2*>(out), n, st);
+}
+cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
+    return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);
 }
 
 }  // namespace rtg

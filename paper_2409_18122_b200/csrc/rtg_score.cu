@@ -289,11 +289,10 @@ constexpr int kDenseGainWpt = 4;
 __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, int list_n, const GRec* __restrict__ grec,
-    const double* __restrict__ guq, long long n_gain_pad, int tiles_per_split, CamK cam,
+    long long n_gain_pad, int tiles_per_split, CamK cam,
     unsigned long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
     unsigned long long* __restrict__ stats) {
     __shared__ __align__(128) GRec s_rec[2][kTile];
-    __shared__ __align__(128) double s_uq[2][kTile];
     __shared__ __align__(8) uint64_t s_bar[2];
     const long long tile0 = (long long)blockIdx.y * tiles_per_split;
     long long ntiles = n_gain_pad / kTile - tile0;
@@ -325,12 +324,11 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
         fence_mbar_init();
     }
     __syncthreads();
-    const uint32_t rb = kTile * sizeof(GRec), qb = kTile * sizeof(double);
+    const uint32_t rb = kTile * sizeof(GRec);
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2 && s < ntiles; ++s) {
-            mbar_expect_tx(&s_bar[s], rb + qb);
+            mbar_expect_tx(&s_bar[s], rb);
             bulk_g2s(s_rec[s], grec + (tile0 + s) * kTile, rb, &s_bar[s]);
-            bulk_g2s(s_uq[s], guq + (tile0 + s) * kTile, qb, &s_bar[s]);
         }
     }
     unsigned nref = 0;
@@ -341,16 +339,16 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
 #pragma unroll
         for (int j = 0; j < kDenseGainWpt; ++j) pc[j] = 0;
         const GRec* rec = s_rec[s];
-        const double* uq = s_uq[s];
 #pragma unroll 2
         for (int g = 0; g < kTile; ++g) {
             const GRec G = rec[g];
-            const double q = uq[g];
+            const double q = __uint2double_rn(G.uc & kUqMask);
+            const int inc = uc_inc(G.uc);
 #pragma unroll
             for (int j = 0; j < kDenseGainWpt; ++j) {
                 if (visible(wf[j], cam, G.x, G.y, G.z, nref)) {
                     accq[j] += q;
-                    pc[j] += G.inc;
+                    pc[j] += inc;
                 }
             }
         }
@@ -361,9 +359,8 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
         }
         __syncthreads();
         if (threadIdx.x == 0 && it + 2 < ntiles) {
-            mbar_expect_tx(&s_bar[s], rb + qb);
+            mbar_expect_tx(&s_bar[s], rb);
             bulk_g2s(s_rec[s], grec + (tile0 + it + 2) * kTile, rb, &s_bar[s]);
-            bulk_g2s(s_uq[s], guq + (tile0 + it + 2) * kTile, qb, &s_bar[s]);
         }
     }
 #pragma unroll
@@ -613,7 +610,7 @@ cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& c
         int tps = (int)((ntiles + splits - 1) / splits);
         splits = (ntiles + tps - 1) / tps;
         dim3 grid(wblocks, (unsigned)splits);
-        note_launch(), k_gain_dense<<<grid, kDenseGainThreads, 0, st>>>(tr->x, tr->y, tr->z, tr->yaw, list, n, m->grec, m->guq,
+        note_launch(), k_gain_dense<<<grid, kDenseGainThreads, 0, st>>>(tr->x, tr->y, tr->z, tr->yaw, list, n, m->grec,
                                                          m->n_gain_pad, tps, cam, (unsigned long long*)wp_gq, wp_nh,
                                                          wp_nl, stats);
     } else {
