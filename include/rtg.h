@@ -131,10 +131,10 @@ typedef struct {
  * z-cells of height gain_cell_z (the culled gain kernel tests individually only Gaussians of
  * cells that straddle the frustum, so thinner rows mean fewer tests but more rows). */
 typedef struct {
-    float gain_cell_xy;  /* visibility grid row height (y) [m]    (default 0.25)           */
-    float gain_cell_z;   /* visibility grid cell height (z) [m]   (default 1.0)            */
+    float gain_cell_xy;  /* visibility grid row height (y) [m]    (default 0.3)            */
+    float gain_cell_z;   /* visibility grid cell height (z) [m]   (default 1.5)            */
     float col_cell;      /* collision grid cell edge [m]          (default max(0.5, r_b/2)) */
-    float gain_cell_x;   /* visibility grid cell width (x) [m]    (default gain_cell_xy/2) */
+    float gain_cell_x;   /* visibility grid cell width (x) [m]    (default gain_cell_xy/4) */
 } rtg_map_options;
 
 /* Read-only facts about a built map (rtg_map_info). */

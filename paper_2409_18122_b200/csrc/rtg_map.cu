@@ -591,9 +591,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     double gq = (104.0 * rho + 6.0) * u32;   // FP32 error bound of q near 1, x2
     m->gq = (float)gq;
     // --- grid geometry
-    double hy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.25;
-    double hx = (opt && opt->gain_cell_x > 0) ? opt->gain_cell_x : 0.5 * hy;
-    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 1.0;
+    double hy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.3;
+    double hx = (opt && opt->gain_cell_x > 0) ? opt->gain_cell_x : 0.25 * hy;
+    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 1.5;
     GainGrid& gg = m->gg;
     if (m->n_gain > 0) {
         float lo[3], hi[3];
