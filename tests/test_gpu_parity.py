@@ -364,3 +364,42 @@ def test_determinism_and_shard_emulation(R, room):
         top = max(b[0] for b in best)
         g_best = min(b[1] for b in best if b[0] == top)
         assert (top, g_best) == full["best"]
+
+
+# ----------------------------------------------------------------- culled kernel geometry edge cases
+
+@pytest.mark.parametrize("cells", [None, (0.5, 0.5, 0.5, 0.5), (0.1, 3.0, 0.0, 0.3), (1.0, 0.25, 0.0, 0.05)])
+def test_culled_equals_dense_axis_yaws_offcentre_cameras(R, room, cells):
+    """The culled kernel's row / column intervals divide by the x-coefficient of each frustum plane,
+    which is exactly 0 at axis-aligned yaws; its cell classification must still be exact for any
+    grid shape and for off-centre principal points.  Gains are exact integers, so culled must equal
+    dense bit for bit (dense is pinned to the oracle by the other tests)."""
+    import dataclasses
+    rng = np.random.default_rng(11)
+    k = np.arange(0, room.K, 97)[:8]
+    T = 12
+    yaws = np.array([0.0, np.pi / 2, np.pi, -np.pi / 2, np.pi / 4, -3 * np.pi / 4, 1e-7, np.pi / 2 + 1e-6,
+                     2.0, -2.5, 0.3, -1.0], np.float32)
+    x = room.x[k, :T].copy()
+    y = room.y[k, :T].copy()
+    z = room.z[k, :T].copy()
+    yaw = np.tile(yaws, (len(k), 1)).astype(np.float32)
+    yaw[1::2] = rng.uniform(-np.pi, np.pi, (len(k) // 2, T)).astype(np.float32)
+    cams = [room.camera,
+            dataclasses.replace(room.camera, cx=0.3 * room.camera.width, cy=0.7 * room.camera.height),
+            dataclasses.replace(room.camera, cx=0.0, cy=float(room.camera.height), z_near=0.0)]
+    for cam in cams:
+        wl = dataclasses.replace(room, camera=cam)
+        out = {}
+        for mode in MODES:
+            m = R.map_from_workload(wl, options=cells if mode == "culled" else None)
+            tr = R.traj_from_workload(wl, x=x, y=y, z=z, yaw=yaw)
+            p = R.make_params(mode=_mode(R, mode), flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
+            d = R.score_debug(m, tr, wl.camera, p)
+            out[mode] = {kk: d[kk].cpu().numpy() for kk in ("wp_gain", "wp_nh", "wp_nl")}
+            m.close()
+            tr.close()
+        for kk in ("wp_nh", "wp_nl"):
+            assert np.array_equal(out["dense"][kk], out["culled"][kk]), (cam, cells, kk)
+        assert np.array_equal(out["dense"]["wp_gain"].view(np.int64), out["culled"]["wp_gain"].view(np.int64))
+        assert out["dense"]["wp_nh"].sum() > 0
