@@ -28,6 +28,11 @@ METRICS = [
     "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "smsp__sass_inst_executed_op_global_ld.sum",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed", "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_wait",
+    "smsp__pcsamp_warps_issue_stalled_short_scoreboard", "smsp__pcsamp_warps_issue_stalled_not_selected",
+    "smsp__pcsamp_warps_issue_stalled_selected", "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
 ]
 
 
@@ -77,6 +82,26 @@ def full(rep, out, key=None):
                 b += float(v.replace(",", "")) * mult.get(u, 1)
         short = name.split("::")[-1].split("<")[0]
         traffic[short] = b
+    # hottest CUDA source lines (instructions executed, warp stall samples): needs -lineinfo
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    cur, rows = None, []
+    for r in csv.reader(io.StringIO(src)):
+        if r and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if not r or not r[0].isdigit():
+            continue
+        try:
+            rows.append((float(r[7] or 0), float(r[4] or 0), cur, int(r[0]), r[1].strip()[:80]))
+        except (ValueError, IndexError):
+            pass
+    if rows:
+        ti = sum(x[0] for x in rows) or 1.0
+        ts = sum(x[1] for x in rows) or 1.0
+        lines.append("\n## hottest source lines: share of instructions executed, share of stall samples")
+        for n, st, f, ln, txt in sorted(rows, reverse=True)[:25]:
+            lines.append(f"{n / ti * 100:5.1f}% inst {st / ts * 100:5.1f}% stall  {f}:{ln}  {txt}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if key:
