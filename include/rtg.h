@@ -236,6 +236,63 @@ rtg_status rtg_score_debug(rtg_map map, rtg_traj traj, const rtg_camera* cam,
                            unsigned int* pair_mask, long long* stats, void* stream);
 
 /*
+ * ---------------------------------------------------------------- planner bookkeeping
+ *
+ * rtg_ledger_update -- N4, the uncertainty ledger: for each of n Gaussians,
+ * w_out[g] = ||mu_cur[g] - mu_prev[g]||_2 (norm of the fp32 differences taken in FP64, rounded
+ * to fp32) when any coordinate of the mean changed, w_prev[g] otherwise ("Gaussians that remain
+ * unchanged in the most recent update retain their previously computed displacement values").
+ * mu_prev, mu_cur [3][N] planar and w_prev [N] are host or device per `kind`; w_out [N] is a
+ * caller-owned device array (may equal w_prev when that is on the device).  Does not synchronise.
+ * Errors: RTG_ERR_INVALID_ARGUMENT (n < 0, NULL pointers, bad device).
+ */
+rtg_status rtg_ledger_update(int device, long long n, rtg_mem kind, const float* mu_prev, const float* mu_cur,
+                             const float* w_prev, float* w_out, void* stream);
+
+/*
+ * rtg_map_update_weights -- N4: replaces the map's information weights (the ledger, [N] in the
+ * map's input order, host or device per `kind`) without repacking its geometry, and reclassifies
+ * the map with its current classification parameters (a2).  Synchronises the stream once
+ * (validation).  Errors: RTG_ERR_INVALID_ARGUMENT on a NULL pointer or any weight that is
+ * non-finite or < 0 (the map is left unchanged); RTG_ERR_BAD_HANDLE; RTG_ERR_CUDA.
+ */
+rtg_status rtg_map_update_weights(rtg_map map, rtg_mem kind, const float* info_w, void* stream);
+
+/*
+ * rtg_region_utility -- N2: the enclosing space is partitioned into cuboidal
+ * regions of edge `size` (2.5 m in the paper) with lower corner origin[3] and dims[3]
+ * regions (flat index (iz * dims[1] + iy) * dims[0] + ix); a gain-eligible Gaussian (ground plane
+ * excluded) with mean mu lies in region floor((mu - origin) / size) (FP64) when that is
+ * inside dims.  count[r] = M_r, omega[r] = (1/M_r) sum_{g in r} w_g (0 for an empty region).  The
+ * sums are exact fixed-point integers (quantum 2^-S, S = floor(52 - log2(sum M * max w))), so the
+ * result is deterministic.  omega [prod dims] (double) and count [prod dims] (int) are caller-owned
+ * device arrays.  Does not synchronise.  Errors: RTG_ERR_INVALID_ARGUMENT (size <= 0, dims < 1,
+ * prod dims >= 2^31), RTG_ERR_BAD_HANDLE, RTG_ERR_CUDA.
+ */
+rtg_status rtg_region_utility(rtg_map map, const double origin[3], double size, const int dims[3], double* omega,
+                              int* count, void* stream);
+
+/*
+ * rtg_traj_view_ring -- N2 viewpoint placement: for each of R region
+ * centroids (planar [3][R], host or device per `kind`), n viewpoints on the circle of radius
+ * d = (size/2) / tan(min(hfov, vfov)/2) around the centroid in the plane z (hfov, vfov: the angles
+ * [0, W] and [0, H] subtend at the optical centre), at angles 2 pi j / n, heading towards the
+ * centroid: a trajectory handle with K = R * n, T = 1 (viewpoint v = r * n + j) that rtg_score
+ * scores as gain-only views (RTG_SCORE_NO_COLLISION).  *view_dist (or NULL) receives d.
+ * Errors: RTG_ERR_INVALID_ARGUMENT (R, n < 1, R * n >= 2^31, size <= 0, bad camera).
+ */
+rtg_status rtg_traj_view_ring(int device, int R, rtg_mem kind, const float* centroids, double size,
+                              const rtg_camera* cam, int n, float z, void* stream, rtg_traj* out, double* view_dist);
+
+/*
+ * rtg_cost_benefit -- N2 guidance selection: argmax over K viewpoints of
+ * omega[j] / e^{d[j]} (FP64; d = path distance to the viewpoint, omega = its utility), ties ->
+ * smaller d, then smaller j.  omega, d are device arrays of K >= 1 values.  Synchronises the
+ * stream.  Errors: RTG_ERR_INVALID_ARGUMENT (NULL pointers, K < 1), RTG_ERR_CUDA.
+ */
+rtg_status rtg_cost_benefit(const double* omega, const double* d, int K, void* stream, rtg_best_result* out);
+
+/*
  * Profiling (process-wide).  When enabled, every library phase is bracketed by CUDA events
  * recorded on the stream it is launched on; rtg_profile_read synchronises those events and
  * returns the accumulated device milliseconds and call counts per phase:

@@ -1,6 +1,7 @@
 // rtg_api.cu -- the extern "C" boundary of librtg (include/rtg.h): argument validation,
 // handle ownership, host<->device staging and launch orchestration.  No compute happens
 // here; every step of the path runs in the kernels of rtg_map.cu / rtg_score.cu.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -579,6 +580,139 @@ rtg_status rtg_best(const double* utility, int K, long long index_base, void* st
         set_error("rtg_best: no feasible trajectory");
         return RTG_ERR_NO_FEASIBLE;
     }
+    return RTG_OK;
+}
+
+// ---------------------------------------------------------------- planner bookkeeping (N2, N4)
+
+rtg_status rtg_ledger_update(int device, long long n, rtg_mem kind, const float* mu_prev, const float* mu_cur,
+                             const float* w_prev, float* w_out, void* stream) {
+    if (n < 0) return invalid("n must be >= 0");
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    if (n > 0 && (!mu_prev || !mu_cur || !w_prev || !w_out)) return invalid("mu_prev, mu_cur, w_prev, w_out required");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return invalid("invalid device ordinal (no CUDA device?)");
+    }
+    API_CK(cudaSetDevice(device), nullptr);
+    ensure_pool(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    float *dp = nullptr, *dc = nullptr, *dw = nullptr;
+    cudaError_t e = stage(mu_prev, 3 * (size_t)n, kind, &dp, st);
+    if (e == cudaSuccess) e = stage(mu_cur, 3 * (size_t)n, kind, &dc, st);
+    if (e == cudaSuccess) e = stage(w_prev, (size_t)n, kind, &dw, st);
+    if (e == cudaSuccess) e = launch_ledger(n, dp, dc, dw, w_out, st);
+    if (kind == RTG_MEM_HOST) {
+        dev_free(dp, st);
+        dev_free(dc, st);
+        dev_free(dw, st);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rtg_ledger_update", nullptr);
+    return RTG_OK;
+}
+
+rtg_status rtg_map_update_weights(rtg_map m, rtg_mem kind, const float* info_w, void* stream) {
+    rtg_status s = check_map(m);
+    if (s != RTG_OK) return s;
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    if (m->n > 0 && !info_w) return invalid("info_w is NULL");
+    API_CK(cudaSetDevice(m->device), nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = m->n;
+    float* dw = nullptr;
+    int* bad = nullptr;
+    API_CK(stage(info_w, (size_t)n, kind, &dw, st), &m->poisoned);
+    API_CK(dev_alloc((void**)&bad, sizeof(int), st), &m->poisoned);
+    API_CK(cudaMemsetAsync(bad, 0, sizeof(int), st), &m->poisoned);
+    API_CK(launch_check_weights(n, dw, bad, st), &m->poisoned);
+    int hbad = 0;
+    API_CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), &m->poisoned);
+    API_CK(cudaStreamSynchronize(st), &m->poisoned);
+    dev_free(bad, st);
+    if (hbad) {
+        if (kind == RTG_MEM_HOST) dev_free(dw, st);
+        return invalid("rtg_map_update_weights: info_w must be finite and >= 0");
+    }
+    if (n > 0) API_CK(cudaMemcpyAsync(m->w_orig, dw, sizeof(float) * n, cudaMemcpyDeviceToDevice, st), &m->poisoned);
+    if (kind == RTG_MEM_HOST) dev_free(dw, st);
+    prof_begin(PH_CLASSIFY, st);
+    s = classify_map(m, m->cls_variant, m->cls_k, m->cls_th_nan ? NAN : m->cls_th, m->cls_tl_nan ? NAN : m->cls_tl, st,
+                     true);
+    prof_end(PH_CLASSIFY, st);
+    if (s != RTG_OK) m->poisoned = true;
+    return s;
+}
+
+rtg_status rtg_region_utility(rtg_map m, const double origin[3], double size, const int dims[3], double* omega,
+                              int* count, void* stream) {
+    rtg_status s = check_map(m);
+    if (s != RTG_OK) return s;
+    if (!origin || !dims || !omega || !count) return invalid("origin, dims, omega and count are required");
+    if (!(size > 0) || !std::isfinite(size)) return invalid("size must be finite and > 0");
+    for (int d = 0; d < 3; ++d) {
+        if (dims[d] < 1) return invalid("dims must be >= 1");
+        if (!std::isfinite(origin[d])) return invalid("origin must be finite");
+    }
+    if ((double)dims[0] * dims[1] * dims[2] >= 2147483647.0) return invalid("prod(dims) must be < 2^31");
+    API_CK(cudaSetDevice(m->device), nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    API_CK(launch_region_utility(m, origin, size, dims, omega, count, st), &m->poisoned);
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_view_ring(int device, int R, rtg_mem kind, const float* centroids, double size,
+                              const rtg_camera* cam, int n, float z, void* stream, rtg_traj* out, double* view_dist) {
+    if (!out) return invalid("out is NULL");
+    *out = nullptr;
+    if (R < 1 || n < 1 || (long long)R * n >= (1LL << 31)) return invalid("need R >= 1, n >= 1, R*n < 2^31");
+    if (!centroids) return invalid("centroids is NULL");
+    if (!(size > 0) || !std::isfinite(size) || !std::isfinite(z)) return invalid("size must be finite and > 0, z finite");
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    rtg_status s = check_camera(cam);
+    if (s != RTG_OK) return s;
+    // viewing distance: the region (edge size) fills the narrower field of view
+    const double hf = std::atan((double)cam->cx / (double)cam->fx) +
+                      std::atan(((double)cam->width - (double)cam->cx) / (double)cam->fx);
+    const double vf = std::atan((double)cam->cy / (double)cam->fy) +
+                      std::atan(((double)cam->height - (double)cam->cy) / (double)cam->fy);
+    const double d = (size / 2.0) / std::tan(std::min(hf, vf) / 2.0);
+    if (view_dist) *view_dist = d;
+    cudaStream_t st = (cudaStream_t)stream;
+    rtg_traj_s* t = nullptr;
+    s = traj_alloc(device, R * n, 1, st, out, &t);
+    if (s != RTG_OK) return s;
+    float* dc = nullptr;
+    cudaError_t e = stage(centroids, 3 * (size_t)R, kind, &dc, st);
+    if (e == cudaSuccess) e = launch_view_ring(R, dc, d, n, z, t, st);
+    if (kind == RTG_MEM_HOST) dev_free(dc, st);
+    if (e != cudaSuccess) {
+        dev_free(t->x, st);
+        delete t;
+        return cuda_fail(e, "rtg_traj_view_ring", nullptr);
+    }
+    *out = t;
+    return RTG_OK;
+}
+
+rtg_status rtg_cost_benefit(const double* omega, const double* d, int K, void* stream, rtg_best_result* out) {
+    if (!out) return invalid("out is NULL");
+    out->score = -INFINITY;
+    out->index = -1;
+    if (!omega || !d || K < 1) return invalid("omega and d must be device arrays of K >= 1 values");
+    cudaStream_t st = (cudaStream_t)stream;
+    void* dv = nullptr;
+    API_CK(dev_alloc(&dv, 16, st), nullptr);
+    API_CK(launch_cost_benefit(omega, d, K, dv, st), nullptr);
+    struct {
+        double score;
+        long long index;
+    } h;
+    API_CK(cudaMemcpyAsync(&h, dv, 16, cudaMemcpyDeviceToHost, st), nullptr);
+    dev_free(dv, st);
+    API_CK(cudaStreamSynchronize(st), nullptr);
+    out->score = h.score;
+    out->index = h.index;
     return RTG_OK;
 }
 

@@ -59,9 +59,17 @@ cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n,
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
-// (re)classification of a built map (rtg_map.cu)
+// (re)classification of a built map (rtg_map.cu); force: even when the parameters are unchanged
 rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi, double tau_lo,
-                        cudaStream_t st);
+                        cudaStream_t st, bool force = false);
+// planner bookkeeping (rtg_plan.cu)
+cudaError_t launch_ledger(long long n, const float* prev, const float* cur, const float* wprev, float* wout,
+                          cudaStream_t st);
+cudaError_t launch_check_weights(long long n, const float* w, int* bad, cudaStream_t st);
+cudaError_t launch_region_utility(rtg_map_s* m, const double origin[3], double size, const int dims[3], double* omega,
+                                  int* count, cudaStream_t st);
+cudaError_t launch_view_ring(int R, const float* cen, double d, int n, float z, rtg_traj_s* tr, cudaStream_t st);
+cudaError_t launch_cost_benefit(const double* omega, const double* d, int K, void* out_dev, cudaStream_t st);
 
 }  // namespace rtg
 

@@ -500,9 +500,9 @@ static void set_class_params(rtg_map_s* m, int variant, double k_sigma, double t
 }
 
 rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi, double tau_lo,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool force) {
     bool has_hi = !std::isnan(tau_hi), has_lo = !std::isnan(tau_lo);
-    if (m->cls_variant == variant && m->cls_k == k_sigma && m->cls_th_nan == !has_hi &&
+    if (!force && m->cls_variant == variant && m->cls_k == k_sigma && m->cls_th_nan == !has_hi &&
         m->cls_tl_nan == !has_lo && (!has_hi || m->cls_th == tau_hi) && (!has_lo || m->cls_tl == tau_lo))
         return RTG_OK;
     cudaError_t e = class_stats(m->n, m->w_orig, m->flags, variant, k_sigma, tau_hi, tau_lo, m->cls, m->red_scratch, st);

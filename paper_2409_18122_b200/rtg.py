@@ -94,6 +94,12 @@ _SIGS = {
     "rtg_best": (_S, [_P, _I, _LL, _P, ctypes.POINTER(BestResult)]),
     "rtg_score_debug": (_S, [_P, _P, ctypes.POINTER(Camera), ctypes.POINTER(ScoreParams), _P, _P, _P, _P, _P,
                              _P, _P]),
+    "rtg_ledger_update": (_S, [_I, _LL, _I, _P, _P, _P, _P, _P]),
+    "rtg_map_update_weights": (_S, [_P, _I, _P, _P]),
+    "rtg_region_utility": (_S, [_P, ctypes.POINTER(ctypes.c_double), ctypes.c_double, ctypes.POINTER(_I), _P, _P, _P]),
+    "rtg_traj_view_ring": (_S, [_I, _I, _I, _P, ctypes.c_double, ctypes.POINTER(Camera), _I, ctypes.c_float, _P,
+                                ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_double)]),
+    "rtg_cost_benefit": (_S, [_P, _P, _I, _P, ctypes.POINTER(BestResult)]),
     "rtg_profile_enable": (_S, [_I]),
     "rtg_profile_read": (_S, [ctypes.POINTER(Profile), _I]),
     "rtg_status_string": (ctypes.c_char_p, [_I]),
@@ -208,6 +214,14 @@ class Map:
                                     ctypes.byref(self.handle))
         _check(s, "rtg_map_create")
 
+    def update_weights(self, info_w, stream=None) -> None:
+        """rtg_map_update_weights: replace the ledger (input order) and reclassify (N4)."""
+        if int(info_w.shape[0]) != self.n:
+            raise ValueError("info_w must have one entry per Gaussian")
+        _check(_lib.rtg_map_update_weights(self.handle, _kind(info_w), _ptr(info_w), _stream(stream)),
+               "rtg_map_update_weights")
+        self._keep = self._keep + (info_w,)
+
     def info(self) -> MapInfo:
         out = MapInfo()
         _check(_lib.rtg_map_info(self.handle, ctypes.byref(out)), "rtg_map_info")
@@ -257,6 +271,19 @@ class Traj:
                                              _stream(stream), ctypes.byref(h)), "rtg_traj_sample_unicycle")
         return cls(h, K, int(T))
 
+    @classmethod
+    def view_ring(cls, centroids, size: float, camera, n: int, z: float, device=0, stream=None):
+        """rtg_traj_view_ring: n viewpoints per region centroid (centroids [3, R]) facing it at the
+        shortest viewing distance (N2).  Returns (Traj with K = R n, T = 1, viewing distance)."""
+        R = int(centroids.shape[-1])
+        cam = camera if isinstance(camera, Camera) else make_camera(camera)
+        h = _P()
+        d = ctypes.c_double()
+        _check(_lib.rtg_traj_view_ring(device, R, _kind(centroids), _ptr(centroids), float(size), ctypes.byref(cam),
+                                       int(n), float(z), _stream(stream), ctypes.byref(h), ctypes.byref(d)),
+               "rtg_traj_view_ring")
+        return cls(h, R * int(n), 1), d.value
+
     def read(self, stream=None):
         torch = _torch()
         out = [torch.empty((self.K, self.T), dtype=torch.float32, device="cuda") for _ in range(4)]
@@ -303,6 +330,37 @@ def best(utility, index_base: int = 0, stream=None):
     out = BestResult()
     _check(_lib.rtg_best(_ptr(utility), int(utility.numel()), int(index_base), _stream(stream), ctypes.byref(out)),
            "rtg_best", allow=(ERR_NO_FEASIBLE,))
+    return out.score, out.index
+
+
+def ledger_update(mu_prev, mu_cur, w_prev, w_out=None, device=0, stream=None):
+    """rtg_ledger_update (N4): w = |mu_cur - mu_prev| where the mean moved, else w_prev (CUDA out)."""
+    torch = _torch()
+    n = int(w_prev.shape[0])
+    w_out = torch.empty(n, dtype=torch.float32, device=f"cuda:{device}") if w_out is None else w_out
+    _check(_lib.rtg_ledger_update(device, n, _kind(mu_prev), _ptr(mu_prev), _ptr(mu_cur), _ptr(w_prev), _ptr(w_out),
+                                  _stream(stream)), "rtg_ledger_update")
+    return w_out
+
+
+def region_utility(m: Map, origin, size: float, dims, stream=None):
+    """rtg_region_utility (N2): (omega [prod dims] float64, count [prod dims] int32) CUDA tensors."""
+    torch = _torch()
+    nr = int(dims[0]) * int(dims[1]) * int(dims[2])
+    omega = torch.empty(nr, dtype=torch.float64, device="cuda")
+    count = torch.empty(nr, dtype=torch.int32, device="cuda")
+    o = (ctypes.c_double * 3)(*[float(v) for v in origin])
+    d = (_I * 3)(*[int(v) for v in dims])
+    _check(_lib.rtg_region_utility(m.handle, o, float(size), d, _ptr(omega), _ptr(count), _stream(stream)),
+           "rtg_region_utility")
+    return omega, count
+
+
+def cost_benefit(omega, d, stream=None):
+    """rtg_cost_benefit (N2): argmax of omega / e^d (ties -> smaller d, then index) -> (score, index)."""
+    out = BestResult()
+    _check(_lib.rtg_cost_benefit(_ptr(omega), _ptr(d), int(omega.numel()), _stream(stream), ctypes.byref(out)),
+           "rtg_cost_benefit")
     return out.score, out.index
 
 

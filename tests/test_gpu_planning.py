@@ -1,0 +1,161 @@
+"""GPU parity of the planner bookkeeping rows against oracle/planning.py,
+through the C ABI."""
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from oracle import planning as P
+from paper_2409_18122_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2409_18122_b200 import build
+    build.build()
+    from paper_2409_18122_b200 import rtg
+    return rtg
+
+
+@pytest.fixture(scope="module")
+def room():
+    return W.room()
+
+
+def _moved(wl, seed=2, frac=0.7, sigma=0.05):
+    rng = np.random.default_rng(seed)
+    cur = wl.means.copy()
+    mv = rng.random(wl.N) < frac
+    cur[:, mv] += rng.normal(0, sigma, (3, int(mv.sum()))).astype(np.float32)
+    return cur
+
+
+# ----------------------------------------------------------------- N4 ledger
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_ledger_update_bit_exact(R, room, on_device):
+    cur = _moved(room)
+    ref = P.ledger_update(room.means, cur, room.info_w)
+    args = (room.means, cur, room.info_w)
+    if on_device:
+        args = tuple(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in args)
+    got = R.ledger_update(*args).cpu().numpy()
+    assert np.array_equal(got, ref)
+    unchanged = np.all(cur == room.means, axis=0)
+    assert unchanged.sum() > 1000 and np.array_equal(got[unchanged], room.info_w[unchanged])
+
+
+def test_update_weights_then_score_matches_oracle(R, room):
+    cur = _moved(room, seed=5)
+    w_new = P.ledger_update(room.means, cur, room.info_w)
+    wl2 = dataclasses.replace(room, info_w=w_new)
+    idx = np.array([3, 200, 517, 1000])
+    sub = dict(x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx])
+    orc = O.score(wl2, **sub)
+    out = {}
+    for mode in (R.MODE_DENSE, R.MODE_CULLED):
+        m = R.map_from_workload(room)                       # built with the old ledger ...
+        m.update_weights(torch.from_numpy(w_new).cuda())     # ... then updated in place (no repack)
+        info = m.info()
+        assert info.tau_hi == pytest.approx(O.classify(w_new, room.flags)["tau_hi"], rel=1e-12)
+        tr = R.traj_from_workload(room, **sub)
+        p = R.make_params(mode=mode, flags=R.SCORE_FULL_GAIN)
+        d = R.score_debug(m, tr, room.camera, p)
+        out[mode] = {k: d[k].cpu().numpy() for k in ("wp_gain", "wp_nh", "wp_nl", "wp_col")}
+        m.close()
+        tr.close()
+    wp = orc["wp"]
+    a = out[R.MODE_CULLED]
+    clean = wp["amb_vis"] == 0
+    assert np.array_equal(a["wp_nh"][clean], wp["nh"][clean]) and np.array_equal(a["wp_nl"][clean], wp["nl"][clean])
+    tol = 1e-5 * np.abs(wp["gain_hi"]) + 1e-6
+    assert np.all(np.abs(a["wp_gain"][clean] - wp["gain"][clean]) <= tol[clean])
+    for k in ("wp_gain", "wp_nh", "wp_nl"):
+        assert np.array_equal(out[R.MODE_DENSE][k], a[k]), k
+
+
+def test_update_weights_rejects_invalid_and_keeps_map(R, room):
+    m = R.map_from_workload(room)
+    before = m.info().tau_hi
+    bad = room.info_w.copy()
+    bad[7] = -1.0
+    with pytest.raises(R.RTGError):
+        m.update_weights(bad)
+    bad[7] = np.nan
+    with pytest.raises(R.RTGError):
+        m.update_weights(bad)
+    assert m.info().tau_hi == before
+    m.close()
+
+
+# ----------------------------------------------------------------- N2 region utility
+
+@pytest.mark.parametrize("box", [((-6.0, -5.0, 0.0), 2.5, (5, 4, 2)), ((-3.3, -2.1, -0.4), 1.1, (7, 3, 4))])
+def test_region_utility_matches_oracle(R, room, box):
+    origin, size, dims = box
+    w = P.ledger_update(room.means, _moved(room, seed=9), room.info_w)
+    om_ref, cnt_ref = P.region_utility(room.means, w, room.flags, origin, size, dims)
+    m = R.map_from_workload(dataclasses.replace(room, info_w=w))
+    om, cnt = R.region_utility(m, origin, size, dims)
+    om, cnt = om.cpu().numpy(), cnt.cpu().numpy()
+    m.close()
+    assert np.array_equal(cnt, cnt_ref)
+    # exact fixed-point sums: the only error is the quantum 2^-S per Gaussian, S >= 52 - log2(M max w)
+    q = 2.0 ** -(52 - math.ceil(math.log2(max(cnt_ref.sum(), 1) * float(w.max()))))
+    assert np.all(np.abs(om - om_ref) <= q + 1e-13 * np.abs(om_ref))
+
+
+def test_region_utility_empty_map(R):
+    wl = W.tiny(K=2, T=2)
+    e = np.zeros((3, 0), np.float32)
+    wl0 = dataclasses.replace(wl, means=e, quats=np.zeros((4, 0), np.float32), scales=e,
+                              opacity=np.zeros(0, np.float32), info_w=np.zeros(0, np.float32))
+    m = R.map_from_workload(wl0)
+    om, cnt = R.region_utility(m, (0, 0, 0), 2.5, (2, 2, 2))
+    assert torch.all(om == 0) and torch.all(cnt == 0)
+    m.close()
+
+
+# ----------------------------------------------------------------- N2 viewpoints and selection
+
+def test_view_ring_and_view_scores_match_oracle(R, room):
+    cam = room.camera
+    cen = np.array([[-3.0, 0.5, 4.0], [2.0, -3.0, 1.5], [1.5, 1.5, 1.5]], np.float32)   # [3, R]
+    tr, d = R.Traj.view_ring(cen, 2.5, cam, 8, 0.5)
+    assert d == pytest.approx(P.view_distance(2.5, cam), rel=1e-15)
+    x, y, z, yaw = (a.cpu().numpy()[:, 0] for a in tr.read())
+    rx, ry, rz, ryaw = P.view_ring(cen.T, 2.5, cam, 8, 0.5)
+    for a, b in ((x, rx), (y, ry), (z, rz), (yaw, ryaw)):
+        assert np.all(np.abs(a - b) <= 2 * np.spacing(np.abs(b).astype(np.float32)) + 1e-7)
+    # the views are scored as gain-only trajectories (T = 1) against the oracle on the same poses
+    m = R.map_from_workload(room)
+    p = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
+    fc, fe, g, u = R.score(m, tr, cam, p)
+    orc = O.score(room, x=x[:, None].copy(), y=y[:, None].copy(), z=z[:, None].copy(), yaw=yaw[:, None].copy(),
+                  no_collision=True)
+    g = g.cpu().numpy()
+    tol = 1e-5 * np.abs(orc["gain_hi"]) + 1e-6
+    assert np.all((g >= orc["gain_lo"] - tol) & (g <= orc["gain_hi"] + tol))
+    assert np.all(fe.cpu().numpy() == 1)
+    m.close()
+    tr.close()
+
+
+def test_cost_benefit_matches_oracle(R):
+    rng = np.random.default_rng(8)
+    for K in (1, 7, 1000, 5000):
+        om = rng.random(K)
+        d = rng.uniform(0, 10, K)
+        if K > 10:   # constructed ties: equal score, smaller d wins; equal (score, d): lower index
+            om[3], d[3] = om[9] * math.e, d[9] + 1.0
+            om[5], d[5] = om[9], d[9]
+        ref = P.cost_benefit(om, d)
+        got = R.cost_benefit(torch.from_numpy(om).cuda(), torch.from_numpy(d).cuda())
+        assert got[1] == ref[0] and got[0] == pytest.approx(ref[1], rel=1e-15)
