@@ -293,6 +293,45 @@ rtg_status rtg_traj_view_ring(int device, int R, rtg_mem kind, const float* cent
 rtg_status rtg_cost_benefit(const double* omega, const double* d, int K, void* stream, rtg_best_result* out);
 
 /*
+ * rtg_plan_tree -- N3, trajectory candidate generation on the device (§IV-B2):
+ * a tree of unicycle motion primitives (fixed controls u = (v, w) over dt; v on a uniform grid of
+ * [0, v_max] with n_v points incl. both ends ({v_max} when n_v = 1), w likewise on
+ * [-omega_max, omega_max] ({0} when n_omega = 1)) is grown from start = {x, y, theta}
+ * layer by layer.  Each layer expands every frontier node by every control; the `samples` states
+ * at t_j = j dt / (samples - 1), j = 1 .. samples - 1 (closed form), are collision-
+ * checked against the map with the a4 test at height z, all in one launch; a primitive with
+ * a colliding sample is discarded.  A child costs g = g_parent + (lambda_t + v^2 + w^2) dt
+ * (Eq. low_level_planner); it is dropped when its (lattice_xy, lattice_xy, lattice_deg) lattice cell
+ * was already reached with a cost <= g (lattice_xy <= 0: no lattice); it is a candidate (not
+ * expanded) when ||p - goal|| <= goal_radius.  The next frontier keeps the `beam` children of
+ * lowest f = g + ||goal - p|| / v_max.  After max_depth layers the n_traj cheapest
+ * candidates are returned (*reached = 1), or, when none reached the goal, the n_traj nodes closest
+ * to it (*reached = 0).  Ties always go to creation order (node, then control).
+ * *out: trajectory handle with K = *n_found (<= n_traj), T = max_depth + 1, waypoint l = the
+ * state after l primitives (l = 0: start; NaN after the candidate's last primitive); cost (host,
+ * n_traj entries or NULL) receives the candidates' g; stats (host long long[4] or NULL):
+ * nodes expanded, nodes created, samples checked, collision candidates tested.  Synchronises the
+ * stream.  Errors: RTG_ERR_INVALID_ARGUMENT (bad parameters), RTG_ERR_NO_FEASIBLE (nothing
+ * collision-free grows from the start: *n_found = 0), RTG_ERR_CUDA.
+ */
+typedef struct {
+    int n_v, n_omega;        /* control grid (3, 5 in the paper)                   */
+    float v_max, omega_max;  /* > 0 [m/s], >= 0 [rad/s] (0.6, 0.9)                */
+    float dt;                /* primitive duration [s] (1)                         */
+    float lambda_t;          /* time weight of the cost (>= 0)                            */
+    int samples;             /* collision samples per primitive incl. both ends (>= 2)   */
+    int max_depth;           /* primitives per trajectory (>= 1)                          */
+    float goal_radius;       /* goal region radius [m] (>= 0)                             */
+    float lattice_xy;        /* dedup lattice cell [m] (<= 0: no dedup)                   */
+    float lattice_deg;       /* dedup lattice heading cell [deg]                          */
+    int beam;                /* frontier nodes kept per layer (>= 1)                      */
+    int n_traj;              /* candidates returned (>= 1)                                */
+    float z;                 /* height of the robot (and camera) [m]                      */
+} rtg_tree_params;
+rtg_status rtg_plan_tree(rtg_map map, const float start[3], const float goal[2], const rtg_tree_params* params,
+                         void* stream, rtg_traj* out, double* cost, int* n_found, int* reached, long long* stats);
+
+/*
  * Profiling (process-wide).  When enabled, every library phase is bracketed by CUDA events
  * recorded on the stream it is launched on; rtg_profile_read synchronises those events and
  * returns the accumulated device milliseconds and call counts per phase:

@@ -1,5 +1,5 @@
-"""CPU oracle of the planner's uncertainty bookkeeping and high-level guidance scoring
-(TEST INFRASTRUCTURE ONLY).
+"""CPU oracle of the planner's uncertainty bookkeeping, high-level guidance scoring and motion-
+primitive tree (TEST INFRASTRUCTURE ONLY).
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s baseline legs may import this
 module; the product path never imports it and shares no code with it.  Plain numpy / Python
@@ -26,6 +26,8 @@ and notation.  Pinned by tests/test_planning_pins.py.
   cost_benefit    P:249: a viewpoint node at path distance d with utility Omega scores
                   Omega / e^d; the maximal score wins, ties -> smaller d, then smaller index
                   (SPEC S:333).
+  plan_tree       P:280-320 (§IV-B2): motion-primitive tree search for trajectory candidates (see
+                  the section comment below).
 """
 from __future__ import annotations
 
@@ -119,3 +121,117 @@ def cost_benefit(omega, d):
         if s > bs or (s == bs and float(dist) < bd):
             best, bs, bd = j, s, float(dist)
     return best, bs
+
+
+# ---------------------------------------------------------------- N3 motion-primitive tree
+# PAPER.md §IV-B2: unicycle motion primitives with fixed controls over dt, N_v x N_w
+# controls sampled uniformly from [0, v_max] x [-w_max, w_max], a fixed number of
+# collision samples per primitive, cost lambda_t tau + int u^T u dt (Eq.
+# low_level_planner), minimum-time heuristic h = ||p_goal - p|| / v_max, the top N_traj
+# candidates.  The search order is the layer-synchronous one DESIGN.md §2 (reading R5)
+# states: every frontier node expanded by every control per layer, a closed lattice keeping the
+# lowest g, a beam of the lowest f = g + h, goal-reaching nodes become candidates; ties go to
+# creation order.
+
+def controls(n_v, n_omega, v_max, omega_max):
+    """v uniform on [0, v_max] incl. endpoints ({v_max} if n_v = 1), w uniform on
+    [-w_max, w_max] incl. endpoints ({0} if n_omega = 1); order: v major, w minor."""
+    v_max, omega_max = float(np.float32(v_max)), float(np.float32(omega_max))
+    out = []
+    for i in range(n_v):
+        v = v_max if n_v == 1 else v_max * i / (n_v - 1)
+        for j in range(n_omega):
+            w = 0.0 if n_omega == 1 else omega_max * (2 * j - (n_omega - 1)) / (n_omega - 1)
+            out.append((v, w))
+    return out
+
+
+def unicycle_at(x0, y0, th0, v, w, t):
+    """SPEC S:392 closed form (not wrapped)."""
+    th = th0 + w * t
+    if abs(w) < 1e-12:
+        vt = v * t
+        return x0 + vt * math.cos(th0), y0 + vt * math.sin(th0), th
+    r = v / w
+    return x0 + r * (math.sin(th) - math.sin(th0)), y0 + r * (math.cos(th0) - math.cos(th)), th
+
+
+def wrap_pi(a):
+    r = math.remainder(a, 2.0 * math.pi)
+    return r + 2.0 * math.pi if r <= -math.pi else r
+
+
+def plan_tree(collides, start, goal, p):
+    """Layer-synchronous motion-primitive tree search.  `collides(points)` takes an [n, 3] float32
+    array of sample points and returns n booleans (the a4 collision decision).  `p` carries the
+    rtg_tree_params fields (n_v, n_omega, v_max, omega_max, dt, lambda_t, samples, max_depth,
+    goal_radius, lattice_xy, lattice_deg, beam, n_traj, z).
+    Returns dict(cands=[node ids], nodes=[(x, y, th, g, parent, depth)], reached, expanded)."""
+    f32 = lambda v: float(np.float32(v))
+    ctl = controls(p.n_v, p.n_omega, p.v_max, p.omega_max)
+    dt, lam, vmax = f32(p.dt), f32(p.lambda_t), f32(p.v_max)
+    pcost = [(lam + v * v + w * w) * dt for v, w in ctl]
+    gx, gy = f32(goal[0]), f32(goal[1])
+    r2 = f32(p.goal_radius) * f32(p.goal_radius)
+    h_of = lambda x, y: math.sqrt((gx - x) * (gx - x) + (gy - y) * (gy - y)) / vmax
+    at_goal = lambda x, y: (x - gx) * (x - gx) + (y - gy) * (y - gy) <= r2
+    lxy, ldeg = f32(p.lattice_xy), f32(p.lattice_deg)
+    dedup = lxy > 0 and ldeg > 0
+    key_of = lambda n: (math.floor(n[0] / lxy), math.floor(n[1] / lxy), math.floor(n[2] * (180.0 / math.pi) / ldeg))
+    nodes = [(f32(start[0]), f32(start[1]), wrap_pi(f32(start[2])), 0.0, -1, 0)]
+    closed = {key_of(nodes[0]): 0.0} if dedup else {}
+    cands, frontier = [], []
+    (cands if at_goal(nodes[0][0], nodes[0][1]) else frontier).append(0)
+    S, z = int(p.samples), f32(p.z)
+    expanded = 0
+    for depth in range(1, int(p.max_depth) + 1):
+        if not frontier:
+            break
+        # every sample of the layer, checked at once
+        prims, pts = [], []
+        for m in frontier:
+            x0, y0, th0 = nodes[m][0], nodes[m][1], nodes[m][2]
+            for pi, (v, w) in enumerate(ctl):
+                last = None
+                for j in range(1, S):
+                    t = (j * dt) / (S - 1)
+                    last = unicycle_at(x0, y0, th0, v, w, t)
+                    pts.append((last[0], last[1], z))
+                prims.append((m, pi, last))
+        hit = np.asarray(collides(np.array(pts, np.float32).reshape(-1, 3)), bool).reshape(len(prims), S - 1)
+        expanded += len(frontier)
+        nxt = []
+        for (m, pi, last), h in zip(prims, hit):
+            if h.any():
+                continue
+            c = (last[0], last[1], wrap_pi(last[2]), nodes[m][3] + pcost[pi], m, depth)
+            if dedup:
+                k = key_of(c)
+                if k in closed and closed[k] <= c[3]:
+                    continue
+                closed[k] = c[3]
+            nodes.append(c)
+            (cands if at_goal(c[0], c[1]) else nxt).append(len(nodes) - 1)
+        nxt.sort(key=lambda i: nodes[i][3] + h_of(nodes[i][0], nodes[i][1]))   # stable: creation order on ties
+        frontier = sorted(nxt[:int(p.beam)])
+    if cands:
+        reached = True
+        pick = sorted(cands, key=lambda i: nodes[i][3])
+    else:
+        reached = False
+        pick = sorted(range(1, len(nodes)), key=lambda i: (h_of(nodes[i][0], nodes[i][1]), nodes[i][3]))
+    return dict(cands=pick[:int(p.n_traj)], nodes=nodes, reached=reached, expanded=expanded)
+
+
+def tree_waypoints(res, max_depth):
+    """Candidate waypoints [K, max_depth + 1] (x, y, yaw; NaN after the last primitive) and costs."""
+    K, T = len(res["cands"]), max_depth + 1
+    out = [np.full((K, T), np.nan, np.float32) for _ in range(3)]
+    cost = np.zeros(K)
+    for c, i in enumerate(res["cands"]):
+        cost[c] = res["nodes"][i][3]
+        while i >= 0:
+            n = res["nodes"][i]
+            out[0][c, n[5]], out[1][c, n[5]], out[2][c, n[5]] = n[0], n[1], n[2]
+            i = n[4]
+    return out[0], out[1], out[2], cost

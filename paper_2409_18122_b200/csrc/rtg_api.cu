@@ -716,6 +716,46 @@ rtg_status rtg_cost_benefit(const double* omega, const double* d, int K, void* s
     return RTG_OK;
 }
 
+rtg_status rtg_plan_tree(rtg_map m, const float start[3], const float goal[2], const rtg_tree_params* p,
+                         void* stream, rtg_traj* out, double* cost, int* n_found, int* reached, long long* stats) {
+    if (!out || !n_found || !reached) return invalid("out, n_found and reached are required");
+    *out = nullptr;
+    *n_found = 0;
+    *reached = 0;
+    rtg_status s = check_map(m);
+    if (s != RTG_OK) return s;
+    if (!start || !goal || !p) return invalid("start, goal and params are required");
+    for (int i = 0; i < 3; ++i)
+        if (!finite_f(start[i])) return invalid("start must be finite");
+    if (!finite_f(goal[0]) || !finite_f(goal[1])) return invalid("goal must be finite");
+    if (p->n_v < 1 || p->n_omega < 1 || !(p->v_max > 0) || !(p->omega_max >= 0) || !(p->dt > 0) ||
+        !(p->lambda_t >= 0) || p->samples < 2 || p->max_depth < 1 || !(p->goal_radius >= 0) || p->beam < 1 ||
+        p->n_traj < 1 || !finite_f(p->v_max) || !finite_f(p->omega_max) || !finite_f(p->dt) ||
+        !finite_f(p->lambda_t) || !finite_f(p->goal_radius) || !finite_f(p->z) || !finite_f(p->lattice_xy) ||
+        !finite_f(p->lattice_deg))
+        return invalid("rtg_tree_params out of range");
+    if ((long long)p->beam * p->n_v * p->n_omega >= (1LL << 31) / 32) return invalid("beam * controls too large");
+    if ((long long)p->n_traj * (p->max_depth + 1) >= (1LL << 31)) return invalid("n_traj * (max_depth + 1) too large");
+    API_CK(cudaSetDevice(m->device), nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<float> wx, wy, wyaw;
+    std::vector<double> c;
+    s = plan_tree(m, start, goal, *p, st, &wx, &wy, &wyaw, &c, reached, stats);
+    if (s != RTG_OK) return s;
+    const int K = (int)c.size();
+    *n_found = K;
+    if (cost)
+        for (int i = 0; i < K; ++i) cost[i] = c[i];
+    if (K == 0) {
+        set_error("rtg_plan_tree: no collision-free primitive grows from the start");
+        return RTG_ERR_NO_FEASIBLE;
+    }
+    const int T = p->max_depth + 1;
+    std::vector<float> wz(wx.size());
+    for (size_t i = 0; i < wx.size(); ++i) wz[i] = std::isnan(wx[i]) ? wx[i] : p->z;
+    return rtg_traj_upload(m->device, K, T, RTG_MEM_HOST, wx.data(), wy.data(), wz.data(), wyaw.data(), stream, out);
+}
+
 rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_score_params* p,
                            unsigned char* wp_col, double* wp_gain, int* wp_nh, int* wp_nl, unsigned int* pair_mask,
                            long long* stats, void* stream) {

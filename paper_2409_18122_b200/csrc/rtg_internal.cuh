@@ -194,6 +194,87 @@ __device__ __forceinline__ bool collide_full(const float* m, float dx, float dy,
     return c;
 }
 
+
+// ------------------------------------------------------------------ culled collision of one point
+struct ColGridK {
+    float ox, oy, oz, h, R;   // collision grid origin, cell edge, stencil radius (>= every r_b)
+    int nx, ny, nz;
+};
+
+__device__ __forceinline__ int clamp_cell(float v, int lo, int hi) {
+    v = fminf(fmaxf(v, (float)lo - 1.0f), (float)hi + 1.0f);
+    int c = (int)floorf(v);
+    return c;
+}
+
+// Warp-cooperative exact collision test of point p against the collidable Gaussians (a4, O2):
+// the cell rows of the +-R box are flattened over the lanes, each candidate gets the sphere reject
+// and, when it passes, the full quadratic form (FP32 + FP64 re-decision in the guard band); stops
+// at the first collision.  Every lane returns the result.  A NaN point collides with nothing.
+__device__ __forceinline__ bool warp_point_collides(float px, float py, float pz, const CRec* __restrict__ crec,
+                                                    const CMat* __restrict__ cmat, const CSrc* __restrict__ csrc,
+                                                    const rtg_robot& rb, const int* __restrict__ cstart,
+                                                    const ColGridK& g, float gq, unsigned& nref,
+                                                    unsigned long long& ntest) {
+    constexpr unsigned kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    bool hit = false;
+    if (!(isfinite(px) && isfinite(py) && isfinite(pz))) return false;
+    int ix0 = max(0, clamp_cell((px - g.R - g.ox) / g.h, 0, g.nx));
+    int ix1 = min(g.nx - 1, clamp_cell((px + g.R - g.ox) / g.h, 0, g.nx));
+    int iy0 = max(0, clamp_cell((py - g.R - g.oy) / g.h, 0, g.ny));
+    int iy1 = min(g.ny - 1, clamp_cell((py + g.R - g.oy) / g.h, 0, g.ny));
+    int iz0 = max(0, clamp_cell((pz - g.R - g.oz) / g.h, 0, g.nz));
+    int iz1 = min(g.nz - 1, clamp_cell((pz + g.R - g.oz) / g.h, 0, g.nz));
+    if (ix0 > ix1 || iy0 > iy1 || iz0 > iz1) return false;
+    const int nyr = iy1 - iy0 + 1;
+    const int nrows = nyr * (iz1 - iz0 + 1);
+    for (int r0 = 0; r0 < nrows && !hit; r0 += 32) {
+        const int r = r0 + lane;
+        int beg = 0, len = 0;
+        if (r < nrows) {
+            int iz = iz0 + r / nyr, iy = iy0 + r % nyr;
+            long long base = ((long long)iz * g.ny + iy) * g.nx;
+            beg = cstart[base + ix0];
+            len = cstart[base + ix1 + 1] - beg;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(kAll, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(kAll, incl, 31);
+        const int roff = beg - (incl - len);
+        for (int b0 = 0; b0 < total; b0 += 32) {
+            const int pos = b0 + lane;
+            // row owning candidate pos: first lane whose inclusive prefix exceeds it
+            int owner = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int v = __shfl_sync(kAll, incl, owner + st - 1);
+                if (v <= pos) owner += st;
+            }
+            const int gi = pos + __shfl_sync(kAll, roff, owner);
+            bool h = false;
+            if (pos < total) {
+                const CRec A = crec[gi];
+                float dx = px - A.x, dy = py - A.y, dz = pz - A.z;
+                float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (d2 < A.rb2)
+                    h = collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, px, py, pz, A.x, A.y, A.z, nref);
+            }
+            ntest += (unsigned long long)min(32, total - b0);
+            if (__any_sync(kAll, h)) {
+                hit = true;
+                break;
+            }
+        }
+        __syncwarp();
+    }
+    return hit;
+}
+
 // ------------------------------------------------------------------ misc helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

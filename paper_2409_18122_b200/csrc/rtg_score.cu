@@ -122,17 +122,6 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
 }
 
 // ===================================================================== culled phase A
-struct ColGridK {
-    float ox, oy, oz, h, R;
-    int nx, ny, nz;
-};
-
-__device__ __forceinline__ int clamp_cell(float v, int lo, int hi) {
-    v = fminf(fmaxf(v, (float)lo - 1.0f), (float)hi + 1.0f);
-    int c = (int)floorf(v);
-    return c;
-}
-
 constexpr int kWarps = 8;   // warps per block of the persistent culled kernels
 
 __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
@@ -153,63 +142,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
         for (int t = 0; t < T; ++t) {
             const long long i = (long long)k * T + t;
             const float px = X[i], py = Y[i], pz = Zw[i];
-            bool hit = false;
-            if (isfinite(px) && isfinite(py) && isfinite(pz)) {
-                int ix0 = max(0, clamp_cell((px - g.R - g.ox) / g.h, 0, g.nx));
-                int ix1 = min(g.nx - 1, clamp_cell((px + g.R - g.ox) / g.h, 0, g.nx));
-                int iy0 = max(0, clamp_cell((py - g.R - g.oy) / g.h, 0, g.ny));
-                int iy1 = min(g.ny - 1, clamp_cell((py + g.R - g.oy) / g.h, 0, g.ny));
-                int iz0 = max(0, clamp_cell((pz - g.R - g.oz) / g.h, 0, g.nz));
-                int iz1 = min(g.nz - 1, clamp_cell((pz + g.R - g.oz) / g.h, 0, g.nz));
-                if (ix0 <= ix1 && iy0 <= iy1 && iz0 <= iz1) {
-                    const int nyr = iy1 - iy0 + 1;
-                    const int nrows = nyr * (iz1 - iz0 + 1);
-                    for (int r0 = 0; r0 < nrows && !hit; r0 += 32) {
-                        const int r = r0 + lane;
-                        int beg = 0, len = 0;
-                        if (r < nrows) {
-                            int iz = iz0 + r / nyr, iy = iy0 + r % nyr;
-                            long long base = ((long long)iz * g.ny + iy) * g.nx;
-                            beg = cstart[base + ix0];
-                            len = cstart[base + ix1 + 1] - beg;
-                        }
-                        int incl = len;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            int v = __shfl_up_sync(kFull, incl, o);
-                            if (lane >= o) incl += v;
-                        }
-                        const int total = __shfl_sync(kFull, incl, 31);
-                        const int roff = beg - (incl - len);
-                        for (int b0 = 0; b0 < total; b0 += 32) {
-                            const int pos = b0 + lane;
-                            // row owning candidate pos: first lane whose inclusive prefix exceeds it
-                            int owner = 0;
-#pragma unroll
-                            for (int st = 16; st > 0; st >>= 1) {
-                                const int v = __shfl_sync(kFull, incl, owner + st - 1);
-                                if (v <= pos) owner += st;
-                            }
-                            const int gi = pos + __shfl_sync(kFull, roff, owner);
-                            bool h = false;
-                            if (pos < total) {
-                                const CRec A = crec[gi];
-                                float dx = px - A.x, dy = py - A.y, dz = pz - A.z;
-                                float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                                if (d2 < A.rb2)
-                                    h = collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, px, py,
-                                                     pz, A.x, A.y, A.z, nref);
-                            }
-                            ntest += (unsigned long long)min(32, total - b0);
-                            if (__any_sync(kFull, h)) {
-                                hit = true;
-                                break;
-                            }
-                        }
-                        __syncwarp();
-                    }
-                }
-            }
+            const bool hit = warp_point_collides(px, py, pz, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
             if (all_waypoints && lane == 0) wp_col[i] = hit ? 1 : 0;
             if (hit) {
                 first = min(first, t);

@@ -68,6 +68,21 @@ class MapInfo(ctypes.Structure):
                 ("device_bytes", ctypes.c_longlong)]
 
 
+class TreeParams(ctypes.Structure):
+    _fields_ = [("n_v", ctypes.c_int), ("n_omega", ctypes.c_int), ("v_max", ctypes.c_float),
+                ("omega_max", ctypes.c_float), ("dt", ctypes.c_float), ("lambda_t", ctypes.c_float),
+                ("samples", ctypes.c_int), ("max_depth", ctypes.c_int), ("goal_radius", ctypes.c_float),
+                ("lattice_xy", ctypes.c_float), ("lattice_deg", ctypes.c_float), ("beam", ctypes.c_int),
+                ("n_traj", ctypes.c_int), ("z", ctypes.c_float)]
+
+
+def make_tree_params(n_v=3, n_omega=5, v_max=0.6, omega_max=0.9, dt=1.0, lambda_t=1.0, samples=5, max_depth=8,
+                     goal_radius=0.5, lattice_xy=0.1, lattice_deg=10.0, beam=4096, n_traj=10, z=0.5) -> "TreeParams":
+    """Defaults: PAPER.md:330 (N_v = 3, v_max = 0.6, N_w = 5, w_max = 0.9, 1 s) and SPEC S:384."""
+    return TreeParams(n_v, n_omega, v_max, omega_max, dt, lambda_t, samples, max_depth, goal_radius, lattice_xy,
+                      lattice_deg, beam, n_traj, z)
+
+
 class Profile(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 8), ("calls", ctypes.c_longlong * 8), ("launches", ctypes.c_longlong)]
 
@@ -100,6 +115,9 @@ _SIGS = {
     "rtg_traj_view_ring": (_S, [_I, _I, _I, _P, ctypes.c_double, ctypes.POINTER(Camera), _I, ctypes.c_float, _P,
                                 ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_double)]),
     "rtg_cost_benefit": (_S, [_P, _P, _I, _P, ctypes.POINTER(BestResult)]),
+    "rtg_plan_tree": (_S, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
+                           ctypes.POINTER(TreeParams), _P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_double),
+                           ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_LL)]),
     "rtg_profile_enable": (_S, [_I]),
     "rtg_profile_read": (_S, [ctypes.POINTER(Profile), _I]),
     "rtg_status_string": (ctypes.c_char_p, [_I]),
@@ -354,6 +372,23 @@ def region_utility(m: Map, origin, size: float, dims, stream=None):
     _check(_lib.rtg_region_utility(m.handle, o, float(size), d, _ptr(omega), _ptr(count), _stream(stream)),
            "rtg_region_utility")
     return omega, count
+
+
+def plan_tree(m: Map, start, goal, params: TreeParams, stream=None):
+    """rtg_plan_tree (N3): -> (Traj of candidates [K, max_depth + 1] or None, costs [K], reached, stats).
+    Raises RTGError(ERR_NO_FEASIBLE) when nothing collision-free grows from the start."""
+    st3 = (ctypes.c_float * 3)(*[float(v) for v in start])
+    g2 = (ctypes.c_float * 2)(*[float(v) for v in goal])
+    h = _P()
+    cost = (ctypes.c_double * int(params.n_traj))()
+    nf, rc = _I(), _I()
+    stats = (_LL * 4)()
+    _check(_lib.rtg_plan_tree(m.handle, st3, g2, ctypes.byref(params), _stream(stream), ctypes.byref(h), cost,
+                              ctypes.byref(nf), ctypes.byref(rc), stats), "rtg_plan_tree")
+    K = nf.value
+    tr = Traj(h, K, int(params.max_depth) + 1)
+    return tr, np.array(cost[:K]), bool(rc.value), dict(expanded=stats[0], created=stats[1], samples=stats[2],
+                                                        candidates_tested=stats[3])
 
 
 def cost_benefit(omega, d, stream=None):

@@ -159,3 +159,65 @@ def test_cost_benefit_matches_oracle(R):
         ref = P.cost_benefit(om, d)
         got = R.cost_benefit(torch.from_numpy(om).cuda(), torch.from_numpy(d).cuda())
         assert got[1] == ref[0] and got[0] == pytest.approx(ref[1], rel=1e-15)
+
+
+# ----------------------------------------------------------------- N3 motion-primitive tree
+
+def _oracle_collides(wl):
+    c = O.classify(wl.info_w, wl.flags)
+
+    def f(pts):
+        n = len(pts)
+        if n == 0:
+            return np.zeros(0, bool)
+        col = lambda a: np.ascontiguousarray(np.asarray(a, np.float32).reshape(n, 1))
+        wp = O.waypoints(wl.means, wl.quats, wl.scales, wl.flags, c["cls"], c["u"], wl.robot, wl.camera,
+                         col(pts[:, 0]), col(pts[:, 1]), col(pts[:, 2]), np.zeros((n, 1), np.float32),
+                         do_collision=True)
+        return np.asarray(wp["col"]).reshape(n).astype(bool)
+    return f
+
+
+@pytest.mark.parametrize("goal,depth,beam,lattice", [((4.0, 2.0), 6, 128, 0.1), ((-3.0, 3.5), 7, 96, 0.1),
+                                                     ((2.5, -1.0), 4, 4000, 0.0), ((40.0, 0.0), 3, 64, 0.1)])
+def test_plan_tree_matches_oracle(R, goal, depth, beam, lattice):
+    wl = W.room(N=20000, K=1, T=1)
+    start = (0.0, 0.0, 0.3)
+    tp = R.make_tree_params(max_depth=depth, beam=beam, lattice_xy=lattice, z=0.5)
+    m = R.map_from_workload(wl)
+    tr, cost, reached, stats = R.plan_tree(m, start, goal, tp)
+    x, y, z, yaw = (a.cpu().numpy() for a in tr.read())
+    res = P.plan_tree(_oracle_collides(wl), start, goal, tp)
+    ox, oy, oyaw, ocost = P.tree_waypoints(res, depth)
+    assert reached == res["reached"] and stats["expanded"] == res["expanded"]
+    assert np.array_equal(cost, ocost)                       # costs depend only on the controls: exact
+    assert np.array_equal(np.isnan(x), np.isnan(ox))
+    ok = ~np.isnan(ox)
+    for a, b in ((x, ox), (y, oy), (yaw, oyaw)):
+        assert np.all(np.abs(a[ok] - b[ok]) <= 1e-5)
+    assert np.all(z[ok] == np.float32(0.5))
+    # the candidates are then scored on their segment end states (Eq. traj_utility) and the best taken
+    p = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
+    fc, fe, g, u = R.score(m, tr, wl.camera, p)
+    orc = O.score(wl, x=ox, y=oy, z=np.where(ok, np.float32(0.5), np.float32(np.nan)).astype(np.float32), yaw=oyaw,
+                  no_collision=True)
+    b = R.best(u)[1]
+    assert b in set(int(v) for v in orc["acceptable"])
+    m.close()
+    tr.close()
+
+
+def test_plan_tree_trapped(R):
+    # start inside a wall of obstacles: no collision-free primitive -> RTG_ERR_NO_FEASIBLE
+    n = 400
+    rng = np.random.default_rng(1)
+    means = np.stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), np.full(n, 0.5)]).astype(np.float32)
+    wl = W.Workload("trap", means, np.tile(np.array([[1], [0], [0], [0]], np.float32), (1, n)),
+                    np.full((3, n), 0.05, np.float32), np.ones(n, np.float32), rng.random(n).astype(np.float32),
+                    None, np.zeros((1, 1), np.float32), np.zeros((1, 1), np.float32), np.full((1, 1), 0.5, np.float32),
+                    np.zeros((1, 1), np.float32), W.Robot(0.3), W.Camera(64, 48, 50, 50, 32, 24, 0.1, 5), 0.1)
+    m = R.map_from_workload(wl)
+    with pytest.raises(R.RTGError) as ei:
+        R.plan_tree(m, (0.0, 0.0, 0.0), (5.0, 0.0), R.make_tree_params(max_depth=3, z=0.5))
+    assert ei.value.status == R.ERR_NO_FEASIBLE
+    m.close()

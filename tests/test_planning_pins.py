@@ -122,3 +122,95 @@ def test_cost_benefit_spec_examples():
     b, _ = P.cost_benefit([1.0, 1.0, 1.0], [0.5, 0.5, 0.5])
     assert b == 0
     assert P.cost_benefit([], []) == (-1, -math.inf)
+
+
+# ----------------------------------------------------------------- N3 motion-primitive tree
+
+class _Params:
+    def __init__(self, **kw):
+        d = dict(n_v=3, n_omega=5, v_max=0.6, omega_max=0.9, dt=1.0, lambda_t=1.0, samples=5, max_depth=8,
+                 goal_radius=0.5, lattice_xy=0.1, lattice_deg=10.0, beam=4096, n_traj=10, z=0.5)
+        d.update(kw)
+        self.__dict__.update(d)
+
+
+def test_controls_paper_grid():
+    c = P.controls(3, 5, 0.6, 0.9)                       # N_v = 3, v_max = 0.6, N_w = 5, w_max = 0.9
+    assert len(c) == 15
+    vs = sorted({v for v, _ in c})
+    ws = sorted({w for _, w in c})
+    assert vs == pytest.approx([0.0, 0.3, 0.6], abs=1e-7)
+    assert ws == pytest.approx([-0.9, -0.45, 0.0, 0.45, 0.9], abs=1e-7)
+    assert P.controls(1, 1, 0.6, 0.9) == [(float(np.float32(0.6)), 0.0)]
+
+
+def test_unicycle_closed_form_spec_examples():
+    assert P.unicycle_at(0, 0, 0, 1.0, 0.0, 1.0) == pytest.approx((1.0, 0.0, 0.0))
+    x, y, th = P.unicycle_at(0, 0, 0, 1.0, math.pi / 2, 1.0)
+    assert (x, y, th) == pytest.approx((2 / math.pi, 2 / math.pi, math.pi / 2), rel=1e-15)
+    assert P.unicycle_at(1.5, -2.0, 0.3, 0.0, 0.0, 1.0) == (1.5, -2.0, 0.3)
+
+
+def test_tree_open_map_straight_goal_cost():
+    """empty map, goal 3 m ahead -> the selected candidate reaches the goal with cost
+    within 10 % of 3 m / v_max (lambda_t + v_max^2)."""
+    res = P.plan_tree(lambda pts: np.zeros(len(pts), bool), (0.0, 0.0, 0.0), (3.0, 0.0), _Params(beam=256))
+    assert res["reached"]
+    best = res["nodes"][res["cands"][0]]
+    assert (best[0] - 3.0) ** 2 + best[1] ** 2 <= 0.25
+    bound = 3.0 / 0.6 * (1.0 + 0.36)
+    assert best[3] <= 1.1 * bound
+    costs = [res["nodes"][i][3] for i in res["cands"]]
+    assert costs == sorted(costs) and len(costs) == 10
+
+
+def test_tree_equals_exhaustive_enumeration():
+    """without the lattice and with an unbounded beam, the cheapest candidate equals the
+    minimum over the exhaustively enumerated control sequences (stopping at the goal region)."""
+    import itertools
+    p = _Params(max_depth=3, lattice_xy=0.0, beam=10 ** 6, goal_radius=0.3)
+    goal = (1.0, 0.4)
+    free = lambda pts: np.zeros(len(pts), bool)
+    res = P.plan_tree(free, (0.0, 0.0, 0.2), goal, p)
+    ctl = P.controls(3, 5, 0.6, 0.9)
+    best = math.inf
+    for seq in itertools.chain.from_iterable(itertools.product(range(15), repeat=d) for d in (1, 2, 3)):
+        x, y, th, g = 0.0, 0.0, float(np.float32(0.2)), 0.0
+        for k, pi in enumerate(seq):
+            v, w = ctl[pi]
+            x, y, th = P.unicycle_at(x, y, th, v, w, 1.0)
+            th = P.wrap_pi(th)
+            g += (1.0 + v * v + w * w) * 1.0
+            if (x - 1.0) ** 2 + (y - float(np.float32(0.4))) ** 2 <= float(np.float32(0.3)) ** 2:
+                if k == len(seq) - 1:
+                    best = min(best, g)
+                break
+    assert res["reached"] and res["nodes"][res["cands"][0]][3] == pytest.approx(best, rel=1e-12)
+
+
+def _primitive_samples(par, child, ctl, S=5):
+    """The sample states of the control leading from node par to node child (found by its end state)."""
+    for v, w in ctl:
+        e = P.unicycle_at(par[0], par[1], par[2], v, w, 1.0)
+        if abs(e[0] - child[0]) < 1e-12 and abs(e[1] - child[1]) < 1e-12:
+            return [P.unicycle_at(par[0], par[1], par[2], v, w, j / (S - 1)) for j in range(1, S)]
+    raise AssertionError("no control reproduces the child")
+
+
+def test_tree_wall_samples_avoid_obstacle_and_fallback():
+    wall = lambda pts: (np.abs(pts[:, 0] - 1.5) < 0.3) & (np.abs(pts[:, 1]) < 1.0)
+    res = P.plan_tree(wall, (0.0, 0.0, 0.0), (3.0, 0.0), _Params(max_depth=6, beam=512))
+    assert res["reached"]
+    ctl = P.controls(3, 5, 0.6, 0.9)
+    nodes = res["nodes"]
+    for i in res["cands"]:      # re-check every sample of every primitive of every candidate
+        while nodes[i][4] >= 0:
+            smp = _primitive_samples(nodes[nodes[i][4]], nodes[i], ctl)
+            assert not np.any(wall(np.array([[x, y, 0.5] for x, y, _ in smp], np.float32)))
+            i = nodes[i][4]
+    # a goal behind a closed wall: nothing reaches it -> the nodes closest to the goal
+    closed = lambda pts: pts[:, 0] > 0.7
+    r2 = P.plan_tree(closed, (0.0, 0.0, 0.0), (3.0, 0.0), _Params(max_depth=2))
+    assert not r2["reached"] and len(r2["cands"]) == 10
+    hs = [math.hypot(3.0 - r2["nodes"][i][0], r2["nodes"][i][1]) for i in r2["cands"]]
+    assert hs == sorted(hs)
