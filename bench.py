@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=-1, help="steps timed per phase (default: all)")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="weak: K trajectories per GPU; strong: the config's K shared by the GPUs "
+                         "(default: strong for the scale config, which fixes the total K, else weak)")
     ap.add_argument("--cells", default=None,
                     help="visibility grid cells 'hy,hx,hz' [m] (rtg_map_options; default: library defaults)")
     return ap.parse_args()
@@ -183,16 +186,22 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    # ---- workload: the map is replicated; the global trajectory set is interleaved over ranks
+    # ---- workload: the map is replicated; the global trajectory set (and the gain-only views of the
+    # scale config) is interleaved over ranks: weak scaling grows it with the ranks, strong keeps it
+    scaling = args.scaling or ("strong" if args.config == "scale" else "weak")
     base = W.make(args.config)
-    Kr = base.K
-    if world > 1:
-        glob = W.make(args.config, K=base.K * world)
-        sel = np.arange(rank, glob.K, world)
-        wl = W.subset_trajectories(glob, sel)
-    else:
-        wl = base
+    glob = base if (world == 1 or scaling == "strong") else W.make(args.config, K=base.K * world)
+    K_glob = glob.K
+    wl = W.subset_trajectories(glob, np.arange(rank, glob.K, world)) if world > 1 else glob
     N, K, T = wl.N, wl.K, wl.T
+    views = None
+    Kv_glob = 0
+    if glob.views is not None:
+        vsel = np.arange(rank, glob.views["x"].shape[0], world)
+        views = [np.ascontiguousarray(glob.views[c][vsel]) for c in ("x", "y", "z", "yaw")]
+        Kv_glob = glob.views["x"].shape[0]
+    vparams = R.make_params(mode=R.MODE_CULLED if args.mode == "culled" else R.MODE_DENSE,
+                            flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
     cam = R.make_camera(wl.camera)
     params = R.make_params(mode=R.MODE_CULLED if args.mode == "culled" else R.MODE_DENSE,
                            info_stride=args.stride)
@@ -202,7 +211,12 @@ def main():
     pin = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     hmap = [pin(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)]
     htraj = [pin(a) for a in (wl.x, wl.y, wl.z, wl.yaw)]
-    h2d_bytes = sum(a.numel() * a.element_size() for a in hmap + htraj if a is not None)
+    dviews = [to_dev(a) for a in views] if views is not None else None
+    hviews = [pin(a) for a in views] if views is not None else None
+    h2d_bytes = sum(a.numel() * a.element_size() for a in hmap + htraj + (hviews or []) if a is not None)
+    Kv = views[0].shape[0] if views is not None else 0
+    vouts = tuple(torch.empty(Kv, dtype=dt, device=dev) for dt in (torch.int32, torch.uint8, torch.float64,
+                                                                    torch.float64)) if Kv else None
     outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
             torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -225,6 +239,12 @@ def main():
         R.score(m, tr, cam, params, *outs)
         s, i = R.best(outs[3])
         res = global_best(s, i)
+        if Kv:   # the scale config's gain-only views (T = 1, no collision): best view by xi
+            tv = R.Traj.upload(*((hviews if host else dviews)), device=local)
+            R.score(m, tv, cam, vparams, *vouts)
+            vs, vi = R.best(vouts[3])
+            res = res + global_best(vs, vi)
+            tv.close()
         m.close()
         tr.close()
         return res
@@ -264,7 +284,7 @@ def main():
     nprof = args.steps
     launches_per_step = prof["launches"] / args.steps
     clock = clocks.summary()
-    pairs = float(K) * T * N * world
+    pairs = float(K_glob) * T * N + float(Kv_glob) * N
     value = pairs / (ms / 1000.0)
 
     # ---- e2e through the same public API from pinned host memory
@@ -308,13 +328,15 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": "outdoor (BASELINE.json configs[3])" if args.config == "outdoor" else args.config,
-                           "N": N, "K_per_gpu": Kr, "T": T, "mode": args.mode, "info_stride": args.stride,
+                           "N": N, "K": K_glob, "K_per_gpu": K, "views": Kv_glob, "T": T, "mode": args.mode,
+                           "info_stride": args.stride,
                            "parallelism": f"traj-shard x{world}, map replicated",
                            "l2": "flushed (512 MiB write) between timed steps"},
                 "best": {"score": res[0], "index": res[1]},
+                **({"best_view": {"score": res[2], "index": res[3]}} if len(res) > 2 else {}),
                 "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
                 "gpu_launches": int(round(launches_per_step)),
                 "clocks": clock, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
