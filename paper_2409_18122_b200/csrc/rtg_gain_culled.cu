@@ -80,7 +80,7 @@ template <bool kStats>
 __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
-    const GRec* __restrict__ grec, const int* __restrict__ gstartA,
+    const double2* __restrict__ trig, const GRec* __restrict__ grec, const int* __restrict__ gstartA,
     const int* __restrict__ gtabB, const int2* __restrict__ zocc, const TabP* __restrict__ gtabP, const GainK g,
     const CamK cam, long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
     int* __restrict__ counter, unsigned long long* __restrict__ stats) {
@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
         if (isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(yw)) {
             WpF f;
             {
-                double cs, sn;
-                wp_setup_cs(px, py, pz, yw, cam, f, cs, sn);
+                const double2 t2 = trig[e];   // FP64 (cos, sin) of the yaw, one per list entry (k_wp_trig)
+                const double cs = t2.x, sn = t2.y;
+                wp_setup_from_cs(px, py, pz, yw, cs, sn, cam, f);
                 const float qx = px - g.ox, qy = py - g.oy;
                 if (lane < 4) {     // vertex = p + Z (c, s) + kZ (s, -c)
                     const float zz = lane < 2 ? g.zn : g.zf;
@@ -414,6 +415,17 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     }
 }
 
+// FP64 cos / sin of each listed waypoint's yaw, once (the gain kernel's warps would otherwise all
+// evaluate the same FP64 sincos on every lane)
+__global__ void k_wp_trig(const int* __restrict__ list, const int* __restrict__ count, const float* __restrict__ Yaw,
+                          double2* __restrict__ trig) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= *count) return;
+    double sn, cs;
+    sincos((double)Yaw[list[e]], &sn, &cs);
+    trig[e] = make_double2(cs, sn);
+}
+
 int g_sms_g = 0, g_occ_g = 0;
 
 }  // namespace
@@ -447,19 +459,26 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     g.kxl = cam.kxh - cam.kxc; g.kxr = cam.kxh + cam.kxc;
     g.kyu = cam.kyh + cam.kyc; g.kyd = cam.kyh - cam.kyc;
     g.kxh = cam.kxh;
+    double2* trig = nullptr;
+    cudaError_t et = dev_alloc((void**)&trig, sizeof(double2) * (size_t)(list_max > 0 ? list_max : 1), st);
+    if (et != cudaSuccess) return et;
+    if (list_max > 0)
+        note_launch(), k_wp_trig<<<(unsigned)((list_max + 255) / 256), 256, 0, st>>>(list, count, tr->yaw, trig);
     long long blocks = (list_max + kWarpsG - 1) / kWarpsG;
     long long cap = (long long)g_sms_g * g_occ_g;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     if (stats)
         note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
+            tr->x, tr->y, tr->z, tr->yaw, list, count, trig, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
             cam, wp_gq, wp_nh, wp_nl, counter, stats);
     else
         note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
+            tr->x, tr->y, tr->z, tr->yaw, list, count, trig, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
             cam, wp_gq, wp_nh, wp_nl, counter, stats);
-    return cudaGetLastError();
+    cudaError_t e2 = cudaGetLastError();
+    dev_free(trig, st);
+    return e2;
 }
 
 }  // namespace rtg

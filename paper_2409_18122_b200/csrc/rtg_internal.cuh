@@ -91,6 +91,15 @@ __device__ __forceinline__ void wp_setup_cs(float x, float y, float z, float yaw
     f.bx = (float)(-cs - (double)k.kxc * sn);
 }
 
+// same, from a precomputed FP64 (cos, sin) of the yaw
+__device__ __forceinline__ void wp_setup_from_cs(float x, float y, float z, float yaw, double cs, double sn,
+                                                 const CamK& k, WpF& f) {
+    f.px = x; f.py = y; f.pz = z; f.yaw = yaw;
+    f.c = (float)cs; f.s = (float)sn;
+    f.ax = (float)(sn - (double)k.kxc * cs);
+    f.bx = (float)(-cs - (double)k.kxc * sn);
+}
+
 __device__ __forceinline__ void wp_setup(float x, float y, float z, float yaw, const CamK& k, WpF& f) {
     double sn, cs;
     sincos((double)yaw, &sn, &cs);
