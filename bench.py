@@ -231,11 +231,19 @@ def main():
         hy, hx, hz = (float(v) for v in args.cells.split(","))
         map_opts = (hy, hz, 0.0, hx)
 
+    aux = torch.cuda.Stream(device=dev)
+
     def step(host: bool):
         src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
         m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
                   device=local, options=map_opts)
-        tr = R.Traj.upload(*src_traj, device=local)
+        if host:
+            # rtg_map_create returns once the map is on the device and its build is enqueued: the
+            # waypoint upload then overlaps the build on a second stream
+            tr = R.Traj.upload(*src_traj, device=local, stream=aux)
+            stream.wait_stream(aux)
+        else:
+            tr = R.Traj.upload(*src_traj, device=local)
         R.score(m, tr, cam, params, *outs)
         s, i = R.best(outs[3])
         res = global_best(s, i)
@@ -246,6 +254,8 @@ def main():
             res = res + global_best(vs, vi)
             tv.close()
         m.close()
+        if host:
+            aux.wait_stream(stream)   # the waypoints are released on their upload stream
         tr.close()
         return res
 
