@@ -434,15 +434,20 @@ __global__ void k_class_records(long long n_rec, GRec* __restrict__ grec, const 
     grec[i].uc = class_of(w[g], variant, cs);
 }
 
-// copy-B start table in z-fastest layout [iy][ix][iz], ix = 0..nx (ix = nx: end of the z-slab):
-// the culled kernel's lanes take consecutive z-cells of a row, so their lookups share lines
-__global__ void k_gather_tabB(GainGrid gg, const int* __restrict__ startB, int* __restrict__ tabB) {
+
+// both z-fastest tables in one pass at map build: the copy-B start of the cell (key order scan)
+// and the exact prefixes there
+__global__ void k_build_tabs(GainGrid gg, const int* __restrict__ startB, const longlong2* __restrict__ pqhl,
+                             int* __restrict__ tabB, TabP* __restrict__ tabP) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long nx1 = gg.nx + 1;
     if (e >= (long long)gg.ny * nx1 * gg.nz) return;
     const long long iz = e % gg.nz, r = e / gg.nz;
     const long long ix = r % nx1, iy = r / nx1;
-    tabB[e] = startB[(iy * gg.nz + iz) * gg.nx + ix];
+    const int s = startB[(iy * gg.nz + iz) * gg.nx + ix];
+    tabB[e] = s;
+    const longlong2 v = pqhl[s];
+    tabP[e] = TabP{(double)v.x, (int)(v.y & 0xffffffffLL), (int)(v.y >> 32)};
 }
 
 // prefixes at every copy-B table entry (same z-fastest layout as gtabB): one lookup per x-run end
@@ -475,7 +480,8 @@ static cudaError_t class_stats(long long n, const float* w, const unsigned char*
 }
 
 // exact prefixes of copy B's (u_q, packed class count) pairs, gathered at the table entries
-static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st) {
+// startB (map build only): the key-order start table; gtabB is then written in the same pass
+static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB = nullptr) {
     const long long ng = m->n_gain;
     long long* pqhl = nullptr;
     cudaError_t e = dev_alloc((void**)&pqhl, 2 * sizeof(long long) * (ng + 1), st);
@@ -483,7 +489,11 @@ static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st) {
     e = exclusive_scan_grec_uc(m->grec + m->n_gain_pad, pqhl, ng, st);
     if (e == cudaSuccess) {
         const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
-        note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, (const longlong2*)pqhl, m->gtabP);
+        if (startB)
+            note_launch(), k_build_tabs<<<nblocks(nt, 256), 256, 0, st>>>(m->gg, startB, (const longlong2*)pqhl, m->gtabB,
+                                                                          m->gtabP);
+        else
+            note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, (const longlong2*)pqhl, m->gtabP);
         e = cudaGetLastError();
     }
     dev_free(pqhl, st);
@@ -679,10 +689,6 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     // cursors (reuse the count arrays)
     MAP_CK(cudaMemcpyAsync(gcountA, m->gstartA, sizeof(int) * gg.ncellsA, cudaMemcpyDeviceToDevice, st));
     MAP_CK(cudaMemcpyAsync(gcountB, gstartB, sizeof(int) * gg.ncellsB, cudaMemcpyDeviceToDevice, st));
-    {
-        const long long nt = (long long)gg.ny * (gg.nx + 1) * gg.nz;
-        note_launch(), k_gather_tabB<<<nblocks(nt, 256), 256, 0, st>>>(gg, gstartB, m->gtabB);
-    }
     MAP_CK(cudaMemcpyAsync(ccount, m->cstart, sizeof(int) * cg.ncells, cudaMemcpyDeviceToDevice, st));
     if (n > 0) {
         note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, gg, gcountA, gcountB, m->n_gain_pad,
@@ -701,10 +707,10 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     dev_free(ckey, st);
     dev_free(gcountA, st);
     dev_free(gcountB, st);
-    dev_free(gstartB, st);
     dev_free(ccount, st);
     // --- default classification (k = 1/2, derived thresholds)
-    MAP_CK(class_prefix(m, st));
+    MAP_CK(class_prefix(m, st, gstartB));
+    dev_free(gstartB, st);
     set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
     return RTG_OK;
 }
