@@ -183,9 +183,11 @@ __global__ void k_zocc_init(int2* zocc, long long n) {
 }
 
 // cell keys: visibility copy B key (iy, iz, ix) (copy A's (iy, ix) follows from it), collision key
-// (iz, iy, ix); per-cell counts and the occupied z-range of every visibility row
+// (iz, iy, ix); per-cell counts, each Gaussian's rank in its cells (the counting-sort slot within
+// the cell, so the scatter needs no second atomic) and the occupied z-range of every row block
 __global__ void k_keys(long long n, const float* __restrict__ means, const unsigned char* __restrict__ flags,
                        GainGrid gg, ColGrid cg, int* __restrict__ gkey, int* __restrict__ ckey,
+                       int2* __restrict__ grank, int* __restrict__ crank,
                        int* __restrict__ gcountA, int* __restrict__ gcountB, int2* __restrict__ zocc,
                        int* __restrict__ ccount) {
     const double igx = 1.0 / gg.hx, igy = 1.0 / gg.hy, igz = 1.0 / gg.hz, icg = 1.0 / cg.h;
@@ -199,8 +201,9 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
             int iy = cell_coord(y, gg.oy, igy, gg.ny);
             int iz = cell_coord(z, gg.oz, igz, gg.nz);
             gk = (int)(((long long)iy * gg.nz + iz) * gg.nx + ix);
-            atomicAdd(&gcountB[gk], 1);
-            atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);
+            const int rb = atomicAdd(&gcountB[gk], 1);
+            const int ra = atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);
+            grank[i] = make_int2(ra, rb);
             int2* zo = zocc + (long long)iy * gg.nxb + ix / kZoccX;
             if (iz < zo->x) atomicMin(&zo->x, iz);
             if (iz > zo->y) atomicMax(&zo->y, iz);
@@ -210,7 +213,7 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
             int iy = cell_coord(y, cg.oy, icg, cg.ny);
             int iz = cell_coord(z, cg.oz, icg, cg.nz);
             ck = (int)(((long long)iz * cg.ny + iy) * cg.nx + ix);
-            atomicAdd(&ccount[ck], 1);
+            crank[i] = atomicAdd(&ccount[ck], 1);
         }
         gkey[i] = gk;
         ckey[i] = ck;
@@ -233,8 +236,9 @@ __device__ __forceinline__ unsigned class_of(float w, int variant, const ClassSt
 // both visibility copies: A at cursorA (relative to 0), B at offB + cursorB, with their packed
 // class and fixed-point u (the classification statistics are computed before the scatter)
 __global__ void k_scatter_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
-                               const int* __restrict__ gkey, GainGrid gg, int* __restrict__ cursorA,
-                               int* __restrict__ cursorB, long long offB, GRec* __restrict__ grec,
+                               const int* __restrict__ gkey, const int2* __restrict__ grank, GainGrid gg,
+                               const int* __restrict__ startA, const int* __restrict__ startB, long long offB,
+                               GRec* __restrict__ grec,
                                int* __restrict__ gidx, int variant, const ClassState* __restrict__ cs) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -243,8 +247,9 @@ __global__ void k_scatter_gain(long long n, const float* __restrict__ means, con
         const long long nzx = (long long)gg.nz * gg.nx;
         const long long iy = k / nzx, ix = k % gg.nx;
         const GRec r{means[i], means[n + i], means[2 * n + i], class_of(w[i], variant, cs)};
-        int sa = atomicAdd(&cursorA[iy * gg.nx + ix], 1);
-        int sb = atomicAdd(&cursorB[k], 1);
+        const int2 rk = grank[i];
+        const int sa = startA[iy * gg.nx + ix] + rk.x;
+        const int sb = startB[k] + rk.y;
         grec[sa] = r;
         gidx[sa] = (int)i;
         grec[offB + sb] = r;
@@ -255,13 +260,14 @@ __global__ void k_scatter_gain(long long n, const float* __restrict__ means, con
 // FP64 packing of the collision record (a1)
 __global__ void k_scatter_col(long long n, const float* __restrict__ means, const float* __restrict__ quats,
                               const float* __restrict__ scales, const int* __restrict__ ckey,
-                              int* __restrict__ cursor, rtg_robot rb, double guard, CRec* __restrict__ crec,
+                              const int* __restrict__ crank, const int* __restrict__ cstart, rtg_robot rb,
+                              double guard, CRec* __restrict__ crec,
                               CMat* __restrict__ cmat, CSrc* __restrict__ csrc) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int k = ckey[i];
         if (k < 0) continue;
-        int slot = atomicAdd(&cursor[k], 1);
+        const int slot = cstart[k] + crank[i];
         CSrc src;
         src.q[0] = quats[i]; src.q[1] = quats[n + i]; src.q[2] = quats[2 * n + i]; src.q[3] = quats[3 * n + i];
         src.s[0] = scales[i]; src.s[1] = scales[n + i]; src.s[2] = scales[2 * n + i];
@@ -670,6 +676,10 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     int *gkey = nullptr, *ckey = nullptr, *gcountA = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
     MAP_CK(dev_alloc((void**)&gkey, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&ckey, sizeof(int) * (n > 0 ? n : 1), st));
+    int2* grank = nullptr;
+    int* crank = nullptr;
+    MAP_CK(dev_alloc((void**)&grank, sizeof(int2) * (n > 0 ? n : 1), st));
+    MAP_CK(dev_alloc((void**)&crank, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&gcountA, sizeof(int) * (gg.ncellsA + 1), st));
     MAP_CK(dev_alloc((void**)&gcountB, sizeof(int) * (gg.ncellsB + 1), st));
     MAP_CK(dev_alloc((void**)&gstartB, sizeof(int) * (gg.ncellsB + 1), st));
@@ -680,21 +690,17 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc, (long long)gg.ny * gg.nxb);
     unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
     if (n > 0)
-        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, gcountA, gcountB, m->zocc,
-                                                  ccount);
+        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, grank, crank, gcountA, gcountB,
+                                                  m->zocc, ccount);
     MAP_CK(cudaGetLastError());
     MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));
     MAP_CK(exclusive_scan_i32(gcountB, gstartB, gg.ncellsB, st));
     MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
-    // cursors (reuse the count arrays)
-    MAP_CK(cudaMemcpyAsync(gcountA, m->gstartA, sizeof(int) * gg.ncellsA, cudaMemcpyDeviceToDevice, st));
-    MAP_CK(cudaMemcpyAsync(gcountB, gstartB, sizeof(int) * gg.ncellsB, cudaMemcpyDeviceToDevice, st));
-    MAP_CK(cudaMemcpyAsync(ccount, m->cstart, sizeof(int) * cg.ncells, cudaMemcpyDeviceToDevice, st));
     if (n > 0) {
-        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, gg, gcountA, gcountB, m->n_gain_pad,
-                                                          m->grec, m->gidx, RTG_VARIANT_XI, m->cls);
-        note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, ccount, rb, gq, m->crec, m->cmat,
-                                          m->csrc);
+        note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, grank, gg, m->gstartA, gstartB,
+                                                          m->n_gain_pad, m->grec, m->gidx, RTG_VARIANT_XI, m->cls);
+        note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq, m->crec,
+                                                         m->cmat, m->csrc);
     }
     if (m->n_gain_pad > m->n_gain)
         note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
@@ -705,6 +711,8 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(cudaGetLastError());
     dev_free(gkey, st);
     dev_free(ckey, st);
+    dev_free(grank, st);
+    dev_free(crank, st);
     dev_free(gcountA, st);
     dev_free(gcountB, st);
     dev_free(ccount, st);
