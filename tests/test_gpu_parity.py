@@ -403,3 +403,25 @@ def test_culled_equals_dense_axis_yaws_offcentre_cameras(R, room, cells):
             assert np.array_equal(out["dense"][kk], out["culled"][kk]), (cam, cells, kk)
         assert np.array_equal(out["dense"]["wp_gain"].view(np.int64), out["culled"]["wp_gain"].view(np.int64))
         assert out["dense"]["wp_nh"].sum() > 0
+
+
+def test_far_from_origin_translation_invariance(R, room):
+    """The same room translated by (+5000, -3000, +40) m: FP32 positions lose resolution there, so
+    the kernels' cell margins and FP64 re-decisions must widen accordingly; the decisions must still
+    equal the FP64 decision on the translated fp32 inputs (oracle) and culled must equal dense."""
+    import dataclasses
+    off = np.array([5000.0, -3000.0, 40.0], np.float32)
+    k = np.arange(0, room.K, 171)[:6]
+    wl = dataclasses.replace(room, means=(room.means + off[:, None]).astype(np.float32),
+                             x=(room.x[k] + off[0]).astype(np.float32), y=(room.y[k] + off[1]).astype(np.float32),
+                             z=(room.z[k] + off[2]).astype(np.float32), yaw=room.yaw[k].copy())
+    orc = O.score(wl)
+    outs = {}
+    for mode in MODES:
+        gpu = gpu_run(R, wl, mode)
+        check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
+        check_trajectories(gpu, orc, wl.T)
+        outs[mode] = gpu
+    for kk in ("wp_nh", "wp_nl", "wp_col"):
+        assert np.array_equal(outs["dense"][kk], outs["culled"][kk]), kk
+    assert np.array_equal(outs["dense"]["wp_gain"].view(np.int64), outs["culled"]["wp_gain"].view(np.int64))
