@@ -25,6 +25,7 @@
 // "inside" strictly inside and "possible" a superset.
 #include <cfloat>
 #include <climits>
+#include <cstdio>
 
 #include "rtg_host.hpp"
 
@@ -36,9 +37,24 @@ constexpr int kWarpsG = 8;
 constexpr int kQCap = 256;    // queued runs per warp
 constexpr int kQFlush = 192;  // test the queue once more runs than this are waiting (an append adds <= 64)
 
+// RTG_BOUNDS_CHECK builds trap on any out-of-range table or record index (debug builds; the
+// sanitizer is not available on the GPU pool)
+#ifdef RTG_BOUNDS_CHECK
+#define RTG_CHECK(cond, what)                                                                     \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("rtg bounds: %s (block %d thread %d)\n", what, (int)blockIdx.x, (int)threadIdx.x); \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define RTG_CHECK(cond, what) ((void)0)
+#endif
+
 struct GainK {
     float ox, oy, oz, hx, hy, hz, inv_hz, eps;
     int nx, ny, nz, nxb, offB;
+    long long nrec, ntabB, ntabA;   // sizes (bounds checks)
     float zn, zf, kxl, kxr, kyu, kyd, kxh;
 };
 
@@ -188,6 +204,9 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         const int ub0 = uy * (g.nx + 1) * g.nz + iz;
                         const int* sb = gtabB + ub0;
                         const bool in = j0 <= j1;
+                        RTG_CHECK(uy >= 0 && uy < g.ny && iz >= 0 && iz < g.nz && q0 >= 0 && q1 + 1 <= g.nx &&
+                                      (long long)ub0 + (long long)(q1 + 1) * g.nz < g.ntabB,
+                                  "unit table index");
                         const int a0 = __ldg(sb + q0 * g.nz), a3 = __ldg(sb + (q1 + 1) * g.nz);
                         const int a1 = !in ? a3 : (j0 == q0 ? a0 : __ldg(sb + j0 * g.nz));
                         const int a2 = !in ? a3 : (j1 == q1 ? a3 : __ldg(sb + (j1 + 1) * g.nz));
@@ -226,6 +245,9 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         // flanks P \ I of copy A (one run when I is empty)
                         const int* sa = gstartA + iy * g.nx;
                         const bool in = ri0 <= ri1;
+                        RTG_CHECK(iy >= 0 && iy < g.ny && p0 >= 0 && p1 + 1 <= g.nx &&
+                                      (long long)iy * g.nx + p1 + 1 < g.ntabA,
+                                  "flank table index");
                         s0 = __ldg(sa + p0);
                         l0 = __ldg(sa + (in ? ri0 : p1 + 1)) - s0;
                         if (in) {
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const int zhi = fcell((zrel + g.kyu * Zmax + g.eps) * g.inv_hz, g.nz);
                             int olo = INT_MAX, ohi = -1;
                             const int2* zo = zocc + iy * g.nxb;
+                            RTG_CHECK(ri1 / kZoccX < g.nxb, "z-occupancy block");
                             for (int b = ri0 / kZoccX; b <= ri1 / kZoccX; ++b) {
                                 const int2 o = __ldg(zo + b);
                                 olo = min(olo, o.x);
@@ -344,6 +367,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const int gpa = gb + lane, gpb = gpa + 32;
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_le)];
                             const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_le)];
+                            RTG_CHECK(gia >= 0 && gia < g.nrec && gib >= 0 && gib < g.nrec, "record index");
                             const GRec Ga = grec[gia], Gb = grec[gib];
                             float Za, Zb;
                             const float ma = vis_margin(f, cam, Ga.x, Ga.y, Ga.z, Za);
@@ -450,6 +474,9 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     g.inv_hz = 1.0f / gg.hz;
     g.nx = gg.nx; g.ny = gg.ny; g.nz = gg.nz; g.nxb = gg.nxb;
     g.offB = (int)m->n_gain_pad;
+    g.nrec = 2 * m->n_gain_pad;
+    g.ntabB = (long long)gg.ny * (gg.nx + 1) * gg.nz;
+    g.ntabA = gg.ncellsA + 1;
     // eps >> the FP32 error of a cell's centre value (a few ulps of the largest term: offsets of
     // at most the grid extent plus the distance of any waypoint to the grid origin)
     double ext = fabs(gg.ox) + fabs(gg.oy) + fabs(gg.oz) + gg.nx * (double)gg.hx + gg.ny * (double)gg.hy +
