@@ -51,9 +51,6 @@ struct ColGrid {
 
 // scans (rtg_scan.cu): exclusive prefix of n values into out[0..n] (out[n] = total)
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_t st);
-cudaError_t exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t st);
-// n pairs (in[2i], in[2i+1]) scanned together into out[0 .. 2n+1]
-cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st);
 // copy-B records' (u_q, nH | nL << 32) pairs (from GRec::uc) scanned into out[0 .. 2n+1]
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st);
 // device allocation through the stream-ordered pool

@@ -47,18 +47,25 @@ struct __align__(32) CSrc { float q[4]; float s[3]; float pad; };
 // a1 in FP64: inflated semi-axes a_i = lambda_g s_i + r_robot (PRINCIPAL_AXIS: every
 // a_i = lambda_g max s + r_robot) and M = diag(1/a) R^T with R the Hamilton rotation of
 // the normalised quaternion (w, x, y, z).  Used for packing and for every FP64 re-decision.
-__device__ __forceinline__ void pack_m64(double qw, double qx, double qy, double qz, double s0, double s1, double s2,
-                                         const rtg_robot& rb, double M[9], double a[3]) {
+__device__ __forceinline__ void semi_axes64(double s0, double s1, double s2, const rtg_robot& rb, double a[3]) {
     if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
         const double r = (double)rb.lambda_g * fmax(s0, fmax(s1, s2)) + (double)rb.r_robot;
         a[0] = a[1] = a[2] = r;
-        for (int j = 0; j < 9; ++j) M[j] = 0.0;
-        M[0] = M[4] = M[8] = 1.0 / r;
         return;
     }
     a[0] = (double)rb.lambda_g * s0 + (double)rb.r_robot;
     a[1] = (double)rb.lambda_g * s1 + (double)rb.r_robot;
     a[2] = (double)rb.lambda_g * s2 + (double)rb.r_robot;
+}
+
+__device__ __forceinline__ void pack_m64(double qw, double qx, double qy, double qz, double s0, double s1, double s2,
+                                         const rtg_robot& rb, double M[9], double a[3]) {
+    semi_axes64(s0, s1, s2, rb, a);
+    if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
+        for (int j = 0; j < 9; ++j) M[j] = 0.0;
+        M[0] = M[4] = M[8] = 1.0 / a[0];
+        return;
+    }
     const double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
     qw /= nq; qx /= nq; qy /= nq; qz /= nq;
     // Hamilton R (columns = local principal axes)

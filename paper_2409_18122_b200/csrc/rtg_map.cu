@@ -59,20 +59,6 @@ __global__ void k_bounds_init(DevBounds* b) {
     b->rhomax = f2o(1.f);
 }
 
-// inflated semi-axes in FP64
-__device__ __forceinline__ void semi_axes(const float* scales, long long n, long long i, const rtg_robot& rb,
-                                          double a[3]) {
-    double s0 = scales[i], s1 = scales[n + i], s2 = scales[2 * n + i];
-    if (rb.collide_rule == RTG_COLLIDE_PRINCIPAL_AXIS) {
-        double sm = fmax(s0, fmax(s1, s2));
-        double r = (double)rb.lambda_g * sm + (double)rb.r_robot;
-        a[0] = a[1] = a[2] = r;
-    } else {
-        a[0] = (double)rb.lambda_g * s0 + (double)rb.r_robot;
-        a[1] = (double)rb.lambda_g * s1 + (double)rb.r_robot;
-        a[2] = (double)rb.lambda_g * s2 + (double)rb.r_robot;
-    }
-}
 
 __global__ void k_bounds(long long n, const float* __restrict__ means, const float* __restrict__ quats,
                          const float* __restrict__ scales, const float* __restrict__ opacity,
@@ -112,7 +98,7 @@ __global__ void k_bounds(long long n, const float* __restrict__ means, const flo
                 cmx[d] = max(cmx[d], o);
             }
             double a[3];
-            semi_axes(scales, n, i, rb, a);
+            semi_axes64(scales[i], scales[n + i], scales[2 * n + i], rb, a);
             double amax = fmax(a[0], fmax(a[1], a[2])), amin = fmin(a[0], fmin(a[1], a[2]));
             if (isfinite(amax)) {
                 rbm = max(rbm, f2o(__double2float_ru(amax)));

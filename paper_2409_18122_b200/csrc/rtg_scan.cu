@@ -23,19 +23,16 @@ struct I64x2 {
     __host__ __device__ I64x2 operator-(const I64x2& o) const { return I64x2(a - o.a, b - o.b); }
 };
 __device__ __forceinline__ int shfl_up(int v, int o) { return __shfl_up_sync(0xffffffffu, v, o); }
-__device__ __forceinline__ long long shfl_up(long long v, int o) { return __shfl_up_sync(0xffffffffu, v, o); }
 __device__ __forceinline__ I64x2 shfl_up(I64x2 v, int o) {
     return I64x2(__shfl_up_sync(0xffffffffu, v.a, o), __shfl_up_sync(0xffffffffu, v.b, o));
 }
 __device__ __forceinline__ int shfl_down(int v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
-__device__ __forceinline__ long long shfl_down(long long v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
 __device__ __forceinline__ I64x2 shfl_down(I64x2 v, int o) {
     return I64x2(__shfl_down_sync(0xffffffffu, v.a, o), __shfl_down_sync(0xffffffffu, v.b, o));
 }
 
 // L2 loads of other tiles' published values (never a stale L1 line)
 __device__ __forceinline__ int load_cg(const int* p) { return __ldcg(p); }
-__device__ __forceinline__ long long load_cg(const long long* p) { return __ldcg(p); }
 __device__ __forceinline__ I64x2 load_cg(const I64x2* p) {
     const long long* q = reinterpret_cast<const long long*>(p);
     return I64x2(__ldcg(q), __ldcg(q + 1));
@@ -191,13 +188,6 @@ cudaError_t scan_impl(Load in, T* out, long long n, cudaStream_t st) {
 
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_t st) {
     return scan_impl<int>(LoadArr<int>{in}, out, n, st);
-}
-cudaError_t exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t st) {
-    return scan_impl<long long>(LoadArr<long long>{in}, out, n, st);
-}
-// pairs of int64 (in[2i], in[2i+1]) scanned together
-cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st) {
-    return scan_impl<I64x2>(LoadArr<I64x2>{reinterpret_cast<const I64x2*>(in)}, reinterpret_cast<I64x2*>(out), n, st);
 }
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
     return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);
