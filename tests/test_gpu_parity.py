@@ -425,3 +425,53 @@ def test_far_from_origin_translation_invariance(R, room):
     for kk in ("wp_nh", "wp_nl", "wp_col"):
         assert np.array_equal(outs["dense"][kk], outs["culled"][kk]), kk
     assert np.array_equal(outs["dense"]["wp_gain"].view(np.int64), outs["culled"]["wp_gain"].view(np.int64))
+
+
+_FUZZ = int(__import__("os").environ.get("RTG_FUZZ_SEEDS", "12"))
+
+
+@pytest.mark.parametrize("seed", range(_FUZZ))
+def test_fuzz_random_maps_cameras_grids(R, seed):
+    """Randomised: map box, density, anisotropy, flags; camera intrinsics (principal point anywhere,
+    z_near may be 0); visibility / collision grid shapes; waypoints inside and outside the map box with
+    random and axis-aligned yaws.  culled == dense bit for bit, and both match the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(50, 3000))
+    lo = rng.uniform(-20, 5, 3)
+    ext = rng.uniform(1, 15, 3)
+    means = (lo[:, None] + ext[:, None] * rng.random((3, n))).astype(np.float32)
+    q = rng.normal(size=(4, n))
+    quats = (q / np.linalg.norm(q, axis=0)).astype(np.float32)
+    scales = np.exp(rng.uniform(np.log(0.01), np.log(0.6), (3, n))).astype(np.float32)
+    flags = (rng.integers(0, 4, n) * (rng.random(n) < 0.3)).astype(np.uint8)
+    w = rng.random(n).astype(np.float32)
+    Wd, Hd = int(rng.integers(16, 800)), int(rng.integers(16, 600))
+    fx, fy = float(rng.uniform(10, 900)), float(rng.uniform(10, 900))
+    cam = W.Camera(Wd, Hd, fx, fy, float(rng.uniform(0, Wd)), float(rng.uniform(0, Hd)),
+                   float(rng.choice([0.0, rng.uniform(0, 1)])), float(rng.uniform(1.5, 25)))
+    K, T = 6, 7
+    px = lo[0] + ext[0] * rng.uniform(-0.3, 1.3, (K, T))
+    py = lo[1] + ext[1] * rng.uniform(-0.3, 1.3, (K, T))
+    pz = lo[2] + ext[2] * rng.uniform(-0.2, 1.2, (K, T))
+    yaw = rng.uniform(-np.pi, np.pi, (K, T))
+    yaw[0] = np.array([0, np.pi / 2, np.pi, -np.pi / 2, np.pi / 4, 0, np.pi])
+    wl = W.Workload("fuzz", means, quats, scales, rng.random(n).astype(np.float32), w, flags,
+                    px.astype(np.float32), py.astype(np.float32), pz.astype(np.float32), yaw.astype(np.float32),
+                    W.Robot(float(rng.uniform(0, 0.5)), float(rng.uniform(1, 3))), cam, 0.1)
+    cells = (float(rng.uniform(0.05, 2)), float(rng.uniform(0.1, 3)), float(rng.uniform(0.3, 3)),
+             float(rng.uniform(0.02, 1)))
+    out = {}
+    for mode in MODES:
+        m = R.map_from_workload(wl, options=cells if mode == "culled" else None)
+        tr = R.traj_from_workload(wl)
+        p = R.make_params(mode=_mode(R, mode), flags=R.SCORE_FULL_GAIN)
+        d = R.score_debug(m, tr, cam, p)
+        out[mode] = {k: d[k].cpu().numpy() for k in ("wp_gain", "wp_nh", "wp_nl", "wp_col")}
+        out[mode]["shift"] = m.info().fixed_point_shift
+        m.close()
+        tr.close()
+    for k in ("wp_nh", "wp_nl", "wp_col"):
+        assert np.array_equal(out["dense"][k], out["culled"][k]), k
+    assert np.array_equal(out["dense"]["wp_gain"].view(np.int64), out["culled"]["wp_gain"].view(np.int64))
+    orc = O.score(wl)
+    check_waypoints(out["culled"], orc, out["culled"]["shift"])
