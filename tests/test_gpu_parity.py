@@ -475,3 +475,29 @@ def test_fuzz_random_maps_cameras_grids(R, seed):
     assert np.array_equal(out["dense"]["wp_gain"].view(np.int64), out["culled"]["wp_gain"].view(np.int64))
     orc = O.score(wl)
     check_waypoints(out["culled"], orc, out["culled"]["shift"])
+
+
+def test_scale_full_size_sampled_with_views(R):
+    """BASELINE.json configs[4] at full size (5M Gaussians, 65,536 x 100 waypoints, 8,192 gain-only
+    views) in the bench launch configuration; sampled trajectories and views against the oracle."""
+    wl = W.scale()
+    gpu = gpu_run(R, wl, "culled", flags=0, debug=False)
+    rng = np.random.default_rng(9)
+    feas = np.nonzero(gpu["feasible"])[0]
+    infeas = np.nonzero(gpu["feasible"] == 0)[0]
+    idx = np.sort(np.concatenate([rng.choice(feas, 2, replace=False), rng.choice(infeas, 1, replace=False)]))
+    orc = O.score(wl, traj_idx=idx)
+    fc, f = gpu["first_col"][idx], gpu["feasible"][idx].astype(bool)
+    assert np.all(orc["first_col_allowed"][np.arange(len(idx)), fc])
+    g = gpu["gain"][idx]
+    tol = 1e-5 * np.abs(orc["gain_hi"][f]) + 1e-9
+    assert np.all((g[f] >= orc["gain_lo"][f] - tol) & (g[f] <= orc["gain_hi"][f] + tol))
+    assert np.all((gpu["utility"][idx][f] >= orc["xi_lo"][f]) & (gpu["utility"][idx][f] <= orc["xi_hi"][f]))
+    # views: T = 1, no collision, full gain
+    vs = np.arange(0, wl.views["x"].shape[0], 1024)
+    v = {c: np.ascontiguousarray(wl.views[c][vs]) for c in ("x", "y", "z", "yaw")}
+    vg = gpu_run(R, wl, "culled", flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION, debug=False, **v)
+    vo = O.score(wl, no_collision=True, **v)
+    tol = 1e-5 * np.abs(vo["gain_hi"]) + 1e-9
+    assert np.all((vg["gain"] >= vo["gain_lo"] - tol) & (vg["gain"] <= vo["gain_hi"] + tol))
+    assert np.all((vg["utility"] >= vo["xi_lo"]) & (vg["utility"] <= vo["xi_hi"]))
