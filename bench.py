@@ -329,7 +329,7 @@ def main():
                     hbm_peak, work, traffic)
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # contract: rank 0 at N = 1 only
         cores = oracle_threads()
         n_traj = max(1, min(K, 2 * cores))
         v, dt, nt = oracle_sample(wl, n_traj)
