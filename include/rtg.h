@@ -158,7 +158,7 @@ typedef struct {
  * classifies with the default parameters and builds the visibility and collision grids.
  * Errors: RTG_ERR_INVALID_ARGUMENT on a bad pointer/size or any invalid element
  * (non-finite value, quaternion norm < 1e-12, scale <= 0, info_w < 0, opacity outside [0,1]);
- * RTG_ERR_OUT_OF_MEMORY; RTG_ERR_CUDA.  Synchronises `stream` once.
+ * RTG_ERR_OUT_OF_MEMORY; RTG_ERR_CUDA.  0 <= n < 2^30 - 4096.  Synchronises `stream` once.
  */
 rtg_status rtg_map_create(int device, long long n, rtg_mem kind,
                           const float* means, const float* quats, const float* scales,

@@ -250,7 +250,8 @@ rtg_status rtg_map_create_ex(int device, long long n, rtg_mem kind, const float*
                              void* stream, rtg_map* out) {
     if (!out) return invalid("out is NULL");
     *out = nullptr;
-    if (n < 0 || n >= (1LL << 31) - 1) return invalid("n must satisfy 0 <= n < 2^31 - 1");
+    // two padded record copies are indexed with 32-bit integers
+    if (n < 0 || n >= (1LL << 30) - 4096) return invalid("n must satisfy 0 <= n < 2^30 - 4096");
     if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
     if (n > 0 && (!means || !quats || !scales || !info_w)) return invalid("means, quats, scales and info_w are required");
     if (!robot) return invalid("robot is NULL");

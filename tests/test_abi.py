@@ -82,3 +82,32 @@ def test_binding_has_no_cpu_fallback():
             if f.endswith((".py", ".cu", ".cuh", ".hpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r'""".*?"""|#.*|//.*', "", txt, flags=re.S), f
+
+
+def test_planner_entry_points_validate_arguments(rtg):
+    """N2-N4 entry points reject bad arguments on the host (no GPU needed)."""
+    lib = rtg._lib
+    h = ctypes.c_void_p()
+    assert lib.rtg_ledger_update(0, -1, 0, None, None, None, None, None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_ledger_update(0, 5, 0, None, None, None, None, None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_map_update_weights(None, 0, None, None) == rtg.ERR_INVALID_ARGUMENT
+    o = (ctypes.c_double * 3)(0, 0, 0)
+    d = (ctypes.c_int * 3)(1, 1, 1)
+    assert lib.rtg_region_utility(None, o, 2.5, d, None, None, None) == rtg.ERR_INVALID_ARGUMENT
+    cam = rtg.Camera(64, 48, 50, 50, 32, 24, 0.1, 5.0)
+    c3 = (ctypes.c_float * 3)(0, 0, 0)
+    dist = ctypes.c_double()
+    assert lib.rtg_traj_view_ring(0, 0, 0, c3, 2.5, ctypes.byref(cam), 8, 0.5, None, ctypes.byref(h),
+                                  ctypes.byref(dist)) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_traj_view_ring(0, 1, 0, c3, -1.0, ctypes.byref(cam), 8, 0.5, None, ctypes.byref(h),
+                                  ctypes.byref(dist)) == rtg.ERR_INVALID_ARGUMENT
+    out = rtg.BestResult()
+    assert lib.rtg_cost_benefit(None, None, 0, None, ctypes.byref(out)) == rtg.ERR_INVALID_ARGUMENT
+    tp = rtg.make_tree_params()
+    nf, rc = ctypes.c_int(), ctypes.c_int()
+    g2 = (ctypes.c_float * 2)(1, 0)
+    assert lib.rtg_plan_tree(None, c3, g2, ctypes.byref(tp), None, ctypes.byref(h), None, ctypes.byref(nf),
+                             ctypes.byref(rc), None) == rtg.ERR_INVALID_ARGUMENT
+    robot = rtg.Robot(0.3, 3.0, 0)
+    assert lib.rtg_map_create(0, 1 << 30, 0, None, None, None, None, None, None, ctypes.byref(robot), None,
+                              ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
