@@ -369,12 +369,11 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_le)];
                             RTG_CHECK(gia >= 0 && gia < g.nrec && gib >= 0 && gib < g.nrec, "record index");
                             const GRec Ga = grec[gia], Gb = grec[gib];
-                            float Za, Zb;
-                            const float ma = vis_margin(f, cam, Ga.x, Ga.y, Ga.z, Za);
-                            const float mb = vis_margin(f, cam, Gb.x, Gb.y, Gb.z, Zb);
+                            float ma, mb, guard_a, guard_b;
+                            vis_margin2(f, cam, Ga.x, Ga.y, Ga.z, Gb.x, Gb.y, Gb.z, ma, mb, guard_a, guard_b);
                             bool visa = ma >= 0.0f, visb = mb >= 0.0f;
-                            const bool amba = fabsf(ma) < fmaf(cam.gam, Za, cam.g0);
-                            const bool ambb = fabsf(mb) < fmaf(cam.gam, Zb, cam.g0);
+                            const bool amba = fabsf(ma) < guard_a;
+                            const bool ambb = fabsf(mb) < guard_b;
                             if (__any_sync(kFullG, amba || ambb)) {
                                 if (amba) {
                                     visa = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], Ga.x, Ga.y,

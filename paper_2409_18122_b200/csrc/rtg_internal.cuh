@@ -131,6 +131,57 @@ __device__ __forceinline__ float vis_margin(const WpF& w, const CamK& k, float m
     return fminf(s1, fminf(s2, s3));
 }
 
+// two items at once with Blackwell's packed FP32 (f32x2: FADD2 / FMUL2 / FFMA2 on register pairs,
+// scalar operands broadcast): each half rounds exactly like vis_margin, so the margins are
+// bit-identical; the |.| terms stay scalar (no packed abs).  Also returns the FP32 guard.
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ void vis_margin2(const WpF& w, const CamK& k, float ax_, float ay_, float az_, float bx_,
+                                            float by_, float bz_, float& ma, float& mb, float& ga, float& gb) {
+    const unsigned long long dx = f2_sub(f2_pack(ax_, bx_), f2_pack(w.px, w.px));
+    const unsigned long long dy = f2_sub(f2_pack(ay_, by_), f2_pack(w.py, w.py));
+    const unsigned long long dz = f2_sub(f2_pack(az_, bz_), f2_pack(w.pz, w.pz));
+    const unsigned long long Z = f2_fma(f2_pack(w.c, w.c), dx, f2_mul(f2_pack(w.s, w.s), dy));
+    const unsigned long long X = f2_fma(f2_pack(w.ax, w.ax), dx, f2_mul(f2_pack(w.bx, w.bx), dy));
+    const unsigned long long Y = f2_fma(f2_pack(-k.kyc, -k.kyc), Z, dz);
+    const unsigned long long D = f2_sub(Z, f2_pack(k.zmid, k.zmid));
+    const unsigned long long G = f2_fma(f2_pack(k.gam, k.gam), Z, f2_pack(k.g0, k.g0));
+    float Za, Zb, Xa, Xb, Ya, Yb, Da, Db;
+    f2_unpack(Z, Za, Zb);
+    f2_unpack(X, Xa, Xb);
+    f2_unpack(Y, Ya, Yb);
+    f2_unpack(D, Da, Db);
+    f2_unpack(G, ga, gb);
+    ma = fminf(k.zhalf - fabsf(Da), fminf(fmaf(k.kxh, Za, -fabsf(Xa)), fmaf(k.kyh, Za, -fabsf(Ya))));
+    mb = fminf(k.zhalf - fabsf(Db), fminf(fmaf(k.kxh, Zb, -fabsf(Xb)), fmaf(k.kyh, Zb, -fabsf(Yb))));
+}
+
 // FP64 decision with the six slacks of the pinhole test (visible <=> all >= 0), cos/sin of the
 // yaw given in FP64.  Every product is an explicit fma/mul so all kernels round identically.
 __device__ __forceinline__ bool vis_decide64_cs(float px, float py, float pz, double cs, double sn, float mx,
