@@ -82,6 +82,13 @@ __device__ __forceinline__ void cut(const float4& C, float Cj, float& plo, float
     }
 }
 
+// 1 << n for n < 32, 0 for any larger n (PTX shl clamps the shift amount: no compare/select)
+__device__ __forceinline__ unsigned bit_or_zero(unsigned n) {
+    unsigned r;
+    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(n));
+    return r;
+}
+
 // acc += u_q and pc += class increment of record word uc when p (64-bit exact integer sum)
 __device__ __forceinline__ void add_if(bool p, unsigned long long& acc, unsigned uc, int& pc) {
     unsigned lo = (unsigned)acc, hi = (unsigned)(acc >> 32);
@@ -359,10 +366,9 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             // runs r0+1 .. r0+64 start at positions pa, pb (relative to gb) >= 1
                             const int ra = r0 + 1 + lane;
                             const int pa = qe[ra] - gb, pb = qe[ra + 32] - gb;
-                            const unsigned hlo = __reduce_or_sync(kFullG, pa < 32 ? 1u << pa : 0u);
-                            const unsigned ua = (unsigned)(pa - 32), ubb = (unsigned)(pb - 32);
+                            const unsigned hlo = __reduce_or_sync(kFullG, bit_or_zero((unsigned)pa));
                             const unsigned hhi = __reduce_or_sync(
-                                kFullG, (ua < 32u ? 1u << ua : 0u) | (ubb < 32u ? 1u << ubb : 0u));
+                                kFullG, bit_or_zero((unsigned)(pa - 32)) | bit_or_zero((unsigned)(pb - 32)));
                             const int na = __popc(hlo);
                             const int gpa = gb + lane, gpb = gpa + 32;
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_le)];
