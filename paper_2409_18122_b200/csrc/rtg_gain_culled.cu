@@ -89,14 +89,13 @@ __device__ __forceinline__ unsigned bit_or_zero(unsigned n) {
     return r;
 }
 
-// acc += u_q and pc += class increment of record word uc when p (64-bit exact integer sum)
-__device__ __forceinline__ void add_if(bool p, unsigned long long& acc, unsigned uc, int& pc) {
-    unsigned lo = (unsigned)acc, hi = (unsigned)(acc >> 32);
-    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.cc.u32 %0, %0, %3;\n\t@pp addc.u32 %1, %1, 0;\n\t}"
-        : "+r"(lo), "+r"(hi)
-        : "r"(0), "r"(uc & kUqMask), "r"((int)p));
-    acc = ((unsigned long long)hi << 32) | lo;
-    if (p) pc += uc_inc(uc);
+// w += uc and pc += class byte of record word uc when p: over at most kFlushPasses passes (2 items
+// each) w - (pc << 24) = sum(u_q) < 2^32 and pc = nH + 128 nL with nH <= 126 (both exact)
+constexpr int kFlushPasses = 63;
+__device__ __forceinline__ void add_if(bool p, unsigned& w, unsigned uc, unsigned& pc) {
+    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.u32 %0, %0, %2;\n\t@pp add.u32 %1, %1, %3;\n\t}"
+        : "+r"(w), "+r"(pc)
+        : "r"(uc), "r"(uc >> kUqBits), "r"((int)p));
 }
 
 template <bool kStats>
@@ -130,7 +129,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
         const int i = list[e];
         const float px = X[i], py = Y[i], pz = Zw[i], yw = Yaw[i];
         unsigned long long acc = 0;  // sum of u_q over visible Gaussians (exact integer)
-        int acch = 0, accl = 0, pc = 0;
+        int acch = 0, accl = 0;
         if (isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(yw)) {
             WpF f;
             {
@@ -360,8 +359,9 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         __syncwarp();
                     }
                     int r0 = 0;   // run holding item gb
-                    for (int gb0 = 0; gb0 < tot; gb0 += 64 * 16384) {   // class counts: flushed every 16384 passes
-                        const int gend = min(tot, gb0 + 64 * 16384);
+                    for (int gb0 = 0; gb0 < tot; gb0 += 64 * kFlushPasses) {   // 32-bit sums: flushed
+                        const int gend = min(tot, gb0 + 64 * kFlushPasses);
+                        unsigned w = 0, pc = 0;
                         for (int gb = gb0; gb < gend; gb += 64) {
                             // runs r0+1 .. r0+64 start at positions pa, pb (relative to gb) >= 1
                             const int ra = r0 + 1 + lane;
@@ -394,14 +394,14 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             }
                             visa = visa && gpa < tot;
                             visb = visb && gpb < tot;
-                            add_if(visa, acc, Ga.uc, pc);
-                            add_if(visb, acc, Gb.uc, pc);
+                            add_if(visa, w, Ga.uc, pc);
+                            add_if(visb, w, Gb.uc, pc);
                             if (kStats) nvis += (unsigned)visa + (unsigned)visb;
                             r0 += na + __popc(hhi) + (__any_sync(kFullG, pa == 64 || pb == 64) ? 1 : 0);
                         }
-                        acch += pc & 0xffff;
-                        accl += pc >> 16;
-                        pc = 0;
+                        acc += w - (pc << kUqBits);
+                        acch += pc & (kClsL - 1);
+                        accl += pc / kClsL;
                     }
                     if (kStats) ntest += (unsigned long long)tot;
                     nq = 0;

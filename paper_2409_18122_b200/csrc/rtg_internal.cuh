@@ -24,14 +24,17 @@ constexpr int kTile = 512;           // dense-mode Gaussians per smem tile
 constexpr int kZoccX = 64;           // x-cells per block of the visibility grid's z-occupancy table
 
 // ------------------------------------------------------------------ records
-// visibility record (sorted by visibility cell): mean + uc = u_q | class << 30 with u_q the
-// fixed-point u (< 2^30, exact integer) and class 1 (H), 2 (L), 0 (O)
+// visibility record (sorted by visibility cell): mean + uc = u_q | c << 24 with u_q the
+// fixed-point u (< 2^24, exact integer) and the class byte c = kClsH (H), kClsL (L), 0 (O): a
+// per-lane 32-bit sum of up to 127 words still separates sum(u_q) and nH + 128 nL (culled kernel)
 struct __align__(16) GRec { float x, y, z; unsigned uc; };
-constexpr unsigned kUqMask = 0x3fffffffu;
+constexpr int kUqBits = 24;
+constexpr unsigned kUqMask = (1u << kUqBits) - 1u;
+constexpr unsigned kClsH = 1u, kClsL = 0x80u;
 // per-lane packed class counter increment of uc: 1 (H), 0x10000 (L), 0 (O)
 __device__ __forceinline__ int uc_inc(unsigned uc) {
-    const int c = (int)(uc >> 30);
-    return c + (c >> 1) * 0xfffe;
+    const unsigned c = uc >> kUqBits;
+    return (int)((c & kClsH) | ((c & kClsL) << 9));
 }
 // collision record (sorted by collision cell): mean + inflated bounding radius^2
 struct __align__(16) CRec { float x, y, z, rb2; };

@@ -211,12 +211,12 @@ __device__ __forceinline__ double u_of(float w, int variant) {
     return variant == RTG_VARIANT_SQ ? u * u : u;
 }
 
-// packed record word uc = u_q | class << 30 of a Gaussian with weight w (a2): class 1 (H,
-// u > tau_hi), 2 (L, u < tau_lo), 0 (O); u_q = round(u 2^S) < 2^30
+// packed record word uc = u_q | c << 24 of a Gaussian with weight w (a2): class byte c =
+// kClsH (u > tau_hi), kClsL (u < tau_lo), 0 (O); u_q = round(u 2^S) < 2^24
 __device__ __forceinline__ unsigned class_of(float w, int variant, const ClassState* __restrict__ cs) {
     const double u = u_of(w, variant);
-    const unsigned c = u > cs->tau_hi ? 1u : (u < cs->tau_lo ? 2u : 0u);
-    return (unsigned)llrint(u * cs->scale) | (c << 30);
+    const unsigned c = u > cs->tau_hi ? kClsH : (u < cs->tau_lo ? kClsL : 0u);
+    return (unsigned)llrint(u * cs->scale) | (c << kUqBits);
 }
 
 // both visibility copies: A at cursorA (relative to 0), B at offB + cursorB, with their packed
@@ -405,8 +405,8 @@ __global__ void k_red2_final(const double* __restrict__ part, int nparts, ClassS
         int shift = 0;
         double tot = cnt * umax;
         if (tot > 0.0) {
-            // sum of all u_q < 2^53 (exact in FP64) and every u_q < 2^30 (packed with the class)
-            shift = (int)floor(fmin(52.0 - log2(tot), 29.0 - log2(umax)));
+            // sum of all u_q < 2^53 (exact in FP64) and every u_q < 2^24 (packed with the class)
+            shift = (int)floor(fmin(52.0 - log2(tot), (double)(kUqBits - 1) - log2(umax)));
             shift = shift > 1000 ? 1000 : (shift < -1000 ? -1000 : shift);
         }
         cs->shift = shift;

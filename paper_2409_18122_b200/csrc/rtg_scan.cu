@@ -77,8 +77,8 @@ struct LoadUc {
     const GRec* __restrict__ p;
     __device__ I64x2 operator()(long long j) const {
         const unsigned uc = p[j].uc;
-        const unsigned c = uc >> 30;
-        return I64x2((long long)(uc & kUqMask), c == 1u ? 1LL : (c == 2u ? (1LL << 32) : 0LL));
+        const unsigned c = uc >> kUqBits;
+        return I64x2((long long)(uc & kUqMask), c == kClsH ? 1LL : (c == kClsL ? (1LL << 32) : 0LL));
     }
 };
 
