@@ -93,9 +93,10 @@ __device__ __forceinline__ unsigned bit_or_zero(unsigned n) {
 // each) w - (pc << 24) = sum(u_q) < 2^32 and pc = nH + 128 nL with nH <= 126 (both exact)
 constexpr int kFlushPasses = 63;
 __device__ __forceinline__ void add_if(bool p, unsigned& w, unsigned uc, unsigned& pc) {
-    asm("{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t@pp add.u32 %0, %0, %2;\n\t@pp add.u32 %1, %1, %3;\n\t}"
-        : "+r"(w), "+r"(pc)
-        : "r"(uc), "r"(uc >> kUqBits), "r"((int)p));
+    if (p) {
+        w += uc;
+        pc += __byte_perm(uc, 0u, 0x4443);   // the class byte (top byte of uc)
+    }
 }
 
 template <bool kStats>
@@ -115,7 +116,6 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     __shared__ __align__(16) int s_ex[kWarpsG][kQCap + 64];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lanes_lt = (1u << lane) - 1u;
-    const unsigned lanes_le = (2u << lane) - 1u;
     int* const qs = s_st[wid];
     int* const qe = s_ex[wid];
     const int L = *list_count;
@@ -363,16 +363,17 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         const int gend = min(tot, gb0 + 64 * kFlushPasses);
                         unsigned w = 0, pc = 0;
                         for (int gb = gb0; gb < gend; gb += 64) {
-                            // runs r0+1 .. r0+64 start at positions pa, pb (relative to gb) >= 1
+                            // runs r0+1 .. r0+64 start at positions 1 + pa, 1 + pb (relative to gb), pa >= 0:
+                            // head bit k of (hhi:hlo) <=> a run starts at item k + 1 of the window
                             const int ra = r0 + 1 + lane;
-                            const int pa = qe[ra] - gb, pb = qe[ra + 32] - gb;
+                            const int pa = qe[ra] - gb - 1, pb = qe[ra + 32] - gb - 1;
                             const unsigned hlo = __reduce_or_sync(kFullG, bit_or_zero((unsigned)pa));
                             const unsigned hhi = __reduce_or_sync(
                                 kFullG, bit_or_zero((unsigned)(pa - 32)) | bit_or_zero((unsigned)(pb - 32)));
                             const int na = __popc(hlo);
                             const int gpa = gb + lane, gpb = gpa + 32;
-                            const int gia = gpa + qs[r0 + __popc(hlo & lanes_le)];
-                            const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_le)];
+                            const int gia = gpa + qs[r0 + __popc(hlo & lanes_lt)];
+                            const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_lt)];
                             RTG_CHECK(gia >= 0 && gia < g.nrec && gib >= 0 && gib < g.nrec, "record index");
                             const GRec Ga = grec[gia], Gb = grec[gib];
                             float ma, mb, guard_a, guard_b;
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             add_if(visa, w, Ga.uc, pc);
                             add_if(visb, w, Gb.uc, pc);
                             if (kStats) nvis += (unsigned)visa + (unsigned)visb;
-                            r0 += na + __popc(hhi) + (__any_sync(kFullG, pa == 64 || pb == 64) ? 1 : 0);
+                            r0 += na + __popc(hhi);
                         }
                         acc += w - (pc << kUqBits);
                         acch += pc & (kClsL - 1);
