@@ -375,9 +375,10 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_lt)];
                             const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_lt)];
                             RTG_CHECK(gia >= 0 && gia < g.nrec && gib >= 0 && gib < g.nrec, "record index");
-                            const GRec Ga = grec[gia], Gb = grec[gib];
-                            float ma, mb, guard_a, guard_b;
-                            vis_margin2(f, cam, Ga.x, Ga.y, Ga.z, Gb.x, Gb.y, Gb.z, ma, mb, guard_a, guard_b);
+                            const GRec Ga = grec[(unsigned)gia], Gb = grec[(unsigned)gib];
+                            float guard_a, guard_b;
+                            const float ma = vis_margin_xy(f, cam, Ga.x, Ga.y, Ga.z, guard_a);
+                            const float mb = vis_margin_xy(f, cam, Gb.x, Gb.y, Gb.z, guard_b);
                             bool visa = ma >= 0.0f, visb = mb >= 0.0f;
                             const bool amba = fabsf(ma) < guard_a;
                             const bool ambb = fabsf(mb) < guard_b;

@@ -134,9 +134,8 @@ __device__ __forceinline__ float vis_margin(const WpF& w, const CamK& k, float m
     return fminf(s1, fminf(s2, s3));
 }
 
-// two items at once with Blackwell's packed FP32 (f32x2: FADD2 / FMUL2 / FFMA2 on register pairs,
-// scalar operands broadcast): each half rounds exactly like vis_margin, so the margins are
-// bit-identical; the |.| terms stay scalar (no packed abs).  Also returns the FP32 guard.
+// Blackwell's packed FP32 (f32x2: FADD2 / FMUL2 / FFMA2 on register pairs, scalar operands
+// broadcast): each half rounds exactly like the scalar instruction.
 __device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
     unsigned long long r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -165,24 +164,17 @@ __device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsig
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
-__device__ __forceinline__ void vis_margin2(const WpF& w, const CamK& k, float ax_, float ay_, float az_, float bx_,
-                                            float by_, float bz_, float& ma, float& mb, float& ga, float& gb) {
-    const unsigned long long dx = f2_sub(f2_pack(ax_, bx_), f2_pack(w.px, w.px));
-    const unsigned long long dy = f2_sub(f2_pack(ay_, by_), f2_pack(w.py, w.py));
-    const unsigned long long dz = f2_sub(f2_pack(az_, bz_), f2_pack(w.pz, w.pz));
-    const unsigned long long Z = f2_fma(f2_pack(w.c, w.c), dx, f2_mul(f2_pack(w.s, w.s), dy));
-    const unsigned long long X = f2_fma(f2_pack(w.ax, w.ax), dx, f2_mul(f2_pack(w.bx, w.bx), dy));
-    const unsigned long long Y = f2_fma(f2_pack(-k.kyc, -k.kyc), Z, dz);
-    const unsigned long long D = f2_sub(Z, f2_pack(k.zmid, k.zmid));
-    const unsigned long long G = f2_fma(f2_pack(k.gam, k.gam), Z, f2_pack(k.g0, k.g0));
-    float Za, Zb, Xa, Xb, Ya, Yb, Da, Db;
-    f2_unpack(Z, Za, Zb);
-    f2_unpack(X, Xa, Xb);
-    f2_unpack(Y, Ya, Yb);
-    f2_unpack(D, Da, Db);
-    f2_unpack(G, ga, gb);
-    ma = fminf(k.zhalf - fabsf(Da), fminf(fmaf(k.kxh, Za, -fabsf(Xa)), fmaf(k.kyh, Za, -fabsf(Ya))));
-    mb = fminf(k.zhalf - fabsf(Db), fminf(fmaf(k.kxh, Zb, -fabsf(Xb)), fmaf(k.kyh, Zb, -fabsf(Yb))));
+// one item with the packed pairs (x, y) and (Z, X') of the same Gaussian, so the record's own
+// register pair feeds the first FADD2 (no re-pairing moves); rounds exactly like vis_margin
+// Also returns the FP32 guard gam Z + g0.
+__device__ __forceinline__ float vis_margin_xy(const WpF& w, const CamK& k, float mx, float my, float mz,
+                                               float& guard) {
+    float dx, dy, Z, X;
+    f2_unpack(f2_sub(f2_pack(mx, my), f2_pack(w.px, w.py)), dx, dy);
+    f2_unpack(f2_fma(f2_pack(w.c, w.ax), f2_pack(dx, dx), f2_mul(f2_pack(w.s, w.bx), f2_pack(dy, dy))), Z, X);
+    const float Y = fmaf(-k.kyc, Z, mz - w.pz);
+    guard = fmaf(k.gam, Z, k.g0);
+    return fminf(k.zhalf - fabsf(Z - k.zmid), fminf(fmaf(k.kxh, Z, -fabsf(X)), fmaf(k.kyh, Z, -fabsf(Y))));
 }
 
 // FP64 decision with the six slacks of the pinhole test (visible <=> all >= 0), cos/sin of the
