@@ -739,22 +739,7 @@ rtg_status rtg_plan_tree(rtg_map m, const float start[3], const float goal[2], c
     if ((long long)p->n_traj * (p->max_depth + 1) >= (1LL << 31)) return invalid("n_traj * (max_depth + 1) too large");
     API_CK(cudaSetDevice(m->device), nullptr);
     cudaStream_t st = (cudaStream_t)stream;
-    std::vector<float> wx, wy, wyaw;
-    std::vector<double> c;
-    s = plan_tree(m, start, goal, *p, st, &wx, &wy, &wyaw, &c, reached, stats);
-    if (s != RTG_OK) return s;
-    const int K = (int)c.size();
-    *n_found = K;
-    if (cost)
-        for (int i = 0; i < K; ++i) cost[i] = c[i];
-    if (K == 0) {
-        set_error("rtg_plan_tree: no collision-free primitive grows from the start");
-        return RTG_ERR_NO_FEASIBLE;
-    }
-    const int T = p->max_depth + 1;
-    std::vector<float> wz(wx.size());
-    for (size_t i = 0; i < wx.size(); ++i) wz[i] = std::isnan(wx[i]) ? wx[i] : p->z;
-    return rtg_traj_upload(m->device, K, T, RTG_MEM_HOST, wx.data(), wy.data(), wz.data(), wyaw.data(), stream, out);
+    return plan_tree(m, start, goal, *p, st, out, cost, n_found, reached, stats);
 }
 
 rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_score_params* p,

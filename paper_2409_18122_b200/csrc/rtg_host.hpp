@@ -67,10 +67,10 @@ cudaError_t launch_region_utility(rtg_map_s* m, const double origin[3], double s
                                   int* count, cudaStream_t st);
 cudaError_t launch_view_ring(int R, const float* cen, double d, int n, float z, rtg_traj_s* tr, cudaStream_t st);
 cudaError_t launch_cost_benefit(const double* omega, const double* d, int K, void* out_dev, cudaStream_t st);
-// motion-primitive tree (rtg_tree.cu): candidate waypoints [K][max_depth + 1] (NaN padded) on the host
+// motion-primitive tree (rtg_tree.cu), on the device; *out: candidate waypoints [K][max_depth + 1], NaN padded
 rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], const rtg_tree_params& p,
-                     cudaStream_t st, std::vector<float>* wx, std::vector<float>* wy, std::vector<float>* wyaw,
-                     std::vector<double>* cost, int* reached, long long stats_out[4]);
+                     cudaStream_t st, rtg_traj_s** out, double* cost, int* n_found, int* reached,
+                     long long stats[4]);
 
 }  // namespace rtg
 

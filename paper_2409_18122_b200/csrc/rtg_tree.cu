@@ -6,22 +6,32 @@
 // layer are checked against the Gaussian map in one launch ("testing collisions of all sampled
 // points with all Gaussians from the map at once while growing the search tree") -- one warp
 // per primitive, the exact culled collision test of a4 per sample, stopping at the first collision.
-// Between layers the host (C++) keeps the search bookkeeping: cost g = sum (lambda_t + v^2 + w^2) dt
-// (Eq. low_level_planner with piecewise-constant u), the minimum-time heuristic
-// h = ||p_goal - p|| / v_max, a closed (x, y, heading) lattice keeping the lowest g, a
-// beam of the lowest f = g + h nodes, and the goal region ||p - p_goal|| <= goal_radius.  Goal-
-// reaching nodes are candidates (not expanded further); the N_traj cheapest are returned,
-// or, when none reaches the goal, the N_traj leaves closest to it.  All tie-breaks
-// use creation order, so the result is deterministic.
+// The search bookkeeping stays on the device too, so a whole plan is one stream of launches and one
+// host synchronisation at the end:
+//   - cost g = sum (lambda_t + v^2 + w^2) dt (Eq. low_level_planner with piecewise-constant u);
+//   - a closed (x, y, heading) lattice keeping the lowest g (a device hash table).  Within a layer
+//     the children are visited in creation order (node, then control): a child is kept iff its g is
+//     below the lattice cell's value before the layer AND below every earlier child of the layer in
+//     the same cell -- the children of a layer are grouped per cell through a per-layer hash table,
+//     so this "strict prefix minimum" is exact whatever the thread order;
+//   - goal region ||p - p_goal|| <= goal_radius: such nodes are candidates (not expanded);
+//   - beam: the `beam` children of lowest f = g + h, h = ||p_goal - p|| / v_max, ties to
+//     creation order -- an exact radix select in one CTA, then an ordered compaction;
+//   - result: the n_traj cheapest candidates, or, when none reached the goal, the n_traj
+//     nodes closest to it, ranked by (key, creation order), parents traced on device.
+// Every double operation that decides a comparison is an explicit round-to-nearest intrinsic (no
+// FMA contraction), so the decisions equal the FP64 oracle's (oracle/planning.py).
 #include <algorithm>
 #include <cmath>
-#include <unordered_map>
 #include <vector>
 
 #include "rtg_host.hpp"
 
 namespace rtg {
 namespace {
+
+constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr int kSelThreads = 1024;
 
 // unicycle closed form from (x0, y0, th0) under (v, w) for time t, FP64 without
 // contraction so the host oracle's rounding is reproduced
@@ -45,25 +55,129 @@ __device__ __forceinline__ double wrap_pi(double a) {   // (-pi, pi]
     return r;
 }
 
-struct ExpandK {
-    int M, P, S;        // frontier nodes, controls, samples per primitive (incl. both endpoints)
-    double dt;
+// search constants (host-computed once per plan)
+struct TreeK {
+    int P, S, beam, W;              // controls, samples per primitive, beam, beam * P
+    double dt, gx, gy, r2, vmax;    // goal region and heuristic
     float z;
+    int dedup;                      // lattice on
+    double lxy, ldeg, rad2deg;      // lattice cell; 180 / pi
+    long long amin, bmin, cmin;     // lattice index offsets
+    int ba, bb;                     // bits of the packed b and c fields (a takes the rest)
+    unsigned long long cmask;       // capacity - 1 of the closed table
+    unsigned long long lmask;       // capacity - 1 of the per-layer table
 };
 
-// one warp per (node m, control p): samples j = 1 .. S-1 at t_j = j dt / (S-1) (j = 0 is the
-// parent's state, checked when it was created); ok = no sample collides; child = state at dt
-__global__ void __launch_bounds__(256) k_expand(ExpandK k, const double* __restrict__ fr, const double* __restrict__ ctl,
+// device state of one plan
+struct Tree {
+    double *nx, *ny, *nth, *ng;     // nodes (creation order), capacity NC
+    int *npar, *ndep;
+    int* frontier;                  // node ids, creation order, <= beam
+    double *cx, *cy, *cth, *cg;     // children of the layer, index w = m * P + p
+    unsigned char* cok;             // primitive collision-free
+    unsigned long long* ckey;       // packed lattice key
+    int *cslot, *cpos;              // per-layer cell slot and position in the slot's bucket
+    int *acc, *rank, *cid;          // kept flag, its exclusive scan, node id
+    unsigned long long* fkey;       // f bits of frontier-eligible children (else kEmptyKey)
+    unsigned long long* tkey;       // closed lattice: key -> lowest g
+    double* tval;
+    unsigned long long* lkey;       // per-layer cells
+    int *lcnt, *loff, *lbucket;
+    int* cand;                      // candidate node ids (any order)
+    int* cnt;                       // 0 M, 1 nodes, 2 candidates, 3 expanded, 4 error, 5 found, 6 reached
+    int *sel, *order;               // final selection: node ids (any order), then ranked
+    unsigned long long *sa, *sb;    // their keys
+};
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long k) {   // splitmix64 finaliser
+    k ^= k >> 30;
+    k *= 0xbf58476d1ce4e5b9ull;
+    k ^= k >> 27;
+    k *= 0x94d049bb133111ebull;
+    k ^= k >> 31;
+    return k;
+}
+
+// lattice cell of a state (SPEC S:384 closed set): floor(x / lxy), floor(y / lxy),
+// floor(th * 180/pi / ldeg), packed with host-derived offsets; error flag if out of range
+__device__ __forceinline__ unsigned long long lattice_key(const TreeK& k, double x, double y, double th, int* err) {
+    const long long a = (long long)floor(__ddiv_rn(x, k.lxy)) - k.amin;
+    const long long b = (long long)floor(__ddiv_rn(y, k.lxy)) - k.bmin;
+    const long long c = (long long)floor(__ddiv_rn(__dmul_rn(th, k.rad2deg), k.ldeg)) - k.cmin;
+    if (a < 0 || b < 0 || c < 0 || b >= (1LL << k.ba) || c >= (1LL << k.bb) || a >= (1LL << (62 - k.ba - k.bb))) {
+        atomicExch(err, 1);
+        return 0;
+    }
+    return ((unsigned long long)a << (k.ba + k.bb)) | ((unsigned long long)b << k.bb) | (unsigned long long)c;
+}
+
+__device__ __forceinline__ double closed_get(const Tree& t, const TreeK& k, unsigned long long key) {
+    for (unsigned long long s = mix64(key) & k.cmask;; s = (s + 1) & k.cmask) {
+        const unsigned long long v = t.tkey[s];
+        if (v == key) return t.tval[s];
+        if (v == kEmptyKey) return INFINITY;
+    }
+}
+
+__device__ __forceinline__ void closed_put(const Tree& t, const TreeK& k, unsigned long long key, double g) {
+    for (unsigned long long s = mix64(key) & k.cmask;; s = (s + 1) & k.cmask) {
+        const unsigned long long prev = atomicCAS(&t.tkey[s], kEmptyKey, key);
+        if (prev == kEmptyKey || prev == key) {
+            t.tval[s] = g;
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ double h_of(const TreeK& k, double x, double y) {
+    const double dx = __dsub_rn(k.gx, x), dy = __dsub_rn(k.gy, y);
+    return __ddiv_rn(sqrt(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))), k.vmax);
+}
+
+__device__ __forceinline__ bool at_goal(const TreeK& k, double x, double y) {
+    const double dx = __dsub_rn(x, k.gx), dy = __dsub_rn(y, k.gy);
+    return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= k.r2;
+}
+
+__device__ __forceinline__ unsigned long long dbits(double v) {   // order-preserving for v >= 0
+    return (unsigned long long)__double_as_longlong(v);
+}
+
+// ---- root: node 0, its lattice cell, the first frontier (or the root is already a candidate)
+__global__ void k_tree_init(Tree t, TreeK k, double x, double y, double th) {
+    t.nx[0] = x; t.ny[0] = y; t.nth[0] = th; t.ng[0] = 0.0;
+    t.npar[0] = -1; t.ndep[0] = 0;
+    t.cnt[1] = 1;
+    if (k.dedup) closed_put(t, k, lattice_key(k, x, y, th, t.cnt + 4), 0.0);
+    if (at_goal(k, x, y)) {
+        t.cand[0] = 0;
+        t.cnt[2] = 1;
+        t.cnt[0] = 0;
+    } else {
+        t.frontier[0] = 0;
+        t.cnt[0] = 1;
+    }
+}
+
+// ---- expansion: one warp per (frontier node m, control p), all W = beam * P warps launched, those
+// past M * P only clear their child.  Samples j = 1 .. S-1 at t_j = j dt / (S-1) (j = 0 is the
+// parent's state, checked when it was created); ok = no sample collides; child = state at dt.
+__global__ void __launch_bounds__(256) k_expand(Tree t, TreeK k, const double* __restrict__ ctl,
                                                 const CRec* __restrict__ crec, const CMat* __restrict__ cmat,
                                                 const CSrc* __restrict__ csrc, const rtg_robot rb,
                                                 const int* __restrict__ cstart, ColGridK g, float gq, int n_col,
-                                                unsigned char* __restrict__ ok, double* __restrict__ child,
                                                 unsigned long long* __restrict__ stats) {
     const int lane = threadIdx.x & 31;
     const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    if (w >= (long long)k.M * k.P) return;
+    if (w >= k.W) return;
+    const int M = t.cnt[0];
+    if (w >= (long long)M * k.P) {
+        if (lane == 0) t.cok[w] = 0;
+        return;
+    }
     const int m = (int)(w / k.P), p = (int)(w - (long long)m * k.P);
-    const double x0 = fr[4 * m], y0 = fr[4 * m + 1], th0 = fr[4 * m + 2];
+    const int par = t.frontier[m];
+    const double x0 = t.nx[par], y0 = t.ny[par], th0 = t.nth[par];
     const double v = ctl[2 * p], om = ctl[2 * p + 1];
     unsigned nref = 0;
     unsigned long long ntest = 0;
@@ -71,8 +185,8 @@ __global__ void __launch_bounds__(256) k_expand(ExpandK k, const double* __restr
     int checked = 0;
     double x = x0, y = y0, th = th0;
     for (int j = 1; j < k.S; ++j) {
-        const double t = __ddiv_rn(__dmul_rn((double)j, k.dt), (double)(k.S - 1));
-        unicycle_at(x0, y0, th0, v, om, t, x, y, th);
+        const double tt = __ddiv_rn(__dmul_rn((double)j, k.dt), (double)(k.S - 1));
+        unicycle_at(x0, y0, th0, v, om, tt, x, y, th);
         if (!hit && n_col > 0) {
             hit = warp_point_collides(__double2float_rn(x), __double2float_rn(y), k.z, crec, cmat, csrc, rb, cstart,
                                       g, gq, nref, ntest);
@@ -80,10 +194,11 @@ __global__ void __launch_bounds__(256) k_expand(ExpandK k, const double* __restr
         }
     }
     if (lane == 0) {
-        ok[w] = hit ? 0 : 1;
-        child[3 * w] = x;
-        child[3 * w + 1] = y;
-        child[3 * w + 2] = wrap_pi(th);
+        t.cok[w] = hit ? 0 : 1;
+        t.cx[w] = x;
+        t.cy[w] = y;
+        t.cth[w] = wrap_pi(th);
+        t.cg[w] = __dadd_rn(t.ng[par], ctl[2 * k.P + p]);   // + the control's cost (after the controls)
         if (stats) {
             atomicAdd(&stats[0], (unsigned long long)checked);
             atomicAdd(&stats[1], ntest);
@@ -92,28 +207,310 @@ __global__ void __launch_bounds__(256) k_expand(ExpandK k, const double* __restr
     }
 }
 
-struct Node {
-    double x, y, th, g;
-    int parent, depth;
+// ---- lattice: each collision-free child joins its cell's bucket of this layer
+__global__ void k_cells(Tree t, TreeK k) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= k.W || !t.cok[w]) return;
+    const unsigned long long key = lattice_key(k, t.cx[w], t.cy[w], t.cth[w], t.cnt + 4);
+    t.ckey[w] = key;
+    for (unsigned long long s = mix64(key) & k.lmask;; s = (s + 1) & k.lmask) {
+        const unsigned long long prev = atomicCAS(&t.lkey[s], kEmptyKey, key);
+        if (prev == kEmptyKey || prev == key) {
+            t.cslot[w] = (int)s;
+            t.cpos[w] = atomicAdd(&t.lcnt[s], 1);
+            return;
+        }
+    }
+}
+
+__global__ void k_bucket(Tree t, TreeK k) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= k.W || !t.cok[w]) return;
+    t.lbucket[t.loff[t.cslot[w]] + t.cpos[w]] = w;
+}
+
+// kept iff g < min(closed value before the layer, g of every earlier child of the layer in the cell)
+__global__ void k_keep(Tree t, TreeK k) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= k.W) return;
+    int keep = t.cok[w];
+    if (keep && k.dedup) {
+        double lim = closed_get(t, k, t.ckey[w]);
+        const int s = t.cslot[w], b0 = t.loff[s], n = t.lcnt[s];
+        for (int i = 0; i < n; ++i) {
+            const int o = t.lbucket[b0 + i];
+            if (o < w) lim = fmin(lim, t.cg[o]);
+        }
+        keep = t.cg[w] < lim;
+    }
+    t.acc[w] = keep;
+}
+
+// the cell's last kept child (largest w; kept children have strictly decreasing g) writes its g
+__global__ void k_close(Tree t, TreeK k) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= k.W || !t.acc[w]) return;
+    const int s = t.cslot[w], b0 = t.loff[s], n = t.lcnt[s];
+    for (int i = 0; i < n; ++i) {
+        const int o = t.lbucket[b0 + i];
+        if (o > w && t.acc[o]) return;
+    }
+    closed_put(t, k, t.ckey[w], t.cg[w]);
+}
+
+// kept children become nodes (ids in creation order); goal nodes are candidates, the others are
+// eligible for the next frontier with key f = g + h
+__global__ void k_create(Tree t, TreeK k, int depth) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= k.W) return;
+    unsigned long long fk = kEmptyKey;
+    if (t.acc[w]) {
+        const int id = t.cnt[1] + t.rank[w];
+        const double x = t.cx[w], y = t.cy[w], g = t.cg[w];
+        t.nx[id] = x; t.ny[id] = y; t.nth[id] = t.cth[w]; t.ng[id] = g;
+        t.npar[id] = t.frontier[w / k.P];
+        t.ndep[id] = depth;
+        t.cid[w] = id;
+        if (at_goal(k, x, y)) t.cand[atomicAdd(&t.cnt[2], 1)] = id;
+        else fk = dbits(__dadd_rn(g, h_of(k, x, y)));
+    }
+    t.fkey[w] = fk;
+}
+
+// ---- exact selection of the `need` smallest keys (a, b, id) among n items in one CTA: radix
+// select, 8 bits per pass from the most significant digit of a, then b, then id (ids are unique, so
+// it always ends exact).  Returns the decided prefix (pa, pb, pi under masks ma, mb, mi); an item is
+// selected iff its masked key is below the prefix, or equal to it.
+struct SelState {
+    unsigned long long pa, pb, ma, mb;
+    unsigned pi, mi;
 };
 
-struct LatticeKey {
-    long long a, b, c;
-    bool operator==(const LatticeKey& o) const { return a == o.a && b == o.b && c == o.c; }
-};
-struct LatticeHash {
-    size_t operator()(const LatticeKey& k) const {
-        return (size_t)(k.a * 73856093LL) ^ (size_t)(k.b * 19349663LL) ^ (size_t)(k.c * 83492791LL);
+template <typename Src>
+__device__ SelState block_select(const Src& src, int n, int need, bool use_b) {
+    __shared__ int hist[256];
+    __shared__ int s_need, s_done;
+    __shared__ SelState s_st;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_st = SelState{0, 0, 0, 0, 0, 0};
+        s_need = need;
+        s_done = 0;
+    }
+    __syncthreads();
+    const int nb = use_b ? 8 : 0, ndig = 8 + nb + 4;
+    for (int d = 0; d < ndig; ++d) {
+        for (int j = tid; j < 256; j += blockDim.x) hist[j] = 0;
+        __syncthreads();
+        const SelState st = s_st;
+        const int which = d < 8 ? 0 : (d < 8 + nb ? 1 : 2);
+        const int sh = which == 0 ? 56 - 8 * d : (which == 1 ? 56 - 8 * (d - 8) : 24 - 8 * (d - 8 - nb));
+        for (int i = tid; i < n; i += blockDim.x) {
+            unsigned long long a, b;
+            unsigned id;
+            if (!src.get(i, a, b, id)) continue;
+            if ((a & st.ma) != st.pa || (b & st.mb) != st.pb || (id & st.mi) != st.pi) continue;
+            const unsigned dg = which == 0 ? (unsigned)(a >> sh) & 255u
+                                           : (which == 1 ? (unsigned)(b >> sh) & 255u : (id >> sh) & 255u);
+            atomicAdd(&hist[dg], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int cum = 0, t = 0;
+            for (; t < 255; ++t) {
+                if (cum + hist[t] >= s_need) break;
+                cum += hist[t];
+            }
+            s_need -= cum;
+            if (hist[t] == s_need) s_done = 1;
+            SelState ns = s_st;
+            if (which == 0) {
+                ns.pa |= (unsigned long long)t << sh;
+                ns.ma |= 255ull << sh;
+            } else if (which == 1) {
+                ns.pb |= (unsigned long long)t << sh;
+                ns.mb |= 255ull << sh;
+            } else {
+                ns.pi |= (unsigned)t << sh;
+                ns.mi |= 255u << sh;
+            }
+            s_st = ns;
+        }
+        __syncthreads();
+        if (s_done) break;
+    }
+    return s_st;
+}
+
+__device__ __forceinline__ bool selected(const SelState& s, unsigned long long a, unsigned long long b, unsigned id) {
+    const unsigned long long xa = a & s.ma, xb = b & s.mb;
+    if (xa != s.pa) return xa < s.pa;
+    if (xb != s.pb) return xb < s.pb;
+    return (id & s.mi) <= s.pi;
+}
+
+struct SrcBeam {   // children eligible for the frontier: (f, -, w)
+    const unsigned long long* fkey;
+    __device__ bool get(int i, unsigned long long& a, unsigned long long& b, unsigned& id) const {
+        a = fkey[i];
+        b = 0;
+        id = (unsigned)i;
+        return a != kEmptyKey;
     }
 };
+
+// ---- next frontier (one CTA): layer totals, beam select, ordered compaction in creation order
+__global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
+    __shared__ int s_warp[kSelThreads / 32];
+    __shared__ int s_base, s_tile, s_elig;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        t.cnt[3] += t.cnt[0];
+        t.cnt[1] += t.rank[k.W - 1] + t.acc[k.W - 1];   // nodes created by this layer
+        s_base = 0;
+        s_elig = 0;
+    }
+    __syncthreads();
+    int loc = 0;
+    for (int i = tid; i < k.W; i += blockDim.x) loc += t.fkey[i] != kEmptyKey;
+    atomicAdd(&s_elig, loc);
+    __syncthreads();
+    const bool all = s_elig <= k.beam;
+    SelState st{0, 0, 0, 0, 0, 0};
+    if (!all) st = block_select(SrcBeam{t.fkey}, k.W, k.beam, false);
+    for (int c0 = 0; c0 < k.W; c0 += blockDim.x) {
+        const int i = c0 + tid;
+        bool s = false;
+        if (i < k.W) {
+            const unsigned long long f = t.fkey[i];
+            s = f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i));
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, s);
+        if (lane == 0) s_warp[wid] = __popc(bal);
+        __syncthreads();
+        if (tid < 32) {
+            const int v = s_warp[tid];
+            int inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (tid >= o) inc += u;
+            }
+            s_warp[tid] = inc - v;
+            if (tid == 31) s_tile = inc;
+        }
+        __syncthreads();
+        if (s) t.frontier[s_base + s_warp[wid] + __popc(bal & ((1u << lane) - 1u))] = t.cid[i];
+        __syncthreads();
+        if (tid == 0) s_base += s_tile;
+        __syncthreads();
+    }
+    if (tid == 0) t.cnt[0] = s_base;
+}
+
+// ---- final selection (one CTA): the n_traj cheapest candidates by (g, id), or, with no candidate,
+// the n_traj nodes (root excluded) closest to the goal by (h, g, id)
+struct SrcCand {
+    const int* cand;
+    const double* ng;
+    __device__ bool get(int i, unsigned long long& a, unsigned long long& b, unsigned& id) const {
+        const int c = cand[i];
+        a = dbits(ng[c]);
+        b = 0;
+        id = (unsigned)c;
+        return true;
+    }
+};
+struct SrcNodes {
+    const double *nx, *ny, *ng;
+    TreeK k;
+    __device__ bool get(int i, unsigned long long& a, unsigned long long& b, unsigned& id) const {
+        a = dbits(h_of(k, nx[i + 1], ny[i + 1]));
+        b = dbits(ng[i + 1]);
+        id = (unsigned)(i + 1);
+        return true;
+    }
+};
+
+template <typename Src>
+__device__ void select_into(const Tree& t, const Src& src, int n, int need, bool use_b) {
+    __shared__ int s_n;
+    const bool all = n <= need;
+    SelState st{0, 0, 0, 0, 0, 0};
+    if (!all) st = block_select(src, n, need, use_b);
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        unsigned long long a, b;
+        unsigned id;
+        src.get(i, a, b, id);
+        if (all || selected(st, a, b, id)) {
+            const int j = atomicAdd(&s_n, 1);
+            t.sel[j] = (int)id;
+            t.sa[j] = a;
+            t.sb[j] = b;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) t.cnt[5] = s_n;
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_final(Tree t, TreeK k, int n_traj) {
+    const int nc = t.cnt[2];
+    if (threadIdx.x == 0) t.cnt[6] = nc > 0;
+    if (nc > 0) select_into(t, SrcCand{t.cand, t.ng}, nc, n_traj, false);
+    else select_into(t, SrcNodes{t.nx, t.ny, t.ng, k}, t.cnt[1] - 1, n_traj, true);
+}
+
+// rank of each selected item by (a, b, id) -> order
+__global__ void k_rank(Tree t) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = t.cnt[5];
+    if (i >= n) return;
+    const unsigned long long a = t.sa[i], b = t.sb[i];
+    const int id = t.sel[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+        const unsigned long long aj = t.sa[j], bj = t.sb[j];
+        r += aj < a || (aj == a && (bj < b || (bj == b && t.sel[j] < id)));
+    }
+    t.order[r] = id;
+}
+
+// waypoints of the ranked candidates: l = depth (l = 0: start; NaN past the candidate's last node)
+__global__ void k_trace(Tree t, TreeK k, int T, float* wx, float* wy, float* wz, float* wyaw, double* cost) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= t.cnt[5]) return;
+    int id = t.order[r];
+    cost[r] = t.ng[id];
+    for (; id >= 0; id = t.npar[id]) {
+        const size_t l = (size_t)r * T + t.ndep[id];
+        wx[l] = (float)t.nx[id];
+        wy[l] = (float)t.ny[id];
+        wz[l] = k.z;
+        wyaw[l] = (float)t.nth[id];
+    }
+}
+
+unsigned long long pow2_at_least(unsigned long long v) {
+    unsigned long long p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+int bits_for(long long range) {   // bits holding 0 .. range - 1
+    int b = 0;
+    while ((1LL << b) < range) ++b;
+    return b;
+}
 
 }  // namespace
 
 rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], const rtg_tree_params& P,
-                     cudaStream_t st, std::vector<float>* wx, std::vector<float>* wy, std::vector<float>* wyaw,
-                     std::vector<double>* cost, int* reached, long long stats_out[4]) {
+                     cudaStream_t st, rtg_traj_s** out, double* cost, int* n_found, int* reached,
+                     long long stats_out[4]) {
     // ---- controls: v on a uniform grid of [0, v_max] incl. endpoints, w likewise on
-    // [-w_max, w_max]; a grid of one point is {v_max} / {0}
+    // [-w_max, w_max]; a grid of one point is {v_max} / {0}.  Then the per-control costs.
     std::vector<double> ctl;
     for (int i = 0; i < P.n_v; ++i) {
         const double v = P.n_v == 1 ? (double)P.v_max : (double)P.v_max * (double)i / (double)(P.n_v - 1);
@@ -126,147 +523,168 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
         }
     }
     const int NP = P.n_v * P.n_omega;
-    std::vector<double> pcost(NP);
     for (int p = 0; p < NP; ++p)
-        pcost[p] = ((double)P.lambda_t + ctl[2 * p] * ctl[2 * p] + ctl[2 * p + 1] * ctl[2 * p + 1]) * (double)P.dt;
-    const double gx = goal[0], gy = goal[1], r2 = (double)P.goal_radius * (double)P.goal_radius;
-    auto h_of = [&](double x, double y) { return std::sqrt((gx - x) * (gx - x) + (gy - y) * (gy - y)) / (double)P.v_max; };
-    auto at_goal = [&](double x, double y) { return (x - gx) * (x - gx) + (y - gy) * (y - gy) <= r2; };
-    const bool dedup = P.lattice_xy > 0 && P.lattice_deg > 0;
-    auto key_of = [&](const Node& n) {
-        return LatticeKey{(long long)std::floor(n.x / (double)P.lattice_xy), (long long)std::floor(n.y / (double)P.lattice_xy),
-                          (long long)std::floor(n.th * (180.0 / M_PI) / (double)P.lattice_deg)};
-    };
-    std::vector<Node> nodes;
-    double th0 = std::remainder((double)start[2], 2.0 * M_PI);   // (-pi, pi]
-    if (th0 <= -M_PI) th0 += 2.0 * M_PI;
-    nodes.push_back(Node{(double)start[0], (double)start[1], th0, 0.0, -1, 0});
-    std::unordered_map<LatticeKey, double, LatticeHash> closed;
-    if (dedup) closed[key_of(nodes[0])] = 0.0;
-    std::vector<int> frontier, cand;
-    if (at_goal(nodes[0].x, nodes[0].y)) cand.push_back(0);   // already in the goal region
-    else frontier.push_back(0);
-    // ---- device scratch
-    ColGridK g;
-    g.ox = m->cg.ox; g.oy = m->cg.oy; g.oz = m->cg.oz; g.h = m->cg.h;
-    g.R = m->rb_max * (1.0f + 2e-5f) + 1e-4f;
-    g.nx = m->cg.nx; g.ny = m->cg.ny; g.nz = m->cg.nz;
-    const long long maxM = std::max(1, P.beam);
-    double *d_fr = nullptr, *d_ctl = nullptr, *d_child = nullptr;
-    unsigned char* d_ok = nullptr;
-    unsigned long long* d_stats = nullptr;
-    cudaError_t e = dev_alloc((void**)&d_fr, sizeof(double) * 4 * maxM, st);
-    if (e == cudaSuccess) e = dev_alloc((void**)&d_ctl, sizeof(double) * 2 * NP, st);
-    if (e == cudaSuccess) e = dev_alloc((void**)&d_child, sizeof(double) * 3 * maxM * NP, st);
-    if (e == cudaSuccess) e = dev_alloc((void**)&d_ok, maxM * NP, st);
-    if (e == cudaSuccess) e = dev_alloc((void**)&d_stats, sizeof(unsigned long long) * 4, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_ctl, ctl.data(), sizeof(double) * 2 * NP, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4, st);
-    long long expanded = 0;
-    std::vector<double> hfr, hchild;
-    std::vector<unsigned char> hok;
-    for (int depth = 1; depth <= P.max_depth && e == cudaSuccess && !frontier.empty(); ++depth) {
-        const int M = (int)frontier.size();
-        hfr.assign(4 * (size_t)M, 0.0);
-        for (int i = 0; i < M; ++i) {
-            const Node& n = nodes[frontier[i]];
-            hfr[4 * i] = n.x; hfr[4 * i + 1] = n.y; hfr[4 * i + 2] = n.th; hfr[4 * i + 3] = n.g;
-        }
-        e = cudaMemcpyAsync(d_fr, hfr.data(), sizeof(double) * 4 * M, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) break;
-        ExpandK k{M, NP, P.samples, (double)P.dt, P.z};
-        const long long warps = (long long)M * NP;
-        note_launch(), k_expand<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
-            k, d_fr, d_ctl, m->crec, m->cmat, m->csrc, m->robot, m->cstart, g, m->gq, (int)m->n_col, d_ok, d_child,
-            d_stats);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) break;
-        hok.resize(warps);
-        hchild.resize(3 * warps);
-        e = cudaMemcpyAsync(hok.data(), d_ok, warps, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hchild.data(), d_child, sizeof(double) * 3 * warps, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) break;
-        expanded += M;
-        std::vector<int> next;
-        for (long long w = 0; w < warps; ++w) {   // creation order: node m ascending, control p ascending
-            if (!hok[w]) continue;
-            const int mi = (int)(w / NP), p = (int)(w % NP);
-            const Node& par = nodes[frontier[mi]];
-            Node c{hchild[3 * w], hchild[3 * w + 1], hchild[3 * w + 2], par.g + pcost[p], frontier[mi], depth};
-            if (dedup) {
-                const LatticeKey key = key_of(c);
-                auto it = closed.find(key);
-                if (it != closed.end() && it->second <= c.g) continue;
-                closed[key] = c.g;
-            }
-            nodes.push_back(c);
-            const int id = (int)nodes.size() - 1;
-            if (at_goal(c.x, c.y)) cand.push_back(id);
-            else next.push_back(id);
-        }
-        // beam: lowest f = g + h, ties -> creation order
-        std::vector<std::pair<double, int>> fv;
-        fv.reserve(next.size());
-        for (int id : next) fv.emplace_back(nodes[id].g + h_of(nodes[id].x, nodes[id].y), id);
-        std::stable_sort(fv.begin(), fv.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
-            return a.first < b.first;
-        });
-        if ((long long)fv.size() > maxM) fv.resize(maxM);
-        frontier.clear();
-        for (auto& pr : fv) frontier.push_back(pr.second);
-        std::sort(frontier.begin(), frontier.end());   // keep creation order within the layer
+        ctl.push_back(((double)P.lambda_t + ctl[2 * p] * ctl[2 * p] + ctl[2 * p + 1] * ctl[2 * p + 1]) * (double)P.dt);
+    TreeK k{};
+    k.P = NP;
+    k.S = P.samples;
+    k.beam = P.beam;
+    k.W = P.beam * NP;
+    k.dt = (double)P.dt;
+    k.gx = goal[0];
+    k.gy = goal[1];
+    k.r2 = (double)P.goal_radius * (double)P.goal_radius;
+    k.vmax = (double)P.v_max;
+    k.z = P.z;
+    k.dedup = P.lattice_xy > 0 && P.lattice_deg > 0;
+    k.lxy = (double)P.lattice_xy;
+    k.ldeg = (double)P.lattice_deg;
+    k.rad2deg = 180.0 / M_PI;
+    const long long NC = 1 + (long long)P.max_depth * k.W;
+    if (NC >= (1LL << 31)) {
+        set_error("rtg_plan_tree: 1 + max_depth * beam * controls must be < 2^31");
+        return RTG_ERR_INVALID_ARGUMENT;
     }
-    unsigned long long hs[4] = {0, 0, 0, 0};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    dev_free(d_fr, st);
-    dev_free(d_ctl, st);
-    dev_free(d_child, st);
-    dev_free(d_ok, st);
-    dev_free(d_stats, st);
+    unsigned long long ccap = 2;
+    const unsigned long long lcap = pow2_at_least(2ull * (unsigned long long)k.W);
+    if (k.dedup) {
+        // lattice indices reachable within max_depth primitives (arc length <= v_max dt each)
+        const double reach = (double)P.max_depth * (double)P.v_max * (double)P.dt + 1.0;
+        k.amin = (long long)std::floor(((double)start[0] - reach) / k.lxy) - 1;
+        k.bmin = (long long)std::floor(((double)start[1] - reach) / k.lxy) - 1;
+        k.cmin = (long long)std::floor(-180.0 / k.ldeg) - 1;
+        const long long na = (long long)std::floor(((double)start[0] + reach) / k.lxy) + 2 - k.amin;
+        const long long nb = (long long)std::floor(((double)start[1] + reach) / k.lxy) + 2 - k.bmin;
+        const long long ncl = (long long)std::floor(180.0 / k.ldeg) + 2 - k.cmin;
+        k.ba = bits_for(nb);
+        k.bb = bits_for(ncl);
+        if (bits_for(na) + k.ba + k.bb > 62) {
+            set_error("rtg_plan_tree: lattice too fine for the reachable area (cell key exceeds 62 bits)");
+            return RTG_ERR_INVALID_ARGUMENT;
+        }
+        const double cells = (double)na * (double)nb * (double)ncl;
+        ccap = pow2_at_least((unsigned long long)std::min((double)NC, cells) * 2ull + 2ull);
+    }
+    k.cmask = ccap - 1;
+    k.lmask = lcap - 1;
+    // ---- device state (one allocation)
+    const size_t W = (size_t)k.W, nc = (size_t)NC, nt = (size_t)P.n_traj, T = (size_t)P.max_depth + 1;
+    size_t off = 0;
+    auto carve = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    const size_t o_n = carve(sizeof(double) * 4 * nc), o_pd = carve(sizeof(int) * 2 * nc);
+    const size_t o_fr = carve(sizeof(int) * (size_t)k.beam), o_c = carve(sizeof(double) * 4 * W);
+    const size_t o_ok = carve(W), o_key = carve(sizeof(unsigned long long) * W), o_i = carve(sizeof(int) * 5 * W);
+    const size_t o_f = carve(sizeof(unsigned long long) * W);
+    const size_t o_t = carve(sizeof(unsigned long long) * ccap), o_tv = carve(sizeof(double) * ccap);
+    const size_t o_l = carve(sizeof(unsigned long long) * lcap), o_lc = carve(sizeof(int) * 2 * lcap);
+    const size_t o_lb = carve(sizeof(int) * W), o_cand = carve(sizeof(int) * nc), o_cnt = carve(sizeof(int) * 8);
+    const size_t o_sel = carve(sizeof(int) * 2 * nt), o_sab = carve(sizeof(unsigned long long) * 2 * nt);
+    const size_t o_w = carve(sizeof(float) * 4 * nt * T), o_cost = carve(sizeof(double) * nt);
+    const size_t o_ctl = carve(sizeof(double) * ctl.size()), o_st = carve(sizeof(unsigned long long) * 4);
+    char* mem = nullptr;
+    cudaError_t e = dev_alloc((void**)&mem, off, st);
     if (e != cudaSuccess) {
         set_error("rtg_plan_tree: %s", cudaGetErrorString(e));
         return e == cudaErrorMemoryAllocation ? RTG_ERR_OUT_OF_MEMORY : RTG_ERR_CUDA;
     }
-    // ---- candidates: cheapest goal-reaching nodes, else the leaves closest to the goal
-    std::vector<int> pick;
-    if (!cand.empty()) {
-        *reached = 1;
-        pick = cand;
-        std::stable_sort(pick.begin(), pick.end(), [&](int a, int b) { return nodes[a].g < nodes[b].g; });
-    } else {
-        *reached = 0;
-        for (int id = 1; id < (int)nodes.size(); ++id) pick.push_back(id);   // every node but the root
-        std::stable_sort(pick.begin(), pick.end(), [&](int a, int b) {
-            const double ha = h_of(nodes[a].x, nodes[a].y), hb = h_of(nodes[b].x, nodes[b].y);
-            if (ha != hb) return ha < hb;
-            return nodes[a].g < nodes[b].g;
-        });
+    Tree t;
+    t.nx = (double*)(mem + o_n); t.ny = t.nx + nc; t.nth = t.ny + nc; t.ng = t.nth + nc;
+    t.npar = (int*)(mem + o_pd); t.ndep = t.npar + nc;
+    t.frontier = (int*)(mem + o_fr);
+    t.cx = (double*)(mem + o_c); t.cy = t.cx + W; t.cth = t.cy + W; t.cg = t.cth + W;
+    t.cok = (unsigned char*)(mem + o_ok);
+    t.ckey = (unsigned long long*)(mem + o_key);
+    t.cslot = (int*)(mem + o_i); t.cpos = t.cslot + W; t.acc = t.cpos + W; t.rank = t.acc + W; t.cid = t.rank + W;
+    t.fkey = (unsigned long long*)(mem + o_f);
+    t.tkey = (unsigned long long*)(mem + o_t); t.tval = (double*)(mem + o_tv);
+    t.lkey = (unsigned long long*)(mem + o_l); t.lcnt = (int*)(mem + o_lc); t.loff = t.lcnt + lcap;
+    t.lbucket = (int*)(mem + o_lb);
+    t.cand = (int*)(mem + o_cand);
+    t.cnt = (int*)(mem + o_cnt);
+    t.sel = (int*)(mem + o_sel); t.order = t.sel + nt;
+    t.sa = (unsigned long long*)(mem + o_sab); t.sb = t.sa + nt;
+    float* wx = (float*)(mem + o_w);
+    float *wy = wx + nt * T, *wz = wy + nt * T, *wyaw = wz + nt * T;
+    double* d_cost = (double*)(mem + o_cost);
+    double* d_ctl = (double*)(mem + o_ctl);
+    unsigned long long* d_stats = (unsigned long long*)(mem + o_st);
+    // ---- root (FP64 heading wrapped to (-pi, pi] like the oracle)
+    double th0 = std::remainder((double)start[2], 2.0 * M_PI);
+    if (th0 <= -M_PI) th0 += 2.0 * M_PI;
+    e = cudaMemcpyAsync(d_ctl, ctl.data(), sizeof(double) * ctl.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(t.cnt, 0, sizeof(int) * 8, st);
+    if (e == cudaSuccess && k.dedup) e = cudaMemsetAsync(t.tkey, 0xff, sizeof(unsigned long long) * ccap, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(wx, 0xff, sizeof(float) * 4 * nt * T, st);   // all-ones: NaN
+    if (e == cudaSuccess) note_launch(), k_tree_init<<<1, 1, 0, st>>>(t, k, (double)start[0], (double)start[1], th0),
+        e = cudaGetLastError();
+    ColGridK g;
+    g.ox = m->cg.ox; g.oy = m->cg.oy; g.oz = m->cg.oz; g.h = m->cg.h;
+    g.R = m->rb_max * (1.0f + 2e-5f) + 1e-4f;
+    g.nx = m->cg.nx; g.ny = m->cg.ny; g.nz = m->cg.nz;
+    const unsigned wblocks = (unsigned)((W * 32 + 255) / 256), tblocks = (unsigned)((W + 255) / 256);
+    for (int depth = 1; depth <= P.max_depth && e == cudaSuccess; ++depth) {
+        note_launch(), k_expand<<<wblocks, 256, 0, st>>>(t, k, d_ctl, m->crec, m->cmat, m->csrc, m->robot, m->cstart,
+                                                          g, m->gq, (int)m->n_col, d_stats);
+        e = cudaGetLastError();
+        if (e == cudaSuccess && k.dedup) {
+            e = cudaMemsetAsync(t.lkey, 0xff, sizeof(unsigned long long) * lcap, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(t.lcnt, 0, sizeof(int) * lcap, st);
+            if (e == cudaSuccess) note_launch(), k_cells<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
+            if (e == cudaSuccess) e = exclusive_scan_i32(t.lcnt, t.loff, (long long)lcap, st);
+            if (e == cudaSuccess) note_launch(), k_bucket<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) note_launch(), k_keep<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
+        if (e == cudaSuccess && k.dedup) note_launch(), k_close<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
+        if (e == cudaSuccess) e = exclusive_scan_i32(t.acc, t.rank, (long long)W, st);
+        if (e == cudaSuccess) note_launch(), k_create<<<tblocks, 256, 0, st>>>(t, k, depth), e = cudaGetLastError();
+        if (e == cudaSuccess) note_launch(), k_beam<<<1, kSelThreads, 0, st>>>(t, k), e = cudaGetLastError();
     }
-    if ((int)pick.size() > P.n_traj) pick.resize(P.n_traj);
-    const int T = P.max_depth + 1;
-    const float nanf_ = std::nanf("");
-    wx->assign((size_t)pick.size() * T, nanf_);
-    wy->assign((size_t)pick.size() * T, nanf_);
-    wyaw->assign((size_t)pick.size() * T, nanf_);
-    cost->assign(pick.size(), 0.0);
-    for (size_t c = 0; c < pick.size(); ++c) {
-        (*cost)[c] = nodes[pick[c]].g;
-        for (int id = pick[c]; id >= 0; id = nodes[id].parent) {
-            const Node& n = nodes[id];
-            (*wx)[c * T + n.depth] = (float)n.x;
-            (*wy)[c * T + n.depth] = (float)n.y;
-            (*wyaw)[c * T + n.depth] = (float)n.th;
+    if (e == cudaSuccess) note_launch(), k_final<<<1, kSelThreads, 0, st>>>(t, k, P.n_traj), e = cudaGetLastError();
+    const unsigned rblocks = (unsigned)((nt + 255) / 256);
+    if (e == cudaSuccess) note_launch(), k_rank<<<rblocks, 256, 0, st>>>(t), e = cudaGetLastError();
+    if (e == cudaSuccess)
+        note_launch(), k_trace<<<rblocks, 256, 0, st>>>(t, k, (int)T, wx, wy, wz, wyaw, d_cost), e = cudaGetLastError();
+    int hc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long hs[4] = {0, 0, 0, 0};
+    std::vector<double> hcost(nt, 0.0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc, t.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hcost.data(), d_cost, sizeof(double) * nt, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    rtg_status s = RTG_OK;
+    if (e != cudaSuccess) {
+        set_error("rtg_plan_tree: %s", cudaGetErrorString(e));
+        s = e == cudaErrorMemoryAllocation ? RTG_ERR_OUT_OF_MEMORY : RTG_ERR_CUDA;
+    } else if (hc[4]) {
+        set_error("rtg_plan_tree: lattice cell out of the reachable range");
+        s = RTG_ERR_CUDA;
+    } else {
+        const int K = std::min(hc[5], P.n_traj);
+        *n_found = K;
+        *reached = hc[6];
+        if (cost)
+            for (int i = 0; i < K; ++i) cost[i] = hcost[i];
+        if (stats_out) {
+            stats_out[0] = hc[3];
+            stats_out[1] = (long long)hc[1] - 1;
+            stats_out[2] = (long long)hs[0];
+            stats_out[3] = (long long)hs[1];
+        }
+        if (K == 0) {
+            set_error("rtg_plan_tree: no collision-free primitive grows from the start");
+            s = RTG_ERR_NO_FEASIBLE;
+        } else {
+            // the first K rows of the (k-major) scratch waypoints are the result
+            s = rtg_traj_upload(m->device, K, (int)T, RTG_MEM_DEVICE, wx, wy, wz, wyaw, st, out);
         }
     }
-    if (stats_out) {
-        stats_out[0] = expanded;
-        stats_out[1] = (long long)nodes.size() - 1;
-        stats_out[2] = (long long)hs[0];
-        stats_out[3] = (long long)hs[1];
-    }
-    return RTG_OK;
+    dev_free(mem, st);
+    return s;
 }
 
 }  // namespace rtg
