@@ -178,12 +178,15 @@ def _oracle_collides(wl):
     return f
 
 
-@pytest.mark.parametrize("goal,depth,beam,lattice", [((4.0, 2.0), 6, 128, 0.1), ((-3.0, 3.5), 7, 96, 0.1),
-                                                     ((2.5, -1.0), 4, 4000, 0.0), ((40.0, 0.0), 3, 64, 0.1)])
-def test_plan_tree_matches_oracle(R, goal, depth, beam, lattice):
+# the last two: a coarse lattice (many children of a layer share a cell: the in-layer prefix-minimum
+# rule) with many candidates ranked, and an unreachable goal with many closest-node results
+@pytest.mark.parametrize("goal,depth,beam,lattice,ldeg,n_traj", [
+    ((4.0, 2.0), 6, 128, 0.1, 10.0, 10), ((-3.0, 3.5), 7, 96, 0.1, 10.0, 10), ((2.5, -1.0), 4, 4000, 0.0, 10.0, 10),
+    ((40.0, 0.0), 3, 64, 0.1, 10.0, 10), ((2.0, 1.0), 6, 80, 0.7, 45.0, 300), ((-30.0, 5.0), 5, 200, 0.3, 30.0, 700)])
+def test_plan_tree_matches_oracle(R, goal, depth, beam, lattice, ldeg, n_traj):
     wl = W.room(N=20000, K=1, T=1)
     start = (0.0, 0.0, 0.3)
-    tp = R.make_tree_params(max_depth=depth, beam=beam, lattice_xy=lattice, z=0.5)
+    tp = R.make_tree_params(max_depth=depth, beam=beam, lattice_xy=lattice, lattice_deg=ldeg, n_traj=n_traj, z=0.5)
     m = R.map_from_workload(wl)
     tr, cost, reached, stats = R.plan_tree(m, start, goal, tp)
     x, y, z, yaw = (a.cpu().numpy() for a in tr.read())
