@@ -1,7 +1,7 @@
 #!/bin/bash
 # usage: tools/sweep.sh "hy,hx,hz" ... -- quick bench sweep over visibility-grid cell sizes (outdoor)
 for c in "$@"; do
-  out=$(timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --cells "$c" 2>&1 | tail -1)
+  out=$(timeout 300 python bench.py --config ${CONFIG:-outdoor} --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --cells "$c" 2>&1 | tail -1)
   python - "$c" "$out" <<'PY'
 import json, sys
 c, line = sys.argv[1], sys.argv[2]
