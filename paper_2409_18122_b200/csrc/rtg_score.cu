@@ -13,6 +13,7 @@
 //           footprint; whole z-cell runs strictly inside the frustum are added from exact
 //           fixed-point prefix sums, the straddling cells' Gaussians are tested one by one.
 // Reduction (a6) per trajectory and argmax (a7).
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -124,6 +125,17 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
 // ===================================================================== culled phase A
 constexpr int kWarps = 8;   // warps per block of the persistent culled kernels
 
+// work item e = (chunk c, trajectory k), chunk-major: waypoints c*kColChunk .. +kColChunk-1 of k,
+// t ascending, stopping at the chunk's first collision; first_col[k] (preset to T) = atomicMin of
+// the chunks' first collisions, so it is the first collision of k whatever the schedule.  A chunk
+// whose trajectory already collided earlier is skipped (chunk-major order: chunk c - 1 of every
+// trajectory was handed out before chunk c), so the early exit of a4 survives the split while the
+// long collision-free trajectories no longer serialise on one warp.
+#ifndef RTG_COL_CHUNK
+#define RTG_COL_CHUNK 10
+#endif
+constexpr int kColChunk = RTG_COL_CHUNK;
+
 __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
     const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CSrc* __restrict__ csrc, const rtg_robot rb,
@@ -131,25 +143,30 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
     unsigned char* __restrict__ wp_col, int all_waypoints, int* __restrict__ counter,
     unsigned long long* __restrict__ stats) {
     const int lane = threadIdx.x & 31;
+    const int nch = (T + kColChunk - 1) / kColChunk;
+    const long long items = (long long)K * nch;
     unsigned nref = 0;
     unsigned long long ntest = 0;
     for (;;) {
-        int k = 0;
-        if (lane == 0) k = atomicAdd(counter, 1);
-        k = __shfl_sync(kFull, k, 0);
-        if (k >= K) break;
-        int first = T;
-        for (int t = 0; t < T; ++t) {
+        int e = 0, fc = 0;
+        if (lane == 0) e = atomicAdd(counter, 1);
+        e = __shfl_sync(kFull, e, 0);
+        if (e >= items) break;
+        const int c = e / K, k = e - c * K;
+        const int t0 = c * kColChunk, t1 = min(T, t0 + kColChunk);
+        if (lane == 0) fc = *(volatile int*)(first_col + k);
+        fc = __shfl_sync(kFull, fc, 0);
+        if (!all_waypoints && fc < t0) continue;
+        for (int t = t0; t < t1; ++t) {
             const long long i = (long long)k * T + t;
             const float px = X[i], py = Y[i], pz = Zw[i];
             const bool hit = warp_point_collides(px, py, pz, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
             if (all_waypoints && lane == 0) wp_col[i] = hit ? 1 : 0;
             if (hit) {
-                first = min(first, t);
+                if (lane == 0) atomicMin(first_col + k, t);
                 if (!all_waypoints) break;
             }
         }
-        if (lane == 0) first_col[k] = first;
     }
     if (stats) {
         nref = __reduce_add_sync(kFull, nref);
@@ -498,7 +515,8 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
         g.ox = m->cg.ox; g.oy = m->cg.oy; g.oz = m->cg.oz; g.h = m->cg.h;
         g.R = m->rb_max * (1.0f + 2e-5f) + 1e-4f;
         g.nx = m->cg.nx; g.ny = m->cg.ny; g.nz = m->cg.nz;
-        int blocks = (K + kWarps - 1) / kWarps;
+        const long long items = (long long)K * ((T + kColChunk - 1) / kColChunk);
+        int blocks = (int)std::min<long long>((items + kWarps - 1) / kWarps, 1LL << 30);
         int cap = g_sms * g_occ_col;
         if (blocks > cap) blocks = cap;
         note_launch(), k_col_culled<<<blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->csrc, m->robot,
