@@ -13,6 +13,7 @@ T=100 waypoints) per GPU; trajectories of the global set are interleaved over ra
 value = nominal waypoint x Gaussian pair-tests per second over all ranks (K*T*N / step time,
 every pair counted once whether or not it was culled); ms_per_step = planning-cycle latency.
 e2e   = the same step from pinned HOST buffers (H2D copies + 16-byte D2H result inside).
+ms_per_step_median / _p90 = per-step latency distribution over the timed steps (max over ranks per step).
 
 `--impl reference` times the CPU oracle (oracle/, the test-only FP64 reference) on a bounded
 sample of the same workload and prints the same JSON line with "impl": "reference".
@@ -40,7 +41,7 @@ L2_FLUSH_BYTES = 512 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="rtg", choices=["rtg", "reference"])
     ap.add_argument("--config", default="outdoor", choices=["tiny", "room", "multi_room", "outdoor", "scale"])
@@ -267,6 +268,7 @@ def main():
             R.profile_read(reset=True)
             R.profile_enable(True)
         total_ms = 0.0
+        per_step = []
         res = None
         for _ in range(steps):
             flush.fill_(1.0)                     # L2 flush between timed steps (not timed)
@@ -280,16 +282,23 @@ def main():
             b.record(stream)
             torch.cuda.synchronize()
             total_ms += a.elapsed_time(b)
+            per_step.append(a.elapsed_time(b))
         if profile:
             R.profile_enable(False)
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms] + per_step, dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()) / steps, res
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)   # total and every step: max over ranks
+        v = t.cpu().tolist()
+        dist_ms["median"] = statistics.median(v[1:])
+        dist_ms["p90"] = sorted(v[1:])[min(len(v) - 2, int(math.ceil(0.9 * (len(v) - 1))) - 1)]
+        return v[0] / steps, res
+
+    dist_ms = {}
 
     # ---- device-resident timing (value), with clocks and per-phase events
     with ClockSampler(local) as clocks:
         ms, res = timed(False, args.steps, args.warmup, profile=True)
+    step_stats = {"median": dist_ms["median"], "p90": dist_ms["p90"]}
     prof = R.profile_read(reset=True)
     nprof = args.steps
     launches_per_step = prof["launches"] / args.steps
@@ -338,7 +347,8 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
+                "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": step_stats["median"],
+                "ms_per_step_p90": step_stats["p90"], "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": "outdoor (BASELINE.json configs[3])" if args.config == "outdoor" else args.config,
                            "N": N, "K": K_glob, "K_per_gpu": K, "views": Kv_glob, "T": T, "mode": args.mode,
