@@ -112,12 +112,12 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     __shared__ float s_v[kWarpsG][8];        // footprint vertices (x0..x3, y0..y3), grid-relative
     // queued test runs: first record -> (first record - items before the run); length -> items before
     // the run.  64 entries of padding hold INT_MAX while the queue is tested.
-    __shared__ __align__(16) int s_st[kWarpsG][kQCap + 64];
-    __shared__ __align__(16) int s_ex[kWarpsG][kQCap + 64];
+    __shared__ __align__(16) int s_q[kWarpsG][2][kQCap + 64];   // [0]: starts, [1]: items before
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned lanes_lt = (1u << lane) - 1u;
-    int* const qs = s_st[wid];
-    int* const qe = s_ex[wid];
+    unsigned lanes_lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_lt));
+    int* const qs = s_q[wid][0];
+    int* const qe = qs + (kQCap + 64);   // one base register for both halves
     const int L = *list_count;
     unsigned nref = 0;
     unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0;
