@@ -107,17 +107,22 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     const int* __restrict__ gtabB, const int2* __restrict__ zocc, const TabP* __restrict__ gtabP, const GainK g,
     const CamK cam, long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
     int* __restrict__ counter, unsigned long long* __restrict__ stats) {
-    __shared__ double s_cs[kWarpsG][2];      // FP64 cos, sin of the waypoint's yaw (re-decisions)
-    __shared__ float4 s_con[kWarpsG][6];     // the frustum's constraints on grid cells
-    __shared__ float s_v[kWarpsG][8];        // footprint vertices (x0..x3, y0..y3), grid-relative
-    // queued test runs: first record -> (first record - items before the run); length -> items before
-    // the run.  64 entries of padding hold INT_MAX while the queue is tested.
-    __shared__ __align__(16) int s_q[kWarpsG][2][kQCap + 64];   // [0]: starts, [1]: items before
+    // per-warp state, one struct per warp so a single base register addresses all of it
+    struct __align__(16) WarpSmem {
+        float4 con[6];                       // the frustum's constraints on grid cells
+        double cs[2];                        // FP64 cos, sin of the waypoint's yaw (re-decisions)
+        float v[8];                          // footprint vertices (x0..x3, y0..y3), grid-relative
+        // queued test runs: [0] first record -> (first record - items before the run), [1] length ->
+        // items before the run.  64 entries of padding hold INT_MAX while the queue is tested.
+        int q[2][kQCap + 64];
+    };
+    __shared__ WarpSmem s_w[kWarpsG];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned lanes_lt;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_lt));
-    int* const qs = s_q[wid][0];
-    int* const qe = qs + (kQCap + 64);   // one base register for both halves
+    WarpSmem& sw = s_w[wid];
+    int* const qs = sw.q[0];
+    int* const qe = sw.q[1];
     const int L = *list_count;
     unsigned nref = 0;
     unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0;
@@ -140,8 +145,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                 if (lane < 4) {     // vertex = p + Z (c, s) + kZ (s, -c)
                     const float zz = lane < 2 ? g.zn : g.zf;
                     const float kk = (lane == 0 || lane == 3) ? -g.kxl : g.kxr;
-                    s_v[wid][lane] = fmaf(zz, fmaf(kk, f.s, f.c), qx);
-                    s_v[wid][4 + lane] = fmaf(zz, fmaf(-kk, f.c, f.s), qy);
+                    sw.v[lane] = fmaf(zz, fmaf(kk, f.s, f.c), qx);
+                    sw.v[4 + lane] = fmaf(zz, fmaf(-kk, f.c, f.s), qy);
                 }
                 if (lane < 6) {
                     // Z = c dx + s dy, X' = ax dx + bx dy (X - kxc Z), constraint j:
@@ -157,18 +162,18 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     const float X0 = fmaf(0.5f, g.hx, -qx), Y0 = fmaf(0.5f, g.hy, -qy);
                     const float Z0 = fmaf(0.5f, g.hz, g.oz - pz);
                     const float A = a * g.hx, B = b * g.hy;
-                    s_con[wid][lane] = make_float4(fmaf(a, X0, fmaf(b, Y0, fmaf(gz, Z0, d))), B,
+                    sw.con[lane] = make_float4(fmaf(a, X0, fmaf(b, Y0, fmaf(gz, Z0, d))), B,
                                                    fabsf(A) > 1e-30f ? 1.0f / A : 1e30f,
                                                    g.eps + 0.5f * (fabsf(A) + fabsf(B) + fabsf(gz) * g.hz));
                 }
                 if (lane == 0) {
-                    s_cs[wid][0] = cs;
-                    s_cs[wid][1] = sn;
+                    sw.cs[0] = cs;
+                    sw.cs[1] = sn;
                 }
                 __syncwarp();
             }
-            const float ymn = fminf(fminf(s_v[wid][4], s_v[wid][5]), fminf(s_v[wid][6], s_v[wid][7])) - g.eps;
-            const float ymx = fmaxf(fmaxf(s_v[wid][4], s_v[wid][5]), fmaxf(s_v[wid][6], s_v[wid][7])) + g.eps;
+            const float ymn = fminf(fminf(sw.v[4], sw.v[5]), fminf(sw.v[6], sw.v[7])) - g.eps;
+            const float ymx = fmaxf(fmaxf(sw.v[4], sw.v[5]), fmaxf(sw.v[6], sw.v[7])) + g.eps;
             const float inv_hy = 1.0f / g.hy;
             const int iy0 = max(0, fcell(ymn * inv_hy, g.ny));
             const int iy1 = min(g.ny - 1, fcell(ymx * inv_hy, g.ny));
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     const float fuy = (float)uy, fiz = (float)iz;
                     float vplo = (float)ui0, vphi = (float)ui1, vilo = vplo, vihi = vphi;
                     {
-                        const float4 Ct = s_con[wid][4], Cb = s_con[wid][5];
+                        const float4 Ct = sw.con[4], Cb = sw.con[5];
                         cut(Ct, fmaf(Ct.y, fuy, fmaf(-g.hz, fiz, Ct.x)), vplo, vphi, vilo, vihi);
                         cut(Cb, fmaf(Cb.y, fuy, fmaf(g.hz, fiz, Cb.x)), vplo, vphi, vilo, vihi);
                     }
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     float plo = 0.f, phi = (float)(g.nx - 1), ilo = 0.f, ihi = phi;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const float4 C = s_con[wid][j];
+                        const float4 C = sw.con[j];
                         cut(C, fmaf(C.y, fiy, C.x), plo, phi, ilo, ihi);
                     }
                     const int p0 = (int)fminf(plo, (float)g.nx);
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             l1 = __ldg(sa + p1 + 1) - s1;
                             // z-cells the inside columns can see: vertical wedge at their largest
                             // depth, cut to the occupied z-range of the x-blocks they span
-                            const float4 Cn = s_con[wid][0];
+                            const float4 Cn = sw.con[0];
                             const float F0 = fmaf(Cn.y, fiy, Cn.x);
                             const float An = 1.0f / Cn.z;
                             const float Zmax =
@@ -384,12 +389,12 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const bool ambb = fabsf(mb) < guard_b;
                             if (__any_sync(kFullG, amba || ambb)) {
                                 if (amba) {
-                                    visa = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], Ga.x, Ga.y,
+                                    visa = vis_decide64_cs(f.px, f.py, f.pz, sw.cs[0], sw.cs[1], Ga.x, Ga.y,
                                                            Ga.z, cam.cam64);
                                     ++nref;
                                 }
                                 if (ambb) {
-                                    visb = vis_decide64_cs(f.px, f.py, f.pz, s_cs[wid][0], s_cs[wid][1], Gb.x, Gb.y,
+                                    visb = vis_decide64_cs(f.px, f.py, f.pz, sw.cs[0], sw.cs[1], Gb.x, Gb.y,
                                                            Gb.z, cam.cam64);
                                     ++nref;
                                 }
