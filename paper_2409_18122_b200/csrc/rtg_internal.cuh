@@ -177,6 +177,35 @@ __device__ __forceinline__ float vis_margin_xy(const WpF& w, const CamK& k, floa
     return fminf(k.zhalf - fabsf(Z - k.zmid), fminf(fmaf(k.kxh, Z, -fabsf(X)), fmaf(k.kyh, Z, -fabsf(Y))));
 }
 
+// two waypoints against one item (dense mode): the waypoints' constants as register pairs, the
+// item broadcast; each half rounds exactly like vis_margin (bit-identical margins)
+struct WpF2 {
+    unsigned long long px, py, pz, c, s, ax, bx;
+};
+__device__ __forceinline__ WpF2 wp_pair(const WpF& a, const WpF& b) {
+    return WpF2{f2_pack(a.px, b.px), f2_pack(a.py, b.py), f2_pack(a.pz, b.pz), f2_pack(a.c, b.c),
+                f2_pack(a.s, b.s),   f2_pack(a.ax, b.ax), f2_pack(a.bx, b.bx)};
+}
+__device__ __forceinline__ void vis_margin_w2(const WpF2& w, const CamK& k, float mx, float my, float mz, float& ma,
+                                              float& mb, float& ga, float& gb) {
+    const unsigned long long dx = f2_sub(f2_pack(mx, mx), w.px);
+    const unsigned long long dy = f2_sub(f2_pack(my, my), w.py);
+    const unsigned long long dz = f2_sub(f2_pack(mz, mz), w.pz);
+    const unsigned long long Z = f2_fma(w.c, dx, f2_mul(w.s, dy));
+    const unsigned long long X = f2_fma(w.ax, dx, f2_mul(w.bx, dy));
+    const unsigned long long Y = f2_fma(f2_pack(-k.kyc, -k.kyc), Z, dz);
+    const unsigned long long D = f2_sub(Z, f2_pack(k.zmid, k.zmid));
+    const unsigned long long G = f2_fma(f2_pack(k.gam, k.gam), Z, f2_pack(k.g0, k.g0));
+    float Za, Zb, Xa, Xb, Ya, Yb, Da, Db;
+    f2_unpack(Z, Za, Zb);
+    f2_unpack(X, Xa, Xb);
+    f2_unpack(Y, Ya, Yb);
+    f2_unpack(D, Da, Db);
+    f2_unpack(G, ga, gb);
+    ma = fminf(k.zhalf - fabsf(Da), fminf(fmaf(k.kxh, Za, -fabsf(Xa)), fmaf(k.kyh, Za, -fabsf(Ya))));
+    mb = fminf(k.zhalf - fabsf(Db), fminf(fmaf(k.kxh, Zb, -fabsf(Xb)), fmaf(k.kyh, Zb, -fabsf(Yb))));
+}
+
 // FP64 decision with the six slacks of the pinhole test (visible <=> all >= 0), cos/sin of the
 // yaw given in FP64.  Every product is an explicit fma/mul so all kernels round identically.
 __device__ __forceinline__ bool vis_decide64_cs(float px, float py, float pz, double cs, double sn, float mx,

@@ -56,6 +56,14 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
         kk[j] = (int)(ii / T);
         tt[j] = (int)(ii % T);
     }
+    static_assert(kDenseColWpt % 2 == 0, "waypoints go in pairs (packed FP32)");
+    unsigned long long P2x[kDenseColWpt / 2], P2y[kDenseColWpt / 2], P2z[kDenseColWpt / 2];
+#pragma unroll
+    for (int j = 0; j < kDenseColWpt; j += 2) {
+        P2x[j / 2] = f2_pack(px[j], px[j + 1]);
+        P2y[j / 2] = f2_pack(py[j], py[j + 1]);
+        P2z[j / 2] = f2_pack(pz[j], pz[j + 1]);
+    }
     if (threadIdx.x == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -89,13 +97,30 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
             for (int g = 0; g < kTile; ++g) {
                 const CRec A = tile[g];
 #pragma unroll
-                for (int j = 0; j < kDenseColWpt; ++j) {
-                    float dx = px[j] - A.x, dy = py[j] - A.y, dz = pz[j] - A.z;
-                    float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    if (d2 < A.rb2 && act[j] && !hit[j]) {
+                for (int j = 0; j < kDenseColWpt; j += 2) {
+                    // two waypoints in one register pair (packed FP32, each half rounds like the
+                    // scalar d = p - mu, d2 = fma(dx, dx, fma(dy, dy, dz * dz)))
+                    const unsigned long long DX = f2_sub(P2x[j / 2], f2_pack(A.x, A.x));
+                    const unsigned long long DY = f2_sub(P2y[j / 2], f2_pack(A.y, A.y));
+                    const unsigned long long DZ = f2_sub(P2z[j / 2], f2_pack(A.z, A.z));
+                    const unsigned long long D2 = f2_fma(DX, DX, f2_fma(DY, DY, f2_mul(DZ, DZ)));
+                    float dxa, dxb, dya, dyb, dza, dzb, d2a, d2b;
+                    f2_unpack(D2, d2a, d2b);
+                    if (d2a < A.rb2 && act[j] && !hit[j]) {
+                        f2_unpack(DX, dxa, dxb);
+                        f2_unpack(DY, dya, dyb);
+                        f2_unpack(DZ, dza, dzb);
                         long long gi = (tile0 + it) * kTile + g;
-                        hit[j] = collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, px[j], py[j],
+                        hit[j] = collide_full(cmat[gi].m, dxa, dya, dza, gq, &csrc[gi], rb, px[j], py[j],
                                               pz[j], A.x, A.y, A.z, nref);
+                    }
+                    if (d2b < A.rb2 && act[j + 1] && !hit[j + 1]) {
+                        f2_unpack(DX, dxa, dxb);
+                        f2_unpack(DY, dya, dyb);
+                        f2_unpack(DZ, dza, dzb);
+                        long long gi = (tile0 + it) * kTile + g;
+                        hit[j + 1] = collide_full(cmat[gi].m, dxb, dyb, dzb, gq, &csrc[gi], rb, px[j + 1],
+                                                  py[j + 1], pz[j + 1], A.x, A.y, A.z, nref);
                     }
                 }
             }
@@ -268,6 +293,10 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
         nh[j] = 0;
         nl[j] = 0;
     }
+    static_assert(kDenseGainWpt % 2 == 0, "waypoints go in pairs (packed FP32)");
+    WpF2 wp2[kDenseGainWpt / 2];
+#pragma unroll
+    for (int j = 0; j < kDenseGainWpt; j += 2) wp2[j / 2] = wp_pair(wf[j], wf[j + 1]);
     if (threadIdx.x == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -285,22 +314,50 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
     for (long long it = 0; it < ntiles; ++it) {
         const int s = (int)(it & 1);
         mbar_wait(&s_bar[s], (uint32_t)((it >> 1) & 1));
+        const GRec* rec = s_rec[s];
+        // exact integer sums per half tile: 256 u_q < 2^24 fit 32 bits, 512 class increments the
+        // packed nH | nL << 16 counter
         int pc[kDenseGainWpt];
 #pragma unroll
         for (int j = 0; j < kDenseGainWpt; ++j) pc[j] = 0;
-        const GRec* rec = s_rec[s];
-#pragma unroll 2
-        for (int g = 0; g < kTile; ++g) {
-            const GRec G = rec[g];
-            const double q = __uint2double_rn(G.uc & kUqMask);
-            const int inc = uc_inc(G.uc);
+        for (int h = 0; h < kTile; h += kTile / 2) {
+            unsigned qs[kDenseGainWpt];
 #pragma unroll
-            for (int j = 0; j < kDenseGainWpt; ++j) {
-                if (visible(wf[j], cam, G.x, G.y, G.z, nref)) {
-                    accq[j] += q;
-                    pc[j] += inc;
+            for (int j = 0; j < kDenseGainWpt; ++j) qs[j] = 0;
+#pragma unroll 2
+            for (int g = h; g < h + kTile / 2; ++g) {
+                const GRec G = rec[g];
+                const unsigned q = G.uc & kUqMask;
+                const int inc = uc_inc(G.uc);
+                float m[kDenseGainWpt], gd[kDenseGainWpt];
+#pragma unroll
+                for (int j = 0; j < kDenseGainWpt; j += 2)
+                    vis_margin_w2(wp2[j / 2], cam, G.x, G.y, G.z, m[j], m[j + 1], gd[j], gd[j + 1]);
+                bool v[kDenseGainWpt], amb = false;
+#pragma unroll
+                for (int j = 0; j < kDenseGainWpt; ++j) {
+                    v[j] = m[j] >= 0.0f;
+                    amb |= fabsf(m[j]) < gd[j];
+                }
+                if (amb) {   // FP32 guard band: FP64 re-decision (rare)
+#pragma unroll
+                    for (int j = 0; j < kDenseGainWpt; ++j) {
+                        if (fabsf(m[j]) < gd[j]) {
+                            v[j] = vis_decide64(wf[j].px, wf[j].py, wf[j].pz, wf[j].yaw, G.x, G.y, G.z, cam.cam64);
+                            ++nref;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kDenseGainWpt; ++j) {
+                    if (v[j]) {
+                        qs[j] += q;
+                        pc[j] += inc;
+                    }
                 }
             }
+#pragma unroll
+            for (int j = 0; j < kDenseGainWpt; ++j) accq[j] += (double)qs[j];
         }
 #pragma unroll
         for (int j = 0; j < kDenseGainWpt; ++j) {
