@@ -26,7 +26,10 @@ constexpr unsigned kFull = 0xffffffffu;
 // ===================================================================== dense phase A
 // Each thread owns 2 waypoints of the flattened K*T index; blockIdx.y splits the Gaussians.
 constexpr int kDenseColThreads = 256;
-constexpr int kDenseColWpt = 2;
+#ifndef RTG_DENSE_COL_WPT
+#define RTG_DENSE_COL_WPT 4
+#endif
+constexpr int kDenseColWpt = RTG_DENSE_COL_WPT;
 
 __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
@@ -96,6 +99,7 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
 #pragma unroll 4
             for (int g = 0; g < kTile; ++g) {
                 const CRec A = tile[g];
+                float dxs[kDenseColWpt], dys[kDenseColWpt], dzs[kDenseColWpt], d2s[kDenseColWpt];
 #pragma unroll
                 for (int j = 0; j < kDenseColWpt; j += 2) {
                     // two waypoints in one register pair (packed FP32, each half rounds like the
@@ -104,23 +108,21 @@ __global__ void __launch_bounds__(kDenseColThreads) k_col_dense(
                     const unsigned long long DY = f2_sub(P2y[j / 2], f2_pack(A.y, A.y));
                     const unsigned long long DZ = f2_sub(P2z[j / 2], f2_pack(A.z, A.z));
                     const unsigned long long D2 = f2_fma(DX, DX, f2_fma(DY, DY, f2_mul(DZ, DZ)));
-                    float dxa, dxb, dya, dyb, dza, dzb, d2a, d2b;
-                    f2_unpack(D2, d2a, d2b);
-                    if (d2a < A.rb2 && act[j] && !hit[j]) {
-                        f2_unpack(DX, dxa, dxb);
-                        f2_unpack(DY, dya, dyb);
-                        f2_unpack(DZ, dza, dzb);
-                        long long gi = (tile0 + it) * kTile + g;
-                        hit[j] = collide_full(cmat[gi].m, dxa, dya, dza, gq, &csrc[gi], rb, px[j], py[j],
-                                              pz[j], A.x, A.y, A.z, nref);
-                    }
-                    if (d2b < A.rb2 && act[j + 1] && !hit[j + 1]) {
-                        f2_unpack(DX, dxa, dxb);
-                        f2_unpack(DY, dya, dyb);
-                        f2_unpack(DZ, dza, dzb);
-                        long long gi = (tile0 + it) * kTile + g;
-                        hit[j + 1] = collide_full(cmat[gi].m, dxb, dyb, dzb, gq, &csrc[gi], rb, px[j + 1],
-                                                  py[j + 1], pz[j + 1], A.x, A.y, A.z, nref);
+                    f2_unpack(DX, dxs[j], dxs[j + 1]);
+                    f2_unpack(DY, dys[j], dys[j + 1]);
+                    f2_unpack(DZ, dzs[j], dzs[j + 1]);
+                    f2_unpack(D2, d2s[j], d2s[j + 1]);
+                }
+                bool near = false;
+#pragma unroll
+                for (int j = 0; j < kDenseColWpt; ++j) near |= d2s[j] < A.rb2 && act[j] && !hit[j];
+                if (near) {   // inside some waypoint's bounding sphere: the full test (rare)
+                    const long long gi = (tile0 + it) * kTile + g;
+#pragma unroll
+                    for (int j = 0; j < kDenseColWpt; ++j) {
+                        if (d2s[j] < A.rb2 && act[j] && !hit[j])
+                            hit[j] = collide_full(cmat[gi].m, dxs[j], dys[j], dzs[j], gq, &csrc[gi], rb, px[j], py[j],
+                                                  pz[j], A.x, A.y, A.z, nref);
                     }
                 }
             }
@@ -259,7 +261,10 @@ __global__ void k_iota(int* __restrict__ list, long long n, int* __restrict__ co
 
 // ===================================================================== dense phase B
 constexpr int kDenseGainThreads = 256;
-constexpr int kDenseGainWpt = 4;
+#ifndef RTG_DENSE_GAIN_WPT
+#define RTG_DENSE_GAIN_WPT 4
+#endif
+constexpr int kDenseGainWpt = RTG_DENSE_GAIN_WPT;
 
 __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
