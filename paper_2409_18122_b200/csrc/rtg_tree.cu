@@ -278,61 +278,123 @@ __global__ void k_create(Tree t, TreeK k, int depth) {
 }
 
 // ---- exact selection of the `need` smallest keys (a, b, id) among n items in one CTA: radix
-// select, 8 bits per pass from the most significant digit of a, then b, then id (ids are unique, so
-// it always ends exact).  Returns the decided prefix (pa, pb, pi under masks ma, mb, mi); an item is
-// selected iff its masked key is below the prefix, or equal to it.
+// select, 11 bits per pass from the most significant digit of a, then b, then id (ids are unique,
+// so it always ends exact).  Returns the decided prefix (pa, pb, pi under masks ma, mb, mi); an item
+// is selected iff its masked key is below the prefix, or equal to it.
 struct SelState {
     unsigned long long pa, pb, ma, mb;
     unsigned pi, mi;
 };
 
+constexpr int kRadixBits = 11, kRadixBins = 1 << kRadixBits;
+
+// digit d of the concatenated key a(64) | b(64, optional) | id(32): the word, shift and width
+__device__ __forceinline__ void digit_pos(int d, bool use_b, int& which, int& sh, int& wd) {
+    const int na = 6, nb = use_b ? 6 : 0;   // 64 bits = 5 digits of 11 + one of 9
+    int dd = d;
+    int top = 64;
+    which = 0;
+    if (dd >= na) {
+        dd -= na;
+        which = 1;
+        if (dd >= nb) {
+            dd -= nb;
+            which = 2;
+            top = 32;
+        }
+    }
+    const int hi = top - kRadixBits * dd;
+    sh = hi > kRadixBits ? hi - kRadixBits : 0;
+    wd = hi - sh;
+}
+
 template <typename Src>
 __device__ SelState block_select(const Src& src, int n, int need, bool use_b) {
-    __shared__ int hist[256];
-    __shared__ int s_need, s_done;
+    __shared__ int hist[kRadixBins];
+    __shared__ int s_wsum[kSelThreads / 32];
+    __shared__ int s_need, s_done, s_t, s_before;
     __shared__ SelState s_st;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) {
         s_st = SelState{0, 0, 0, 0, 0, 0};
         s_need = need;
         s_done = 0;
     }
     __syncthreads();
-    const int nb = use_b ? 8 : 0, ndig = 8 + nb + 4;
+    const int ndig = 6 + (use_b ? 6 : 0) + 3;
     for (int d = 0; d < ndig; ++d) {
-        for (int j = tid; j < 256; j += blockDim.x) hist[j] = 0;
+        for (int j = tid; j < kRadixBins; j += blockDim.x) hist[j] = 0;
         __syncthreads();
         const SelState st = s_st;
-        const int which = d < 8 ? 0 : (d < 8 + nb ? 1 : 2);
-        const int sh = which == 0 ? 56 - 8 * d : (which == 1 ? 56 - 8 * (d - 8) : 24 - 8 * (d - 8 - nb));
-        for (int i = tid; i < n; i += blockDim.x) {
-            unsigned long long a, b;
-            unsigned id;
-            if (!src.get(i, a, b, id)) continue;
-            if ((a & st.ma) != st.pa || (b & st.mb) != st.pb || (id & st.mi) != st.pi) continue;
-            const unsigned dg = which == 0 ? (unsigned)(a >> sh) & 255u
-                                           : (which == 1 ? (unsigned)(b >> sh) & 255u : (id >> sh) & 255u);
-            atomicAdd(&hist[dg], 1);
+        int which, sh, wd;
+        digit_pos(d, use_b, which, sh, wd);
+        const unsigned dmask = (1u << wd) - 1u;
+        for (int i0 = tid; i0 < n; i0 += 4 * blockDim.x) {
+            unsigned long long a[4], b[4];
+            unsigned id[4];
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {   // four independent loads in flight
+                const int i = i0 + u * blockDim.x;
+                ok[u] = i < n && src.get(i, a[u], b[u], id[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!ok[u] || (a[u] & st.ma) != st.pa || (b[u] & st.mb) != st.pb || (id[u] & st.mi) != st.pi)
+                    continue;
+                const unsigned dg = which == 0 ? (unsigned)(a[u] >> sh) & dmask
+                                               : (which == 1 ? (unsigned)(b[u] >> sh) & dmask : (id[u] >> sh) & dmask);
+                atomicAdd(&hist[dg], 1);
+            }
+        }
+        __syncthreads();
+        // the bin where the running count reaches `need`: block scan, two bins per thread
+        const int b0 = 2 * tid;
+        const int h0 = hist[b0], h1 = hist[b0 + 1];
+        int inc = h0 + h1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) s_wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            const int v = s_wsum[lane];
+            int w = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += u;
+            }
+            s_wsum[lane] = w - v;
+        }
+        __syncthreads();
+        const int before = s_wsum[wid] + inc - (h0 + h1);   // items in bins < b0
+        const int nd = s_need;
+        if (before < nd && before + h0 >= nd) {
+            s_t = b0;
+            s_before = before;
+        } else if (before + h0 < nd && before + h0 + h1 >= nd) {
+            s_t = b0 + 1;
+            s_before = before + h0;
         }
         __syncthreads();
         if (tid == 0) {
-            int cum = 0, t = 0;
-            for (; t < 255; ++t) {
-                if (cum + hist[t] >= s_need) break;
-                cum += hist[t];
-            }
-            s_need -= cum;
+            const int t = s_t;
+            s_need -= s_before;
             if (hist[t] == s_need) s_done = 1;
             SelState ns = s_st;
+            const unsigned long long mk = (unsigned long long)dmask << sh;
             if (which == 0) {
                 ns.pa |= (unsigned long long)t << sh;
-                ns.ma |= 255ull << sh;
+                ns.ma |= mk;
             } else if (which == 1) {
                 ns.pb |= (unsigned long long)t << sh;
-                ns.mb |= 255ull << sh;
+                ns.mb |= mk;
             } else {
                 ns.pi |= (unsigned)t << sh;
-                ns.mi |= 255u << sh;
+                ns.mi |= (unsigned)mk;
             }
             s_st = ns;
         }
@@ -362,50 +424,65 @@ struct SrcBeam {   // children eligible for the frontier: (f, -, w)
 // ---- next frontier (one CTA): layer totals, beam select, ordered compaction in creation order
 __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     __shared__ int s_warp[kSelThreads / 32];
-    __shared__ int s_base, s_tile, s_elig;
+    __shared__ int s_elig, s_n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) {
-        t.cnt[3] += t.cnt[0];
+        const int M = t.cnt[0];
+        s_n = M * k.P;                                  // this layer's children
+        t.cnt[3] += M;
         t.cnt[1] += t.rank[k.W - 1] + t.acc[k.W - 1];   // nodes created by this layer
-        s_base = 0;
         s_elig = 0;
     }
     __syncthreads();
+    const int n = s_n;
     int loc = 0;
-    for (int i = tid; i < k.W; i += blockDim.x) loc += t.fkey[i] != kEmptyKey;
-    atomicAdd(&s_elig, loc);
+    for (int i = tid; i < n; i += blockDim.x) loc += t.fkey[i] != kEmptyKey;
+    loc = __reduce_add_sync(0xffffffffu, loc);
+    if (lane == 0) atomicAdd(&s_elig, loc);
     __syncthreads();
     const bool all = s_elig <= k.beam;
     SelState st{0, 0, 0, 0, 0, 0};
-    if (!all) st = block_select(SrcBeam{t.fkey}, k.W, k.beam, false);
-    for (int c0 = 0; c0 < k.W; c0 += blockDim.x) {
-        const int i = c0 + tid;
-        bool s = false;
-        if (i < k.W) {
+    if (!all) st = block_select(SrcBeam{t.fkey}, n, k.beam, false);
+    // ordered compaction: warp w owns the contiguous children [c0, c1), read 32 at a time (coalesced)
+    const int nw = blockDim.x >> 5;
+    const int per = ((n + nw - 1) / nw + 31) & ~31;
+    const int c0 = min(n, wid * per), c1 = min(n, c0 + per);
+    int cnt = 0;
+    for (int b = c0; b < c1; b += 32) {
+        const int i = b + lane;
+        bool sel = false;
+        if (i < c1) {
             const unsigned long long f = t.fkey[i];
-            s = f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i));
+            sel = f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i));
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, s);
-        if (lane == 0) s_warp[wid] = __popc(bal);
-        __syncthreads();
-        if (tid < 32) {
-            const int v = s_warp[tid];
-            int inc = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, inc, o);
-                if (tid >= o) inc += u;
-            }
-            s_warp[tid] = inc - v;
-            if (tid == 31) s_tile = inc;
-        }
-        __syncthreads();
-        if (s) t.frontier[s_base + s_warp[wid] + __popc(bal & ((1u << lane) - 1u))] = t.cid[i];
-        __syncthreads();
-        if (tid == 0) s_base += s_tile;
-        __syncthreads();
+        cnt += __popc(__ballot_sync(0xffffffffu, sel));
     }
-    if (tid == 0) t.cnt[0] = s_base;
+    if (lane == 0) s_warp[wid] = cnt;
+    __syncthreads();
+    if (wid == 0) {
+        const int v = lane < nw ? s_warp[lane] : 0;
+        int w = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += u;
+        }
+        if (lane < nw) s_warp[lane] = w - v;
+        if (lane == 31) t.cnt[0] = w;                  // the next frontier's size
+    }
+    __syncthreads();
+    int pos = s_warp[wid];
+    for (int b = c0; b < c1; b += 32) {
+        const int i = b + lane;
+        bool sel = false;
+        if (i < c1) {
+            const unsigned long long f = t.fkey[i];
+            sel = f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i));
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, sel);
+        if (sel) t.frontier[pos + __popc(bal & ((1u << lane) - 1u))] = t.cid[i];
+        pos += __popc(bal);
+    }
 }
 
 // ---- final selection (one CTA): the n_traj cheapest candidates by (g, id), or, with no candidate,
