@@ -3,7 +3,8 @@ calling stream, warm-up first; one JSON line per measurement.
 
   N3  rtg_plan_tree, the Fig. 4 analogue: paper defaults (N_v = 3, N_w = 5, v_max = 0.6,
       w_max = 0.9, 1 s primitives), goal 5 m ahead, depth 8, beam 4096, 5 samples per
-      primitive, on outdoor-recipe maps of N = 1e5 .. 5e6 Gaussians (fixed 100 m x 100 m area).
+      primitive, on outdoor-recipe maps of N = 1e5 .. 5e6 Gaussians (fixed 100 m x 100 m area);
+      then the whole low-level cycle: 1024 tree candidates scored (rtg_score) and the argmax.
   N4  rtg_ledger_update + rtg_map_update_weights (ledger -> reclassified map, no repacking), N = 2M.
   N2  rtg_region_utility over a 2.5 m partition of the outdoor map, and 8,192 gain-only
       views (rtg_traj_view_ring around the top regions + rtg_score) + rtg_cost_benefit.
@@ -57,6 +58,20 @@ def main():
         print(json.dumps({"row": "N3 rtg_plan_tree", "N": n, "ms": ms, "reached": reached, "candidates": len(cost),
                           "best_cost": float(cost[0]) if len(cost) else None, **stats}), flush=True)
         tr.close()
+        # the whole low-level cycle of P:307-320: tree candidates -> scored at their segment end states
+        # (Eq. traj_utility, gain-only on the collision-free primitives) -> argmax
+        sp = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
+        tp_many = R.make_tree_params(max_depth=8, beam=4096, z=h0, n_traj=1024)
+
+        def cycle():
+            t2, c2, r2, _ = R.plan_tree(m, (0.0, 0.0, 0.0), (5.0, 0.0), tp_many)
+            out = R.score(m, t2, wl.camera, sp)
+            b = R.best(out[3])
+            t2.close()
+            return b
+        ms_c, b = timed(cycle, args.reps)
+        print(json.dumps({"row": "N3 plan cycle (tree -> 1024 candidates -> rtg_score -> rtg_best)", "N": n,
+                          "ms": ms_c, "best": list(b)}), flush=True)
         m.close()
     # ---- N4: ledger update and in-place reclassification, 2M
     wl = W.outdoor()
