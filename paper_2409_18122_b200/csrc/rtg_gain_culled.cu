@@ -224,10 +224,13 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         const int a1 = !in ? a3 : (j0 == q0 ? a0 : __ldg(sb + j0 * g.nz));
                         const int a2 = !in ? a3 : (j1 == q1 ? a3 : __ldg(sb + (j1 + 1) * g.nz));
                         if (in) {
-                            const TabP hi = gtabP[ub0 + (j1 + 1) * g.nz], lo = gtabP[ub0 + j0 * g.nz];
-                            acc += (unsigned long long)__double2ll_rn(hi.q - lo.q);
-                            acch += hi.nh - lo.nh;
-                            accl += hi.nl - lo.nl;
+                            // one 128-bit load per TabP entry {q (FP64 integer), nh, nl}
+                            const int4 hi = __ldg(reinterpret_cast<const int4*>(gtabP + ub0 + (j1 + 1) * g.nz));
+                            const int4 lo = __ldg(reinterpret_cast<const int4*>(gtabP + ub0 + j0 * g.nz));
+                            acc += (unsigned long long)__double2ll_rn(__hiloint2double(hi.y, hi.x) -
+                                                                      __hiloint2double(lo.y, lo.x));
+                            acch += hi.z - lo.z;
+                            accl += hi.w - lo.w;
                             if (kStats) nagg += 1;
                         }
                         s0 = g.offB + a0;
