@@ -64,11 +64,15 @@ __device__ __forceinline__ int region_of(const GRec& r, const RegionK& g) {
 }
 
 // pass 1: largest weight of a Gaussian inside the regions (non-negative floats order as ints)
+// (also records each Gaussian's region for pass 2: the FP64 divisions run once)
 __global__ void k_region_max(long long n, const GRec* __restrict__ rec, const int* __restrict__ gidx,
-                             const float* __restrict__ w, RegionK g, int* __restrict__ wmax_bits, int* __restrict__ cnt) {
+                             const float* __restrict__ w, RegionK g, int* __restrict__ wmax_bits, int* __restrict__ cnt,
+                             int* __restrict__ rid) {
     int mx = 0, c = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        if (region_of(rec[i], g) < 0) continue;
+        const int r = region_of(rec[i], g);
+        rid[i] = r;
+        if (r < 0) continue;
         mx = max(mx, __float_as_int(w[gidx[i]]));
         ++c;
     }
@@ -94,15 +98,37 @@ __global__ void k_region_scale(const int* __restrict__ wmax_bits, const int* __r
     sc[1] = ldexp(1.0, -s);
 }
 
-__global__ void k_region_acc(long long n, const GRec* __restrict__ rec, const int* __restrict__ gidx,
-                             const float* __restrict__ w, RegionK g, const double* __restrict__ sc,
+// pass 2: each thread walks kRegionRun consecutive records (copy A is sorted by visibility cell, so
+// neighbours mostly share a region) and issues one pair of atomics per run of equal regions
+constexpr int kRegionRun = 16;
+__global__ void k_region_acc(long long n, const int* __restrict__ rid, const int* __restrict__ gidx,
+                             const float* __restrict__ w, const double* __restrict__ sc,
                              unsigned long long* __restrict__ qsum, int* __restrict__ count) {
     const double scale = sc[0];
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const int r = region_of(rec[i], g);
-        if (r < 0) continue;
-        atomicAdd(&qsum[r], (unsigned long long)llrint((double)w[gidx[i]] * scale));
-        atomicAdd(&count[r], 1);
+    const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * kRegionRun;
+    if (i0 >= n) return;
+    const long long i1 = min(n, i0 + kRegionRun);
+    int cur = -1, c = 0;
+    unsigned long long q = 0;
+    for (long long i = i0; i < i1; ++i) {
+        const int r = rid[i];
+        if (r != cur) {
+            if (cur >= 0) {
+                atomicAdd(&qsum[cur], q);
+                atomicAdd(&count[cur], c);
+            }
+            cur = r;
+            q = 0;
+            c = 0;
+        }
+        if (r >= 0) {
+            q += (unsigned long long)llrint((double)w[gidx[i]] * scale);
+            ++c;
+        }
+    }
+    if (cur >= 0) {
+        atomicAdd(&qsum[cur], q);
+        atomicAdd(&count[cur], c);
     }
 }
 
@@ -201,21 +227,24 @@ cudaError_t launch_region_utility(rtg_map_s* m, const double origin[3], double s
     const long long nr = (long long)dims[0] * dims[1] * dims[2];
     char* scratch = nullptr;
     const size_t qb = sizeof(unsigned long long) * (size_t)nr;
-    cudaError_t e = dev_alloc((void**)&scratch, qb + 64, st);
+    const long long ng = m->n_gain;
+    cudaError_t e = dev_alloc((void**)&scratch, qb + 64 + sizeof(int) * (size_t)(ng > 0 ? ng : 1), st);
     if (e != cudaSuccess) return e;
     unsigned long long* qsum = (unsigned long long*)scratch;
     int* mx = (int*)(scratch + qb);
     int* cnt = mx + 1;
     double* sc = (double*)(scratch + qb + 16);
+    int* rid = (int*)(scratch + qb + 64);
     e = cudaMemsetAsync(scratch, 0, qb + 64, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(count, 0, sizeof(int) * (size_t)nr, st);
     if (e != cudaSuccess) return e;
     const long long n = m->n_gain;   // copy A: the gain-eligible Gaussians (ground plane excluded)
     const unsigned nb = nblk(n, 256) > 2048 ? 2048 : nblk(n, 256);
     if (n > 0) {
-        note_launch(), k_region_max<<<nb, 256, 0, st>>>(n, m->grec, m->gidx, m->w_orig, g, mx, cnt);
+        note_launch(), k_region_max<<<nb, 256, 0, st>>>(n, m->grec, m->gidx, m->w_orig, g, mx, cnt, rid);
         note_launch(), k_region_scale<<<1, 1, 0, st>>>(mx, cnt, sc);
-        note_launch(), k_region_acc<<<nb, 256, 0, st>>>(n, m->grec, m->gidx, m->w_orig, g, sc, qsum, count);
+        note_launch(), k_region_acc<<<nblk((n + kRegionRun - 1) / kRegionRun, 256), 256, 0, st>>>(
+                           n, rid, m->gidx, m->w_orig, sc, qsum, count);
     } else {
         note_launch(), k_region_scale<<<1, 1, 0, st>>>(mx, cnt, sc);
     }
