@@ -175,7 +175,9 @@ rtg_status rtg_map_info(rtg_map map, rtg_map_info_t* out);
 /*
  * rtg_traj_upload -- candidate trajectories.  K >= 1, T >= 1,
  * K*T < 2^31; x, y, z, yaw each [K][T] (trajectory-major), waypoint t of trajectory k at
- * index k*T + t.  Copies into a handle-owned device SoA.
+ * index k*T + t.  Copies into a handle-owned device SoA.  Non-finite values are padding
+ * (R8): such a waypoint sees nothing, and with a non-finite position it collides with
+ * nothing.
  */
 rtg_status rtg_traj_upload(int device, int K, int T, rtg_mem kind,
                            const float* x, const float* y, const float* z, const float* yaw,

@@ -101,13 +101,14 @@ void orc_visibility_slacks(const double mu[3], const double pose[4], const doubl
     scale[4] = scale[5] = fy * fabs(Y) + my * aZ;
 }
 
-/* visibility decision: returns nominal (all sigma >= 0); *amb = band case. */
+/* visibility decision: returns nominal (all sigma >= 0); *amb = band case.  A non-finite pose
+ * (trajectory padding) gives NaN slacks and sees nothing (reading R8). */
 static int orc_visible(const double mu[3], const double pose[4], const double cam[8], int* amb) {
     double sg[6], sc[6];
     orc_visibility_slacks(mu, pose, cam, sg, sc);
     int nominal = 1, definitely_out = 0, near = 0;
     for (int j = 0; j < 6; ++j) {
-        if (sg[j] < 0.0) nominal = 0;
+        if (!(sg[j] >= 0.0)) nominal = 0;
         if (sg[j] < -ORC_BAND * sc[j]) definitely_out = 1;
         if (fabs(sg[j]) <= ORC_BAND * sc[j]) near = 1;
     }

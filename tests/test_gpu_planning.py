@@ -178,11 +178,13 @@ def _oracle_collides(wl):
     return f
 
 
-# the last two: a coarse lattice (many children of a layer share a cell: the in-layer prefix-minimum
-# rule) with many candidates ranked, and an unreachable goal with many closest-node results
+# then: a coarse lattice (many children of a layer share a cell: the in-layer prefix-minimum rule) with
+# many candidates ranked; an unreachable goal with many closest-node results; a beam of one; a fine
+# lattice with more candidates requested than nodes exist
 @pytest.mark.parametrize("goal,depth,beam,lattice,ldeg,n_traj", [
     ((4.0, 2.0), 6, 128, 0.1, 10.0, 10), ((-3.0, 3.5), 7, 96, 0.1, 10.0, 10), ((2.5, -1.0), 4, 4000, 0.0, 10.0, 10),
-    ((40.0, 0.0), 3, 64, 0.1, 10.0, 10), ((2.0, 1.0), 6, 80, 0.7, 45.0, 300), ((-30.0, 5.0), 5, 200, 0.3, 30.0, 700)])
+    ((40.0, 0.0), 3, 64, 0.1, 10.0, 10), ((2.0, 1.0), 6, 80, 0.7, 45.0, 300), ((-30.0, 5.0), 5, 200, 0.3, 30.0, 700),
+    ((1.5, 0.5), 5, 1, 0.1, 10.0, 50), ((-20.0, -20.0), 3, 16, 0.05, 2.0, 5000)])
 def test_plan_tree_matches_oracle(R, goal, depth, beam, lattice, ldeg, n_traj):
     wl = W.room(N=20000, K=1, T=1)
     start = (0.0, 0.0, 0.3)
@@ -199,15 +201,19 @@ def test_plan_tree_matches_oracle(R, goal, depth, beam, lattice, ldeg, n_traj):
     for a, b in ((x, ox), (y, oy), (yaw, oyaw)):
         assert np.all(np.abs(a[ok] - b[ok]) <= 1e-5)
     assert np.all(z[ok] == np.float32(0.5))
-    # the candidates are then scored on their segment end states (Eq. traj_utility) and the best taken
+    # the candidates are then scored on their segment end states (Eq. traj_utility) and the best taken.
+    # Both sides score the oracle's candidates (the tree's own states agree only to fp32 rounding, which
+    # can flip a frustum decision): the scoring is checked on identical inputs
+    oz = np.where(ok, np.float32(0.5), np.float32(np.nan)).astype(np.float32)
     p = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
-    fc, fe, g, u = R.score(m, tr, wl.camera, p)
-    orc = O.score(wl, x=ox, y=oy, z=np.where(ok, np.float32(0.5), np.float32(np.nan)).astype(np.float32), yaw=oyaw,
-                  no_collision=True)
+    to = R.traj_from_workload(wl, x=ox, y=oy, z=oz, yaw=oyaw)
+    fc, fe, g, u = R.score(m, to, wl.camera, p)
+    orc = O.score(wl, x=ox, y=oy, z=oz, yaw=oyaw, no_collision=True)
     b = R.best(u)[1]
     assert b in set(int(v) for v in orc["acceptable"])
     m.close()
     tr.close()
+    to.close()
 
 
 def test_plan_tree_trapped(R):

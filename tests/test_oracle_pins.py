@@ -310,6 +310,21 @@ def test_no_gain_flag_and_beyond_far_contribute_zero():
     assert r["gain"][0] == 0.0 and r["nh"][0] == 0
 
 
+def test_non_finite_waypoint_sees_and_hits_nothing():
+    """Reading R8: a waypoint with a non-finite coordinate (trajectory padding, e.g. rtg_plan_tree's NaN
+    after a candidate's last primitive) sees nothing -- not a NaN-propagated "every slack passes" -- and,
+    when its position is non-finite, collides with nothing (the collision test reads the position only)."""
+    w = [0.9, 0.1, 0.5]
+    m, q, s = _front_map(w, dist=0.2)          # within the robot radius of the origin: collides when finite
+    r, _ = _wp(m, q, s, w, pose=(0.0, 0.0, 0.0, 0.0))
+    assert r["col"][0] == 1
+    for pose in ((np.nan, 0.0, 0.0, 0.0), (0.0, np.nan, 0.0, 0.0), (0.0, 0.0, np.nan, 0.0), (np.inf, 0.0, 0.0, 0.0),
+                 (0.0, 0.0, 0.0, np.nan)):
+        r, _ = _wp(m, q, s, w, pose=pose)
+        assert r["gain"][0] == 0.0 and r["nh"][0] == 0 and r["nl"][0] == 0, pose
+        assert r["col"][0] == (1 if np.isfinite(pose[:3]).all() else 0), pose
+
+
 # ----------------------------------------------------------------- trajectories (O6/O7)
 
 def test_brute_force_pipeline_by_hand():
