@@ -455,6 +455,9 @@ def test_fuzz_random_maps_cameras_grids(R, seed):
     pz = lo[2] + ext[2] * rng.uniform(-0.2, 1.2, (K, T))
     yaw = rng.uniform(-np.pi, np.pi, (K, T))
     yaw[0] = np.array([0, np.pi / 2, np.pi, -np.pi / 2, np.pi / 4, 0, np.pi])
+    px[1, 2] = np.nan     # padding (reading R8): sees nothing, collides with nothing
+    yaw[2, 3] = np.nan    # non-finite heading only: sees nothing, still collides by position
+    pz[3, 4] = np.inf
     wl = W.Workload("fuzz", means, quats, scales, rng.random(n).astype(np.float32), w, flags,
                     px.astype(np.float32), py.astype(np.float32), pz.astype(np.float32), yaw.astype(np.float32),
                     W.Robot(float(rng.uniform(0, 0.5)), float(rng.uniform(1, 3))), cam, 0.1)
