@@ -164,6 +164,8 @@ def test_dense_equals_culled_bitwise(R, room):
     (0, 1, 0.5, None, 0),        # lambda_xi != 1
     (0, 1, 1.0, (0.7, 0.3), 0),  # caller thresholds
     (0, 1, 1.0, None, 1),        # principal-axis collision rule
+    (0, 7, 1.0, None, 0),        # a stride that does not divide T = 50
+    (0, 60, 1.0, None, 0),       # a stride beyond T: no info waypoint, utility 0 when feasible
 ])
 def test_room_variants(R, room, variant, stride, lam, tau, rule):
     import dataclasses
@@ -200,7 +202,7 @@ def test_outdoor_full_size_sampled(R):
     feas = np.nonzero(gpu["feasible"])[0]
     infeas = np.nonzero(gpu["feasible"] == 0)[0]
     assert len(feas) > 1000 and len(infeas) > 1000
-    idx = np.sort(np.concatenate([rng.choice(feas, 2, replace=False), rng.choice(infeas, 2, replace=False)]))
+    idx = np.sort(np.concatenate([rng.choice(feas, 6, replace=False), rng.choice(infeas, 6, replace=False)]))
     orc = O.score(wl, traj_idx=idx)
     sub = {k: gpu[k][idx] for k in ("first_col", "feasible", "gain", "utility")}
     sub["best"] = (None, -2)
