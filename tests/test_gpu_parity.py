@@ -332,6 +332,25 @@ def test_unicycle_sampler_matches_oracle(R):
     tr.close()
 
 
+def test_unicycle_sampler_edge_controls(R):
+    """omega exactly 0, below and above the straight-line switch (|w| < 1e-12), v = 0, large |omega|,
+    headings near the +-pi wrap, a start far from the origin and a long horizon."""
+    start = np.array([1234.5, -987.25, 0.5, 3.1], np.float32)
+    v = np.array([1.0, 1.0, 1.0, 0.0, 2.0, 0.7, 1.5], np.float32)
+    w = np.array([0.0, 1e-13, 1e-11, 0.9, -3.0, 2.5, -1e-7], np.float32)
+    T, dt = 300, 0.1
+    tr = R.Traj.sample_unicycle(torch.from_numpy(v).cuda(), torch.from_numpy(w).cuda(), T, dt, start)
+    X, Y, Z, YW = (a.cpu().numpy() for a in tr.read())
+    for k in range(len(v)):
+        ox, oy, oz, oyaw = O.unicycle(start, v[k], w[k], np.float32(dt), T)   # the ABI's dt is fp32
+        assert np.all(np.abs(X[k] - ox) <= 2 * np.spacing(np.float32(np.abs(ox) + 1))), k
+        assert np.all(np.abs(Y[k] - oy) <= 2 * np.spacing(np.float32(np.abs(oy) + 1))), k
+        assert np.all(Z[k] == np.float32(oz))
+        assert np.all(np.abs(np.angle(np.exp(1j * (YW[k] - oyaw)))) < 1e-6), k
+        assert np.all((YW[k] > -np.pi) & (YW[k] <= np.float32(np.pi))), k
+    tr.close()
+
+
 def test_best_ties_and_index_base(R):
     u = torch.tensor([1.0, 5.0, 5.0, -math.inf, 2.0], dtype=torch.float64, device="cuda")
     assert R.best(u) == (5.0, 1)
