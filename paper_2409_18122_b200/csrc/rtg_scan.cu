@@ -9,8 +9,12 @@ namespace rtg {
 namespace {
 
 constexpr int kScanThreads = 512;
-constexpr int kScanPer = 8;
-constexpr int kScanTile = kScanThreads * kScanPer;   // elements per tile
+// elements per thread: 8 ints / 4 pairs, so the shared-memory stage (below) fits the static limit
+template <typename T> struct ScanPer { static constexpr int v = sizeof(T) <= 4 ? 8 : 4; };
+template <typename T> constexpr int scan_tile() { return kScanThreads * ScanPer<T>::v; }
+// stage index with one pad word per 32: thread t's contiguous elements and the striped (coalesced)
+// order both hit distinct banks
+__device__ __forceinline__ int stage_ix(int q) { return q + (q >> 5); }
 
 // a pair of 64-bit sums (u_q prefix, packed class counts) scanned together
 struct I64x2 {
@@ -85,19 +89,28 @@ struct LoadUc {
 template <typename T, typename Load>
 __global__ void __launch_bounds__(kScanThreads) k_scan(Load in, T* __restrict__ out, long long n,
                                                         int* __restrict__ ticket, volatile int* flag, T* agg, T* inc) {
+    constexpr int PER = ScanPer<T>::v, TILE = scan_tile<T>();
     __shared__ T sh[kScanThreads / 32];
     __shared__ T s_prefix;
     __shared__ int s_tile;
+    __shared__ T stage[TILE + TILE / 32];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
     const int tile = s_tile;
-    const long long base = (long long)tile * kScanTile + (long long)threadIdx.x * kScanPer;
-    T loc[kScanPer];
+    const long long tbase = (long long)tile * TILE;
+    // coalesced load of the tile into shared memory, then each thread takes PER consecutive elements
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int q = i * kScanThreads + threadIdx.x;
+        const long long j = tbase + q;
+        stage[stage_ix(q)] = j < n ? in(j) : T(0);
+    }
+    __syncthreads();
+    T loc[PER];
     T s = T(0);
 #pragma unroll
-    for (int i = 0; i < kScanPer; ++i) {
-        const long long j = base + i;
-        loc[i] = j < n ? in(j) : T(0);
+    for (int i = 0; i < PER; ++i) {
+        loc[i] = stage[stage_ix(threadIdx.x * PER + i)];
         s += loc[i];
     }
     T total;
@@ -148,16 +161,105 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Load in, T* __restrict__ 
     __syncthreads();
     pre += s_prefix;
 #pragma unroll
-    for (int i = 0; i < kScanPer; ++i) {
-        const long long j = base + i;
-        if (j < n) out[j] = pre;
+    for (int i = 0; i < PER; ++i) {
+        stage[stage_ix(threadIdx.x * PER + i)] = pre;
         pre += loc[i];
-        if (j == n - 1) out[n] = pre;   // total
+        if (tbase + threadIdx.x * PER + i == n - 1) out[n] = pre;   // total
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {   // coalesced store
+        const int q = i * kScanThreads + threadIdx.x;
+        const long long j = tbase + q;
+        if (j < n) out[j] = stage[stage_ix(q)];
     }
 }
 
 template <typename T>
 __global__ void k_scan_empty(T* out) { out[0] = T(0); }
+
+// ---- large inputs: reduce-then-scan (no serial look-back chain over thousands of tiles)
+// pass 1: per-tile sums (coalesced, striped)
+template <typename T, typename Load>
+__global__ void __launch_bounds__(kScanThreads) k_tile_sums(Load in, long long n, T* __restrict__ sums) {
+    constexpr int PER = ScanPer<T>::v, TILE = scan_tile<T>();
+    __shared__ T sh[kScanThreads / 32];
+    const long long tbase = (long long)blockIdx.x * TILE;
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const long long j = tbase + i * kScanThreads + threadIdx.x;
+        if (j < n) s += in(j);
+    }
+    T total;
+    block_exclusive_scan<T>(s, sh, total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// pass 2: exclusive scan of the tile sums in one block (sums[nt] = grand total)
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(T* __restrict__ sums, int nt) {
+    __shared__ T sh[kScanThreads / 32];
+    __shared__ T s_carry;
+    if (threadIdx.x == 0) s_carry = T(0);
+    __syncthreads();
+    for (int b = 0; b < nt; b += kScanThreads) {
+        const int i = b + threadIdx.x;
+        const T v = i < nt ? sums[i] : T(0);
+        T total;
+        const T ex = block_exclusive_scan<T>(v, sh, total);
+        const T carry = s_carry;
+        if (i < nt) sums[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[nt] = s_carry;
+}
+
+// pass 3: each tile rescans its elements (staged, coalesced) from its offset
+template <typename T, typename Load>
+__global__ void __launch_bounds__(kScanThreads) k_tile_apply(Load in, T* __restrict__ out, long long n,
+                                                             const T* __restrict__ sums, int nt) {
+    constexpr int PER = ScanPer<T>::v, TILE = scan_tile<T>();
+    __shared__ T sh[kScanThreads / 32];
+    __shared__ T stage[TILE + TILE / 32];
+    const long long tbase = (long long)blockIdx.x * TILE;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int q = i * kScanThreads + threadIdx.x;
+        const long long j = tbase + q;
+        stage[stage_ix(q)] = j < n ? in(j) : T(0);
+    }
+    __syncthreads();
+    T loc[PER];
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        loc[i] = stage[stage_ix(threadIdx.x * PER + i)];
+        s += loc[i];
+    }
+    T total;
+    T pre = block_exclusive_scan<T>(s, sh, total) + sums[blockIdx.x];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        stage[stage_ix(threadIdx.x * PER + i)] = pre;
+        pre += loc[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int q = i * kScanThreads + threadIdx.x;
+        const long long j = tbase + q;
+        if (j < n) out[j] = stage[stage_ix(q)];
+    }
+    if (blockIdx.x == nt - 1 && threadIdx.x == 0) out[n] = sums[nt];   // total
+}
+
+// up to this many tiles the single-pass look-back scan (one launch); beyond, reduce-then-scan (the
+// look-back chain over thousands of concurrently running tiles costs more than two extra launches)
+constexpr long long kChainTiles = 64;
 
 template <typename T, typename Load>
 cudaError_t scan_impl(Load in, T* out, long long n, cudaStream_t st) {
@@ -165,8 +267,19 @@ cudaError_t scan_impl(Load in, T* out, long long n, cudaStream_t st) {
         note_launch(), k_scan_empty<T><<<1, 1, 0, st>>>(out);
         return cudaGetLastError();
     }
-    const long long nt = (n + kScanTile - 1) / kScanTile;
+    const long long nt = (n + scan_tile<T>() - 1) / scan_tile<T>();
     if (nt >= (1LL << 31)) return cudaErrorInvalidValue;
+    if (nt > kChainTiles) {
+        T* sums = nullptr;
+        cudaError_t e = dev_alloc((void**)&sums, sizeof(T) * (size_t)(nt + 1), st);
+        if (e != cudaSuccess) return e;
+        note_launch(), k_tile_sums<T, Load><<<(unsigned)nt, kScanThreads, 0, st>>>(in, n, sums);
+        note_launch(), k_scan_sums<T><<<1, kScanThreads, 0, st>>>(sums, (int)nt);
+        note_launch(), k_tile_apply<T, Load><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, sums, (int)nt);
+        e = cudaGetLastError();
+        dev_free(sums, st);
+        return e;
+    }
     // scratch: ticket + flags (zeroed), aggregates, inclusive prefixes
     const size_t fb = sizeof(int) * (size_t)(nt + 1), vb = sizeof(T) * (size_t)nt;
     char* mem = nullptr;

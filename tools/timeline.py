@@ -1,0 +1,70 @@
+"""GPU timeline of one outdoor planning cycle (torch.profiler / CUPTI kernel activity): every kernel
+and memcpy/memset with its start offset and duration, and the idle gaps between them.
+
+usage: python tools/timeline.py [--config outdoor] [--top 40]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2409_18122_b200 import rtg as R  # noqa: E402
+from paper_2409_18122_b200 import workloads as W  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="outdoor")
+    ap.add_argument("--top", type=int, default=40)
+    args = ap.parse_args()
+    wl = W.make(args.config)
+    dev = torch.device("cuda", 0)
+    to_dev = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    dmap = [to_dev(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)]
+    dtraj = [to_dev(a) for a in (wl.x, wl.y, wl.z, wl.yaw)]
+    cam = R.make_camera(wl.camera)
+    params = R.make_params(mode=R.MODE_CULLED)
+    K = wl.K
+    outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
+            torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
+
+    def step():
+        m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
+        tr = R.Traj.upload(*dtraj)
+        R.score(m, tr, cam, params, *outs)
+        r = R.best(outs[3])
+        m.close()
+        tr.close()
+        return r
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    from torch.profiler import profile, ProfilerActivity
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(3):            # the last of three profiled cycles is reported (the first pays
+            torch.cuda.synchronize()  # the profiler's own start-up)
+            step()
+            torch.cuda.synchronize()
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    ev.sort(key=lambda e: e.time_range.start)
+    starts = [i for i, e in enumerate(ev) if "k_bounds_init" in e.name]
+    ev = ev[starts[-1]:]
+    t0 = ev[0].time_range.start
+    prev_end = t0
+    gaps = 0.0
+    print(f"{'start_us':>9} {'dur_us':>8} {'gap_us':>7}  name")
+    for e in ev:
+        s, d = e.time_range.start, e.time_range.end - e.time_range.start
+        gap = max(0.0, s - prev_end)
+        gaps += gap
+        print(f"{s - t0:9.1f} {d:8.1f} {gap:7.1f}  {e.name[:90]}")
+        prev_end = max(prev_end, e.time_range.end)
+    print(f"total {prev_end - t0:.1f} us, idle gaps {gaps:.1f} us")
+
+
+if __name__ == "__main__":
+    main()
