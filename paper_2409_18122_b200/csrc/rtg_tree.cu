@@ -32,6 +32,7 @@ namespace {
 
 constexpr unsigned long long kEmptyKey = ~0ull;
 constexpr int kSelThreads = 1024;
+constexpr int kMaxBeamWords = 4096;   // selection bits of up to 131,072 children per layer (k_beam)
 
 // unicycle closed form from (x0, y0, th0) under (v, w) for time t, FP64 without
 // contraction so the host oracle's rounding is reproduced
@@ -436,26 +437,47 @@ __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     __syncthreads();
     const int n = s_n;
     int loc = 0;
-    for (int i = tid; i < n; i += blockDim.x) loc += t.fkey[i] != kEmptyKey;
+    for (int i0 = tid; i0 < n; i0 += 8 * blockDim.x) {   // eight loads in flight per thread
+        unsigned long long f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            f[u] = i < n ? t.fkey[i] : kEmptyKey;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) loc += f[u] != kEmptyKey;
+    }
     loc = __reduce_add_sync(0xffffffffu, loc);
     if (lane == 0) atomicAdd(&s_elig, loc);
     __syncthreads();
     const bool all = s_elig <= k.beam;
     SelState st{0, 0, 0, 0, 0, 0};
     if (!all) st = block_select(SrcBeam{t.fkey}, n, k.beam, false);
-    // ordered compaction: warp w owns the contiguous children [c0, c1), read 32 at a time (coalesced)
+    // ordered compaction: warp w owns the contiguous children [c0, c1), 32 per ballot word; pass 1
+    // keeps the selection bits in shared memory, pass 2 writes the selected node ids in order
+    __shared__ unsigned s_bits[kMaxBeamWords];
+    const bool use_bits = n <= 32 * kMaxBeamWords;
     const int nw = blockDim.x >> 5;
     const int per = ((n + nw - 1) / nw + 31) & ~31;
     const int c0 = min(n, wid * per), c1 = min(n, c0 + per);
     int cnt = 0;
-    for (int b = c0; b < c1; b += 32) {
-        const int i = b + lane;
-        bool sel = false;
-        if (i < c1) {
-            const unsigned long long f = t.fkey[i];
-            sel = f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i));
+    for (int b0 = c0; b0 < c1; b0 += 4 * 32) {
+        unsigned long long f[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = b0 + 32 * u + lane;
+            f[u] = i < c1 ? t.fkey[i] : kEmptyKey;
         }
-        cnt += __popc(__ballot_sync(0xffffffffu, sel));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int b = b0 + 32 * u;
+            const bool sel = f[u] != kEmptyKey && (all || selected(st, f[u], 0, (unsigned)(b + lane)));
+            const unsigned bal = __ballot_sync(0xffffffffu, sel);
+            if (b < c1) {
+                if (lane == 0 && use_bits) s_bits[b >> 5] = bal;
+                cnt += __popc(bal);
+            }
+        }
     }
     if (lane == 0) s_warp[wid] = cnt;
     __syncthreads();
@@ -473,14 +495,15 @@ __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     __syncthreads();
     int pos = s_warp[wid];
     for (int b = c0; b < c1; b += 32) {
-        const int i = b + lane;
-        bool sel = false;
-        if (i < c1) {
-            const unsigned long long f = t.fkey[i];
-            sel = f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i));
+        unsigned bal;
+        if (use_bits) {
+            bal = s_bits[b >> 5];
+        } else {   // more children than the bit buffer holds: evaluate the selection again
+            const int i = b + lane;
+            const unsigned long long f = i < c1 ? t.fkey[i] : kEmptyKey;
+            bal = __ballot_sync(0xffffffffu, f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i)));
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, sel);
-        if (sel) t.frontier[pos + __popc(bal & ((1u << lane) - 1u))] = t.cid[i];
+        if ((bal >> lane) & 1u) t.frontier[pos + __popc(bal & ((1u << lane) - 1u))] = t.cid[b + lane];
         pos += __popc(bal);
     }
 }

@@ -1,7 +1,8 @@
 """GPU timeline of one outdoor planning cycle (torch.profiler / CUPTI kernel activity): every kernel
 and memcpy/memset with its start offset and duration, and the idle gaps between them.
 
-usage: python tools/timeline.py [--config outdoor] [--top 40]
+usage: python tools/timeline.py [--config outdoor] [--tree]
+  --tree: one rtg_plan_tree call (depth 8, beam 4096, goal 5 m ahead) on the config's map instead
 """
 import argparse
 import os
@@ -18,7 +19,7 @@ from paper_2409_18122_b200 import workloads as W  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="outdoor")
-    ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--tree", action="store_true")
     args = ap.parse_args()
     wl = W.make(args.config)
     dev = torch.device("cuda", 0)
@@ -31,7 +32,17 @@ def main():
     outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
             torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
 
+    tree_map = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule) \
+        if args.tree else None
+    tp = R.make_tree_params(max_depth=8, beam=4096, z=float(wl.z.reshape(-1)[0]))
+
+    def tree_step():
+        t2, _, _, _ = R.plan_tree(tree_map, (0.0, 0.0, 0.0), (5.0, 0.0), tp)
+        t2.close()
+
     def step():
+        if args.tree:
+            return tree_step()
         m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
         tr = R.Traj.upload(*dtraj)
         R.score(m, tr, cam, params, *outs)
@@ -51,7 +62,8 @@ def main():
             torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     ev.sort(key=lambda e: e.time_range.start)
-    starts = [i for i, e in enumerate(ev) if "k_bounds_init" in e.name]
+    first = "k_tree_init" if args.tree else "k_bounds_init"
+    starts = [i for i, e in enumerate(ev) if first in e.name]
     ev = ev[starts[-1]:]
     t0 = ev[0].time_range.start
     prev_end = t0
