@@ -184,15 +184,27 @@ __global__ void __launch_bounds__(256) k_expand(Tree t, TreeK k, const double* _
     unsigned long long ntest = 0;
     bool hit = false;
     int checked = 0;
+    // the samples' states 32 at a time in parallel (lane l computes sample j0 + l: FP64 sin/cos once
+    // per sample), then the warp tests them in order with the early exit; the last sample is the child
     double x = x0, y = y0, th = th0;
-    for (int j = 1; j < k.S; ++j) {
-        const double tt = __ddiv_rn(__dmul_rn((double)j, k.dt), (double)(k.S - 1));
-        unicycle_at(x0, y0, th0, v, om, tt, x, y, th);
-        if (!hit && n_col > 0) {
-            hit = warp_point_collides(__double2float_rn(x), __double2float_rn(y), k.z, crec, cmat, csrc, rb, cstart,
-                                      g, gq, nref, ntest);
-            ++checked;
+    for (int j0 = 1; j0 < k.S; j0 += 32) {
+        double lx = x0, ly = y0, lth = th0;
+        if (j0 + lane < k.S) {
+            const double tt = __ddiv_rn(__dmul_rn((double)(j0 + lane), k.dt), (double)(k.S - 1));
+            unicycle_at(x0, y0, th0, v, om, tt, lx, ly, lth);
         }
+        const float sx = __double2float_rn(lx), sy = __double2float_rn(ly);
+        const int nj = min(32, k.S - j0);
+        for (int jj = 0; jj < nj; ++jj) {
+            const float px = __shfl_sync(0xffffffffu, sx, jj), py = __shfl_sync(0xffffffffu, sy, jj);
+            if (!hit && n_col > 0) {
+                hit = warp_point_collides(px, py, k.z, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
+                ++checked;
+            }
+        }
+        x = __shfl_sync(0xffffffffu, lx, nj - 1);
+        y = __shfl_sync(0xffffffffu, ly, nj - 1);
+        th = __shfl_sync(0xffffffffu, lth, nj - 1);
     }
     if (lane == 0) {
         t.cok[w] = hit ? 0 : 1;
