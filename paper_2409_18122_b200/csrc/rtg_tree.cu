@@ -72,6 +72,7 @@ struct TreeK {
 // device state of one plan
 struct Tree {
     double *nx, *ny, *nth, *ng;     // nodes (creation order), capacity NC
+    double* nh;                     // their heuristic h (for the no-candidate ranking)
     int *npar, *ndep;
     int* frontier;                  // node ids, creation order, <= beam
     double *cx, *cy, *cth, *cg;     // children of the layer, index w = m * P + p
@@ -147,6 +148,7 @@ __device__ __forceinline__ unsigned long long dbits(double v) {   // order-prese
 // ---- root: node 0, its lattice cell, the first frontier (or the root is already a candidate)
 __global__ void k_tree_init(Tree t, TreeK k, double x, double y, double th) {
     t.nx[0] = x; t.ny[0] = y; t.nth[0] = th; t.ng[0] = 0.0;
+    t.nh[0] = h_of(k, x, y);
     t.npar[0] = -1; t.ndep[0] = 0;
     t.cnt[1] = 1;
     if (k.dedup) closed_put(t, k, lattice_key(k, x, y, th, t.cnt + 4), 0.0);
@@ -284,8 +286,10 @@ __global__ void k_create(Tree t, TreeK k, int depth) {
         t.npar[id] = t.frontier[w / k.P];
         t.ndep[id] = depth;
         t.cid[w] = id;
+        const double h = h_of(k, x, y);
+        t.nh[id] = h;
         if (at_goal(k, x, y)) t.cand[atomicAdd(&t.cnt[2], 1)] = id;
-        else fk = dbits(__dadd_rn(g, h_of(k, x, y)));
+        else fk = dbits(__dadd_rn(g, h));
     }
     t.fkey[w] = fk;
 }
@@ -534,10 +538,9 @@ struct SrcCand {
     }
 };
 struct SrcNodes {
-    const double *nx, *ny, *ng;
-    TreeK k;
+    const double *nh, *ng;
     __device__ bool get(int i, unsigned long long& a, unsigned long long& b, unsigned& id) const {
-        a = dbits(h_of(k, nx[i + 1], ny[i + 1]));
+        a = dbits(nh[i + 1]);
         b = dbits(ng[i + 1]);
         id = (unsigned)(i + 1);
         return true;
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kSelThreads) k_final(Tree t, TreeK k, int n_tr
     const int nc = t.cnt[2];
     if (threadIdx.x == 0) t.cnt[6] = nc > 0;
     if (nc > 0) select_into(t, SrcCand{t.cand, t.ng}, nc, n_traj, false);
-    else select_into(t, SrcNodes{t.nx, t.ny, t.ng, k}, t.cnt[1] - 1, n_traj, true);
+    else select_into(t, SrcNodes{t.nh, t.ng}, t.cnt[1] - 1, n_traj, true);
 }
 
 // rank of each selected item by (a, b, id) -> order
@@ -687,7 +690,7 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
         off += (bytes + 255) & ~(size_t)255;
         return o;
     };
-    const size_t o_n = carve(sizeof(double) * 4 * nc), o_pd = carve(sizeof(int) * 2 * nc);
+    const size_t o_n = carve(sizeof(double) * 5 * nc), o_pd = carve(sizeof(int) * 2 * nc);
     const size_t o_fr = carve(sizeof(int) * (size_t)k.beam), o_c = carve(sizeof(double) * 4 * W);
     const size_t o_ok = carve(W), o_key = carve(sizeof(unsigned long long) * W), o_i = carve(sizeof(int) * 5 * W);
     const size_t o_f = carve(sizeof(unsigned long long) * W);
@@ -704,7 +707,7 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
         return e == cudaErrorMemoryAllocation ? RTG_ERR_OUT_OF_MEMORY : RTG_ERR_CUDA;
     }
     Tree t;
-    t.nx = (double*)(mem + o_n); t.ny = t.nx + nc; t.nth = t.ny + nc; t.ng = t.nth + nc;
+    t.nx = (double*)(mem + o_n); t.ny = t.nx + nc; t.nth = t.ny + nc; t.ng = t.nth + nc; t.nh = t.ng + nc;
     t.npar = (int*)(mem + o_pd); t.ndep = t.npar + nc;
     t.frontier = (int*)(mem + o_fr);
     t.cx = (double*)(mem + o_c); t.cy = t.cx + W; t.cth = t.cy + W; t.cg = t.cth + W;
