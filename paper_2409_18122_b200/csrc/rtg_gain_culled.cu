@@ -36,6 +36,7 @@ constexpr unsigned kFullG = 0xffffffffu;
 constexpr int kWarpsG = 4;     // warps per CTA; RTG_GAIN_MINB CTAs per SM: 36 warps at 56 registers
 constexpr int kQCap = 256;    // queued runs per warp
 constexpr int kQFlush = 192;  // test the queue once more runs than this are waiting (an append adds <= 64)
+constexpr int kMaxUnits = 1024;   // units of a row chunk with a shared-memory owner table (else: search)
 
 // RTG_BOUNDS_CHECK builds trap on any out-of-range table or record index (debug builds; the
 // sanitizer is not available on the GPU pool)
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
         // queued test runs: [0] first record -> (first record - items before the run), [1] length ->
         // items before the run.  64 entries of padding hold INT_MAX while the queue is tested.
         int q[2][kQCap + 64];
+        unsigned char owner[kMaxUnits];      // row (lane) of each unit of the current chunk
     };
     __shared__ WarpSmem s_w[kWarpsG];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -194,10 +196,14 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     // ---- unit window: (row, z-cell) units ub .. ub + 31 of the current chunk
                     const int pos = ub + lane;
                     int owner = 0;   // first lane whose inclusive prefix exceeds pos
+                    if (U <= kMaxUnits) {
+                        owner = pos < U ? sw.owner[pos] : 31;
+                    } else {
 #pragma unroll
-                    for (int st = 16; st > 0; st >>= 1) {
-                        const int v = __shfl_sync(kFullG, incl, owner + st - 1);
-                        if (v <= pos) owner += st;
+                        for (int st = 16; st > 0; st >>= 1) {
+                            const int v = __shfl_sync(kFullG, incl, owner + st - 1);
+                            if (v <= pos) owner += st;
+                        }
                     }
                     const int iz = pos + __shfl_sync(kFullG, zoff, owner);
                     const int ui0 = __shfl_sync(kFullG, ri0, owner), ui1 = __shfl_sync(kFullG, ri1, owner);
@@ -301,6 +307,10 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     U = __shfl_sync(kFullG, incl, 31);
                     zoff = izlo - (incl - nu);
                     ub = 0;
+                    if (U <= kMaxUnits) {
+                        for (int u = incl - nu; u < incl; ++u) sw.owner[u] = (unsigned char)lane;
+                        __syncwarp();
+                    }
                 } else {
                     done = true;
                 }
