@@ -288,10 +288,18 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             int olo = INT_MAX, ohi = -1;
                             const int2* zo = zocc + iy * g.nxb;
                             RTG_CHECK(ri1 / kZoccX < g.nxb, "z-occupancy block");
-                            for (int b = ri0 / kZoccX; b <= ri1 / kZoccX; ++b) {
-                                const int2 o = __ldg(zo + b);
-                                olo = min(olo, o.x);
-                                ohi = max(ohi, o.y);
+                            // four blocks per step: the loads are issued before any is used
+                            const int bend = ri1 / kZoccX;
+                            for (int b = ri0 / kZoccX; b <= bend; b += 4) {
+                                int2 o[4];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+                                    o[u] = b + u <= bend ? __ldg(zo + b + u) : make_int2(INT_MAX, -1);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    olo = min(olo, o[u].x);
+                                    ohi = max(ohi, o[u].y);
+                                }
                             }
                             izlo = max(zlo, olo);
                             nu = max(0, min(zhi, ohi) - izlo + 1);
