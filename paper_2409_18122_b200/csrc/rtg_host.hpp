@@ -51,6 +51,10 @@ struct ColGrid {
 
 // scans (rtg_scan.cu): exclusive prefix of n values into out[0..n] (out[n] = total)
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_t st);
+// single-pass scan into caller scratch whose first scan_i32_zero_ints(n) ints are zero (n small)
+long long scan_i32_zero_ints(long long n);
+long long scan_i32_scratch_ints(long long n);
+cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* scratch, cudaStream_t st);
 // copy-B records' (u_q, nH | nL << 32) pairs (from GRec::uc) scanned into out[0 .. 2n+1]
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st);
 // device allocation through the stream-ordered pool

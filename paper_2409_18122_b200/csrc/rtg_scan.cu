@@ -302,6 +302,24 @@ cudaError_t scan_impl(Load in, T* out, long long n, cudaStream_t st) {
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_t st) {
     return scan_impl<int>(LoadArr<int>{in}, out, n, st);
 }
+
+// single-pass scan into caller scratch (scan_i32_scratch_ints(n) ints, of which the first
+// scan_i32_zero_ints(n) must be zero at launch): one launch, no allocation -- for the per-layer scans
+// of rtg_plan_tree, whose scratch is cleared by the preceding kernel.  n <= kChainTiles tiles.
+long long scan_i32_tiles(long long n) { return (n + scan_tile<int>() - 1) / scan_tile<int>(); }
+long long scan_i32_zero_ints(long long n) { return scan_i32_tiles(n) + 1; }
+long long scan_i32_scratch_ints(long long n) { return scan_i32_zero_ints(n) + 2 * scan_i32_tiles(n); }
+cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* scratch, cudaStream_t st) {
+    const long long nt = scan_i32_tiles(n);
+    if (n <= 0 || nt > kChainTiles) return cudaErrorInvalidValue;
+    int* ticket = scratch;
+    int* flags = ticket + 1;
+    int* agg = flags + nt;
+    int* inc = agg + nt;
+    note_launch(), k_scan<int, LoadArr<int>><<<(unsigned)nt, kScanThreads, 0, st>>>(LoadArr<int>{in}, out, n, ticket,
+                                                                                   flags, agg, inc);
+    return cudaGetLastError();
+}
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
     return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);
 }

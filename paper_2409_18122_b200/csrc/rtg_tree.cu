@@ -88,6 +88,8 @@ struct Tree {
     int* cand;                      // candidate node ids (any order)
     int* cnt;                       // 0 M, 1 nodes, 2 candidates, 3 expanded, 4 error, 5 found, 6 reached
     int *sel, *order;               // final selection: node ids (any order), then ranked
+    int *scanA, *scanB;             // per-layer scan scratch (cell counts, kept flags); NULL: allocate
+    int zeroA, zeroB;               // their leading ints that k_expand clears
     unsigned long long *sa, *sb;    // their keys
 };
 
@@ -171,7 +173,14 @@ __global__ void __launch_bounds__(256) k_expand(Tree t, TreeK k, const double* _
                                                 const int* __restrict__ cstart, ColGridK g, float gq, int n_col,
                                                 unsigned long long* __restrict__ stats) {
     const int lane = threadIdx.x & 31;
-    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k.dedup && gt <= (long long)k.lmask) {   // this layer's cell table starts empty (W * 32 >= capacity)
+        t.lkey[gt] = kEmptyKey;
+        t.lcnt[gt] = 0;
+    }
+    if (t.scanA && gt < t.zeroA) t.scanA[gt] = 0;   // and so do this layer's scan tickets and flags
+    if (t.scanB && gt < t.zeroB) t.scanB[gt] = 0;
+    const long long w = gt >> 5;
     if (w >= k.W) return;
     const int M = t.cnt[0];
     if (w >= (long long)M * k.P) {
@@ -700,6 +709,11 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
     const size_t o_sel = carve(sizeof(int) * 2 * nt), o_sab = carve(sizeof(unsigned long long) * 2 * nt);
     const size_t o_w = carve(sizeof(float) * 4 * nt * T), o_cost = carve(sizeof(double) * nt);
     const size_t o_ctl = carve(sizeof(double) * ctl.size()), o_st = carve(sizeof(unsigned long long) * 4);
+    // the per-layer scans run from pre-cleared scratch when they fit one single-pass launch
+    const bool fastA = (long long)lcap <= 64LL * 4096;
+    const bool fastB = (long long)W <= 64LL * 4096;
+    const size_t o_sa = carve(sizeof(int) * (size_t)scan_i32_scratch_ints((long long)lcap));
+    const size_t o_sb = carve(sizeof(int) * (size_t)scan_i32_scratch_ints((long long)W));
     char* mem = nullptr;
     cudaError_t e = dev_alloc((void**)&mem, off, st);
     if (e != cudaSuccess) {
@@ -722,6 +736,10 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
     t.cnt = (int*)(mem + o_cnt);
     t.sel = (int*)(mem + o_sel); t.order = t.sel + nt;
     t.sa = (unsigned long long*)(mem + o_sab); t.sb = t.sa + nt;
+    t.scanA = fastA && k.dedup ? (int*)(mem + o_sa) : nullptr;
+    t.scanB = fastB ? (int*)(mem + o_sb) : nullptr;
+    t.zeroA = (int)scan_i32_zero_ints((long long)lcap);
+    t.zeroB = (int)scan_i32_zero_ints((long long)W);
     float* wx = (float*)(mem + o_w);
     float *wy = wx + nt * T, *wz = wy + nt * T, *wyaw = wz + nt * T;
     double* d_cost = (double*)(mem + o_cost);
@@ -747,15 +765,17 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
                                                           g, m->gq, (int)m->n_col, d_stats);
         e = cudaGetLastError();
         if (e == cudaSuccess && k.dedup) {
-            e = cudaMemsetAsync(t.lkey, 0xff, sizeof(unsigned long long) * lcap, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(t.lcnt, 0, sizeof(int) * lcap, st);
-            if (e == cudaSuccess) note_launch(), k_cells<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
-            if (e == cudaSuccess) e = exclusive_scan_i32(t.lcnt, t.loff, (long long)lcap, st);
+            note_launch(), k_cells<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
+            if (e == cudaSuccess)
+                e = t.scanA ? exclusive_scan_i32_into(t.lcnt, t.loff, (long long)lcap, t.scanA, st)
+                            : exclusive_scan_i32(t.lcnt, t.loff, (long long)lcap, st);
             if (e == cudaSuccess) note_launch(), k_bucket<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
         }
         if (e == cudaSuccess) note_launch(), k_keep<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
         if (e == cudaSuccess && k.dedup) note_launch(), k_close<<<tblocks, 256, 0, st>>>(t, k), e = cudaGetLastError();
-        if (e == cudaSuccess) e = exclusive_scan_i32(t.acc, t.rank, (long long)W, st);
+        if (e == cudaSuccess)
+            e = t.scanB ? exclusive_scan_i32_into(t.acc, t.rank, (long long)W, t.scanB, st)
+                        : exclusive_scan_i32(t.acc, t.rank, (long long)W, st);
         if (e == cudaSuccess) note_launch(), k_create<<<tblocks, 256, 0, st>>>(t, k, depth), e = cudaGetLastError();
         if (e == cudaSuccess) note_launch(), k_beam<<<1, kSelThreads, 0, st>>>(t, k), e = cudaGetLastError();
     }
