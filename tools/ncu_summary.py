@@ -33,6 +33,11 @@ METRICS = [
     "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_wait",
     "smsp__pcsamp_warps_issue_stalled_short_scoreboard", "smsp__pcsamp_warps_issue_stalled_not_selected",
     "smsp__pcsamp_warps_issue_stalled_selected", "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
+    # SURVEY §8(d) metric 3: FP32-pipe thread instructions per cycle over the chip's FP32 peak
+    "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed",
+    "sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained",
 ]
 
 
@@ -82,6 +87,13 @@ def full(rep, out, key=None):
                 b += float(v.replace(",", "")) * mult.get(u, 1)
         short = name.split("::")[-1].split("<")[0]
         traffic[short] = b
+        fp = [w for w in METRICS if "thread_inst_executed_op_f" in w and "per_cycle_elapsed" in w]
+        pk = "sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained"
+        if all(w in got for w in fp) and pk in got:
+            ops = sum(float(got[w][1].replace(",", "")) for w in fp)
+            peak = float(got[pk][1].replace(",", ""))
+            lines.append(f"{'scalar FP32 thread instr / FP32 peak (packed f32x2 not counted)':60s} {'%':10s} "
+                         f"{100.0 * ops / peak:.2f}")
     # hottest CUDA source lines (instructions executed, warp stall samples): needs -lineinfo
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
