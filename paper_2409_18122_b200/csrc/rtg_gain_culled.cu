@@ -1,28 +1,30 @@
 // rtg_gain_culled.cu -- exact culled visibility + information gain.
 //
-// One warp per info waypoint (persistent warps pull waypoints from an atomic counter in
-// (k, t) order, so neighbouring warps share frusta and L1/L2 lines).  The frustum is six linear
-// constraints f_j(p) = a_j dx + b_j dy + g_j dz + d_j >= 0 (the pinhole slacks of O3: near, far,
-// two side planes through the camera centre, top and bottom); over a grid cell (box) the
-// minimum / maximum of each is its centre value -/+ a radius, and along a grid row the centre
-// value is linear in the x-cell index, so the cells of a row that are possibly visible / fully
-// inside form index intervals found with one division per constraint.  Per waypoint:
-//   1. lanes take the grid rows (y bands) the frustum's footprint covers; per row the four
-//      horizontal constraints give the x-interval P of possibly visible columns and its
+// One warp per info waypoint (persistent warps, 4-warp CTAs x 9 per SM at 56 registers, pull
+// waypoints from an atomic counter in (k, t) order).  The frustum is six linear constraints
+// f_j(p) = a_j dx + b_j dy + g_j dz + d_j >= 0 (the pinhole slacks of O3: near, far, two side planes
+// through the camera centre, top and bottom); over a grid cell (box) the minimum / maximum of each is
+// its centre value -/+ a radius, and along a grid row the centre value is linear in the x-cell
+// index, so the cells of a row that are possibly visible / fully inside form index intervals found
+// with one multiply per constraint.  Per waypoint:
+//   1. lanes take the grid rows (y bands) the frustum's footprint covers, 32 at a time; per row the
+//      four horizontal constraints give the x-interval P of possibly visible columns and its
 //      sub-interval I of columns whose whole column box is horizontally inside;
 //   2. the flanks P \ I are tested Gaussian by Gaussian from record copy A (sorted by
 //      (row, x-cell)): each flank is ONE contiguous record run (all z);
 //   3. the inside columns I are walked z-cell by z-cell from copy B (sorted by (row, z-cell,
-//      x-cell), so a row's z-slab is x-contiguous): per (row, z-cell) unit the two vertical
-//      constraints cut I into an x-run fully inside (added from exact per-record prefixes: two
-//      loads) and at most two straddling x-runs (tested); the z-cells a row can see come from
-//      the vertical wedge at the row's largest depth and the row's occupied z-range;
-//   4. tested runs go to a per-warp queue and are tested 32 Gaussians per warp instruction
-//      regardless of run lengths (run owner of each lane from a ballot-OR of run heads), with
-//      the shared exact pair test (FP32 + FP64 re-decision inside the proven guard band).
-// Sums are exact integers (u_q in FP64 below 2^53; packed class counts): order free, so the
-// result is bit-identical to the dense kernel.  eps (>> FP32 error of the cell tests) keeps
-// "inside" strictly inside and "possible" a superset.
+//      x-cell), so a row's z-slab is x-contiguous): per (row, z-cell) unit (lanes flattened over the
+//      chunk's units through a shared-memory owner table) the two vertical constraints cut I into an
+//      x-run fully inside (added from the exact prefixes of the z-fastest table: two loads) and at
+//      most two straddling x-runs (tested); the z-cells a row can see come from the vertical wedge
+//      at the row's largest depth and the row's occupied z-range;
+//   4. tested runs go to a per-warp queue; a flush tests 64 items per pass, two per lane, whatever
+//      the run lengths (each lane's run from a 64-bit head mask built with two REDUX.OR), with the
+//      shared exact pair test (packed FP32 + FP64 re-decision inside the proven guard band).
+// Sums are exact integers (24-bit u_q and a class byte per record, 32-bit per-lane sums flushed
+// into 64-bit ones; FP64-exact prefixes): order free, so the result is bit-identical to the dense
+// kernel.  eps (>> FP32 error of the cell tests) keeps "inside" strictly inside and "possible" a
+// superset.
 #include <cfloat>
 #include <climits>
 #include <cstdio>
