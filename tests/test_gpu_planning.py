@@ -216,6 +216,69 @@ def test_plan_tree_matches_oracle(R, goal, depth, beam, lattice, ldeg, n_traj):
     to.close()
 
 
+_TREE_FUZZ = int(__import__("os").environ.get("RTG_TREE_FUZZ_SEEDS", "8"))
+
+
+@pytest.mark.parametrize("seed", range(_TREE_FUZZ))
+def test_plan_tree_fuzz(R, seed):
+    """Random obstacle fields, starts, goals and search parameters: the tree equals the oracle's
+    (reached, nodes expanded, costs bit for bit, states within fp32 rounding)."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(100, 2500))
+    means = np.stack([rng.uniform(-8, 8, n), rng.uniform(-8, 8, n), rng.uniform(0, 1.5, n)]).astype(np.float32)
+    q = rng.normal(size=(4, n))
+    quats = (q / np.linalg.norm(q, axis=0)).astype(np.float32)
+    scales = np.exp(rng.uniform(np.log(0.02), np.log(0.3), (3, n))).astype(np.float32)
+    z1 = np.zeros((1, 1), np.float32)
+    wl = W.Workload("treefuzz", means, quats, scales, np.ones(n, np.float32), rng.random(n).astype(np.float32),
+                    None, z1, z1, np.full((1, 1), 0.5, np.float32), z1, W.Robot(float(rng.uniform(0.1, 0.4))),
+                    W.Camera(64, 48, 50, 50, 32, 24, 0.1, 5), 0.1)
+    # a start cleared of obstacles so the search usually grows
+    keep = np.hypot(means[0], means[1]) > 1.0
+    wl = W.Workload("treefuzz", means[:, keep], quats[:, keep], scales[:, keep], np.ones(int(keep.sum()), np.float32),
+                    wl.info_w[keep], None, z1, z1, np.full((1, 1), 0.5, np.float32), z1, wl.robot, wl.camera, 0.1)
+    depth = int(rng.integers(2, 6))
+    lat = float(rng.choice([0.0, 0.1, 0.25, 0.5]))
+    tp = R.make_tree_params(n_v=int(rng.integers(1, 4)), n_omega=int(rng.integers(1, 6)),
+                            v_max=float(rng.uniform(0.3, 1.5)), omega_max=float(rng.uniform(0.0, 1.5)),
+                            samples=int(rng.integers(2, 7)), max_depth=depth, goal_radius=float(rng.uniform(0.2, 1.5)),
+                            lattice_xy=lat, lattice_deg=float(rng.choice([5.0, 10.0, 30.0])),
+                            beam=int(rng.integers(1, 300)), n_traj=int(rng.integers(1, 60)), z=0.5)
+    start = (float(rng.uniform(-0.3, 0.3)), float(rng.uniform(-0.3, 0.3)), float(rng.uniform(-np.pi, np.pi)))
+    goal = (float(rng.uniform(-6, 6)), float(rng.uniform(-6, 6)))
+    m = R.map_from_workload(wl)
+    res = P.plan_tree(_oracle_collides(wl), start, goal, tp)
+    if not res["cands"]:
+        with pytest.raises(R.RTGError):
+            R.plan_tree(m, start, goal, tp)
+        m.close()
+        return
+    tr, cost, reached, stats = R.plan_tree(m, start, goal, tp)
+    x, y, z, yaw = (a.cpu().numpy() for a in tr.read())
+    ox, oy, oyaw, ocost = P.tree_waypoints(res, depth)
+    assert reached == res["reached"] and stats["expanded"] == res["expanded"]
+    # the states come from FP64 sin/cos, which the device rounds within 2 ulp of the host's: keys equal
+    # to that rounding (h of the closest nodes, here) may rank in either order, so the candidates are
+    # compared as a set -- each GPU candidate matches one oracle candidate (cost within 1e-12 relative,
+    # same length, states within fp32 rounding)
+    assert len(cost) == len(ocost)
+    assert np.allclose(np.sort(cost), np.sort(ocost), rtol=1e-12, atol=0)
+    free = list(range(len(ocost)))
+    for c in range(len(cost)):
+        hit = None
+        for o in free:
+            if abs(cost[c] - ocost[o]) <= 1e-12 * abs(ocost[o]) and np.array_equal(np.isnan(x[c]), np.isnan(ox[o])):
+                ok = ~np.isnan(ox[o])
+                if (np.all(np.abs(x[c][ok] - ox[o][ok]) <= 1e-5) and np.all(np.abs(y[c][ok] - oy[o][ok]) <= 1e-5)
+                        and np.all(np.abs(np.angle(np.exp(1j * (yaw[c][ok] - oyaw[o][ok])))) <= 1e-5)):
+                    hit = o
+                    break
+        assert hit is not None, c
+        free.remove(hit)
+    m.close()
+    tr.close()
+
+
 def test_plan_tree_trapped(R):
     # start inside a wall of obstacles: no collision-free primitive -> RTG_ERR_NO_FEASIBLE
     n = 400
