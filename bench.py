@@ -244,12 +244,12 @@ def main():
             tr = R.Traj.upload(*src_traj, device=local, stream=aux)
             stream.wait_stream(aux)
         else:
-            tr = R.Traj.upload(*src_traj, device=local)
+            tr = R.Traj.wrap(*src_traj, device=local)   # resident waypoints: borrowed, no copy
         R.score(m, tr, cam, params, *outs)
         s, i = R.best(outs[3])
         res = global_best(s, i)
         if Kv:   # the scale config's gain-only views (T = 1, no collision): best view by xi
-            tv = R.Traj.upload(*((hviews if host else dviews)), device=local)
+            tv = R.Traj.upload(*hviews, device=local) if host else R.Traj.wrap(*dviews, device=local)
             R.score(m, tv, cam, vparams, *vouts)
             vs, vi = R.best(vouts[3])
             res = res + global_best(vs, vi)

@@ -191,6 +191,15 @@ rtg_status rtg_traj_upload(int device, int K, int T, rtg_mem kind,
 rtg_status rtg_traj_sample_unicycle(int device, int K, int T, float dt, const float start[4],
                                     const float* v, const float* omega, rtg_mem kind,
                                     void* stream, rtg_traj* out);
+/*
+ * rtg_traj_wrap -- zero-copy borrow of caller DEVICE arrays x, y, z, yaw (each K*T floats,
+ * trajectory-major, on `device`) as a trajectory handle.  The library only
+ * reads them; the caller keeps them alive and unchanged until rtg_traj_destroy (which does not free
+ * them).  Errors: RTG_ERR_INVALID_ARGUMENT (NULL or non-device pointers, K < 1, T < 1,
+ * K*T >= 2^31, bad device).
+ */
+rtg_status rtg_traj_wrap(int device, int K, int T, const float* x, const float* y, const float* z,
+                         const float* yaw, rtg_traj* out);
 /* Copies the trajectory SoA into caller device buffers (each K*T floats). */
 rtg_status rtg_traj_read(rtg_traj traj, float* x, float* y, float* z, float* yaw, void* stream);
 rtg_status rtg_traj_destroy(rtg_traj traj);

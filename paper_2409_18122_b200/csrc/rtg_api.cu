@@ -446,10 +446,47 @@ rtg_status rtg_traj_read(rtg_traj t, float* x, float* y, float* z, float* yaw, v
     return RTG_OK;
 }
 
+static bool is_device_ptr(const void* p, int device) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.device == device;
+}
+
+rtg_status rtg_traj_wrap(int device, int K, int T, const float* x, const float* y, const float* z, const float* yaw,
+                         rtg_traj* out) {
+    if (!out) return invalid("out is NULL");
+    *out = nullptr;
+    if (!x || !y || !z || !yaw) return invalid("x, y, z and yaw are required");
+    if (K < 1 || T < 1 || (long long)K * T >= (1LL << 31)) return invalid("need K >= 1, T >= 1, K*T < 2^31");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return invalid("invalid device ordinal (no CUDA device?)");
+    }
+    if (!is_device_ptr(x, device) || !is_device_ptr(y, device) || !is_device_ptr(z, device) ||
+        !is_device_ptr(yaw, device))
+        return invalid("rtg_traj_wrap needs device arrays on the handle's device");
+    rtg_traj_s* t = new (std::nothrow) rtg_traj_s();
+    if (!t) return RTG_ERR_OUT_OF_MEMORY;
+    t->device = device;
+    t->K = K;
+    t->T = T;
+    t->x = const_cast<float*>(x);
+    t->y = const_cast<float*>(y);
+    t->z = const_cast<float*>(z);
+    t->yaw = const_cast<float*>(yaw);
+    t->borrowed = true;
+    *out = t;
+    return RTG_OK;
+}
+
 rtg_status rtg_traj_destroy(rtg_traj t) {
     if (!t) return invalid("trajectory handle is NULL");
     cudaSetDevice(t->device);
-    dev_free(t->x, t->stream);
+    if (!t->borrowed) dev_free(t->x, t->stream);
     delete t;
     return RTG_OK;
 }

@@ -128,4 +128,5 @@ struct rtg_traj_s {
     float* y = nullptr;
     float* z = nullptr;
     float* yaw = nullptr;
+    bool borrowed = false;   // rtg_traj_wrap: the arrays belong to the caller
 };

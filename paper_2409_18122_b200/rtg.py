@@ -101,6 +101,7 @@ _SIGS = {
     "rtg_map_destroy": (_S, [_P]),
     "rtg_map_info": (_S, [_P, ctypes.POINTER(MapInfo)]),
     "rtg_traj_upload": (_S, [_I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.POINTER(_P)]),
+    "rtg_traj_wrap": (_S, [_I, _I, _I, _P, _P, _P, _P, ctypes.POINTER(_P)]),
     "rtg_traj_sample_unicycle": (_S, [_I, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_float), _P, _P, _I, _P,
                                       ctypes.POINTER(_P)]),
     "rtg_traj_read": (_S, [_P, _P, _P, _P, _P, _P]),
@@ -279,6 +280,17 @@ class Traj:
         _check(_lib.rtg_traj_upload(device, K, T, kind, _ptr(x), _ptr(y), _ptr(z), _ptr(yaw), _stream(stream),
                                     ctypes.byref(h)), "rtg_traj_upload")
         return cls(h, K, T)
+
+    @classmethod
+    def wrap(cls, x, y, z, yaw, device=0) -> "Traj":
+        """rtg_traj_wrap: borrow device tensors [K, T] without copying (kept referenced here)."""
+        K, T = (int(s) for s in x.shape)
+        h = _P()
+        _check(_lib.rtg_traj_wrap(device, K, T, _ptr(x), _ptr(y), _ptr(z), _ptr(yaw), ctypes.byref(h)),
+               "rtg_traj_wrap")
+        t = cls(h, K, T)
+        t._borrowed = (x, y, z, yaw)
+        return t
 
     @classmethod
     def sample_unicycle(cls, v, omega, T: int, dt: float, start, device=0, stream=None) -> "Traj":

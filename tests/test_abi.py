@@ -60,6 +60,10 @@ def test_invalid_arguments_rejected_before_any_launch(rtg):
     # trajectories: K = 0
     x = (ctypes.c_float * 1)()
     assert lib.rtg_traj_upload(0, 0, 5, 0, x, x, x, x, None, ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    # wrap: K = 0, NULL arrays, and (checked before any device query) host arrays are refused
+    assert lib.rtg_traj_wrap(0, 0, 5, x, x, x, x, ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_traj_wrap(0, 2, 5, None, x, x, x, ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_traj_wrap(0, 2, 5, x, x, x, x, ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
     # best on nothing
     out = rtg.BestResult()
     assert lib.rtg_best(None, 0, 0, None, ctypes.byref(out)) == rtg.ERR_INVALID_ARGUMENT

@@ -525,3 +525,27 @@ def test_scale_full_size_sampled_with_views(R):
     tol = 1e-5 * np.abs(vo["gain_hi"]) + 1e-9
     assert np.all((vg["gain"] >= vo["gain_lo"] - tol) & (vg["gain"] <= vo["gain_hi"] + tol))
     assert np.all((vg["utility"] >= vo["xi_lo"]) & (vg["utility"] <= vo["xi_hi"]))
+
+
+def test_traj_wrap_equals_upload(R, room):
+    """rtg_traj_wrap borrows the caller's device arrays: same scores as an uploaded copy; destroying
+    the handle leaves the arrays intact; host arrays are refused."""
+    idx = np.arange(0, room.K, 8)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a[idx])).cuda()
+    xs = [dev(a) for a in (room.x, room.y, room.z, room.yaw)]
+    m = R.map_from_workload(room)
+    p = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN)
+    tu = R.Traj.upload(*xs)
+    tw = R.Traj.wrap(*xs)
+    a = [t.cpu().numpy() for t in R.score(m, tu, room.camera, p)]
+    b = [t.cpu().numpy() for t in R.score(m, tw, room.camera, p)]
+    for u, v in zip(a, b):
+        assert np.array_equal(u.view(np.uint8), v.view(np.uint8))
+    before = xs[0].clone()
+    tw.close()
+    tu.close()
+    torch.cuda.synchronize()
+    assert torch.equal(xs[0], before)
+    with pytest.raises(R.RTGError):
+        R.Traj.wrap(*[np.ascontiguousarray(a[idx]) for a in (room.x, room.y, room.z, room.yaw)])
+    m.close()
