@@ -192,6 +192,16 @@ rtg_status rtg_traj_sample_unicycle(int device, int K, int T, float dt, const fl
                                     const float* v, const float* omega, rtg_mem kind,
                                     void* stream, rtg_traj* out);
 /*
+ * rtg_traj_sample_double_integrator -- on-device double-integrator primitives (BASELINE.json
+ * configs[2]; SURVEY §8(b) optional sampler): trajectory k accelerates at the constant
+ * (ax[k], ay[k]) from start = {x, y, z} with velocity v0 = {vx, vy}; waypoint l is the closed-form
+ * state at t = (l+1)*dt: p = p0 + v0 t + a t^2 / 2 (FP64, stored as FP32), z constant, heading
+ * atan2(vy + ay t, vx + ax t) (0 at zero velocity).  ax / ay are host or device per `kind`.
+ */
+rtg_status rtg_traj_sample_double_integrator(int device, int K, int T, float dt, const float start[3],
+                                             const float v0[2], const float* ax, const float* ay,
+                                             rtg_mem kind, void* stream, rtg_traj* out);
+/*
  * rtg_traj_wrap -- zero-copy borrow of caller DEVICE arrays x, y, z, yaw (each K*T floats,
  * trajectory-major, on `device`) as a trajectory handle.  The library only
  * reads them; the caller keeps them alive and unchanged until rtg_traj_destroy (which does not free

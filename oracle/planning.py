@@ -156,6 +156,24 @@ def unicycle_at(x0, y0, th0, v, w, t):
     return x0 + r * (math.sin(th) - math.sin(th0)), y0 + r * (math.cos(th0) - math.cos(th)), th
 
 
+def double_integrator(start, v0, a, dt, T):
+    """Double-integrator motion primitive (BASELINE.json configs[2], SURVEY §8(b) optional sampler):
+    constant acceleration a = (ax, ay) from p0 = start[0:2] with velocity v0, sampled at
+    t_l = (l+1) dt: p(t) = p0 + v0 t + a t^2 / 2, z constant, heading along the velocity
+    atan2(v0y + ay t, v0x + ax t) (0 when the velocity is zero).  FP64 (x, y, z, yaw) arrays."""
+    f = lambda v: float(np.float32(v))
+    x0, y0, z0 = f(start[0]), f(start[1]), f(start[2])
+    vx, vy, ax, ay, dt = f(v0[0]), f(v0[1]), f(a[0]), f(a[1]), f(dt)
+    out = [np.zeros(T) for _ in range(4)]
+    for l in range(T):
+        t = (l + 1) * dt
+        out[0][l] = x0 + vx * t + 0.5 * ax * t * t
+        out[1][l] = y0 + vy * t + 0.5 * ay * t * t
+        out[2][l] = z0
+        out[3][l] = math.atan2(vy + ay * t, vx + ax * t)
+    return tuple(out)
+
+
 def wrap_pi(a):
     r = math.remainder(a, 2.0 * math.pi)
     return r + 2.0 * math.pi if r <= -math.pi else r

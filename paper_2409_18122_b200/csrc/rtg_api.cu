@@ -100,6 +100,8 @@ cudaError_t launch_reduce(rtg_map_s* m, rtg_traj_s* tr, const rtg_score_params& 
 cudaError_t launch_debug_wp(long long n, const long long* wp_gq, const ClassState* cs, double* out, cudaStream_t st);
 cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaStream_t st);
 cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st);
+cudaError_t launch_sampler_di(int K, int T, double dt, const float* start, const float* v0, const float* ax,
+                              const float* ay, rtg_traj_s* tr, cudaStream_t st);
 cudaError_t launch_sampler(int K, int T, double dt, const float* start, const float* v, const float* om,
                            rtg_traj_s* tr, cudaStream_t st);
 
@@ -427,6 +429,36 @@ rtg_status rtg_traj_sample_unicycle(int device, int K, int T, float dt, const fl
         dev_free(t->x, st);
         delete t;
         return cuda_fail(e, "rtg_traj_sample_unicycle", nullptr);
+    }
+    *out = t;
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_sample_double_integrator(int device, int K, int T, float dt, const float start[3],
+                                             const float v0[2], const float* ax, const float* ay, rtg_mem kind,
+                                             void* stream, rtg_traj* out) {
+    if (!start || !v0 || !ax || !ay) return invalid("start, v0, ax and ay are required");
+    if (kind != RTG_MEM_HOST && kind != RTG_MEM_DEVICE) return invalid("unknown memory kind");
+    if (!(dt >= 0) || !finite_f(dt)) return invalid("dt must be finite and >= 0");
+    for (int i = 0; i < 3; ++i)
+        if (!finite_f(start[i])) return invalid("start state must be finite");
+    if (!finite_f(v0[0]) || !finite_f(v0[1])) return invalid("v0 must be finite");
+    cudaStream_t st = (cudaStream_t)stream;
+    rtg_traj_s* t = nullptr;
+    rtg_status s = traj_alloc(device, K, T, st, out, &t);
+    if (s != RTG_OK) return s;
+    float *dax = nullptr, *day = nullptr;
+    cudaError_t e = stage(ax, (size_t)K, kind, &dax, st);
+    if (e == cudaSuccess) e = stage(ay, (size_t)K, kind, &day, st);
+    if (e == cudaSuccess) e = launch_sampler_di(K, T, (double)dt, start, v0, dax, day, t, st);
+    if (kind == RTG_MEM_HOST) {
+        dev_free(dax, st);
+        dev_free(day, st);
+    }
+    if (e != cudaSuccess) {
+        dev_free(t->x, st);
+        delete t;
+        return cuda_fail(e, "rtg_traj_sample_double_integrator", nullptr);
     }
     *out = t;
     return RTG_OK;

@@ -520,6 +520,24 @@ __global__ void k_sample_unicycle(int K, int T, double dt, double x0, double y0,
     Yaw[i] = (float)wr;
 }
 
+// double-integrator primitives (BASELINE.json configs[2]): constant acceleration (ax, ay)[k] from
+// (x0, y0) with velocity (vx, vy); t_l = (l+1) dt; heading along the velocity; FP64, stored as FP32
+__global__ void k_sample_double_integrator(int K, int T, double dt, double x0, double y0, double z0, double vx,
+                                           double vy, const float* __restrict__ ax, const float* __restrict__ ay,
+                                           float* __restrict__ X, float* __restrict__ Y, float* __restrict__ Zw,
+                                           float* __restrict__ Yaw) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= (long long)K * T) return;
+    const int k = (int)(i / T), l = (int)(i % T);
+    const double a = ax[k], b = ay[k];
+    const double t = __dmul_rn((double)(l + 1), dt);
+    const double t2 = __dmul_rn(t, t);
+    X[i] = (float)__dadd_rn(__dadd_rn(x0, __dmul_rn(vx, t)), __dmul_rn(__dmul_rn(0.5, a), t2));
+    Y[i] = (float)__dadd_rn(__dadd_rn(y0, __dmul_rn(vy, t)), __dmul_rn(__dmul_rn(0.5, b), t2));
+    Zw[i] = (float)z0;
+    Yaw[i] = (float)atan2(__dadd_rn(vy, __dmul_rn(b, t)), __dadd_rn(vx, __dmul_rn(a, t)));
+}
+
 // ===================================================================== host launchers
 cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, const int* list, const int* count,
                                long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl, int* counter,
@@ -661,6 +679,14 @@ cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaS
 
 cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st) {
     note_launch(), k_best<<<1, 1024, 0, st>>>(u, K, base, (BestDev*)out_dev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sampler_di(int K, int T, double dt, const float* start, const float* v0, const float* ax,
+                              const float* ay, rtg_traj_s* tr, cudaStream_t st) {
+    const long long n = (long long)K * T;
+    note_launch(), k_sample_double_integrator<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+                       K, T, dt, start[0], start[1], start[2], v0[0], v0[1], ax, ay, tr->x, tr->y, tr->z, tr->yaw);
     return cudaGetLastError();
 }
 

@@ -102,6 +102,8 @@ _SIGS = {
     "rtg_map_info": (_S, [_P, ctypes.POINTER(MapInfo)]),
     "rtg_traj_upload": (_S, [_I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.POINTER(_P)]),
     "rtg_traj_wrap": (_S, [_I, _I, _I, _P, _P, _P, _P, ctypes.POINTER(_P)]),
+    "rtg_traj_sample_double_integrator": (_S, [_I, _I, _I, ctypes.c_float, _P, _P, _P, _P, _I, _P,
+                                               ctypes.POINTER(_P)]),
     "rtg_traj_sample_unicycle": (_S, [_I, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_float), _P, _P, _I, _P,
                                       ctypes.POINTER(_P)]),
     "rtg_traj_read": (_S, [_P, _P, _P, _P, _P, _P]),
@@ -291,6 +293,19 @@ class Traj:
         t = cls(h, K, T)
         t._borrowed = (x, y, z, yaw)
         return t
+
+    @classmethod
+    def sample_double_integrator(cls, ax, ay, T: int, dt: float, start, v0, device=0, stream=None) -> "Traj":
+        """rtg_traj_sample_double_integrator: constant accelerations (ax, ay)[K] from start (x, y, z)
+        with velocity v0 (vx, vy)."""
+        K = int(ax.shape[0])
+        st3 = (ctypes.c_float * 3)(*[float(s) for s in start[:3]])
+        v2 = (ctypes.c_float * 2)(float(v0[0]), float(v0[1]))
+        h = _P()
+        _check(_lib.rtg_traj_sample_double_integrator(device, K, int(T), float(dt), st3, v2, _ptr(ax), _ptr(ay),
+                                                      _kind(ax), _stream(stream), ctypes.byref(h)),
+               "rtg_traj_sample_double_integrator")
+        return cls(h, K, int(T))
 
     @classmethod
     def sample_unicycle(cls, v, omega, T: int, dt: float, start, device=0, stream=None) -> "Traj":

@@ -549,3 +549,29 @@ def test_traj_wrap_equals_upload(R, room):
     with pytest.raises(R.RTGError):
         R.Traj.wrap(*[np.ascontiguousarray(a[idx]) for a in (room.x, room.y, room.z, room.yaw)])
     m.close()
+
+
+def test_double_integrator_sampler_matches_oracle(R):
+    """rtg_traj_sample_double_integrator against the oracle's closed form (oracle/planning.py), incl.
+    a trajectory that brakes through rest (the heading flips) and zero acceleration."""
+    from oracle import planning as P
+    rng = np.random.default_rng(11)
+    K, T, dt = 33, 60, 0.1
+    ax = rng.uniform(-1, 1, K).astype(np.float32)
+    ay = rng.uniform(-1, 1, K).astype(np.float32)
+    ax[0], ay[0] = np.float32(-1.0), np.float32(0.0)    # rest at t = 1 s (v0x = 1)
+    ax[1], ay[1] = np.float32(0.0), np.float32(0.0)
+    start, v0 = (5.0, -2.5, 0.5), (1.0, 0.0)
+    tr = R.Traj.sample_double_integrator(torch.from_numpy(ax).cuda(), torch.from_numpy(ay).cuda(), T, dt, start, v0)
+    X, Y, Z, YW = (a.cpu().numpy() for a in tr.read())
+    for k in range(K):
+        ox, oy, oz, oyaw = P.double_integrator(start, v0, (ax[k], ay[k]), dt, T)
+        assert np.all(np.abs(X[k] - ox) <= 2 * np.spacing(np.float32(np.abs(ox) + 1))), k
+        assert np.all(np.abs(Y[k] - oy) <= 2 * np.spacing(np.float32(np.abs(oy) + 1))), k
+        assert np.all(Z[k] == np.float32(oz))
+        assert np.all(np.abs(np.angle(np.exp(1j * (YW[k] - oyaw)))) < 1e-6), k
+    # host accelerations give the same trajectories
+    th = R.Traj.sample_double_integrator(ax, ay, T, dt, start, v0)
+    assert all(torch.equal(a, b) for a, b in zip(th.read(), tr.read()))
+    th.close()
+    tr.close()

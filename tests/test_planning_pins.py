@@ -214,3 +214,21 @@ def test_tree_wall_samples_avoid_obstacle_and_fallback():
     assert not r2["reached"] and len(r2["cands"]) == 10
     hs = [math.hypot(3.0 - r2["nodes"][i][0], r2["nodes"][i][1]) for i in r2["cands"]]
     assert hs == sorted(hs)
+
+
+def test_double_integrator_matches_ode_and_heading():
+    """The double-integrator sampler's oracle against an ODE integration of p'' = a, and its heading
+    against the velocity direction; zero velocity has heading 0 (atan2(0, 0))."""
+    from scipy.integrate import solve_ivp
+    start, v0, a, dt, T = (5.0, -1.0, 0.5, 0.0), (1.0, 0.25), (-0.5, 0.75), 0.1, 40
+    x, y, z, yaw = P.double_integrator(start, v0, a, dt, T)
+    f = lambda v: float(np.float32(v))
+    sol = solve_ivp(lambda t, s: [s[2], s[3], f(a[0]), f(a[1])], (0, T * f(dt)),
+                    [f(start[0]), f(start[1]), f(v0[0]), f(v0[1])], t_eval=(np.arange(T) + 1) * f(dt),
+                    rtol=1e-12, atol=1e-12)
+    assert np.allclose(x, sol.y[0], atol=1e-9) and np.allclose(y, sol.y[1], atol=1e-9)
+    assert np.allclose(yaw, np.arctan2(sol.y[3], sol.y[2]), atol=1e-9)
+    assert np.all(z == f(start[2]))
+    # braking to rest at t = 1 s exactly: heading 0 there, and reversing after
+    x, y, z, yaw = P.double_integrator((0, 0, 0, 0), (1.0, 0.0), (-1.0, 0.0), 0.5, 4)
+    assert yaw[1] == 0.0 and abs(yaw[2]) == math.pi and x[1] == 0.5
