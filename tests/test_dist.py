@@ -80,3 +80,74 @@ def test_global_best_gloo_world2(case):
         k = int(np.argmax(u))
         expect = (float(u[k]), k)
     assert res[0] == res[1] == expect
+
+
+def test_packed_key_orders_like_reduce_best():
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        W = int(rng.integers(1, 6))
+        pairs = []
+        for r in range(W):
+            if rng.random() < 0.2:
+                pairs.append((-math.inf, -1))
+            else:
+                pairs.append((float(rng.integers(-5, 5)), int(rng.integers(0, (1 << 32) - 1))))
+        keys = [D.pack_key(s, i) for s, i in pairs]
+        assert D.unpack_key(max(keys)) == D.reduce_best(np.array(pairs, dtype=object))
+    for s, i in ((0.0, 0), (-(2.0 ** 31), (1 << 32) - 2), (2.0 ** 31 - 1, 5), (-1.0, 3)):
+        assert D.unpack_key(D.pack_key(s, i)) == (s, i)
+    with pytest.raises(ValueError):
+        D.pack_key(1.5, 0)
+    with pytest.raises(ValueError):
+        D.pack_key(2.0 ** 31, 0)
+    with pytest.raises(ValueError):
+        D.pack_key(-(2.0 ** 31), (1 << 32) - 1)
+
+
+def _worker_outputs(rank, world, port, fc, fe, g, u, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K = len(u)
+        idx = D.shard_indices(K, rank, world)
+        out = D.gather_outputs(torch.from_numpy(fc[idx]), fe[idx], g[idx], torch.from_numpy(u[idx]), K, rank, world)
+        loc = u[idx]
+        if len(loc) == 0 or np.all(np.isneginf(loc)):
+            s, j = -math.inf, -1
+        else:
+            j = int(np.argmax(loc))
+            s = float(loc[j])
+        q.put((rank, out, D.global_best_packed(s, j, rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("K", [101, 1, 0])
+def test_gather_outputs_and_packed_best_gloo_world2(K):
+    rng = np.random.default_rng(5)
+    fc = rng.integers(-1, 100, size=K).astype(np.int32)
+    fe = (fc < 0).astype(np.uint8)
+    g = rng.normal(size=K)
+    g[fe == 0] = np.nan
+    u = np.where(fe == 1, rng.integers(-3, 4, size=K).astype(np.float64), -np.inf)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_outputs, args=(r, world, port, fc, fe, g, u, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: (o, b) for r, o, b in (q.get(timeout=120) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if K == 0 or np.all(np.isneginf(u)):
+        expect_best = (-math.inf, -1)
+    else:
+        expect_best = (float(u.max()), int(np.argmax(u)))
+    for r in range(world):
+        o, b = res[r]
+        assert np.array_equal(o[0], fc) and np.array_equal(o[1], fe)
+        assert np.array_equal(o[2], g, equal_nan=True) and np.array_equal(o[3], u)
+        assert b == expect_best
