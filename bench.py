@@ -340,7 +340,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:   # contract: rank 0 at N = 1 only
         cores = oracle_threads()
-        n_traj = max(1, min(K, 2 * cores))
+        # ~20 s of oracle work: ~2.1e7 pair-tests/s per core measured (r1), whole multiples of the cores
+        n_traj = int(20.0 * 2.1e7 * cores / (float(T) * max(N, 1)))
+        n_traj = max(1, min(K, max(cores, n_traj // cores * cores)))
         v, dt, nt = oracle_sample(wl, n_traj)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{nt} random trajectories x T={T} x N={N} of this workload ({dt:.1f} s)"}
