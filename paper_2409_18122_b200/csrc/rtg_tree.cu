@@ -91,6 +91,7 @@ struct Tree {
     int *scanA, *scanB;             // per-layer scan scratch (cell counts, kept flags); NULL: allocate
     int zeroA, zeroB;               // their leading ints that k_expand clears
     unsigned long long *sa, *sb;    // their keys
+    unsigned long long* fstat;      // this layer's eligible children: count, min key, max key (k_create)
 };
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long k) {   // splitmix64 finaliser
@@ -153,6 +154,7 @@ __global__ void k_tree_init(Tree t, TreeK k, double x, double y, double th) {
     t.nh[0] = h_of(k, x, y);
     t.npar[0] = -1; t.ndep[0] = 0;
     t.cnt[1] = 1;
+    t.fstat[0] = 0; t.fstat[1] = kEmptyKey; t.fstat[2] = 0;
     if (k.dedup) closed_put(t, k, lattice_key(k, x, y, th, t.cnt + 4), 0.0);
     if (at_goal(k, x, y)) {
         t.cand[0] = 0;
@@ -286,9 +288,8 @@ __global__ void k_close(Tree t, TreeK k) {
 // eligible for the next frontier with key f = g + h
 __global__ void k_create(Tree t, TreeK k, int depth) {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= k.W) return;
     unsigned long long fk = kEmptyKey;
-    if (t.acc[w]) {
+    if (w < k.W && t.acc[w]) {
         const int id = t.cnt[1] + t.rank[w];
         const double x = t.cx[w], y = t.cy[w], g = t.cg[w];
         t.nx[id] = x; t.ny[id] = y; t.nth[id] = t.cth[w]; t.ng[id] = g;
@@ -300,7 +301,22 @@ __global__ void k_create(Tree t, TreeK k, int depth) {
         if (at_goal(k, x, y)) t.cand[atomicAdd(&t.cnt[2], 1)] = id;
         else fk = dbits(__dadd_rn(g, h));
     }
-    t.fkey[w] = fk;
+    if (w < k.W) t.fkey[w] = fk;
+    // the layer's eligible count and key range for k_beam (one atomic triple per warp)
+    const bool el = fk != kEmptyKey && w < t.cnt[0] * k.P;
+    const unsigned bal = __ballot_sync(0xffffffffu, el);
+    if (bal == 0) return;
+    unsigned long long lo = el ? fk : kEmptyKey, hi = el ? fk : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&t.fstat[0], (unsigned long long)__popc(bal));
+        atomicMin(&t.fstat[1], lo);
+        atomicMax(&t.fstat[2], hi);
+    }
 }
 
 // ---- exact selection of the `need` smallest keys (a, b, id) among n items in one CTA: radix
@@ -437,47 +453,132 @@ __device__ __forceinline__ bool selected(const SelState& s, unsigned long long a
     return (id & s.mi) <= s.pi;
 }
 
-struct SrcBeam {   // children eligible for the frontier: (f, -, w)
-    const unsigned long long* fkey;
-    __device__ bool get(int i, unsigned long long& a, unsigned long long& b, unsigned& id) const {
-        a = fkey[i];
-        b = 0;
-        id = (unsigned)i;
-        return a != kEmptyKey;
+// exact selection of the `need` smallest (f, w) among the n children for the beam: the eligible keys
+// all lie in [kmin, kmax], so their common bit prefix is decided before the first pass and the radix
+// digits start at the highest bit where kmin and kmax differ; then the child index w (unique) decides
+// ties.  Keys are read two per 16-byte load, eight loads in flight per thread.
+__device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int n, int need, unsigned long long kmin,
+                                unsigned long long kmax) {
+    __shared__ int hist[kRadixBins];
+    __shared__ int s_wsum[kSelThreads / 32];
+    __shared__ int s_need, s_done, s_t, s_before;
+    __shared__ SelState s_st;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int top;   // bits still undecided: [top - 1 .. 0] of the 96-bit key f(64) | w(32)
+    if (tid == 0) {
+        SelState z{0, 0, 0, 0, 0, 0};
+        const unsigned long long x = kmin ^ kmax;
+        const int hb = x ? 64 - __clzll((long long)x) : 0;
+        z.ma = hb == 64 ? 0ull : (~0ull << hb);
+        z.pa = kmin & z.ma;
+        s_st = z;
+        s_need = need;
+        s_done = 0;
+        s_t = 32 + hb;
     }
-};
+    __syncthreads();
+    top = s_t;
+    const int npair = (n + 1) >> 1;
+    const ulonglong2* f2 = reinterpret_cast<const ulonglong2*>(fkey);
+    while (top > 0) {
+        for (int j = tid; j < kRadixBins; j += blockDim.x) hist[j] = 0;
+        __syncthreads();
+        const SelState st = s_st;
+        const int wd = top > 32 ? min(kRadixBits, top - 32) : min(kRadixBits, top);
+        const int lo = top - wd;
+        const unsigned dmask = (1u << wd) - 1u;
+        for (int j0 = tid; j0 < npair; j0 += 8 * blockDim.x) {
+            ulonglong2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = j0 + u * blockDim.x;
+                v[u] = j < npair ? f2[j] : make_ulonglong2(kEmptyKey, kEmptyKey);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const unsigned long long a = h ? v[u].y : v[u].x;
+                    const unsigned id = (unsigned)(2 * (j0 + u * blockDim.x) + h);
+                    if (a == kEmptyKey || (int)id >= n || (a & st.ma) != st.pa || (id & st.mi) != st.pi) continue;
+                    const unsigned dg = lo >= 32 ? (unsigned)(a >> (lo - 32)) & dmask : (id >> lo) & dmask;
+                    atomicAdd(&hist[dg], 1);
+                }
+            }
+        }
+        __syncthreads();
+        const int b0 = 2 * tid;
+        const int h0 = hist[b0], h1 = hist[b0 + 1];
+        int inc = h0 + h1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) s_wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            const int v = s_wsum[lane];
+            int w = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += u;
+            }
+            s_wsum[lane] = w - v;
+        }
+        __syncthreads();
+        const int before = s_wsum[wid] + inc - (h0 + h1);
+        const int nd = s_need;
+        if (before < nd && before + h0 >= nd) {
+            s_t = b0;
+            s_before = before;
+        } else if (before + h0 < nd && before + h0 + h1 >= nd) {
+            s_t = b0 + 1;
+            s_before = before + h0;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned t = (unsigned)s_t;
+            s_need -= s_before;
+            if (hist[t] == s_need) s_done = 1;
+            SelState ns = s_st;
+            if (lo >= 32) {
+                ns.pa |= (unsigned long long)t << (lo - 32);
+                ns.ma |= (unsigned long long)dmask << (lo - 32);
+            } else {
+                ns.pi |= t << lo;
+                ns.mi |= dmask << lo;
+            }
+            s_st = ns;
+        }
+        __syncthreads();
+        if (s_done) break;
+        top = lo;
+    }
+    return s_st;
+}
 
 // ---- next frontier (one CTA): layer totals, beam select, ordered compaction in creation order
 __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     __shared__ int s_warp[kSelThreads / 32];
-    __shared__ int s_elig, s_n;
+    __shared__ int s_n;
+    __shared__ unsigned long long s_fs[3];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) {
         const int M = t.cnt[0];
         s_n = M * k.P;                                  // this layer's children
         t.cnt[3] += M;
         t.cnt[1] += t.rank[k.W - 1] + t.acc[k.W - 1];   // nodes created by this layer
-        s_elig = 0;
+        // eligible count and key range gathered by k_create; cleared for the next layer
+        s_fs[0] = t.fstat[0]; s_fs[1] = t.fstat[1]; s_fs[2] = t.fstat[2];
+        t.fstat[0] = 0; t.fstat[1] = kEmptyKey; t.fstat[2] = 0;
     }
     __syncthreads();
     const int n = s_n;
-    int loc = 0;
-    for (int i0 = tid; i0 < n; i0 += 8 * blockDim.x) {   // eight loads in flight per thread
-        unsigned long long f[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * blockDim.x;
-            f[u] = i < n ? t.fkey[i] : kEmptyKey;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) loc += f[u] != kEmptyKey;
-    }
-    loc = __reduce_add_sync(0xffffffffu, loc);
-    if (lane == 0) atomicAdd(&s_elig, loc);
-    __syncthreads();
-    const bool all = s_elig <= k.beam;
+    const bool all = s_fs[0] <= (unsigned long long)k.beam;
     SelState st{0, 0, 0, 0, 0, 0};
-    if (!all) st = block_select(SrcBeam{t.fkey}, n, k.beam, false);
+    if (!all) st = beam_select(t.fkey, n, k.beam, s_fs[1], s_fs[2]);
     // ordered compaction: warp w owns the contiguous children [c0, c1), 32 per ballot word; pass 1
     // keeps the selection bits in shared memory, pass 2 writes the selected node ids in order
     __shared__ unsigned s_bits[kMaxBeamWords];
@@ -486,15 +587,15 @@ __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     const int per = ((n + nw - 1) / nw + 31) & ~31;
     const int c0 = min(n, wid * per), c1 = min(n, c0 + per);
     int cnt = 0;
-    for (int b0 = c0; b0 < c1; b0 += 4 * 32) {
-        unsigned long long f[4];
+    for (int b0 = c0; b0 < c1; b0 += 8 * 32) {
+        unsigned long long f[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int i = b0 + 32 * u + lane;
             f[u] = i < c1 ? t.fkey[i] : kEmptyKey;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int b = b0 + 32 * u;
             const bool sel = f[u] != kEmptyKey && (all || selected(st, f[u], 0, (unsigned)(b + lane)));
             const unsigned bal = __ballot_sync(0xffffffffu, sel);
@@ -519,17 +620,30 @@ __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     }
     __syncthreads();
     int pos = s_warp[wid];
-    for (int b = c0; b < c1; b += 32) {
-        unsigned bal;
-        if (use_bits) {
-            bal = s_bits[b >> 5];
-        } else {   // more children than the bit buffer holds: evaluate the selection again
-            const int i = b + lane;
-            const unsigned long long f = i < c1 ? t.fkey[i] : kEmptyKey;
-            bal = __ballot_sync(0xffffffffu, f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i)));
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b0 = c0; b0 < c1; b0 += 8 * 32) {   // eight words per step: their id loads in flight together
+        unsigned bal[8];
+        int id[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int b = b0 + 32 * u;
+            if (b >= c1) {
+                bal[u] = 0u;
+            } else if (use_bits) {
+                bal[u] = s_bits[b >> 5];
+            } else {   // more children than the bit buffer holds: evaluate the selection again
+                const int i = b + lane;
+                const unsigned long long f = i < c1 ? t.fkey[i] : kEmptyKey;
+                bal[u] = __ballot_sync(0xffffffffu, f != kEmptyKey && (all || selected(st, f, 0, (unsigned)i)));
+            }
         }
-        if ((bal >> lane) & 1u) t.frontier[pos + __popc(bal & ((1u << lane) - 1u))] = t.cid[b + lane];
-        pos += __popc(bal);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) id[u] = ((bal[u] >> lane) & 1u) ? t.cid[b0 + 32 * u + lane] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if ((bal[u] >> lane) & 1u) t.frontier[pos + __popc(bal[u] & lt)] = id[u];
+            pos += __popc(bal[u]);
+        }
     }
 }
 
@@ -709,6 +823,7 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
     const size_t o_sel = carve(sizeof(int) * 2 * nt), o_sab = carve(sizeof(unsigned long long) * 2 * nt);
     const size_t o_w = carve(sizeof(float) * 4 * nt * T), o_cost = carve(sizeof(double) * nt);
     const size_t o_ctl = carve(sizeof(double) * ctl.size()), o_st = carve(sizeof(unsigned long long) * 4);
+    const size_t o_fs = carve(sizeof(unsigned long long) * 3);
     // the per-layer scans run from pre-cleared scratch when they fit one single-pass launch
     const bool fastA = (long long)lcap <= 64LL * 4096;
     const bool fastB = (long long)W <= 64LL * 4096;
@@ -736,6 +851,7 @@ rtg_status plan_tree(rtg_map_s* m, const float start[3], const float goal[2], co
     t.cnt = (int*)(mem + o_cnt);
     t.sel = (int*)(mem + o_sel); t.order = t.sel + nt;
     t.sa = (unsigned long long*)(mem + o_sab); t.sb = t.sa + nt;
+    t.fstat = (unsigned long long*)(mem + o_fs);
     t.scanA = fastA && k.dedup ? (int*)(mem + o_sa) : nullptr;
     t.scanB = fastB ? (int*)(mem + o_sb) : nullptr;
     t.zeroA = (int)scan_i32_zero_ints((long long)lcap);
