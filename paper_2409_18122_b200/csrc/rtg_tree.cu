@@ -456,13 +456,18 @@ __device__ __forceinline__ bool selected(const SelState& s, unsigned long long a
 // exact selection of the `need` smallest (f, w) among the n children for the beam: the eligible keys
 // all lie in [kmin, kmax], so their common bit prefix is decided before the first pass and the radix
 // digits start at the highest bit where kmin and kmax differ; then the child index w (unique) decides
-// ties.  Keys are read two per 16-byte load, eight loads in flight per thread.
-__device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int n, int need, unsigned long long kmin,
-                                unsigned long long kmax) {
+// ties.  Keys are read two per 16-byte load, eight loads in flight per thread; once at most kBeamCand
+// items match the decided prefix, the pass that reads them also copies them to shared memory and the
+// remaining passes read only that copy.
+constexpr int kBeamCand = 1024;
+__device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int n, int need, int elig,
+                                unsigned long long kmin, unsigned long long kmax) {
     __shared__ int hist[kRadixBins];
     __shared__ int s_wsum[kSelThreads / 32];
-    __shared__ int s_need, s_done, s_t, s_before;
+    __shared__ int s_need, s_done, s_t, s_before, s_match, s_nc, s_ncw;
     __shared__ SelState s_st;
+    __shared__ unsigned long long s_ca[kBeamCand];
+    __shared__ unsigned s_ci[kBeamCand];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int top;   // bits still undecided: [top - 1 .. 0] of the 96-bit key f(64) | w(32)
     if (tid == 0) {
@@ -475,6 +480,9 @@ __device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int
         s_need = need;
         s_done = 0;
         s_t = 32 + hb;
+        s_match = elig;   // items matching the decided prefix
+        s_nc = -1;        // shared-memory copy: not taken
+        s_ncw = 0;
     }
     __syncthreads();
     top = s_t;
@@ -487,7 +495,16 @@ __device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int
         const int wd = top > 32 ? min(kRadixBits, top - 32) : min(kRadixBits, top);
         const int lo = top - wd;
         const unsigned dmask = (1u << wd) - 1u;
-        for (int j0 = tid; j0 < npair; j0 += 8 * blockDim.x) {
+        const int nc = s_nc;
+        const bool take = nc < 0 && s_match <= kBeamCand;
+        for (int i = tid; i < nc; i += blockDim.x) {   // from the shared copy (nc < 0: skipped)
+            const unsigned long long a = s_ca[i];
+            const unsigned id = s_ci[i];
+            if ((a & st.ma) != st.pa || (id & st.mi) != st.pi) continue;
+            const unsigned dg = lo >= 32 ? (unsigned)(a >> (lo - 32)) & dmask : (id >> lo) & dmask;
+            atomicAdd(&hist[dg], 1);
+        }
+        for (int j0 = tid; nc < 0 && j0 < npair; j0 += 8 * blockDim.x) {
             ulonglong2 v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -503,6 +520,11 @@ __device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int
                     if (a == kEmptyKey || (int)id >= n || (a & st.ma) != st.pa || (id & st.mi) != st.pi) continue;
                     const unsigned dg = lo >= 32 ? (unsigned)(a >> (lo - 32)) & dmask : (id >> lo) & dmask;
                     atomicAdd(&hist[dg], 1);
+                    if (take) {
+                        const int c = atomicAdd(&s_ncw, 1);
+                        s_ca[c] = a;
+                        s_ci[c] = id;
+                    }
                 }
             }
         }
@@ -542,6 +564,8 @@ __device__ SelState beam_select(const unsigned long long* __restrict__ fkey, int
             const unsigned t = (unsigned)s_t;
             s_need -= s_before;
             if (hist[t] == s_need) s_done = 1;
+            s_match = hist[t];
+            if (take) s_nc = s_ncw;
             SelState ns = s_st;
             if (lo >= 32) {
                 ns.pa |= (unsigned long long)t << (lo - 32);
@@ -578,7 +602,7 @@ __global__ void __launch_bounds__(kSelThreads) k_beam(Tree t, TreeK k) {
     const int n = s_n;
     const bool all = s_fs[0] <= (unsigned long long)k.beam;
     SelState st{0, 0, 0, 0, 0, 0};
-    if (!all) st = beam_select(t.fkey, n, k.beam, s_fs[1], s_fs[2]);
+    if (!all) st = beam_select(t.fkey, n, k.beam, (int)s_fs[0], s_fs[1], s_fs[2]);
     // ordered compaction: warp w owns the contiguous children [c0, c1), 32 per ballot word; pass 1
     // keeps the selection bits in shared memory, pass 2 writes the selected node ids in order
     __shared__ unsigned s_bits[kMaxBeamWords];
