@@ -166,10 +166,16 @@ __global__ void k_tree_init(Tree t, TreeK k, double x, double y, double th) {
     }
 }
 
+// resident 256-thread blocks per SM for k_expand: 3 = 80 registers, spill-free (4 = 64 registers with
+// spills measured 1 % slower at N = 5M, equal at 2M)
+#ifndef RTG_EXPAND_MINB
+#define RTG_EXPAND_MINB 3
+#endif
+
 // ---- expansion: one warp per (frontier node m, control p), all W = beam * P warps launched, those
 // past M * P only clear their child.  Samples j = 1 .. S-1 at t_j = j dt / (S-1) (j = 0 is the
 // parent's state, checked when it was created); ok = no sample collides; child = state at dt.
-__global__ void __launch_bounds__(256) k_expand(Tree t, TreeK k, const double* __restrict__ ctl,
+__global__ void __launch_bounds__(256, RTG_EXPAND_MINB) k_expand(Tree t, TreeK k, const double* __restrict__ ctl,
                                                 const CRec* __restrict__ crec, const CMat* __restrict__ cmat,
                                                 const CSrc* __restrict__ csrc, const rtg_robot rb,
                                                 const int* __restrict__ cstart, ColGridK g, float gq, int n_col,
