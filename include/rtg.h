@@ -331,7 +331,8 @@ rtg_status rtg_cost_benefit(const double* omega, const double* d, int K, void* s
  * *out: trajectory handle with K = *n_found (<= n_traj), T = max_depth + 1, waypoint l = the
  * state after l primitives (l = 0: start; NaN after the candidate's last primitive); cost (host,
  * n_traj entries or NULL) receives the candidates' g; stats (host long long[4] or NULL):
- * nodes expanded, nodes created, samples checked, collision candidates tested.  Synchronises the
+ * nodes expanded, nodes created, samples checked (a primitive's samples are tested together, so
+ * every sample of an expanded primitive counts), collision candidates tested.  Synchronises the
  * stream.  Errors: RTG_ERR_INVALID_ARGUMENT (bad parameters), RTG_ERR_NO_FEASIBLE (nothing
  * collision-free grows from the start: *n_found = 0), RTG_ERR_CUDA.
  */

@@ -166,6 +166,85 @@ __global__ void k_tree_init(Tree t, TreeK k, double x, double y, double th) {
     }
 }
 
+// does any of the nj points held by lanes 0 .. nj-1 (px, py; height z) collide?  The candidates of
+// the union of their cell boxes are loaded once and each is tested against every point: a Gaussian
+// outside a point's own box lies beyond g.R > its bounding radius, so the sphere test rejects it for
+// that point and every decision equals the one-point test (warp_point_collides).
+__device__ bool warp_points_collide_any(float px, float py, float z, int nj, const CRec* __restrict__ crec,
+                                        const CMat* __restrict__ cmat, const CSrc* __restrict__ csrc,
+                                        const rtg_robot& rb, const int* __restrict__ cstart, const ColGridK& g,
+                                        float gq, unsigned& nref, unsigned long long& ntest) {
+    constexpr unsigned kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool mine = lane < nj && isfinite(px) && isfinite(py) && isfinite(z);
+    int ix0 = INT_MAX, ix1 = -1, iy0 = INT_MAX, iy1 = -1;
+    if (mine) {
+        ix0 = max(0, clamp_cell((px - g.R - g.ox) / g.h, 0, g.nx));
+        ix1 = min(g.nx - 1, clamp_cell((px + g.R - g.ox) / g.h, 0, g.nx));
+        iy0 = max(0, clamp_cell((py - g.R - g.oy) / g.h, 0, g.ny));
+        iy1 = min(g.ny - 1, clamp_cell((py + g.R - g.oy) / g.h, 0, g.ny));
+        if (ix0 > ix1 || iy0 > iy1) { ix0 = iy0 = INT_MAX; ix1 = iy1 = -1; }
+    }
+    ix0 = __reduce_min_sync(kAll, ix0);
+    ix1 = __reduce_max_sync(kAll, ix1);
+    iy0 = __reduce_min_sync(kAll, iy0);
+    iy1 = __reduce_max_sync(kAll, iy1);
+    const int iz0 = max(0, clamp_cell((z - g.R - g.oz) / g.h, 0, g.nz));
+    const int iz1 = min(g.nz - 1, clamp_cell((z + g.R - g.oz) / g.h, 0, g.nz));
+    if (ix0 > ix1 || iy0 > iy1 || iz0 > iz1) return false;
+    const unsigned live = __ballot_sync(kAll, mine);
+    const int nyr = iy1 - iy0 + 1;
+    const int nrows = nyr * (iz1 - iz0 + 1);
+    bool hit = false;
+    for (int r0 = 0; r0 < nrows && !hit; r0 += 32) {
+        const int r = r0 + lane;
+        int beg = 0, len = 0;
+        if (r < nrows) {
+            const int iz = iz0 + r / nyr, iy = iy0 + r % nyr;
+            const long long base = ((long long)iz * g.ny + iy) * g.nx;
+            beg = cstart[base + ix0];
+            len = cstart[base + ix1 + 1] - beg;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kAll, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(kAll, incl, 31);
+        const int roff = beg - (incl - len);
+        for (int b0 = 0; b0 < total; b0 += 32) {
+            const int pos = b0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int v = __shfl_sync(kAll, incl, owner + st - 1);
+                if (v <= pos) owner += st;
+            }
+            const int gi = pos + __shfl_sync(kAll, roff, owner);
+            CRec A;
+            if (pos < total) A = crec[gi];
+            bool h = false;
+            for (unsigned lv = live; lv; lv &= lv - 1) {   // every live point (warp-uniform loop)
+                const int jj = __ffs(lv) - 1;
+                const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj);
+                if (pos < total && !h) {
+                    const float dx = qx - A.x, dy = qy - A.y, dz = z - A.z;
+                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (d2 < A.rb2) h = collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, qx, qy, z, A.x, A.y, A.z, nref);
+                }
+            }
+            ntest += (unsigned long long)min(32, total - b0) * __popc(live);
+            if (__any_sync(kAll, h)) {
+                hit = true;
+                break;
+            }
+        }
+        __syncwarp();
+    }
+    return hit;
+}
+
 // resident 256-thread blocks per SM for k_expand: 3 = 80 registers, spill-free (4 = 64 registers with
 // spills measured 1 % slower at N = 5M, equal at 2M)
 #ifndef RTG_EXPAND_MINB
@@ -214,12 +293,9 @@ __global__ void __launch_bounds__(256, RTG_EXPAND_MINB) k_expand(Tree t, TreeK k
         }
         const float sx = __double2float_rn(lx), sy = __double2float_rn(ly);
         const int nj = min(32, k.S - j0);
-        for (int jj = 0; jj < nj; ++jj) {
-            const float px = __shfl_sync(0xffffffffu, sx, jj), py = __shfl_sync(0xffffffffu, sy, jj);
-            if (!hit && n_col > 0) {
-                hit = warp_point_collides(px, py, k.z, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
-                ++checked;
-            }
+        if (!hit && n_col > 0) {   // the chunk's samples tested together (cok = no sample collides)
+            hit = warp_points_collide_any(sx, sy, k.z, nj, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
+            checked += nj;
         }
         x = __shfl_sync(0xffffffffu, lx, nj - 1);
         y = __shfl_sync(0xffffffffu, ly, nj - 1);
