@@ -366,6 +366,95 @@ __device__ __forceinline__ bool warp_point_collides(float px, float py, float pz
     return hit;
 }
 
+// which of the nj points held by lanes 0 .. nj-1 collide (bit j: lane j's point; warp-uniform)?
+// The candidates of the union of their cell boxes are loaded once and each is tested against every
+// point: a Gaussian outside a point's own box lies beyond g.R, past its bounding radius, so the sphere
+// test rejects it for that point and every decision equals the one-point test above.  Points at or
+// past the lowest colliding one are skipped when only the first collision matters (first_only).
+__device__ __forceinline__ unsigned warp_points_collide_mask(float px, float py, float pz, int nj, bool first_only,
+                                                             const CRec* __restrict__ crec,
+                                                             const CMat* __restrict__ cmat,
+                                                             const CSrc* __restrict__ csrc, const rtg_robot& rb,
+                                                             const int* __restrict__ cstart, const ColGridK& g,
+                                                             float gq, unsigned& nref, unsigned long long& ntest) {
+    constexpr unsigned kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool mine = lane < nj && isfinite(px) && isfinite(py) && isfinite(pz);
+    int ix0 = INT_MAX, ix1 = -1, iy0 = INT_MAX, iy1 = -1, iz0 = INT_MAX, iz1 = -1;
+    if (mine) {
+        const int a0 = max(0, clamp_cell((px - g.R - g.ox) / g.h, 0, g.nx));
+        const int a1 = min(g.nx - 1, clamp_cell((px + g.R - g.ox) / g.h, 0, g.nx));
+        const int b0 = max(0, clamp_cell((py - g.R - g.oy) / g.h, 0, g.ny));
+        const int b1 = min(g.ny - 1, clamp_cell((py + g.R - g.oy) / g.h, 0, g.ny));
+        const int c0 = max(0, clamp_cell((pz - g.R - g.oz) / g.h, 0, g.nz));
+        const int c1 = min(g.nz - 1, clamp_cell((pz + g.R - g.oz) / g.h, 0, g.nz));
+        if (a0 <= a1 && b0 <= b1 && c0 <= c1) {
+            ix0 = a0; ix1 = a1; iy0 = b0; iy1 = b1; iz0 = c0; iz1 = c1;
+        }
+    }
+    const unsigned live = __ballot_sync(kAll, ix0 <= ix1);
+    if (!live) return 0u;
+    ix0 = __reduce_min_sync(kAll, ix0);
+    ix1 = __reduce_max_sync(kAll, ix1);
+    iy0 = __reduce_min_sync(kAll, iy0);
+    iy1 = __reduce_max_sync(kAll, iy1);
+    iz0 = __reduce_min_sync(kAll, iz0);
+    iz1 = __reduce_max_sync(kAll, iz1);
+    const int nyr = iy1 - iy0 + 1;
+    const int nrows = nyr * (iz1 - iz0 + 1);
+    unsigned hits = 0u, todo = live;
+    for (int r0 = 0; r0 < nrows && todo; r0 += 32) {
+        const int r = r0 + lane;
+        int beg = 0, len = 0;
+        if (r < nrows) {
+            const int iz = iz0 + r / nyr, iy = iy0 + r % nyr;
+            const long long base = ((long long)iz * g.ny + iy) * g.nx;
+            beg = cstart[base + ix0];
+            len = cstart[base + ix1 + 1] - beg;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kAll, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(kAll, incl, 31);
+        const int roff = beg - (incl - len);
+        for (int b0 = 0; b0 < total && todo; b0 += 32) {
+            const int pos = b0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int v = __shfl_sync(kAll, incl, owner + st - 1);
+                if (v <= pos) owner += st;
+            }
+            const int gi = pos + __shfl_sync(kAll, roff, owner);
+            CRec A;
+            if (pos < total) A = crec[gi];
+            unsigned mh = 0u;
+            for (unsigned lv = todo; lv; lv &= lv - 1) {   // warp-uniform loop over the open points
+                const int jj = __ffs(lv) - 1;
+                const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj),
+                            qz = __shfl_sync(kAll, pz, jj);
+                if (pos < total) {
+                    const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
+                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (d2 < A.rb2 && collide_full(cmat[gi].m, dx, dy, dz, gq, &csrc[gi], rb, qx, qy, qz, A.x, A.y,
+                                                   A.z, nref))
+                        mh |= 1u << jj;
+                }
+            }
+            ntest += (unsigned long long)min(32, total - b0) * __popc(todo);
+            mh = __reduce_or_sync(kAll, mh);
+            hits |= mh;
+            todo &= ~mh;
+            if (first_only && hits) todo &= (1u << (__ffs(hits) - 1)) - 1u;   // only earlier points matter
+        }
+        __syncwarp();
+    }
+    return hits;
+}
+
 // ------------------------------------------------------------------ misc helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

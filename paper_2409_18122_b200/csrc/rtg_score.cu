@@ -184,16 +184,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
         if (lane == 0) fc = *(volatile int*)(first_col + k);
         fc = __shfl_sync(kFull, fc, 0);
         if (!all_waypoints && fc < t0) continue;
-        for (int t = t0; t < t1; ++t) {
-            const long long i = (long long)k * T + t;
-            const float px = X[i], py = Y[i], pz = Zw[i];
-            const bool hit = warp_point_collides(px, py, pz, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
-            if (all_waypoints && lane == 0) wp_col[i] = hit ? 1 : 0;
-            if (hit) {
-                if (lane == 0) atomicMin(first_col + k, t);
-                if (!all_waypoints) break;
-            }
+        // the chunk's waypoints tested together (lane j holds waypoint t0 + j)
+        const long long i0 = (long long)k * T + t0;
+        const int nj = t1 - t0;
+        float px = NAN, py = NAN, pz = NAN;
+        if (lane < nj) {
+            px = X[i0 + lane];
+            py = Y[i0 + lane];
+            pz = Zw[i0 + lane];
         }
+        const unsigned hits = warp_points_collide_mask(px, py, pz, nj, !all_waypoints, crec, cmat, csrc, rb, cstart, g,
+                                                       gq, nref, ntest);
+        if (all_waypoints && lane < nj) wp_col[i0 + lane] = (hits >> lane) & 1u;
+        if (hits && lane == 0) atomicMin(first_col + k, t0 + __ffs(hits) - 1);
     }
     if (stats) {
         nref = __reduce_add_sync(kFull, nref);
