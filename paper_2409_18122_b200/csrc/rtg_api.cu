@@ -82,6 +82,16 @@ void dev_free(void* p, cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
 }
 
+// frees a stream-ordered device block on every return path (the API_CK early returns included)
+struct DevFreeGuard {
+    void** p;
+    cudaStream_t st;
+    ~DevFreeGuard() {
+        if (*p) dev_free(*p, st);
+        *p = nullptr;
+    }
+};
+
 // defined in rtg_map.cu / rtg_score.cu
 rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const float* scales, const float* opacity,
                      const float* w, const unsigned char* flags, const rtg_map_options* opt, cudaStream_t st);
@@ -588,6 +598,7 @@ rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_sc
     const long long per = T / p->info_stride;
     const long long list_max = K * per;
     Scratch sc;
+    DevFreeGuard sc_guard{&sc.block, st};
     prof_begin(PH_OTHER, st);
     API_CK(scratch_alloc(sc, K, T, list_max, cam, st), &m->poisoned);
     const CamK ck = make_cam(*cam, sc.cam64);
@@ -622,8 +633,7 @@ rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_sc
     API_CK(launch_reduce(m, tr, pp, sc.first_col, sc.wp_gq, sc.wp_nh, sc.wp_nl, first_col, feasible, gain, utility, st),
            &m->poisoned);
     prof_end(PH_REDUCE, st);
-    dev_free(sc.block, st);
-    return RTG_OK;
+    return RTG_OK;   // sc_guard frees the scratch block (stream-ordered)
 }
 
 rtg_status rtg_best(const double* utility, int K, long long index_base, void* stream, rtg_best_result* out) {
@@ -634,15 +644,17 @@ rtg_status rtg_best(const double* utility, int K, long long index_base, void* st
     cudaStream_t st = (cudaStream_t)stream;
     void* d = nullptr;
     API_CK(dev_alloc(&d, 16, st), nullptr);
-    prof_begin(PH_BEST, st);
-    API_CK(launch_best(utility, K, index_base, d, st), nullptr);
-    prof_end(PH_BEST, st);
     struct {
         double score;
         long long index;
     } h;
-    API_CK(cudaMemcpyAsync(&h, d, 16, cudaMemcpyDeviceToHost, st), nullptr);
-    dev_free(d, st);
+    {
+        DevFreeGuard d_guard{&d, st};
+        prof_begin(PH_BEST, st);
+        API_CK(launch_best(utility, K, index_base, d, st), nullptr);
+        prof_end(PH_BEST, st);
+        API_CK(cudaMemcpyAsync(&h, d, 16, cudaMemcpyDeviceToHost, st), nullptr);
+    }
     API_CK(cudaStreamSynchronize(st), nullptr);
     out->score = h.score;
     out->index = h.index;
@@ -773,13 +785,15 @@ rtg_status rtg_cost_benefit(const double* omega, const double* d, int K, void* s
     cudaStream_t st = (cudaStream_t)stream;
     void* dv = nullptr;
     API_CK(dev_alloc(&dv, 16, st), nullptr);
-    API_CK(launch_cost_benefit(omega, d, K, dv, st), nullptr);
     struct {
         double score;
         long long index;
     } h;
-    API_CK(cudaMemcpyAsync(&h, dv, 16, cudaMemcpyDeviceToHost, st), nullptr);
-    dev_free(dv, st);
+    {
+        DevFreeGuard dv_guard{&dv, st};
+        API_CK(launch_cost_benefit(omega, d, K, dv, st), nullptr);
+        API_CK(cudaMemcpyAsync(&h, dv, 16, cudaMemcpyDeviceToHost, st), nullptr);
+    }
     API_CK(cudaStreamSynchronize(st), nullptr);
     out->score = h.score;
     out->index = h.index;
@@ -828,6 +842,7 @@ rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const 
     s = classify_map(m, p->variant, p->k_sigma, p->tau_hi, p->tau_lo, st);
     if (s != RTG_OK) return s;
     Scratch sc;
+    DevFreeGuard sc_guard{&sc.block, st};
     API_CK(scratch_alloc(sc, K, T, KT, cam, st), &m->poisoned);
     const CamK ck = make_cam(*cam, sc.cam64);
     note_launch(), k_fill_int<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(sc.first_col, K, (int)T);
@@ -849,6 +864,7 @@ rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const 
     unsigned long long hs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     API_CK(cudaMemcpyAsync(hs, sc.stats, sizeof(hs), cudaMemcpyDeviceToHost, st), &m->poisoned);
     dev_free(sc.block, st);
+    sc.block = nullptr;
     API_CK(cudaStreamSynchronize(st), &m->poisoned);
     if (stats)
         for (int i = 0; i < 8; ++i) stats[i] = (long long)hs[i];

@@ -366,6 +366,8 @@ __device__ __forceinline__ bool warp_point_collides(float px, float py, float pz
     return hit;
 }
 
+constexpr int kUnionFactor = 3;
+
 // which of the nj points held by lanes 0 .. nj-1 collide (bit j: lane j's point; warp-uniform)?
 // The candidates of the union of their cell boxes are loaded once and each is tested against every
 // point: a Gaussian outside a point's own box lies beyond g.R, past its bounding radius, so the sphere
@@ -394,12 +396,29 @@ __device__ __forceinline__ unsigned warp_points_collide_mask(float px, float py,
     }
     const unsigned live = __ballot_sync(kAll, ix0 <= ix1);
     if (!live) return 0u;
+    // the union box grows with the square (cube) of the points' spread: sparse or diagonal waypoints
+    // (1 s primitives, user trajectories) would load far more candidates than their own boxes hold.
+    // Above kUnionFactor x the sum of the per-point boxes, test the points one at a time instead.
+    const unsigned own = ix0 <= ix1 ? (unsigned)((ix1 - ix0 + 1) * (iy1 - iy0 + 1) * (iz1 - iz0 + 1)) : 0u;
+    const unsigned own_sum = __reduce_add_sync(kAll, own);
     ix0 = __reduce_min_sync(kAll, ix0);
     ix1 = __reduce_max_sync(kAll, ix1);
     iy0 = __reduce_min_sync(kAll, iy0);
     iy1 = __reduce_max_sync(kAll, iy1);
     iz0 = __reduce_min_sync(kAll, iz0);
     iz1 = __reduce_max_sync(kAll, iz1);
+    if ((long long)(ix1 - ix0 + 1) * (iy1 - iy0 + 1) * (iz1 - iz0 + 1) > (long long)kUnionFactor * own_sum) {
+        unsigned hits = 0u;
+        for (unsigned lv = live; lv; lv &= lv - 1) {   // ascending: the first hit is the lowest point
+            const int jj = __ffs(lv) - 1;
+            const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj), qz = __shfl_sync(kAll, pz, jj);
+            if (warp_point_collides(qx, qy, qz, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest)) {
+                hits |= 1u << jj;
+                if (first_only) break;
+            }
+        }
+        return hits;
+    }
     const int nyr = iy1 - iy0 + 1;
     const int nrows = nyr * (iz1 - iz0 + 1);
     unsigned hits = 0u, todo = live;

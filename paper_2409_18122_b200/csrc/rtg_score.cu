@@ -162,6 +162,7 @@ constexpr int kWarps = 8;   // warps per block of the persistent culled kernels
 #define RTG_COL_CHUNK 10
 #endif
 constexpr int kColChunk = RTG_COL_CHUNK;
+static_assert(kColChunk >= 1 && kColChunk <= 32, "k_col_culled holds one waypoint of a chunk per lane");
 
 __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,

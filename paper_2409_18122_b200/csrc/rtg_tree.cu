@@ -185,6 +185,8 @@ __device__ bool warp_points_collide_any(float px, float py, float z, int nj, con
         iy1 = min(g.ny - 1, clamp_cell((py + g.R - g.oy) / g.h, 0, g.ny));
         if (ix0 > ix1 || iy0 > iy1) { ix0 = iy0 = INT_MAX; ix1 = iy1 = -1; }
     }
+    const unsigned own = ix0 <= ix1 ? (unsigned)((ix1 - ix0 + 1) * (iy1 - iy0 + 1)) : 0u;
+    const unsigned own_sum = __reduce_add_sync(kAll, own);
     ix0 = __reduce_min_sync(kAll, ix0);
     ix1 = __reduce_max_sync(kAll, ix1);
     iy0 = __reduce_min_sync(kAll, iy0);
@@ -193,6 +195,16 @@ __device__ bool warp_points_collide_any(float px, float py, float z, int nj, con
     const int iz1 = min(g.nz - 1, clamp_cell((z + g.R - g.oz) / g.h, 0, g.nz));
     if (ix0 > ix1 || iy0 > iy1 || iz0 > iz1) return false;
     const unsigned live = __ballot_sync(kAll, mine);
+    // spread-out points (long primitives): the union box would hold many times the candidates of the
+    // points' own boxes -- test them one at a time (same decisions, see warp_points_collide_mask)
+    if ((long long)(ix1 - ix0 + 1) * (iy1 - iy0 + 1) > (long long)kUnionFactor * own_sum) {
+        for (unsigned lv = live; lv; lv &= lv - 1) {
+            const int jj = __ffs(lv) - 1;
+            const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj);
+            if (warp_point_collides(qx, qy, z, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest)) return true;
+        }
+        return false;
+    }
     const int nyr = iy1 - iy0 + 1;
     const int nrows = nyr * (iz1 - iz0 + 1);
     bool hit = false;

@@ -80,18 +80,27 @@ def unpack_key(key: int) -> Tuple[float, int]:
 
 
 def global_best_packed(score: float, local_idx: int, rank: int, world: int, device=None) -> Tuple[float, int]:
-    """Like global_best, with one all_reduce(MAX) of an 8-byte key instead of an all_gather.
-    Raises ValueError when the local best is not an integer utility (use global_best then)."""
+    """Like global_best, with one all_reduce(MAX) of a 16-byte (key, invalid) pair instead of an
+    all_gather.  A rank whose local best cannot be packed (not an integer utility, or an index
+    beyond 2^32 - 2) does not raise before the collective -- that would leave the other ranks
+    blocked in it -- but sets `invalid`; when any rank did, every rank falls back to global_best."""
     import torch
     import torch.distributed as dist
     gidx = local_to_global(local_idx, rank, world)
-    key = pack_key(score, gidx)
+    try:
+        key, invalid = pack_key(score, gidx), 0
+    except ValueError:
+        if world == 1:
+            raise
+        key, invalid = _KEY_NONE, 1
     if world == 1:
         return unpack_key(key)
     dev = device if device is not None else torch.device("cpu")
-    t = torch.tensor([key], dtype=torch.int64, device=dev)
+    t = torch.tensor([key, invalid], dtype=torch.int64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return unpack_key(int(t.item()))
+    if int(t[1].item()):
+        return global_best(score, local_idx, rank, world, device=device)
+    return unpack_key(int(t[0].item()))
 
 
 def gather_outputs(first_col, feasible, gain, utility, K: int, rank: int, world: int, device=None):

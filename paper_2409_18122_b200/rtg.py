@@ -183,6 +183,32 @@ def _ptr(a) -> Optional[int]:
     return a.data_ptr()
 
 
+_DT = {"float32": "float32", "torch.float32": "float32", "float64": "float64", "torch.float64": "float64",
+       "int32": "int32", "torch.int32": "int32", "uint8": "uint8", "torch.uint8": "uint8"}
+
+
+def _arg(name: str, a, dtype: str, shape=None, device: Optional[int] = None, cuda: bool = False, optional=False):
+    """Validate one array argument against the C ABI before its pointer crosses it: dtype (the ABI
+    reads raw memory, so a float64 numpy map would be read as float32 garbage), shape (a short
+    output buffer would be written past its end), contiguity and, for device memory, that the
+    tensor lives on the handle's device.  Returns the pointer (None for an optional NULL)."""
+    if a is None:
+        if optional:
+            return None
+        raise ValueError(f"{name}: required")
+    dt = _DT.get(str(a.dtype))
+    if dt != dtype:
+        raise TypeError(f"{name}: dtype {a.dtype}, the C ABI expects {dtype}")
+    if shape is not None and tuple(int(s) for s in a.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(a.shape)}, expected {tuple(shape)}")
+    is_cuda = (not isinstance(a, np.ndarray)) and a.is_cuda
+    if cuda and not is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    if is_cuda and device is not None and a.device.index != device:
+        raise ValueError(f"{name}: on cuda:{a.device.index}, the handle is on cuda:{device}")
+    return _ptr(a)
+
+
 def _kind(a) -> int:
     if isinstance(a, np.ndarray):
         return MEM_HOST
@@ -219,27 +245,28 @@ class Map:
         for a in (quats, scales, opacity, info_w, flags):
             if a is not None and _kind(a) != kind:
                 raise ValueError("all map arrays must live in the same memory (host or device)")
+        ptrs = (_arg("means", means, "float32", (3, n), device), _arg("quats", quats, "float32", (4, n), device),
+                _arg("scales", scales, "float32", (3, n), device), _arg("opacity", opacity, "float32", (n,), device),
+                _arg("info_w", info_w, "float32", (n,), device),
+                _arg("flags", flags, "uint8", (n,), device, optional=True))
         self._robot = Robot(float(r_robot), float(lambda_g), int(collide_rule))
         self.handle = _P()
         self.n = n
+        self.device = device
         self._keep = (means, quats, scales, opacity, info_w, flags)
         st = _stream(stream)
         if options is not None:
             opt = MapOptions(*[float(x) for x in options])
-            s = _lib.rtg_map_create_ex(device, n, kind, _ptr(means), _ptr(quats), _ptr(scales), _ptr(opacity),
-                                       _ptr(info_w), _ptr(flags), ctypes.byref(self._robot), ctypes.byref(opt), st,
+            s = _lib.rtg_map_create_ex(device, n, kind, *ptrs, ctypes.byref(self._robot), ctypes.byref(opt), st,
                                        ctypes.byref(self.handle))
         else:
-            s = _lib.rtg_map_create(device, n, kind, _ptr(means), _ptr(quats), _ptr(scales), _ptr(opacity),
-                                    _ptr(info_w), _ptr(flags), ctypes.byref(self._robot), st,
-                                    ctypes.byref(self.handle))
+            s = _lib.rtg_map_create(device, n, kind, *ptrs, ctypes.byref(self._robot), st, ctypes.byref(self.handle))
         _check(s, "rtg_map_create")
 
     def update_weights(self, info_w, stream=None) -> None:
         """rtg_map_update_weights: replace the ledger (input order) and reclassify (N4)."""
-        if int(info_w.shape[0]) != self.n:
-            raise ValueError("info_w must have one entry per Gaussian")
-        _check(_lib.rtg_map_update_weights(self.handle, _kind(info_w), _ptr(info_w), _stream(stream)),
+        p = _arg("info_w", info_w, "float32", (self.n,), self.device)
+        _check(_lib.rtg_map_update_weights(self.handle, _kind(info_w), p, _stream(stream)),
                "rtg_map_update_weights")
         self._keep = self._keep + (info_w,)
 
@@ -269,28 +296,38 @@ class Map:
 class Traj:
     """rtg_traj handle: x, y, z, yaw each [K, T] (trajectory-major)."""
 
-    def __init__(self, handle: _P, K: int, T: int):
+    def __init__(self, handle: _P, K: int, T: int, device: int = 0):
         self.handle = handle
         self.K = K
         self.T = T
+        self.device = device
+
+    @staticmethod
+    def _xyzyaw(x, y, z, yaw, device, cuda=False):
+        if len(x.shape) != 2:
+            raise ValueError("x: expected [K, T]")
+        K, T = (int(s) for s in x.shape)
+        kind = _kind(x)
+        for a in (y, z, yaw):
+            if _kind(a) != kind:
+                raise ValueError("x, y, z, yaw must live in the same memory (host or device)")
+        return K, T, kind, [_arg(nm, a, "float32", (K, T), device, cuda=cuda)
+                            for nm, a in (("x", x), ("y", y), ("z", z), ("yaw", yaw))]
 
     @classmethod
     def upload(cls, x, y, z, yaw, device=0, stream=None) -> "Traj":
-        K, T = (int(s) for s in x.shape)
-        kind = _kind(x)
+        K, T, kind, ptrs = cls._xyzyaw(x, y, z, yaw, device)
         h = _P()
-        _check(_lib.rtg_traj_upload(device, K, T, kind, _ptr(x), _ptr(y), _ptr(z), _ptr(yaw), _stream(stream),
-                                    ctypes.byref(h)), "rtg_traj_upload")
-        return cls(h, K, T)
+        _check(_lib.rtg_traj_upload(device, K, T, kind, *ptrs, _stream(stream), ctypes.byref(h)), "rtg_traj_upload")
+        return cls(h, K, T, device)
 
     @classmethod
     def wrap(cls, x, y, z, yaw, device=0) -> "Traj":
         """rtg_traj_wrap: borrow device tensors [K, T] without copying (kept referenced here)."""
-        K, T = (int(s) for s in x.shape)
+        K, T, _, ptrs = cls._xyzyaw(x, y, z, yaw, device, cuda=True)
         h = _P()
-        _check(_lib.rtg_traj_wrap(device, K, T, _ptr(x), _ptr(y), _ptr(z), _ptr(yaw), ctypes.byref(h)),
-               "rtg_traj_wrap")
-        t = cls(h, K, T)
+        _check(_lib.rtg_traj_wrap(device, K, T, *ptrs, ctypes.byref(h)), "rtg_traj_wrap")
+        t = cls(h, K, T, device)
         t._borrowed = (x, y, z, yaw)
         return t
 
@@ -299,39 +336,46 @@ class Traj:
         """rtg_traj_sample_double_integrator: constant accelerations (ax, ay)[K] from start (x, y, z)
         with velocity v0 (vx, vy)."""
         K = int(ax.shape[0])
+        if _kind(ay) != _kind(ax):
+            raise ValueError("ax, ay must live in the same memory")
+        pa, pb = _arg("ax", ax, "float32", (K,), device), _arg("ay", ay, "float32", (K,), device)
         st3 = (ctypes.c_float * 3)(*[float(s) for s in start[:3]])
         v2 = (ctypes.c_float * 2)(float(v0[0]), float(v0[1]))
         h = _P()
-        _check(_lib.rtg_traj_sample_double_integrator(device, K, int(T), float(dt), st3, v2, _ptr(ax), _ptr(ay),
+        _check(_lib.rtg_traj_sample_double_integrator(device, K, int(T), float(dt), st3, v2, pa, pb,
                                                       _kind(ax), _stream(stream), ctypes.byref(h)),
                "rtg_traj_sample_double_integrator")
-        return cls(h, K, int(T))
+        return cls(h, K, int(T), device)
 
     @classmethod
     def sample_unicycle(cls, v, omega, T: int, dt: float, start, device=0, stream=None) -> "Traj":
         K = int(v.shape[0])
+        if _kind(omega) != _kind(v):
+            raise ValueError("v, omega must live in the same memory")
+        pv, pw = _arg("v", v, "float32", (K,), device), _arg("omega", omega, "float32", (K,), device)
         st4 = (ctypes.c_float * 4)(*[float(s) for s in start])
         h = _P()
-        _check(_lib.rtg_traj_sample_unicycle(device, K, int(T), float(dt), st4, _ptr(v), _ptr(omega), _kind(v),
+        _check(_lib.rtg_traj_sample_unicycle(device, K, int(T), float(dt), st4, pv, pw, _kind(v),
                                              _stream(stream), ctypes.byref(h)), "rtg_traj_sample_unicycle")
-        return cls(h, K, int(T))
+        return cls(h, K, int(T), device)
 
     @classmethod
     def view_ring(cls, centroids, size: float, camera, n: int, z: float, device=0, stream=None):
         """rtg_traj_view_ring: n viewpoints per region centroid (centroids [3, R]) facing it at the
         shortest viewing distance (N2).  Returns (Traj with K = R n, T = 1, viewing distance)."""
         R = int(centroids.shape[-1])
+        pc = _arg("centroids", centroids, "float32", (3, R), device)
         cam = camera if isinstance(camera, Camera) else make_camera(camera)
         h = _P()
         d = ctypes.c_double()
-        _check(_lib.rtg_traj_view_ring(device, R, _kind(centroids), _ptr(centroids), float(size), ctypes.byref(cam),
+        _check(_lib.rtg_traj_view_ring(device, R, _kind(centroids), pc, float(size), ctypes.byref(cam),
                                        int(n), float(z), _stream(stream), ctypes.byref(h), ctypes.byref(d)),
                "rtg_traj_view_ring")
-        return cls(h, R * int(n), 1), d.value
+        return cls(h, R * int(n), 1, device), d.value
 
     def read(self, stream=None):
         torch = _torch()
-        out = [torch.empty((self.K, self.T), dtype=torch.float32, device="cuda") for _ in range(4)]
+        out = [torch.empty((self.K, self.T), dtype=torch.float32, device=f"cuda:{self.device}") for _ in range(4)]
         _check(_lib.rtg_traj_read(self.handle, *[_ptr(o) for o in out], _stream(stream)), "rtg_traj_read")
         return out
 
@@ -359,21 +403,30 @@ def score(m: Map, tr: Traj, camera, params: ScoreParams, first_col=None, feasibl
     """rtg_score into caller-owned CUDA tensors (allocated here when None). Returns them."""
     torch = _torch()
     K = tr.K
-    dev = torch.device("cuda")
+    dev = torch.device("cuda", m.device)
     first_col = torch.empty(K, dtype=torch.int32, device=dev) if first_col is None else first_col
     feasible = torch.empty(K, dtype=torch.uint8, device=dev) if feasible is None else feasible
     gain = torch.empty(K, dtype=torch.float64, device=dev) if gain is None else gain
     utility = torch.empty(K, dtype=torch.float64, device=dev) if utility is None else utility
+    outs = (("first_col", first_col, "int32"), ("feasible", feasible, "uint8"), ("gain", gain, "float64"),
+            ("utility", utility, "float64"))
+    ptrs = [_arg(nm, a, dt, (K,), m.device) for nm, a, dt in outs]
+    for nm, a, _ in outs:
+        if isinstance(a, np.ndarray) or not a.is_cuda:
+            raise ValueError(f"{nm}: must be a CUDA tensor (rtg_score writes device memory)")
     cam = camera if isinstance(camera, Camera) else make_camera(camera)
-    _check(_lib.rtg_score(m.handle, tr.handle, ctypes.byref(cam), ctypes.byref(params), _ptr(first_col),
-                          _ptr(feasible), _ptr(gain), _ptr(utility), _stream(stream)), "rtg_score")
+    _check(_lib.rtg_score(m.handle, tr.handle, ctypes.byref(cam), ctypes.byref(params), *ptrs, _stream(stream)),
+           "rtg_score")
     return first_col, feasible, gain, utility
 
 
 def best(utility, index_base: int = 0, stream=None):
     """rtg_best -> (score, global index); index -1 / score -inf when nothing is feasible."""
     out = BestResult()
-    _check(_lib.rtg_best(_ptr(utility), int(utility.numel()), int(index_base), _stream(stream), ctypes.byref(out)),
+    if len(utility.shape) != 1:
+        raise ValueError("utility: expected [K]")
+    p = _arg("utility", utility, "float64", cuda=True)
+    _check(_lib.rtg_best(p, int(utility.numel()), int(index_base), _stream(stream), ctypes.byref(out)),
            "rtg_best", allow=(ERR_NO_FEASIBLE,))
     return out.score, out.index
 
@@ -383,8 +436,12 @@ def ledger_update(mu_prev, mu_cur, w_prev, w_out=None, device=0, stream=None):
     torch = _torch()
     n = int(w_prev.shape[0])
     w_out = torch.empty(n, dtype=torch.float32, device=f"cuda:{device}") if w_out is None else w_out
-    _check(_lib.rtg_ledger_update(device, n, _kind(mu_prev), _ptr(mu_prev), _ptr(mu_cur), _ptr(w_prev), _ptr(w_out),
-                                  _stream(stream)), "rtg_ledger_update")
+    kind = _kind(mu_prev)
+    if _kind(mu_cur) != kind or _kind(w_prev) != kind:
+        raise ValueError("mu_prev, mu_cur, w_prev must live in the same memory")
+    ptrs = (_arg("mu_prev", mu_prev, "float32", (3, n), device), _arg("mu_cur", mu_cur, "float32", (3, n), device),
+            _arg("w_prev", w_prev, "float32", (n,), device), _arg("w_out", w_out, "float32", (n,), device, cuda=True))
+    _check(_lib.rtg_ledger_update(device, n, kind, *ptrs, _stream(stream)), "rtg_ledger_update")
     return w_out
 
 
@@ -392,8 +449,8 @@ def region_utility(m: Map, origin, size: float, dims, stream=None):
     """rtg_region_utility (N2): (omega [prod dims] float64, count [prod dims] int32) CUDA tensors."""
     torch = _torch()
     nr = int(dims[0]) * int(dims[1]) * int(dims[2])
-    omega = torch.empty(nr, dtype=torch.float64, device="cuda")
-    count = torch.empty(nr, dtype=torch.int32, device="cuda")
+    omega = torch.empty(nr, dtype=torch.float64, device=f"cuda:{m.device}")
+    count = torch.empty(nr, dtype=torch.int32, device=f"cuda:{m.device}")
     o = (ctypes.c_double * 3)(*[float(v) for v in origin])
     d = (_I * 3)(*[int(v) for v in dims])
     _check(_lib.rtg_region_utility(m.handle, o, float(size), d, _ptr(omega), _ptr(count), _stream(stream)),
@@ -421,8 +478,10 @@ def plan_tree(m: Map, start, goal, params: TreeParams, stream=None):
 def cost_benefit(omega, d, stream=None):
     """rtg_cost_benefit (N2): argmax of omega / e^d (ties -> smaller d, then index) -> (score, index)."""
     out = BestResult()
-    _check(_lib.rtg_cost_benefit(_ptr(omega), _ptr(d), int(omega.numel()), _stream(stream), ctypes.byref(out)),
-           "rtg_cost_benefit")
+    R = int(omega.numel())
+    po = _arg("omega", omega, "float64", (R,), cuda=True)
+    pd = _arg("d", d, "float64", (R,), cuda=True)
+    _check(_lib.rtg_cost_benefit(po, pd, R, _stream(stream), ctypes.byref(out)), "rtg_cost_benefit")
     return out.score, out.index
 
 
@@ -430,7 +489,7 @@ def score_debug(m: Map, tr: Traj, camera, params: ScoreParams, pair_mask: bool =
     """rtg_score_debug: per-waypoint arrays for every waypoint (+ optional pair mask, stats)."""
     torch = _torch()
     KT = tr.K * tr.T
-    dev = torch.device("cuda")
+    dev = torch.device("cuda", m.device)
     wp_col = torch.empty(KT, dtype=torch.uint8, device=dev)
     wp_gain = torch.empty(KT, dtype=torch.float64, device=dev)
     wp_nh = torch.empty(KT, dtype=torch.int32, device=dev)

@@ -115,3 +115,60 @@ def test_planner_entry_points_validate_arguments(rtg):
     robot = rtg.Robot(0.3, 3.0, 0)
     assert lib.rtg_map_create(0, 1 << 30, 0, None, None, None, None, None, None, ctypes.byref(robot), None,
                               ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+
+
+def test_binding_rejects_wrong_dtype_shape_and_memory(rtg):
+    """The binding checks every array against the ABI's dtype / shape / memory before a pointer
+    crosses it (a float64 numpy map would otherwise be read as float32 garbage, a short
+    or float32 output buffer written past its end).  All of these fail on the host, no GPU needed."""
+    import numpy as np
+    import torch
+    n = 4
+    good = dict(means=np.zeros((3, n), np.float32), quats=np.zeros((4, n), np.float32),
+                scales=np.ones((3, n), np.float32), opacity=np.ones(n, np.float32), info_w=np.ones(n, np.float32))
+    for key, bad, exc in [("means", np.zeros((3, n)), TypeError),                      # numpy default float64
+                          ("quats", np.zeros((3, n), np.float32), ValueError),         # wrong shape
+                          ("scales", np.ones((3, n), np.float16), TypeError),
+                          ("opacity", np.ones(n + 1, np.float32), ValueError),
+                          ("info_w", np.ones(n, np.float64), TypeError)]:
+        kw = dict(good)
+        kw[key] = bad
+        with pytest.raises(exc, match=key):
+            rtg.Map(**kw)
+    with pytest.raises(TypeError, match="flags"):
+        rtg.Map(**good, flags=np.zeros(n, np.int32))
+    with pytest.raises(TypeError, match="info_w"):
+        rtg.Map(**dict(good, info_w=torch.ones(n, dtype=torch.float64)))
+    K, T = 3, 5
+    f = lambda: np.zeros((K, T), np.float32)
+    with pytest.raises(TypeError, match="yaw"):
+        rtg.Traj.upload(f(), f(), f(), np.zeros((K, T)))
+    with pytest.raises(ValueError, match="z"):
+        rtg.Traj.upload(f(), f(), np.zeros((K, T + 1), np.float32), f())
+    with pytest.raises(ValueError, match="CUDA"):
+        rtg.Traj.wrap(*[torch.zeros(K, T) for _ in range(4)])
+    with pytest.raises(TypeError, match="omega"):
+        rtg.Traj.sample_unicycle(np.ones(K, np.float32), np.ones(K), T, 0.1, (0, 0, 0, 0))
+    # score outputs: dtype, length and device are checked against the trajectory handle
+    m = object.__new__(rtg.Map)
+    m.handle, m.device, m.n = rtg._P(), 0, n
+    tr = rtg.Traj(rtg._P(), K, T, 0)
+    cam = rtg.Camera(64, 48, 50, 50, 32, 24, 0.1, 5.0)
+    outs = dict(first_col=torch.zeros(K, dtype=torch.int32), feasible=torch.zeros(K, dtype=torch.uint8),
+                gain=torch.zeros(K, dtype=torch.float64), utility=torch.zeros(K, dtype=torch.float64))
+    for key, bad, exc in [("utility", torch.zeros(K, dtype=torch.float32), TypeError),
+                          ("gain", torch.zeros(K - 1, dtype=torch.float64), ValueError),
+                          ("first_col", torch.zeros(K, dtype=torch.int64), TypeError),
+                          ("feasible", torch.zeros(K, dtype=torch.bool), TypeError)]:
+        kw = dict(outs)
+        kw[key] = bad
+        with pytest.raises(exc, match=key):
+            rtg.score(m, tr, cam, rtg.make_params(), **kw)
+    with pytest.raises(ValueError, match="CUDA"):          # right dtypes, but host memory
+        rtg.score(m, tr, cam, rtg.make_params(), **outs)
+    with pytest.raises(TypeError, match="utility"):
+        rtg.best(torch.zeros(K, dtype=torch.float32))
+    with pytest.raises(ValueError, match="CUDA"):
+        rtg.best(torch.zeros(K, dtype=torch.float64))
+    with pytest.raises(ValueError, match="omega"):
+        rtg.cost_benefit(torch.zeros(K, dtype=torch.float64), torch.zeros(K, dtype=torch.float64))

@@ -35,19 +35,22 @@ def _free_port():
     return p
 
 
+def _rtg_best_shaped(local):
+    """This rank's local best exactly as rtg.best() returns it from rtg_best (include/rtg.h): the
+    (score, LOCAL index) pair of the oracle's O7 rule (max, ties -> lowest index),
+    which rtg_best is parity-tested against on the GPU, and (-inf, -1) with RTG_ERR_NO_FEASIBLE."""
+    from oracle import oracle as O
+    j = O.best(np.asarray(local, np.float64))
+    return (float(local[j]), j) if j >= 0 else (-math.inf, -1)
+
+
 def _worker(rank, world, port, utility, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         idx = D.shard_indices(len(utility), rank, world)
-        local = utility[idx]
-        # local argmax exactly as rtg_best computes it: max, ties -> lowest local index
-        if np.all(np.isneginf(local)):
-            s, j = -math.inf, -1
-        else:
-            j = int(np.argmax(local))
-            s = float(local[j])
+        s, j = _rtg_best_shaped(utility[idx])
         q.put((rank, D.global_best(s, j, rank, world)))
     finally:
         dist.destroy_process_group()
@@ -112,12 +115,7 @@ def _worker_outputs(rank, world, port, fc, fe, g, u, q):
         K = len(u)
         idx = D.shard_indices(K, rank, world)
         out = D.gather_outputs(torch.from_numpy(fc[idx]), fe[idx], g[idx], torch.from_numpy(u[idx]), K, rank, world)
-        loc = u[idx]
-        if len(loc) == 0 or np.all(np.isneginf(loc)):
-            s, j = -math.inf, -1
-        else:
-            j = int(np.argmax(loc))
-            s = float(loc[j])
+        s, j = _rtg_best_shaped(u[idx])
         q.put((rank, out, D.global_best_packed(s, j, rank, world)))
     finally:
         dist.destroy_process_group()
@@ -151,3 +149,31 @@ def test_gather_outputs_and_packed_best_gloo_world2(K):
         assert np.array_equal(o[0], fc) and np.array_equal(o[1], fe)
         assert np.array_equal(o[2], g, equal_nan=True) and np.array_equal(o[3], u)
         assert b == expect_best
+
+
+def _worker_packed_invalid(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank 1's best is not an integer utility (e.g. the SUM variant): it must not raise before
+        # the collective (rank 0 would block in it); every rank falls back to the all_gather
+        s, j = (3.0, 0) if rank == 0 else (3.5, 2)
+        q.put((rank, D.global_best_packed(s, j, rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_packed_best_falls_back_on_every_rank_when_one_is_invalid():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_packed_invalid, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] == (3.5, 1 + 2 * 2)     # rank 1, local 2 -> global 5

@@ -630,10 +630,40 @@ def test_band_points_match_fp64_decision(R):
     xs = (a * np.sqrt(1.0 + eps)).astype(np.float32)
     one = lambda v: np.array(v, np.float32).reshape(1, 1)
     for e, x in zip(eps, xs):
-        wl = W.Workload("band_col", one([0.0, 0.0, 0.0]).reshape(3, 1), np.array([[1], [0], [0], [0]], np.float32),
+        wl = W.Workload("band_col", np.zeros((3, 1), np.float32), np.array([[1], [0], [0], [0]], np.float32),
                         np.full((3, 1), 0.125, np.float32), np.ones(1, np.float32), np.ones(1, np.float32), None,
                         one(x), one(0.0), one(0.0), one(np.pi / 2), W.Robot(0.25), cam, 0.1)
         orc = O.score(wl)
         for mode in MODES:
             gpu = gpu_run(R, wl, mode)
             assert bool(gpu["wp_col"][0]) == bool(orc["wp"]["col"][0]) == (e < 0), (mode, e)
+
+
+def test_sparse_diagonal_waypoints_collision(R):
+    """k_col_culled tests a chunk's waypoints against the union of their cell boxes; for
+    sparse or diagonal waypoints (2.5 m apart here, a 1 s primitive at 2.5 m/s) that union would hold
+    many times the candidates of the per-point boxes, so the kernel falls back to per-point boxes.
+    Decisions must not depend on the route: culled equals dense bit for bit at every waypoint, and
+    both equal the oracle's on a sample."""
+    wl = W.outdoor(N=300_000, K=96, T=30)
+    rng = np.random.default_rng(17)
+    K, T = wl.K, wl.T
+    th = rng.uniform(-np.pi, np.pi, K)
+    th[: K // 2] = np.pi / 4 + (np.arange(K // 2) % 4) * np.pi / 2        # exact diagonals
+    x0, y0 = rng.uniform(-40, 40, K), rng.uniform(-40, 40, K)
+    s = 2.5 * (np.arange(T) + 1)
+    x = (x0[:, None] + np.cos(th)[:, None] * s).astype(np.float32)
+    y = (y0[:, None] + np.sin(th)[:, None] * s).astype(np.float32)
+    z = np.broadcast_to(rng.uniform(0.8, 3.0, K)[:, None], (K, T)).astype(np.float32).copy()
+    yaw = np.broadcast_to(th[:, None], (K, T)).astype(np.float32).copy()
+    a = gpu_run(R, wl, "dense", x=x, y=y, z=z, yaw=yaw)
+    b = gpu_run(R, wl, "culled", x=x, y=y, z=z, yaw=yaw)
+    assert np.array_equal(a["wp_col"], b["wp_col"]) and np.array_equal(a["first_col"], b["first_col"])
+    assert 0.05 < b["wp_col"].mean() < 0.95
+    idx = np.arange(0, K, 12)
+    orc = O.score(wl, traj_idx=idx, x=x, y=y, z=z, yaw=yaw)
+    wp = orc["wp"]
+    assert int(wp["amb_col"].sum()) == 0
+    assert np.array_equal(b["wp_col"].reshape(K, T)[idx].reshape(-1).astype(bool), wp["col"])
+    g = gpu_run(R, wl, "culled", flags=0, x=x, y=y, z=z, yaw=yaw, debug=False)
+    assert np.array_equal(g["first_col"], b["first_col"])
