@@ -101,10 +101,15 @@ void orc_visibility_slacks(const double mu[3], const double pose[4], const doubl
     scale[4] = scale[5] = fy * fabs(Y) + my * aZ;
 }
 
-/* visibility decision: returns nominal (all sigma >= 0); *amb = band case.  A non-finite pose
- * (trajectory padding) gives NaN slacks and sees nothing (reading R8). */
+/* visibility decision: returns nominal (all sigma >= 0); *amb = band case.  A pose with any
+ * non-finite coordinate (trajectory padding) sees nothing, definitely: no slack is evaluated, so
+ * no infinite slack/scale pair can report a band case (reading R8). */
 static int orc_visible(const double mu[3], const double pose[4], const double cam[8], int* amb) {
     double sg[6], sc[6];
+    if (!(isfinite(pose[0]) && isfinite(pose[1]) && isfinite(pose[2]) && isfinite(pose[3]))) {
+        *amb = 0;
+        return 0;
+    }
     orc_visibility_slacks(mu, pose, cam, sg, sc);
     int nominal = 1, definitely_out = 0, near = 0;
     for (int j = 0; j < 6; ++j) {

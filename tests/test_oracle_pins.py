@@ -319,9 +319,11 @@ def test_non_finite_waypoint_sees_and_hits_nothing():
     r, _ = _wp(m, q, s, w, pose=(0.0, 0.0, 0.0, 0.0))
     assert r["col"][0] == 1
     for pose in ((np.nan, 0.0, 0.0, 0.0), (0.0, np.nan, 0.0, 0.0), (0.0, 0.0, np.nan, 0.0), (np.inf, 0.0, 0.0, 0.0),
-                 (0.0, 0.0, 0.0, np.nan)):
+                 (0.0, 0.0, np.inf, 0.0), (0.0, -np.inf, 0.0, 0.0), (0.0, 0.0, 0.0, np.nan)):
         r, _ = _wp(m, q, s, w, pose=pose)
         assert r["gain"][0] == 0.0 and r["nh"][0] == 0 and r["nl"][0] == 0, pose
+        # definitely nothing: no band case either (an infinite slack over an infinite scale is not one)
+        assert r["amb_vis"][0] == 0 and r["gain_hi"][0] == 0.0 and r["nh_hi"][0] == 0, pose
         assert r["col"][0] == (1 if np.isfinite(pose[:3]).all() else 0), pose
 
 
