@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="weak: K trajectories per GPU; strong: the config's K shared by the GPUs "
                          "(default: strong for the scale config, which fixes the total K, else weak)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: exercise the multi-rank code path with "
+                         "several ranks on one GPU; the (score, index) exchange then runs on the host)")
     ap.add_argument("--cells", default=None,
                     help="visibility grid cells 'hy,hx,hz' [m] (rtg_map_options; default: library defaults)")
     return ap.parse_args()
@@ -154,6 +157,11 @@ def run_reference(args):
     ms_full = 1000.0 * wl.K * wl.T * wl.N / value
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_full, "higher_is_better": True,
+            # ms_per_step is NOT measured: each timed step scores a sample of the workload; the full
+            # planning cycle's time is that sample's rate extrapolated linearly in trajectories
+            "extrapolated": {"ms_per_step": True, "measured_ms_per_sample_step": 1000.0 * statistics.median(times),
+                             "sample_trajectories": n_traj, "full_trajectories": wl.K,
+                             "factor": wl.K / n_traj, "method": "linear in trajectories (oracle cost is per pair)"},
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} (BASELINE.json configs[3])" if args.config == "outdoor"
                        else args.config, "N": wl.N, "K": wl.K, "T": wl.T},
@@ -182,10 +190,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if world > ndev and args.backend == "nccl":
+        raise SystemExit(f"{world} ranks need {world} GPUs with NCCL ({ndev} visible); use --backend gloo")
+    local_dev = local % ndev                    # gloo on one GPU: every rank shares cuda:0
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    cdev = dev if args.backend == "nccl" else torch.device("cpu")   # where collective tensors live
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     # ---- workload: the map is replicated; the global trajectory set (and the gain-only views of the
     # scale config) is interleaved over ranks: weak scaling grows it with the ranks, strong keeps it
@@ -225,7 +241,7 @@ def main():
 
     def global_best(score, idx):
         # one NCCL all_gather of (score, global index) per step (paper_2409_18122_b200/dist.py)
-        return D.global_best(score, idx, rank, world, device=dev)
+        return D.global_best(score, idx, rank, world, device=cdev)
 
     map_opts = None
     if args.cells:
@@ -237,19 +253,19 @@ def main():
     def step(host: bool):
         src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
         m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
-                  device=local, options=map_opts)
+                  device=local_dev, options=map_opts)
         if host:
             # rtg_map_create returns once the map is on the device and its build is enqueued: the
             # waypoint upload then overlaps the build on a second stream
-            tr = R.Traj.upload(*src_traj, device=local, stream=aux)
+            tr = R.Traj.upload(*src_traj, device=local_dev, stream=aux)
             stream.wait_stream(aux)
         else:
-            tr = R.Traj.wrap(*src_traj, device=local)   # resident waypoints: borrowed, no copy
+            tr = R.Traj.wrap(*src_traj, device=local_dev)   # resident waypoints: borrowed, no copy
         R.score(m, tr, cam, params, *outs)
         s, i = R.best(outs[3])
         res = global_best(s, i)
         if Kv:   # the scale config's gain-only views (T = 1, no collision): best view by xi
-            tv = R.Traj.upload(*hviews, device=local) if host else R.Traj.wrap(*dviews, device=local)
+            tv = R.Traj.upload(*hviews, device=local_dev) if host else R.Traj.wrap(*dviews, device=local_dev)
             R.score(m, tv, cam, vparams, *vouts)
             vs, vi = R.best(vouts[3])
             res = res + global_best(vs, vi)
@@ -285,7 +301,7 @@ def main():
             per_step.append(a.elapsed_time(b))
         if profile:
             R.profile_enable(False)
-        t = torch.tensor([total_ms] + per_step, dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms] + per_step, dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)   # total and every step: max over ranks
         v = t.cpu().tolist()
@@ -296,7 +312,7 @@ def main():
     dist_ms = {}
 
     # ---- device-resident timing (value), with clocks and per-phase events
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_dev) as clocks:
         ms, res = timed(False, args.steps, args.warmup, profile=True)
     step_stats = {"median": dist_ms["median"], "p90": dist_ms["p90"]}
     prof = R.profile_read(reset=True)
@@ -327,7 +343,7 @@ def main():
     work = None
     if args.mode == "culled":
         m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
-                  device=local, options=map_opts)
+                  device=local_dev, options=map_opts)
         work = work_sample(R, m, wl, cam, params, feasible)
         m.close()
     traffic = None
@@ -368,9 +384,14 @@ def main():
     return 0
 
 
-# Algorithmic work per unit:
-I_TEST = 20.0     # FP32/ALU lane instructions of one exact visibility pair test + accumulate
-I_UNIT = 25.0     # lane instructions to cut one (row, z-cell) unit of inside columns (2 vertical cuts, 4 loads)
+# Algorithmic work per unit, SURVEY §8(d) (SURVEY.md:709, [A5]): ~10 lane-instructions per individually
+# tested Gaussian, ~25 per grid cell classified (here: per (row, z-cell) unit and per footprint row, each
+# a cell-interval classification); dense gain-only path ~15 FP32 instructions per pair (SURVEY §8(d)
+# "Dense fused kernel": "~15 in the gain-only phase").  DESIGN.md "Roofline accounting".
+I_TEST = 10.0
+I_UNIT = 25.0
+I_ROW = 25.0
+I_DENSE_PAIR = 15.0
 I_SPHERE = 8.0    # collision sphere reject per candidate pair (3 FADD, 3 FMA, compare, branch)
 KERNEL = {("visibility_gain", "culled"): "k_gain_culled", ("collision", "culled"): "k_col_culled",
           ("visibility_gain", "dense"): "k_gain_dense", ("collision", "dense"): "k_col_dense",
@@ -393,12 +414,16 @@ def work_sample(R, m, wl, cam, params, feasible, n=96):
     return {k: v / nwp for k, v in d["stats"].items()}
 
 
-def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, traffic):
-    """Roofline object of the dominant phase (achieved = algorithmic work per launch / launch time)."""
+def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, ncu):
+    """Roofline object of the dominant phase (achieved = algorithmic work per launch / launch time).
+    `ncu` holds the committed ncu --set full figures of the same kernel (profiles/traffic.json)."""
     sm_mhz = (clock.get("sm_mhz") or 1965.0)
     peak_ti = 148 * 128 * sm_mhz * 1e6 / 1e12          # lane-instruction issue peak, T/s (guide unit counts)
     kname = KERNEL.get((phase, mode), "")
-    tr = traffic.get(kname, None) if traffic else None
+    k_ncu = ncu.get(kname) if ncu else None
+    if isinstance(k_ncu, (int, float)):                # older records: DRAM bytes only
+        k_ncu = {"dram_bytes": k_ncu}
+    tr = k_ncu.get("dram_bytes") if k_ncu else None
     if phase == "map_build":
         n = wl.N
         alg_bytes = n * 49 + n * (16 + 8 + 4) * 2 + (n // 2) * (16 + 48 + 72)
@@ -406,17 +431,29 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, tra
         return {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                 "traffic": tr, "phase": phase, "kernel_ms": ms}
     n_info = n_feasible * (wl.T // stride)
+    units = None
     if phase == "visibility_gain":
         if mode == "dense":
-            lane_instr = n_info * float(wl.N) * I_TEST
+            units = {"pairs_per_info_waypoint": float(wl.N), "I_pair": I_DENSE_PAIR}
+            lane_instr = n_info * float(wl.N) * I_DENSE_PAIR
         else:
-            lane_instr = n_info * (I_TEST * work["tested"] + I_UNIT * work["units"])
+            rows = work.get("rows", 0.0)
+            units = {"info_waypoints": n_info, "tested_per_wp": work["tested"], "units_per_wp": work["units"],
+                     "rows_per_wp": rows, "I_test": I_TEST, "I_unit": I_UNIT, "I_row": I_ROW}
+            lane_instr = n_info * (I_TEST * work["tested"] + I_UNIT * work["units"] + I_ROW * rows)
     else:
         lane_instr = wl.K * wl.T * (work["col_tested"] if work else 0.0) * I_SPHERE
     ach = lane_instr / (ms / 1e3) / 1e12
-    return {"bound": "alu", "achieved": ach, "peak": peak_ti, "unit": "T lane-instr/s", "frac": ach / peak_ti,
-            "traffic": tr, "phase": phase, "kernel": kname, "kernel_ms": ms,
-            "work_per_waypoint": work}
+    out = {"bound": "alu", "achieved": ach, "peak": peak_ti, "unit": "T lane-instr/s", "frac": ach / peak_ti,
+           "traffic": tr, "phase": phase, "kernel": kname, "kernel_ms": ms,
+           "peak_basis": "148 SMs x 128 FP32 lanes x measured SM clock (B200_PROFILING.md unit counts)",
+           "work_units": units, "work_per_waypoint": work}
+    if k_ncu:
+        out["ncu"] = {k: v for k, v in k_ncu.items() if k != "dram_bytes"}
+        wi = k_ncu.get("warp_inst")
+        if wi:   # executed lane slots per launch vs the algorithmic lane instructions above
+            out["ncu"]["algorithmic_share_of_executed"] = lane_instr / (32.0 * wi)
+    return out
 
 
 if __name__ == "__main__":

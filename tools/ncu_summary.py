@@ -86,7 +86,11 @@ def full(rep, out, key=None):
                 u, v = got[w]
                 b += float(v.replace(",", "")) * mult.get(u, 1)
         short = name.split("::")[-1].split("<")[0]
-        traffic[short] = b
+        num = lambda w: float(got[w][1].replace(",", "")) if w in got else None
+        traffic[short] = {"dram_bytes": b, "warp_inst": num("smsp__inst_executed.sum"),
+                          "fma_pipe_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                          "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                          "ms": num("gpu__time_duration.sum")}
         fp = [w for w in METRICS if "thread_inst_executed_op_f" in w and "per_cycle_elapsed" in w]
         pk = "sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained"
         if all(w in got for w in fp) and pk in got:
