@@ -244,13 +244,14 @@ rtg_status rtg_best(const double* utility, int K, long long index_base, void* st
  * every t regardless of info_stride): wp_col[K*T] (uint8 collision), wp_gain[K*T] (double),
  * wp_nh[K*T], wp_nl[K*T] (visible H / L counts), computed by the `params->mode` kernels.
  * pair_mask (or NULL): ceil(K*T*N/32) words, bit (i*N + g) = waypoint i collides with
- * Gaussian g (original index), only when K*T*N <= 2^32.  stats (host, or NULL): 8 counters
- * {collision pairs FP64-redecided, visibility pairs FP64-redecided, visibility pairs tested
- * individually, (row, z-cell) x-runs added whole, collision candidates tested, visibility pairs
- * tested in the horizontally straddling flanks of rows, (row, z-cell) units cut, individually
- * tested pairs visible}
+ * Gaussian g (original index), only when K*T*N <= 2^32.  stats (host, or NULL): RTG_DEBUG_STATS
+ * (= 12) counters {collision pairs FP64-redecided, visibility pairs FP64-redecided, visibility
+ * pairs tested individually, (row, z-cell) x-runs added whole, collision candidates tested,
+ * visibility pairs tested in the horizontally straddling flanks of rows, (row, z-cell) units cut,
+ * individually tested pairs visible, footprint rows classified, test segments, 0, 0}
  * (culled mode; dense mode fills the first two).  Synchronises the stream.
  */
+enum { RTG_DEBUG_STATS = 12 };
 rtg_status rtg_score_debug(rtg_map map, rtg_traj traj, const rtg_camera* cam,
                            const rtg_score_params* params,
                            unsigned char* wp_col, double* wp_gain, int* wp_nh, int* wp_nl,

@@ -558,7 +558,7 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     size_t o_list = o_nl + al(sizeof(int) * KT);
     size_t o_ints = o_list + al(sizeof(int) * (list_max > 0 ? list_max : 1));
     size_t o_stats = o_ints + al(sizeof(int) * 8);
-    size_t o_cam = o_stats + al(sizeof(unsigned long long) * 8);
+    size_t o_cam = o_stats + al(sizeof(unsigned long long) * RTG_DEBUG_STATS);
     size_t o_ranked = o_cam + al(sizeof(double) * 8);
     size_t total = o_ranked + al(sizeof(int) * K);
     cudaError_t e = dev_alloc(&s.block, total, st);
@@ -577,7 +577,7 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     double c64[8] = {(double)cam->width, (double)cam->height, cam->fx, cam->fy, cam->cx, cam->cy, cam->z_near, cam->z_far};
     cudaError_t e2 = cudaMemcpyAsync(s.cam64, c64, sizeof(c64), cudaMemcpyHostToDevice, st);
     if (e2 != cudaSuccess) return e2;
-    return cudaMemsetAsync(b + o_ints, 0, o_stats + al(sizeof(unsigned long long) * 8) - o_ints, st);
+    return cudaMemsetAsync(b + o_ints, 0, o_stats + al(sizeof(unsigned long long) * RTG_DEBUG_STATS) - o_ints, st);
 }
 
 rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_score_params* p, int* first_col,
@@ -861,13 +861,13 @@ rtg_status rtg_score_debug(rtg_map m, rtg_traj tr, const rtg_camera* cam, const 
         API_CK(cudaMemsetAsync(pair_mask, 0, sizeof(unsigned) * (words ? words : 1), st), &m->poisoned);
         API_CK(launch_pair_mask(m, tr, pair_mask, st), &m->poisoned);
     }
-    unsigned long long hs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long hs[RTG_DEBUG_STATS] = {};
     API_CK(cudaMemcpyAsync(hs, sc.stats, sizeof(hs), cudaMemcpyDeviceToHost, st), &m->poisoned);
     dev_free(sc.block, st);
     sc.block = nullptr;
     API_CK(cudaStreamSynchronize(st), &m->poisoned);
     if (stats)
-        for (int i = 0; i < 8; ++i) stats[i] = (long long)hs[i];
+        for (int i = 0; i < RTG_DEBUG_STATS; ++i) stats[i] = (long long)hs[i];
     return RTG_OK;
 }
 

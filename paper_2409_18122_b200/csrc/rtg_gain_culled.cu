@@ -19,8 +19,11 @@
 //      most two straddling x-runs (tested); the z-cells a row can see come from the vertical wedge
 //      at the row's largest depth and the row's occupied z-range;
 //   4. tested runs go to a per-warp queue; a flush tests 64 items per pass, two per lane, whatever
-//      the run lengths (each lane's run from a 64-bit head mask built with two REDUX.OR), with the
-//      shared exact pair test (packed FP32 + FP64 re-decision inside the proven guard band).
+//      the run lengths: a shared-memory bitmap marks the items where runs start, so each lane finds
+//      its run from a 64-bit window of it (one broadcast load, two funnel shifts, popc); items past
+//      the queue fall in a sentinel run of NaN padding records (never visible, so no bound check).
+//      The pair test is the shared exact one (packed FP32 + FP64 re-decision inside the proven
+//      guard band).
 // Sums are exact integers (24-bit u_q and a class byte per record, 32-bit per-lane sums flushed
 // into 64-bit ones; FP64-exact prefixes): order free, so the result is bit-identical to the dense
 // kernel.  eps (>> FP32 error of the cell tests) keeps "inside" strictly inside and "possible" a
@@ -39,6 +42,7 @@ constexpr int kWarpsG = 4;     // warps per CTA; RTG_GAIN_MINB CTAs per SM: 36 w
 constexpr int kQCap = 256;    // queued runs per warp
 constexpr int kQFlush = 192;  // test the queue once more runs than this are waiting (an append adds <= 64)
 constexpr int kMaxUnits = 1024;   // units of a row chunk with a shared-memory owner table (else: search)
+constexpr int kHeadWords = (64 * 63 + 64 + 32) / 32 + 1;   // a flush chunk (kFlushPasses passes) + the window tail
 
 // RTG_BOUNDS_CHECK builds trap on any out-of-range table or record index (debug builds; the
 // sanitizer is not available on the GPU pool)
@@ -58,6 +62,7 @@ struct GainK {
     float ox, oy, oz, hx, hy, hz, inv_hz, eps;
     int nx, ny, nz, nxb, offB;
     long long nrec, ntabB, ntabA;   // sizes (bounds checks)
+    int nan_rec;                    // first of >= 64 NaN padding records (copy A's tail): sentinel run
     float zn, zf, kxl, kxr, kyu, kyd, kxh;
 };
 
@@ -117,9 +122,10 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
         float4 con[6];                       // the frustum's constraints on grid cells
         double cs[2];                        // FP64 cos, sin of the waypoint's yaw (re-decisions)
         float v[8];                          // footprint vertices (x0..x3, y0..y3), grid-relative
-        // queued test runs: [0] first record -> (first record - items before the run), [1] length ->
-        // items before the run.  64 entries of padding hold INT_MAX while the queue is tested.
+        // queued test runs: [0] first record -> (first record - items before the run), [1] length;
+        // entry nq of [0] is the sentinel run (NaN records) while the queue is tested
         int q[2][kQCap + 64];
+        unsigned head[kHeadWords];           // run-start bitmap of the flush chunk being tested
         unsigned char owner[kMaxUnits];      // row (lane) of each unit of the current chunk
     };
     __shared__ WarpSmem s_w[kWarpsG];
@@ -129,9 +135,11 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     WarpSmem& sw = s_w[wid];
     int* const qs = sw.q[0];
     int* const qe = sw.q[1];
+    for (int j = lane; j < kHeadWords; j += 32) sw.head[j] = 0u;   // kept all-zero between flush chunks
+    __syncwarp();
     const int L = *list_count;
     unsigned nref = 0;
-    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0;
+    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0, nrow = 0;
     for (;;) {
         int e = 0;
         if (lane == 0) e = atomicAdd(counter, 1);
@@ -254,6 +262,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     rnext += 32;
                     const int iy = rcur + lane;
                     const float fiy = (float)iy;
+                    if (kStats) nrow += iy <= iy1;
                     float plo = 0.f, phi = (float)(g.nx - 1), ilo = 0.f, ihi = phi;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
@@ -379,27 +388,49 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         eb.w = eb.z + lb.z;
                         sa.x -= ea.x; sa.y -= ea.y; sa.z -= ea.z; sa.w -= ea.w;
                         sb.x -= eb.x; sb.y -= eb.y; sb.z -= eb.z; sb.w -= eb.w;
-                        *reinterpret_cast<int4*>(qe + 8 * lane) = ea;
-                        *reinterpret_cast<int4*>(qe + 8 * lane + 4) = eb;
                         *reinterpret_cast<int4*>(qs + 8 * lane) = sa;
                         *reinterpret_cast<int4*>(qs + 8 * lane + 4) = sb;
-                        __syncwarp();
-                        qe[nq + lane] = INT_MAX;
-                        qe[nq + 32 + lane] = INT_MAX;
-                        __syncwarp();
+                        // a run of zero-length entries past the queue never starts inside a window
+                        if (r8 < 1) ea.x = INT_MAX;
+                        if (r8 < 2) ea.y = INT_MAX;
+                        if (r8 < 3) ea.z = INT_MAX;
+                        if (r8 < 4) ea.w = INT_MAX;
+                        if (r8 < 5) eb.x = INT_MAX;
+                        if (r8 < 6) eb.y = INT_MAX;
+                        if (r8 < 7) eb.z = INT_MAX;
+                        if (r8 < 8) eb.w = INT_MAX;
+                        *reinterpret_cast<int4*>(qe + 8 * lane) = ea;   // items before each run
+                        *reinterpret_cast<int4*>(qe + 8 * lane + 4) = eb;
+                        // sentinel run nq from item tot on: NaN padding records (never visible, never
+                        // ambiguous), so the passes need no per-item bound check
+                        if (lane == 0) qs[nq] = g.nan_rec - tot;
                     }
                     int r0 = 0;   // run holding item gb
                     for (int gb0 = 0; gb0 < tot; gb0 += 64 * kFlushPasses) {   // 32-bit sums: flushed
                         const int gend = min(tot, gb0 + 64 * kFlushPasses);
+                        // head bitmap of this chunk: bit b <=> a run (or the sentinel) starts at item gb0 + b
+                        __syncwarp();
+                        {
+                            const int4 ea = *reinterpret_cast<const int4*>(qe + 8 * lane);
+                            const int4 eb = *reinterpret_cast<const int4*>(qe + 8 * lane + 4);
+                            const unsigned span = (unsigned)(kHeadWords * 32);
+                            auto mark = [&](int e) {
+                                const unsigned b = (unsigned)(e - gb0);
+                                if (b < span) atomicOr(&sw.head[b >> 5], 1u << (b & 31));
+                            };
+                            mark(ea.x); mark(ea.y); mark(ea.z); mark(ea.w);
+                            mark(eb.x); mark(eb.y); mark(eb.z); mark(eb.w);
+                            if (lane == 0) mark(tot);
+                        }
+                        __syncwarp();
                         unsigned w = 0, pc = 0;
                         for (int gb = gb0; gb < gend; gb += 64) {
-                            // runs r0+1 .. r0+64 start at positions 1 + pa, 1 + pb (relative to gb), pa >= 0:
-                            // head bit k of (hhi:hlo) <=> a run starts at item k + 1 of the window
-                            const int ra = r0 + 1 + lane;
-                            const int pa = qe[ra] - gb - 1, pb = qe[ra + 32] - gb - 1;
-                            const unsigned hlo = __reduce_or_sync(kFullG, bit_or_zero((unsigned)pa));
-                            const unsigned hhi = __reduce_or_sync(
-                                kFullG, bit_or_zero((unsigned)(pa - 32)) | bit_or_zero((unsigned)(pb - 32)));
+                            // head bit k of (hhi:hlo) <=> a run starts at item gb + k + 1
+                            const int hw = (gb - gb0) >> 5;
+                            const uint2 h01 = *reinterpret_cast<const uint2*>(sw.head + hw);
+                            const unsigned h2 = sw.head[hw + 2];
+                            const unsigned hlo = __funnelshift_r(h01.x, h01.y, 1);
+                            const unsigned hhi = __funnelshift_r(h01.y, h2, 1);
                             const int na = __popc(hlo);
                             const int gpa = gb + lane, gpb = gpa + 32;
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_lt)];
@@ -424,8 +455,6 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                                     ++nref;
                                 }
                             }
-                            visa = visa && gpa < tot;
-                            visb = visb && gpb < tot;
                             add_if(visa, w, Ga.uc, pc);
                             add_if(visb, w, Gb.uc, pc);
                             if (kStats) nvis += (unsigned)visa + (unsigned)visb;
@@ -434,6 +463,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         acc += w - (pc << kUqBits);
                         acch += pc & (kClsL - 1);
                         accl += pc / kClsL;
+                        __syncwarp();
+                        for (int j = lane; j < kHeadWords; j += 32) sw.head[j] = 0u;
                     }
                     if (kStats) ntest += (unsigned long long)tot;
                     nq = 0;
@@ -464,6 +495,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
             nunit += __shfl_xor_sync(kFullG, nunit, o);
             nflank += __shfl_xor_sync(kFullG, nflank, o);
             nvis += __shfl_xor_sync(kFullG, nvis, o);
+            nrow += __shfl_xor_sync(kFullG, nrow, o);
         }
         if (lane == 0) {
             if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
@@ -472,6 +504,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
             atomicAdd(&stats[5], nflank);
             atomicAdd(&stats[6], nunit);
             atomicAdd(&stats[7], nvis);
+            atomicAdd(&stats[8], nrow);
         }
     }
 }
@@ -512,6 +545,7 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     g.nx = gg.nx; g.ny = gg.ny; g.nz = gg.nz; g.nxb = gg.nxb;
     g.offB = (int)m->n_gain_pad;
     g.nrec = 2 * m->n_gain_pad;
+    g.nan_rec = (int)m->n_gain;     // n_gain_pad >= n_gain + 64 (rtg_map.cu): copy A's NaN tail
     g.ntabB = (long long)gg.ny * (gg.nx + 1) * gg.nz;
     g.ntabA = gg.ncellsA + 1;
     // eps >> the FP32 error of a cell's centre value (a few ulps of the largest term: offsets of

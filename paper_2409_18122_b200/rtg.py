@@ -34,6 +34,7 @@ COLLIDE_ELLIPSOID, COLLIDE_PRINCIPAL_AXIS = 0, 1
 VARIANT_XI, VARIANT_SUM, VARIANT_SQ = 0, 1, 2
 MODE_DENSE, MODE_CULLED = 0, 1
 SCORE_FULL_GAIN, SCORE_NO_COLLISION = 1, 2
+DEBUG_STATS = 12
 
 
 class Robot(ctypes.Structure):
@@ -498,14 +499,15 @@ def score_debug(m: Map, tr: Traj, camera, params: ScoreParams, pair_mask: bool =
     if pair_mask:
         words = (KT * m.n + 31) // 32
         mask = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
-    stats = (ctypes.c_longlong * 8)()
+    stats = (ctypes.c_longlong * DEBUG_STATS)()
     cam = camera if isinstance(camera, Camera) else make_camera(camera)
     _check(_lib.rtg_score_debug(m.handle, tr.handle, ctypes.byref(cam), ctypes.byref(params), _ptr(wp_col),
                                 _ptr(wp_gain), _ptr(wp_nh), _ptr(wp_nl), _ptr(mask), stats, _stream(stream)),
            "rtg_score_debug")
     return dict(wp_col=wp_col, wp_gain=wp_gain, wp_nh=wp_nh, wp_nl=wp_nl, pair_mask=mask,
                 stats=dict(col_refined=stats[0], vis_refined=stats[1], tested=stats[2], cells_aggregated=stats[3],
-                           col_tested=stats[4], tested_flank=stats[5], units=stats[6], tested_visible=stats[7]))
+                           col_tested=stats[4], tested_flank=stats[5], units=stats[6], tested_visible=stats[7],
+                           rows=stats[8], segments=stats[9]))
 
 
 def unpack_pair_mask(mask, KT: int, N: int) -> np.ndarray:
