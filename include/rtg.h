@@ -80,7 +80,12 @@ enum {
 /* rtg_score_params.flags */
 enum {
     RTG_SCORE_FULL_GAIN = 1u,     /* compute gain/xi for infeasible trajectories too (else NaN)  */
-    RTG_SCORE_NO_COLLISION = 2u   /* gain-only viewpoints: skip collision, all feasible          */
+    RTG_SCORE_NO_COLLISION = 2u,  /* gain-only viewpoints: skip collision, all feasible          */
+    RTG_SCORE_INCLUDE_START = 4u  /* the shared start state x_i(0) is info state l = 0 of every
+                                     trajectory (Eq. equ:traj_utility sums l = 0..L):
+                                     its gain and xi are added to every computed trajectory.  The
+                                     start is the handle's (rtg_traj_set_start; the samplers set
+                                     it); it is not collision-checked (it must be free) */
 };
 
 typedef struct rtg_map_s* rtg_map;
@@ -210,6 +215,14 @@ rtg_status rtg_traj_sample_double_integrator(int device, int K, int T, float dt,
  */
 rtg_status rtg_traj_wrap(int device, int K, int T, const float* x, const float* y, const float* z,
                          const float* yaw, rtg_traj* out);
+/*
+ * rtg_traj_set_start -- the shared start state {x, y, z, yaw} (host array) of the handle's K
+ * trajectories, i.e. x_i(0) of Eq. equ:traj_utility, used by rtg_score with
+ * RTG_SCORE_INCLUDE_START.  rtg_traj_sample_unicycle sets it to its start, the double-integrator
+ * sampler to {start, atan2(v0)} (0 at zero velocity).  Errors: RTG_ERR_INVALID_ARGUMENT (NULL or
+ * non-finite start), RTG_ERR_BAD_HANDLE.
+ */
+rtg_status rtg_traj_set_start(rtg_traj traj, const float start[4]);
 /* Copies the trajectory SoA into caller device buffers (each K*T floats). */
 rtg_status rtg_traj_read(rtg_traj traj, float* x, float* y, float* z, float* yaw, void* stream);
 rtg_status rtg_traj_destroy(rtg_traj traj);
@@ -223,6 +236,8 @@ rtg_status rtg_traj_destroy(rtg_traj traj);
  *   gain[k]       sum over info waypoints of the trace proxy sum_{visible} u_g (Eq. eq:nbv
  *                 with binary J); NaN for infeasible k unless RTG_SCORE_FULL_GAIN
  *   utility[k]    feasible ? sum over info waypoints of xi (XI, SQ) or gain (SUM) : -inf
+ * With RTG_SCORE_INCLUDE_START the info states are the start state plus the info waypoints
+ * (RTG_ERR_INVALID_ARGUMENT when the handle has no start).
  * Any output pointer may be NULL (not written).  Reclassifies the map if params ask for a
  * classification other than the current one.  Does not synchronise.
  */

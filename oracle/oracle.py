@@ -187,8 +187,12 @@ def unicycle(start, v, omega, dt, T):
 # ---------------------------------------------------------------- O6 / O7
 
 def reduce_trajectories(wp: Dict[str, np.ndarray], K: int, T: int, lambda_xi=1.0, variant=VARIANT_XI,
-                        info_stride=1) -> Dict[str, np.ndarray]:
-    """O6 per trajectory, written out step by step from the per-waypoint arrays."""
+                        info_stride=1, start_wp: Optional[Dict[str, np.ndarray]] = None) -> Dict[str, np.ndarray]:
+    """O6 per trajectory, written out step by step from the per-waypoint arrays.
+
+    start_wp (optional): the O5 record of the shared start state x_i(0).  Eq. equ:traj_utility
+     sums xi over l = 0..L, and l = 0 is the start, common to every trajectory:
+    its gain / counts are added to every trajectory's info sums (SURVEY Q7 include_start)."""
     col = wp["col"].reshape(K, T)
     col_def = wp["col_def"].reshape(K, T)
     col_amb = wp["col_amb"].reshape(K, T)
@@ -219,6 +223,13 @@ def reduce_trajectories(wp: Dict[str, np.ndarray], K: int, T: int, lambda_xi=1.0
     xi = xi_wp[:, S].sum(1).astype(np.float64)
     xi_lo = xi_wp_lo[:, S].sum(1).astype(np.float64)
     xi_hi = xi_wp_hi[:, S].sum(1).astype(np.float64)
+    if start_wp is not None:     # + info state l = 0 (the shared start)
+        g = g + start_wp["gain"][0]
+        g_lo = g_lo + start_wp["gain_lo"][0]
+        g_hi = g_hi + start_wp["gain_hi"][0]
+        xi = xi + float(start_wp["nh"][0] - lambda_xi * start_wp["nl"][0])
+        xi_lo = xi_lo + float(start_wp["nh_lo"][0] - lambda_xi * start_wp["nl_hi"][0])
+        xi_hi = xi_hi + float(start_wp["nh_hi"][0] - lambda_xi * start_wp["nl_lo"][0])
     if variant == VARIANT_SUM:
         util, u_lo, u_hi = g.copy(), g_lo.copy(), g_hi.copy()
     else:
@@ -253,8 +264,9 @@ def acceptable_best(util_lo: np.ndarray, util_hi: np.ndarray, tol=1e-5) -> np.nd
 
 def score(wl, lambda_xi=1.0, k_sigma=0.5, variant=VARIANT_XI, info_stride=1, tau_hi=float("nan"),
           tau_lo=float("nan"), traj_idx: Optional[np.ndarray] = None, no_collision=False,
-          x=None, y=None, z=None, yaw=None) -> Dict[str, object]:
-    """Whole oracle pipeline O1-O7 on a workloads.Workload (optionally a trajectory subset)."""
+          x=None, y=None, z=None, yaw=None, start=None) -> Dict[str, object]:
+    """Whole oracle pipeline O1-O7 on a workloads.Workload (optionally a trajectory subset).
+    start = (x, y, z, yaw) scores the shared start state as info state l = 0 (include_start)."""
     c = classify(wl.info_w, wl.flags, variant, k_sigma, tau_hi, tau_lo)
     X = wl.x if x is None else x
     Y = wl.y if y is None else y
@@ -265,7 +277,12 @@ def score(wl, lambda_xi=1.0, k_sigma=0.5, variant=VARIANT_XI, info_stride=1, tau
     K, T = X.shape
     wp = waypoints(wl.means, wl.quats, wl.scales, wl.flags, c["cls"], c["u"], wl.robot, wl.camera,
                    X, Y, Z, YW, do_collision=not no_collision)
-    tr = reduce_trajectories(wp, K, T, lambda_xi, variant, info_stride)
+    start_wp = None
+    if start is not None:        # the start's view only: it is the robot's current state (not checked)
+        st = np.asarray(start, np.float32)
+        start_wp = waypoints(wl.means, wl.quats, wl.scales, wl.flags, c["cls"], c["u"], wl.robot, wl.camera,
+                             st[0:1], st[1:2], st[2:3], st[3:4], do_collision=False)
+    tr = reduce_trajectories(wp, K, T, lambda_xi, variant, info_stride, start_wp)
     tr["best"] = best(tr["utility"])
     tr["acceptable"] = acceptable_best(tr["utility_lo"], tr["utility_hi"])
     tr["wp"] = wp

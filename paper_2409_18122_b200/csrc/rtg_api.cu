@@ -105,8 +105,9 @@ cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& c
                            const int* count, long long list_max, long long* wp_gq, int* wp_nh, int* wp_nl,
                            int* counter, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_reduce(rtg_map_s* m, rtg_traj_s* tr, const rtg_score_params& p, const int* first_col,
-                          const long long* wp_gq, const int* wp_nh, const int* wp_nl, int* out_first,
+                          const long long* wp_gq, const int* wp_nh, const int* wp_nl, const StartState* start, int* out_first,
                           unsigned char* out_feasible, double* out_gain, double* out_util, cudaStream_t st);
+cudaError_t launch_start_setup(const float pose[4], StartState* st_dev, cudaStream_t st);
 cudaError_t launch_debug_wp(long long n, const long long* wp_gq, const ClassState* cs, double* out, cudaStream_t st);
 cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaStream_t st);
 cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st);
@@ -171,7 +172,8 @@ rtg_status check_params(const rtg_score_params* p) {
     if (p->variant < RTG_VARIANT_XI || p->variant > RTG_VARIANT_SQ) return invalid("unknown variant");
     if (p->info_stride < 1) return invalid("info_stride must be >= 1");
     if (p->mode != RTG_MODE_DENSE && p->mode != RTG_MODE_CULLED) return invalid("unknown mode");
-    if (p->flags & ~(unsigned)(RTG_SCORE_FULL_GAIN | RTG_SCORE_NO_COLLISION)) return invalid("unknown flag bits");
+    if (p->flags & ~(unsigned)(RTG_SCORE_FULL_GAIN | RTG_SCORE_NO_COLLISION | RTG_SCORE_INCLUDE_START))
+        return invalid("unknown flag bits");
     if (std::isinf(p->tau_hi) || std::isinf(p->tau_lo)) return invalid("tau must be finite or NaN");
     return RTG_OK;
 }
@@ -440,6 +442,8 @@ rtg_status rtg_traj_sample_unicycle(int device, int K, int T, float dt, const fl
         delete t;
         return cuda_fail(e, "rtg_traj_sample_unicycle", nullptr);
     }
+    for (int i = 0; i < 4; ++i) t->start[i] = start[i];
+    t->has_start = true;
     *out = t;
     return RTG_OK;
 }
@@ -470,7 +474,21 @@ rtg_status rtg_traj_sample_double_integrator(int device, int K, int T, float dt,
         delete t;
         return cuda_fail(e, "rtg_traj_sample_double_integrator", nullptr);
     }
+    for (int i = 0; i < 3; ++i) t->start[i] = start[i];
+    t->start[3] = (v0[0] == 0.f && v0[1] == 0.f) ? 0.f : (float)std::atan2((double)v0[1], (double)v0[0]);
+    t->has_start = true;
     *out = t;
+    return RTG_OK;
+}
+
+rtg_status rtg_traj_set_start(rtg_traj t, const float start[4]) {
+    rtg_status s = check_traj(t);
+    if (s != RTG_OK) return s;
+    if (!start) return invalid("start is NULL");
+    for (int i = 0; i < 4; ++i)
+        if (!finite_f(start[i])) return invalid("start state must be finite");
+    for (int i = 0; i < 4; ++i) t->start[i] = start[i];
+    t->has_start = true;
     return RTG_OK;
 }
 
@@ -543,7 +561,8 @@ struct Scratch {
     int* ints = nullptr;                  // [0] list count, [1] phase-A counter, [2] phase-B counter
     double* cam64 = nullptr;              // FP64 camera for the re-decision branch
     int* ranked = nullptr;                // computed trajectories in order (info list build)
-    unsigned long long* stats = nullptr;  // 8 counters (rtg_score_debug)
+    unsigned long long* stats = nullptr;  // RTG_DEBUG_STATS counters (rtg_score_debug)
+    StartState* start = nullptr;          // the shared start state as a 1-waypoint list (INCLUDE_START)
     void* block = nullptr;
 };
 
@@ -560,7 +579,8 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     size_t o_stats = o_ints + al(sizeof(int) * 8);
     size_t o_cam = o_stats + al(sizeof(unsigned long long) * RTG_DEBUG_STATS);
     size_t o_ranked = o_cam + al(sizeof(double) * 8);
-    size_t total = o_ranked + al(sizeof(int) * K);
+    size_t o_start = o_ranked + al(sizeof(int) * K);
+    size_t total = o_start + al(sizeof(StartState));
     cudaError_t e = dev_alloc(&s.block, total, st);
     if (e != cudaSuccess) return e;
     char* b = (char*)s.block;
@@ -573,6 +593,7 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     s.stats = (unsigned long long*)(b + o_stats);
     s.cam64 = (double*)(b + o_cam);
     s.ranked = (int*)(b + o_ranked);
+    s.start = (StartState*)(b + o_start);
     // the FP64 camera (8 doubles) for the re-decision branch: pageable copy, stream-ordered
     double c64[8] = {(double)cam->width, (double)cam->height, cam->fx, cam->fy, cam->cx, cam->cy, cam->z_near, cam->z_far};
     cudaError_t e2 = cudaMemcpyAsync(s.cam64, c64, sizeof(c64), cudaMemcpyHostToDevice, st);
@@ -588,6 +609,9 @@ rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_sc
     if (s == RTG_OK) s = check_params(p);
     if (s != RTG_OK) return s;
     if (m->device != tr->device) return invalid("map and trajectories live on different devices");
+    const bool with_start = (p->flags & RTG_SCORE_INCLUDE_START) != 0;
+    if (with_start && !tr->has_start)
+        return invalid("RTG_SCORE_INCLUDE_START needs the trajectories' start state (rtg_traj_set_start)");
     API_CK(cudaSetDevice(m->device), nullptr);
     cudaStream_t st = (cudaStream_t)stream;
     prof_begin(PH_CLASSIFY, st);
@@ -627,10 +651,29 @@ rtg_status rtg_score(rtg_map m, rtg_traj tr, const rtg_camera* cam, const rtg_sc
                &m->poisoned);
         prof_end(PH_GAIN, st);
     }
+    if (with_start) {
+        // info state l = 0: the shared start scored once as a one-waypoint list, added per trajectory
+        prof_begin(PH_GAIN, st);
+        API_CK(launch_start_setup(tr->start, sc.start, st), &m->poisoned);
+        rtg_traj_s one;
+        one.device = tr->device;
+        one.K = 1;
+        one.T = 1;
+        one.x = sc.start->pose + 0;
+        one.y = sc.start->pose + 1;
+        one.z = sc.start->pose + 2;
+        one.yaw = sc.start->pose + 3;
+        one.borrowed = true;
+        API_CK(launch_phase_b(m, &one, p->mode, ck, sc.start->list, sc.start->count, 1, &sc.start->gq,
+                              &sc.start->nh, &sc.start->nl, sc.start->counter, nullptr, st),
+               &m->poisoned);
+        prof_end(PH_GAIN, st);
+    }
     rtg_score_params pp = *p;
     if (per == 0) pp.info_stride = (int)T + 1;   // no info waypoint: sums are empty
     prof_begin(PH_REDUCE, st);
-    API_CK(launch_reduce(m, tr, pp, sc.first_col, sc.wp_gq, sc.wp_nh, sc.wp_nl, first_col, feasible, gain, utility, st),
+    API_CK(launch_reduce(m, tr, pp, sc.first_col, sc.wp_gq, sc.wp_nh, sc.wp_nl, with_start ? sc.start : nullptr,
+                         first_col, feasible, gain, utility, st),
            &m->poisoned);
     prof_end(PH_REDUCE, st);
     return RTG_OK;   // sc_guard frees the scratch block (stream-ordered)

@@ -92,13 +92,6 @@ __device__ __forceinline__ void cut(const float4& C, float Cj, float& plo, float
     }
 }
 
-// 1 << n for n < 32, 0 for any larger n (PTX shl clamps the shift amount: no compare/select)
-__device__ __forceinline__ unsigned bit_or_zero(unsigned n) {
-    unsigned r;
-    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(n));
-    return r;
-}
-
 // w += uc and pc += class byte of record word uc when p: over at most kFlushPasses passes (2 items
 // each) w - (pc << 24) = sum(u_q) < 2^32 and pc = nH + 128 nL with nH <= 126 (both exact)
 constexpr int kFlushPasses = 63;

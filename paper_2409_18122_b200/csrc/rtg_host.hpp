@@ -119,6 +119,14 @@ struct rtg_map_s {
     std::vector<void*> allocs;
 };
 
+// the shared start state as a one-waypoint info list (rtg_score with RTG_SCORE_INCLUDE_START)
+struct StartState {
+    float pose[4];             // x, y, z, yaw
+    long long gq;              // exact fixed-point gain sum of the start's view
+    int nh, nl;                // visible H / L counts
+    int list[1], count[1], counter[1], pad[1];
+};
+
 struct rtg_traj_s {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -129,4 +137,6 @@ struct rtg_traj_s {
     float* z = nullptr;
     float* yaw = nullptr;
     bool borrowed = false;   // rtg_traj_wrap: the arrays belong to the caller
+    bool has_start = false;  // shared start state x_i(0) (rtg_traj_set_start, samplers)
+    float start[4] = {0.f, 0.f, 0.f, 0.f};
 };

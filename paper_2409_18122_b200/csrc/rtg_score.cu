@@ -394,6 +394,7 @@ __global__ void __launch_bounds__(kDenseGainThreads) k_gain_dense(
 __global__ void k_reduce(int K, int T, int stride, int variant, float lambda_xi, int full_gain,
                          const int* __restrict__ first_col, const long long* __restrict__ wp_gq,
                          const int* __restrict__ wp_nh, const int* __restrict__ wp_nl,
+                         const StartState* __restrict__ start,
                          const ClassState* __restrict__ cs, int* __restrict__ out_first,
                          unsigned char* __restrict__ out_feasible, double* __restrict__ out_gain,
                          double* __restrict__ out_util) {
@@ -405,6 +406,11 @@ __global__ void k_reduce(int K, int T, int stride, int variant, float lambda_xi,
     const bool computed = feasible || full_gain;
     long long q = 0, h = 0, l = 0;
     if (computed) {
+        if (start && lane == 0) {   // info state l = 0, the shared start (Eq. equ:traj_utility)
+            q = start->gq;
+            h = start->nh;
+            l = start->nl;
+        }
         for (int t = stride - 1 + lane * stride; t < T; t += 32 * stride) {
             long long i = (long long)k * T + t;
             q += wp_gq[i];
@@ -654,15 +660,36 @@ cudaError_t launch_phase_b(rtg_map_s* m, rtg_traj_s* tr, int mode, const CamK& c
     return cudaGetLastError();
 }
 
+__global__ void k_start_setup(float x, float y, float z, float yaw, StartState* __restrict__ s) {
+    if (threadIdx.x == 0) {
+        s->pose[0] = x;
+        s->pose[1] = y;
+        s->pose[2] = z;
+        s->pose[3] = yaw;
+        s->gq = 0;
+        s->nh = 0;
+        s->nl = 0;
+        s->list[0] = 0;
+        s->count[0] = 1;
+        s->counter[0] = 0;
+    }
+}
+
+cudaError_t launch_start_setup(const float pose[4], StartState* s, cudaStream_t st) {
+    note_launch(), k_start_setup<<<1, 32, 0, st>>>(pose[0], pose[1], pose[2], pose[3], s);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_reduce(rtg_map_s* m, rtg_traj_s* tr, const rtg_score_params& p, const int* first_col,
-                          const long long* wp_gq, const int* wp_nh, const int* wp_nl, int* out_first,
-                          unsigned char* out_feasible, double* out_gain, double* out_util, cudaStream_t st) {
+                          const long long* wp_gq, const int* wp_nh, const int* wp_nl, const StartState* start,
+                          int* out_first, unsigned char* out_feasible, double* out_gain, double* out_util,
+                          cudaStream_t st) {
     int K = tr->K;
     int threads = 256;
     int blocks = (int)(((long long)K * 32 + threads - 1) / threads);
     note_launch(), k_reduce<<<blocks, threads, 0, st>>>(K, tr->T, p.info_stride, p.variant, p.lambda_xi,
                                          (p.flags & RTG_SCORE_FULL_GAIN) ? 1 : 0, first_col, wp_gq, wp_nh, wp_nl,
-                                         m->cls, out_first, out_feasible, out_gain, out_util);
+                                         start, m->cls, out_first, out_feasible, out_gain, out_util);
     return cudaGetLastError();
 }
 

@@ -33,7 +33,7 @@ G_NO_COLLIDE, G_NO_GAIN = 1, 2
 COLLIDE_ELLIPSOID, COLLIDE_PRINCIPAL_AXIS = 0, 1
 VARIANT_XI, VARIANT_SUM, VARIANT_SQ = 0, 1, 2
 MODE_DENSE, MODE_CULLED = 0, 1
-SCORE_FULL_GAIN, SCORE_NO_COLLISION = 1, 2
+SCORE_FULL_GAIN, SCORE_NO_COLLISION, SCORE_INCLUDE_START = 1, 2, 4
 DEBUG_STATS = 12
 
 
@@ -108,6 +108,7 @@ _SIGS = {
     "rtg_traj_sample_unicycle": (_S, [_I, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_float), _P, _P, _I, _P,
                                       ctypes.POINTER(_P)]),
     "rtg_traj_read": (_S, [_P, _P, _P, _P, _P, _P]),
+    "rtg_traj_set_start": (_S, [_P, ctypes.POINTER(ctypes.c_float)]),
     "rtg_traj_destroy": (_S, [_P]),
     "rtg_score": (_S, [_P, _P, ctypes.POINTER(Camera), ctypes.POINTER(ScoreParams), _P, _P, _P, _P, _P]),
     "rtg_best": (_S, [_P, _I, _LL, _P, ctypes.POINTER(BestResult)]),
@@ -373,6 +374,13 @@ class Traj:
                                        int(n), float(z), _stream(stream), ctypes.byref(h), ctypes.byref(d)),
                "rtg_traj_view_ring")
         return cls(h, R * int(n), 1, device), d.value
+
+    def set_start(self, start) -> "Traj":
+        """rtg_traj_set_start: the shared start state {x, y, z, yaw} (x_i(0) of Eq. equ:traj_utility),
+        scored as info state l = 0 with SCORE_INCLUDE_START."""
+        st4 = (ctypes.c_float * 4)(*[float(v) for v in start])
+        _check(_lib.rtg_traj_set_start(self.handle, st4), "rtg_traj_set_start")
+        return self
 
     def read(self, stream=None):
         torch = _torch()

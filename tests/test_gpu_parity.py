@@ -39,10 +39,13 @@ def _mode(R, name):
 
 
 def gpu_run(R, wl, mode, flags=None, stride=1, variant=0, lambda_xi=1.0, tau=(float("nan"), float("nan")),
-            pair_mask=False, x=None, y=None, z=None, yaw=None, debug=True):
+            pair_mask=False, x=None, y=None, z=None, yaw=None, debug=True, start=None):
     flags = R.SCORE_FULL_GAIN if flags is None else flags
     m = R.map_from_workload(wl)
     tr = R.traj_from_workload(wl, x=x, y=y, z=z, yaw=yaw)
+    if start is not None:
+        tr.set_start(start)
+        flags |= R.SCORE_INCLUDE_START
     p = R.make_params(lambda_xi=lambda_xi, variant=variant, info_stride=stride, mode=_mode(R, mode), flags=flags,
                       tau_hi=tau[0], tau_lo=tau[1])
     fc, fe, g, u = R.score(m, tr, wl.camera, p)
@@ -198,6 +201,43 @@ def test_room_variants(R, room, variant, stride, lam, tau, rule):
                       stride=stride, lambda_xi=lam, tau=t)
         check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
         check_trajectories(gpu, orc, wl.T)
+
+
+@pytest.mark.parametrize("variant,stride", [(0, 1), (0, 10), (1, 1), (2, 7)])
+def test_room_include_start(R, room, variant, stride):
+    """N1 include_start: the shared start state is info state l = 0 of Eq. equ:traj_utility
+    (PAPER.md:313-319), added to every computed trajectory; both modes against the oracle."""
+    idx = np.arange(5, room.K, 32)
+    start = (0.0, 0.0, 0.5, 0.3)          # the room recipe's start, heading turned to see walls and boxes
+    orc = O.score(room, traj_idx=idx, variant=variant, info_stride=stride, start=start)
+    base = O.score(room, traj_idx=idx, variant=variant, info_stride=stride)
+    f = base["feasible"]
+    assert np.any(orc["xi"][f] != base["xi"][f])          # the start sees something: the pin is not vacuous
+    for mode in MODES:
+        gpu = gpu_run(R, room, mode, x=room.x[idx], y=room.y[idx], z=room.z[idx], yaw=room.yaw[idx],
+                      variant=variant, stride=stride, start=start)
+        check_trajectories(gpu, orc, room.T)
+
+
+def test_include_start_needs_a_start(R, room):
+    """Uploaded trajectories carry no start: INCLUDE_START is refused; the unicycle sampler records
+    its start, so a sampled handle scores it (equal to an explicit set_start)."""
+    m = R.map_from_workload(room)
+    tr = R.traj_from_workload(room, x=room.x[:4], y=room.y[:4], z=room.z[:4], yaw=room.yaw[:4])
+    p = R.make_params(flags=R.SCORE_FULL_GAIN | R.SCORE_INCLUDE_START)
+    with pytest.raises(R.RTGError):
+        R.score(m, tr, room.camera, p)
+    v = torch.full((4,), 0.8, device="cuda")
+    w = torch.linspace(-0.5, 0.5, 4, device="cuda")
+    ts = R.Traj.sample_unicycle(v, w, 20, 0.1, (0.0, 0.0, 0.5, 0.3))
+    a = [t.cpu().numpy() for t in R.score(m, ts, room.camera, p)]
+    xs = ts.read()
+    tu = R.Traj.upload(*xs).set_start((0.0, 0.0, 0.5, 0.3))
+    b = [t.cpu().numpy() for t in R.score(m, tu, room.camera, p)]
+    for u, v2 in zip(a, b):
+        assert np.array_equal(u.view(np.uint8), v2.view(np.uint8))
+    for h in (tr, ts, tu, m):
+        h.close()
 
 
 # ----------------------------------------------------------------- multi-room (configs[2]), sample

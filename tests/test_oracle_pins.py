@@ -361,6 +361,16 @@ def test_brute_force_pipeline_by_hand():
     # info_stride 5 keeps waypoints l = 4, 9 only
     r5 = O.score(wl, tau_hi=0.5, tau_lo=0.2, info_stride=5)
     assert r5["xi"][1] == 2.0
+    # include_start (Eq. equ:traj_utility sums l = 0..L): the shared start (origin,
+    # z 0.5, heading +x) sees A at depth 1.05 (w 0.1 < tau_lo: class L -> xi -1, gain 0.1) and not B
+    # (depth 0): every trajectory gains xi - 1 and gain + 0.1; the winner stays 1
+    rs = O.score(wl, tau_hi=0.5, tau_lo=0.2, start=(0.0, 0.0, 0.5, 0.0))
+    assert list(rs["xi"]) == [r["xi"][0] - 1.0, 9.0, -1.0]
+    assert rs["gain"][2] == pytest.approx(float(np.float32(0.1)), rel=1e-12)
+    assert list(rs["utility"][1:]) == [9.0, -1.0] and np.isneginf(rs["utility"][0])
+    assert rs["best"] == 1
+    rs5 = O.score(wl, tau_hi=0.5, tau_lo=0.2, info_stride=5, start=(0.0, 0.0, 0.5, np.pi / 2))
+    assert rs5["xi"][1] == 3.0          # start facing +y sees B (H): l = 0, 4, 9
 
 
 def test_argmax_ties_permutation_and_none():
