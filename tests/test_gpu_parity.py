@@ -253,31 +253,56 @@ def test_multi_room_sample_parity(R):
 
 # ----------------------------------------------------------------- outdoor (configs[3]) at full size
 
-def test_outdoor_full_size_sampled(R):
-    """Full map (2M) and full K=16384 x T=100 in the bench launch configuration (culled, early
-    exit); outputs of sampled trajectories compared with the oracle one by one."""
-    wl = W.outdoor()
+def _full_size_sampled(R, wl, n_feas, n_infeas, n_top, n_debug, seed):
+    """Full map and full K x T in the bench launch configuration (culled, early exit): a sample of
+    trajectories -- random feasible and infeasible ones plus the GPU's n_top best by utility -- is
+    scored by the oracle one by one.  The argmax (Eq. equ:traj_utility): the GPU's
+    winner is in the sample's acceptable set and its utility equals the oracle's exactly (integer xi)."""
     gpu = gpu_run(R, wl, "culled", flags=0, debug=False)
-    rng = np.random.default_rng(5)
+    rng = np.random.default_rng(seed)
+    u = gpu["utility"]
     feas = np.nonzero(gpu["feasible"])[0]
     infeas = np.nonzero(gpu["feasible"] == 0)[0]
-    assert len(feas) > 1000 and len(infeas) > 1000
-    idx = np.sort(np.concatenate([rng.choice(feas, 6, replace=False), rng.choice(infeas, 6, replace=False)]))
+    assert len(feas) > n_feas and len(infeas) > n_infeas
+    top = np.argsort(-u, kind="stable")[:n_top]                     # the GPU's best first (ties: lowest k)
+    idx = np.unique(np.concatenate([rng.choice(feas, n_feas, replace=False),
+                                    rng.choice(infeas, n_infeas, replace=False), top]))
     orc = O.score(wl, traj_idx=idx)
-    sub = {k: gpu[k][idx] for k in ("first_col", "feasible", "gain", "utility")}
-    sub["best"] = (None, -2)
     K = len(idx)
     allowed = orc["first_col_allowed"]
-    assert np.all(allowed[np.arange(K), sub["first_col"]])
-    f = sub["feasible"].astype(bool)
-    assert np.all(np.isnan(sub["gain"][~f])) and np.all(np.isneginf(sub["utility"][~f]))
+    fc = gpu["first_col"][idx]
+    assert np.all(allowed[np.arange(K), fc])
+    f = gpu["feasible"][idx].astype(bool)
+    assert np.array_equal(f, fc == wl.T)
+    g, uu = gpu["gain"][idx], u[idx]
+    assert np.all(np.isnan(g[~f])) and np.all(np.isneginf(uu[~f]))
     tol = 1e-5 * np.abs(orc["gain_hi"][f]) + 1e-9
-    assert np.all((sub["gain"][f] >= orc["gain_lo"][f] - tol) & (sub["gain"][f] <= orc["gain_hi"][f] + tol))
-    assert np.all((sub["utility"][f] >= orc["xi_lo"][f]) & (sub["utility"][f] <= orc["xi_hi"][f]))
-    # the argmax is a property of all K: its utility is the maximum and ties go to the lowest index
-    u = gpu["utility"]
+    assert np.all((g[f] >= orc["gain_lo"][f] - tol) & (g[f] <= orc["gain_hi"][f] + tol))
+    assert np.all((uu[f] >= orc["xi_lo"][f]) & (uu[f] <= orc["xi_hi"][f]))
+    # the argmax over all K is the GPU's top trajectory; within the sample (which holds the GPU's
+    # top n_top) it must be acceptable to the oracle, with the oracle's exact utility
     b = gpu["best"][1]
-    assert u[b] == np.max(u) and np.all(u[:b] < u[b])
+    assert b == top[0] and u[b] == np.max(u) and np.all(u[:b] < u[b])
+    pos = int(np.nonzero(idx == b)[0][0])
+    acc = set(int(idx[a]) for a in orc["acceptable"] if a >= 0)
+    assert b in acc, (b, sorted(acc)[:10])
+    # exact: the GPU takes every decision in FP64 (DESIGN R2), so its integer xi equals the oracle's
+    # nominal FP64 value, also when some of the winner's pairs lie in the 1e-6 band
+    assert orc["xi_lo"][pos] <= u[b] <= orc["xi_hi"][pos] and u[b] == orc["utility"][pos]
+    assert orc["best"] >= 0 and idx[orc["best"]] in acc
+    # per-waypoint debug arrays of n_debug sampled trajectories (the top one among them)
+    dbg = np.concatenate([[b], idx[idx != b][:n_debug - 1]])
+    d = gpu_run(R, wl, "culled", x=wl.x[dbg], y=wl.y[dbg], z=wl.z[dbg], yaw=wl.yaw[dbg])
+    od = O.score(wl, traj_idx=dbg)
+    check_waypoints(d, od, d["info"].fixed_point_shift)
+    check_trajectories(d, od, wl.T)
+    return gpu, idx, orc
+
+
+def test_outdoor_full_size_sampled(R):
+    """BASELINE.json configs[3] (2M Gaussians, 16,384 x 100): 40+ trajectories incl. the GPU's top 8
+    against the oracle, per-waypoint arrays for 4 of them."""
+    _full_size_sampled(R, W.outdoor(), n_feas=16, n_infeas=16, n_top=8, n_debug=4, seed=5)
 
 
 # ----------------------------------------------------------------- hand cases (golden fixtures)
@@ -565,18 +590,7 @@ def test_scale_full_size_sampled_with_views(R):
     """BASELINE.json configs[4] at full size (5M Gaussians, 65,536 x 100 waypoints, 8,192 gain-only
     views) in the bench launch configuration; sampled trajectories and views against the oracle."""
     wl = W.scale()
-    gpu = gpu_run(R, wl, "culled", flags=0, debug=False)
-    rng = np.random.default_rng(9)
-    feas = np.nonzero(gpu["feasible"])[0]
-    infeas = np.nonzero(gpu["feasible"] == 0)[0]
-    idx = np.sort(np.concatenate([rng.choice(feas, 2, replace=False), rng.choice(infeas, 1, replace=False)]))
-    orc = O.score(wl, traj_idx=idx)
-    fc, f = gpu["first_col"][idx], gpu["feasible"][idx].astype(bool)
-    assert np.all(orc["first_col_allowed"][np.arange(len(idx)), fc])
-    g = gpu["gain"][idx]
-    tol = 1e-5 * np.abs(orc["gain_hi"][f]) + 1e-9
-    assert np.all((g[f] >= orc["gain_lo"][f] - tol) & (g[f] <= orc["gain_hi"][f] + tol))
-    assert np.all((gpu["utility"][idx][f] >= orc["xi_lo"][f]) & (gpu["utility"][idx][f] <= orc["xi_hi"][f]))
+    _full_size_sampled(R, wl, n_feas=4, n_infeas=2, n_top=4, n_debug=2, seed=9)
     # views: T = 1, no collision, full gain
     vs = np.arange(0, wl.views["x"].shape[0], 1024)
     v = {c: np.ascontiguousarray(wl.views[c][vs]) for c in ("x", "y", "z", "yaw")}
