@@ -4,7 +4,7 @@
 for rep in 1 2; do
   for v in "$@"; do
     cp "$v" paper_2409_18122_b200/librtg.so
-    out=$(timeout 600 python bench.py --config ${CONFIG:-outdoor} --mode ${MODE:-culled} --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline 2>&1 | tail -1)
+    out=$(timeout 600 python bench.py --config ${CONFIG:-outdoor} --mode ${MODE:-culled} --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline ${EXTRA:-} 2>&1 | tail -1)
     python - "$v" "$out" <<'PY'
 import json, sys
 v, line = sys.argv[1], sys.argv[2]
