@@ -60,51 +60,99 @@ __global__ void k_bounds_init(DevBounds* b) {
 }
 
 
-__global__ void k_bounds(long long n, const float* __restrict__ means, const float* __restrict__ quats,
-                         const float* __restrict__ scales, const float* __restrict__ opacity,
-                         const float* __restrict__ w, const unsigned char* __restrict__ flags, rtg_robot rb,
-                         DevBounds* __restrict__ out) {
+struct BoundsAcc {
     int err = 0, ng = 0, nc = 0;
     int gmn[3] = {INT_MAX, INT_MAX, INT_MAX}, gmx[3] = {INT_MIN, INT_MIN, INT_MIN};
     int cmn[3] = {INT_MAX, INT_MAX, INT_MAX}, cmx[3] = {INT_MIN, INT_MIN, INT_MIN};
     int rbm = INT_MIN, rhm = INT_MIN;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        float p[3] = {means[i], means[n + i], means[2 * n + i]};
-        float q0 = quats[i], q1 = quats[n + i], q2 = quats[2 * n + i], q3 = quats[3 * n + i];
-        float s0 = scales[i], s1 = scales[n + i], s2 = scales[2 * n + i];
-        float wi = w[i];
-        float op = opacity ? opacity[i] : 0.5f;
-        if (!(isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]))) err |= 1;
-        double qn = (double)q0 * q0 + (double)q1 * q1 + (double)q2 * q2 + (double)q3 * q3;
-        if (!(qn >= 1e-24) || !isfinite(qn)) err |= 2;
-        if (!(s0 > 0.f && s1 > 0.f && s2 > 0.f) || !isfinite(s0) || !isfinite(s1) || !isfinite(s2)) err |= 4;
-        if (!(wi >= 0.f) || !isfinite(wi)) err |= 8;
-        if (!(op >= 0.f && op <= 1.f)) err |= 16;
-        unsigned f = flags ? flags[i] : 0u;
-        if (!(f & RTG_G_NO_GAIN)) {
-            ++ng;
-            for (int d = 0; d < 3; ++d) {
-                int o = f2o(p[d]);
-                gmn[d] = min(gmn[d], o);
-                gmx[d] = max(gmx[d], o);
-            }
+};
+
+// validation + bounds of one Gaussian's fp32 inputs
+__device__ __forceinline__ void bounds_one(BoundsAcc& A, float px, float py, float pz, float q0, float q1, float q2,
+                                           float q3, float s0, float s1, float s2, float op, float wi, unsigned f,
+                                           const rtg_robot& rb) {
+    const float p[3] = {px, py, pz};
+    if (!(isfinite(px) && isfinite(py) && isfinite(pz))) A.err |= 1;
+    double qn = (double)q0 * q0 + (double)q1 * q1 + (double)q2 * q2 + (double)q3 * q3;
+    if (!(qn >= 1e-24) || !isfinite(qn)) A.err |= 2;
+    if (!(s0 > 0.f && s1 > 0.f && s2 > 0.f) || !isfinite(s0) || !isfinite(s1) || !isfinite(s2)) A.err |= 4;
+    if (!(wi >= 0.f) || !isfinite(wi)) A.err |= 8;
+    if (!(op >= 0.f && op <= 1.f)) A.err |= 16;
+    if (!(f & RTG_G_NO_GAIN)) {
+        ++A.ng;
+        for (int d = 0; d < 3; ++d) {
+            int o = f2o(p[d]);
+            A.gmn[d] = min(A.gmn[d], o);
+            A.gmx[d] = max(A.gmx[d], o);
         }
-        if (!(f & RTG_G_NO_COLLIDE)) {
-            ++nc;
-            for (int d = 0; d < 3; ++d) {
-                int o = f2o(p[d]);
-                cmn[d] = min(cmn[d], o);
-                cmx[d] = max(cmx[d], o);
-            }
-            double a[3];
-            semi_axes64(scales[i], scales[n + i], scales[2 * n + i], rb, a);
-            double amax = fmax(a[0], fmax(a[1], a[2])), amin = fmin(a[0], fmin(a[1], a[2]));
-            if (isfinite(amax)) {
-                rbm = max(rbm, f2o(__double2float_ru(amax)));
-                rhm = max(rhm, f2o(__double2float_ru(amax / amin)));
-            }
+    }
+    if (!(f & RTG_G_NO_COLLIDE)) {
+        ++A.nc;
+        for (int d = 0; d < 3; ++d) {
+            int o = f2o(p[d]);
+            A.cmn[d] = min(A.cmn[d], o);
+            A.cmx[d] = max(A.cmx[d], o);
         }
+        double a[3];
+        semi_axes64(s0, s1, s2, rb, a);
+        double amax = fmax(a[0], fmax(a[1], a[2])), amin = fmin(a[0], fmin(a[1], a[2]));
+        if (isfinite(amax)) {
+            A.rbm = max(A.rbm, f2o(__double2float_ru(amax)));
+            A.rhm = max(A.rhm, f2o(__double2float_ru(amax / amin)));
+        }
+    }
+}
+
+// one streaming pass over the inputs: validation, bounds, and the map's own copies of the weights
+// and flags (w_out, flags_out); kVec: four consecutive Gaussians per step with 128-bit loads of every
+// planar array (needs n % 4 == 0 and 16-byte aligned arrays)
+template <bool kVec>
+__global__ void k_bounds(long long n, const float* __restrict__ means, const float* __restrict__ quats,
+                         const float* __restrict__ scales, const float* __restrict__ opacity,
+                         const float* __restrict__ w, const unsigned char* __restrict__ flags, rtg_robot rb,
+                         float* __restrict__ w_out, unsigned char* __restrict__ flags_out,
+                         DevBounds* __restrict__ out) {
+    BoundsAcc A;
+    if (kVec) {
+        const long long n4 = n >> 2;
+        for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n4;
+             j += (long long)gridDim.x * blockDim.x) {
+            const float4 mx = __ldg(reinterpret_cast<const float4*>(means) + j);
+            const float4 my = __ldg(reinterpret_cast<const float4*>(means + n) + j);
+            const float4 mz = __ldg(reinterpret_cast<const float4*>(means + 2 * n) + j);
+            const float4 qa = __ldg(reinterpret_cast<const float4*>(quats) + j);
+            const float4 qb = __ldg(reinterpret_cast<const float4*>(quats + n) + j);
+            const float4 qc = __ldg(reinterpret_cast<const float4*>(quats + 2 * n) + j);
+            const float4 qd = __ldg(reinterpret_cast<const float4*>(quats + 3 * n) + j);
+            const float4 sa = __ldg(reinterpret_cast<const float4*>(scales) + j);
+            const float4 sb = __ldg(reinterpret_cast<const float4*>(scales + n) + j);
+            const float4 sc = __ldg(reinterpret_cast<const float4*>(scales + 2 * n) + j);
+            const float4 wv = __ldg(reinterpret_cast<const float4*>(w) + j);
+            const float4 ov = opacity ? __ldg(reinterpret_cast<const float4*>(opacity) + j) : make_float4(.5f, .5f, .5f, .5f);
+            const unsigned fv = flags ? __ldg(reinterpret_cast<const unsigned*>(flags) + j) : 0u;
+            reinterpret_cast<float4*>(w_out)[j] = wv;
+            if (flags) reinterpret_cast<unsigned*>(flags_out)[j] = fv;
+            bounds_one(A, mx.x, my.x, mz.x, qa.x, qb.x, qc.x, qd.x, sa.x, sb.x, sc.x, ov.x, wv.x, fv & 0xffu, rb);
+            bounds_one(A, mx.y, my.y, mz.y, qa.y, qb.y, qc.y, qd.y, sa.y, sb.y, sc.y, ov.y, wv.y, (fv >> 8) & 0xffu, rb);
+            bounds_one(A, mx.z, my.z, mz.z, qa.z, qb.z, qc.z, qd.z, sa.z, sb.z, sc.z, ov.z, wv.z, (fv >> 16) & 0xffu, rb);
+            bounds_one(A, mx.w, my.w, mz.w, qa.w, qb.w, qc.w, qd.w, sa.w, sb.w, sc.w, ov.w, wv.w, fv >> 24, rb);
+        }
+    } else {
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const float wi = w[i];
+            const unsigned f = flags ? flags[i] : 0u;
+            w_out[i] = wi;
+            if (flags) flags_out[i] = (unsigned char)f;
+            bounds_one(A, means[i], means[n + i], means[2 * n + i], quats[i], quats[n + i], quats[2 * n + i],
+                       quats[3 * n + i], scales[i], scales[n + i], scales[2 * n + i], opacity ? opacity[i] : 0.5f,
+                       wi, f, rb);
+        }
+    }
+    int err = A.err, ng = A.ng, nc = A.nc, rbm = A.rbm, rhm = A.rhm;
+    int gmn[3], gmx[3], cmn[3], cmx[3];
+    for (int d = 0; d < 3; ++d) {
+        gmn[d] = A.gmn[d]; gmx[d] = A.gmx[d]; cmn[d] = A.cmn[d]; cmx[d] = A.cmx[d];
     }
     // warp aggregate, one atomic per warp
     unsigned full = 0xffffffffu;
@@ -597,16 +645,31 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     // --- bounds + validation (one sync)
     DevBounds* db = nullptr;
     MAP_CK(dev_alloc((void**)&db, sizeof(DevBounds), st));
+    // the map's own weights and flags (input order), written by the validation pass
+    MAP_CK(map_alloc(m, &m->w_orig, n, st));
+    if (flags) MAP_CK(map_alloc(m, &m->flags, n, st));
     // the default classification's statistics (k = 1/2, derived thresholds) depend only on
     // the inputs: they run while the host reads the bounds back, and the scatter then writes final
     // records (class increments, fixed-point u)
     MAP_CK(map_alloc(m, &m->cls, 1, st));
     MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
     note_launch(), k_bounds_init<<<1, 1, 0, st>>>(db);
-    if (n > 0)
-        note_launch(), k_bounds<<<nblocks(n, 256) > 592 ? 592 : nblocks(n, 256), 256, 0, st>>>(
-                           n, means, quats, scales, opacity, w, flags, rb, db);
-    DevBounds hb;
+    if (n > 0) {
+        auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
+        const bool vec = (n % 4 == 0) && al16(means) && al16(quats) && al16(scales) && al16(opacity) && al16(w) &&
+                         ((uintptr_t)flags & 3u) == 0 && al16(m->w_orig) && ((uintptr_t)m->flags & 3u) == 0;
+        if (vec)
+            note_launch(), k_bounds<true><<<nblocks(n / 4, 256) > 1184 ? 1184 : nblocks(n / 4, 256), 256, 0, st>>>(
+                               n, means, quats, scales, opacity, w, flags, rb, m->w_orig, m->flags, db);
+        else
+            note_launch(), k_bounds<false><<<nblocks(n, 256) > 1184 ? 1184 : nblocks(n, 256), 256, 0, st>>>(
+                               n, means, quats, scales, opacity, w, flags, rb, m->w_orig, m->flags, db);
+    }
+    // pinned staging (one per host thread) keeps the readback asynchronous: the classification
+    // statistics below are enqueued while it is in flight
+    thread_local DevBounds* hbp = nullptr;
+    if (!hbp) MAP_CK(cudaMallocHost((void**)&hbp, sizeof(DevBounds)));
+    DevBounds& hb = *hbp;
     MAP_CK(cudaMemcpyAsync(&hb, db, sizeof(DevBounds), cudaMemcpyDeviceToHost, st));
     cudaEvent_t ev;
     MAP_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -680,11 +743,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     cg.h = (float)hc;
     cg.ncells = (long long)cg.nx * cg.ny * cg.nz;
     // --- allocations
-    // >= 64 NaN records after each copy: the culled kernel's idle lanes read past a run's end
+    // >= 64 NaN records after each copy: the culled kernel's sentinel run (items past its queue)
     m->n_gain_pad = m->n_gain > 0 ? ((m->n_gain + 64 + kTile - 1) / kTile) * kTile : 0;
     m->n_col_pad = ((m->n_col + kTile - 1) / kTile) * kTile;
-    MAP_CK(map_alloc(m, &m->w_orig, n, st));
-    if (flags) MAP_CK(map_alloc(m, &m->flags, n, st));
     MAP_CK(map_alloc(m, &m->grec, 2 * m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gidx, 2 * m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gstartA, gg.ncellsA + 1, st));
@@ -695,8 +756,6 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->csrc, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
-    if (n > 0) MAP_CK(cudaMemcpyAsync(m->w_orig, w, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
-    if (flags && n > 0) MAP_CK(cudaMemcpyAsync(m->flags, flags, n, cudaMemcpyDeviceToDevice, st));
     // --- counting sort into both grids
     int *gkey = nullptr, *ckey = nullptr, *gcountA = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
     MAP_CK(dev_alloc((void**)&gkey, sizeof(int) * (n > 0 ? n : 1), st));
@@ -705,13 +764,13 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     int* crank = nullptr;
     MAP_CK(dev_alloc((void**)&grank, sizeof(int2) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&crank, sizeof(int) * (n > 0 ? n : 1), st));
-    MAP_CK(dev_alloc((void**)&gcountA, sizeof(int) * (gg.ncellsA + 1), st));
-    MAP_CK(dev_alloc((void**)&gcountB, sizeof(int) * (gg.ncellsB + 1), st));
+    // the three cell-count arrays in one block, cleared by one memset
+    const long long ncnt = (gg.ncellsA + 1) + (gg.ncellsB + 1) + (cg.ncells + 1);
+    MAP_CK(dev_alloc((void**)&gcountA, sizeof(int) * ncnt, st));
+    gcountB = gcountA + (gg.ncellsA + 1);
+    ccount = gcountB + (gg.ncellsB + 1);
     MAP_CK(dev_alloc((void**)&gstartB, sizeof(int) * (gg.ncellsB + 1), st));
-    MAP_CK(dev_alloc((void**)&ccount, sizeof(int) * (cg.ncells + 1), st));
-    MAP_CK(cudaMemsetAsync(gcountA, 0, sizeof(int) * (gg.ncellsA + 1), st));
-    MAP_CK(cudaMemsetAsync(gcountB, 0, sizeof(int) * (gg.ncellsB + 1), st));
-    MAP_CK(cudaMemsetAsync(ccount, 0, sizeof(int) * (cg.ncells + 1), st));
+    MAP_CK(cudaMemsetAsync(gcountA, 0, sizeof(int) * ncnt, st));
     note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc, (long long)gg.ny * gg.nxb);
     unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
     if (n > 0)
@@ -749,9 +808,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     dev_free(ckey, st);
     dev_free(grank, st);
     dev_free(crank, st);
-    dev_free(gcountA, st);
-    dev_free(gcountB, st);
-    dev_free(ccount, st);
+    dev_free(gcountA, st);   // (gcountB, ccount live in the same block)
     // --- default classification (k = 1/2, derived thresholds)
     MAP_CK(class_prefix(m, st, gstartB));
     dev_free(gstartB, st);
