@@ -436,6 +436,8 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, ncu
         if mode == "dense":
             units = {"pairs_per_info_waypoint": float(wl.N), "I_pair": I_DENSE_PAIR}
             lane_instr = n_info * float(wl.N) * I_DENSE_PAIR
+        elif work is None:     # nothing feasible (tiny): no info waypoint was scored
+            units, lane_instr = {"info_waypoints": 0}, 0.0
         else:
             rows = work.get("rows", 0.0)
             units = {"info_waypoints": n_info, "tested_per_wp": work["tested"], "units_per_wp": work["units"],
