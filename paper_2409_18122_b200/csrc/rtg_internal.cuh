@@ -368,6 +368,27 @@ __device__ __forceinline__ bool warp_point_collides(float px, float py, float pz
 
 constexpr int kUnionFactor = 3;
 
+// the points of `live` (lanes) one at a time, ascending (the first hit is the lowest point); out of line,
+// so the common union-box path keeps its registers
+static __device__ __noinline__ unsigned warp_points_collide_each(float px, float py, float pz, unsigned live,
+                                                                 bool first_only, const CRec* __restrict__ crec,
+                                                                 const CMat* __restrict__ cmat,
+                                                                 const CSrc* __restrict__ csrc, const rtg_robot rb,
+                                                                 const int* __restrict__ cstart, const ColGridK g,
+                                                                 float gq, unsigned& nref, unsigned long long& ntest) {
+    constexpr unsigned kAll = 0xffffffffu;
+    unsigned hits = 0u;
+    for (unsigned lv = live; lv; lv &= lv - 1) {
+        const int jj = __ffs(lv) - 1;
+        const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj), qz = __shfl_sync(kAll, pz, jj);
+        if (warp_point_collides(qx, qy, qz, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest)) {
+            hits |= 1u << jj;
+            if (first_only) break;
+        }
+    }
+    return hits;
+}
+
 // which of the nj points held by lanes 0 .. nj-1 collide (bit j: lane j's point; warp-uniform)?
 // The candidates of the union of their cell boxes are loaded once and each is tested against every
 // point: a Gaussian outside a point's own box lies beyond g.R, past its bounding radius, so the sphere
@@ -407,18 +428,8 @@ __device__ __forceinline__ unsigned warp_points_collide_mask(float px, float py,
     iy1 = __reduce_max_sync(kAll, iy1);
     iz0 = __reduce_min_sync(kAll, iz0);
     iz1 = __reduce_max_sync(kAll, iz1);
-    if ((long long)(ix1 - ix0 + 1) * (iy1 - iy0 + 1) * (iz1 - iz0 + 1) > (long long)kUnionFactor * own_sum) {
-        unsigned hits = 0u;
-        for (unsigned lv = live; lv; lv &= lv - 1) {   // ascending: the first hit is the lowest point
-            const int jj = __ffs(lv) - 1;
-            const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj), qz = __shfl_sync(kAll, pz, jj);
-            if (warp_point_collides(qx, qy, qz, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest)) {
-                hits |= 1u << jj;
-                if (first_only) break;
-            }
-        }
-        return hits;
-    }
+    if ((long long)(ix1 - ix0 + 1) * (iy1 - iy0 + 1) * (iz1 - iz0 + 1) > (long long)kUnionFactor * own_sum)
+        return warp_points_collide_each(px, py, pz, live, first_only, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest);
     const int nyr = iy1 - iy0 + 1;
     const int nrows = nyr * (iz1 - iz0 + 1);
     unsigned hits = 0u, todo = live;

@@ -197,14 +197,8 @@ __device__ bool warp_points_collide_any(float px, float py, float z, int nj, con
     const unsigned live = __ballot_sync(kAll, mine);
     // spread-out points (long primitives): the union box would hold many times the candidates of the
     // points' own boxes -- test them one at a time (same decisions, see warp_points_collide_mask)
-    if ((long long)(ix1 - ix0 + 1) * (iy1 - iy0 + 1) > (long long)kUnionFactor * own_sum) {
-        for (unsigned lv = live; lv; lv &= lv - 1) {
-            const int jj = __ffs(lv) - 1;
-            const float qx = __shfl_sync(kAll, px, jj), qy = __shfl_sync(kAll, py, jj);
-            if (warp_point_collides(qx, qy, z, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest)) return true;
-        }
-        return false;
-    }
+    if ((long long)(ix1 - ix0 + 1) * (iy1 - iy0 + 1) > (long long)kUnionFactor * own_sum)
+        return warp_points_collide_each(px, py, z, live, true, crec, cmat, csrc, rb, cstart, g, gq, nref, ntest) != 0u;
     const int nyr = iy1 - iy0 + 1;
     const int nrows = nyr * (iz1 - iz0 + 1);
     bool hit = false;
