@@ -95,7 +95,7 @@ def main():
     iz, iy, ix = top // (dims[0] * dims[1]), (top // dims[0]) % dims[1], top % dims[0]
     cen = np.stack([lo[0] + (ix + 0.5) * 2.5, lo[1] + (iy + 0.5) * 2.5, lo[2] + (iz + 0.5) * 2.5]).astype(np.float32)
     p = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
-    d = torch.from_numpy(np.linalg.norm(cen[:2], axis=0).repeat(8)).cuda()   # stand-in path distances
+    d = torch.from_numpy(np.linalg.norm(cen[:2], axis=0).astype(np.float64).repeat(8)).cuda()   # stand-in path distances (FP64, as the ABI reads them)
 
     def views():
         tr, _ = R.Traj.view_ring(torch.from_numpy(cen).cuda(), 2.5, wl.camera, 8, float(cen[2].mean()))
