@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         for (int gb = gb0; gb < gend; gb += 64) {
                             // head bit k of (hhi:hlo) <=> a run starts at item gb + k + 1
                             const int hw = (gb - gb0) >> 5;
+                            RTG_CHECK(hw + 2 < kHeadWords, "head bitmap window");
                             const uint2 h01 = *reinterpret_cast<const uint2*>(sw.head + hw);
                             const unsigned h2 = sw.head[hw + 2];
                             const unsigned hlo = __funnelshift_r(h01.x, h01.y, 1);
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                             const int gpa = gb + lane, gpb = gpa + 32;
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_lt)];
                             const int gib = gpb + qs[r0 + na + __popc(hhi & lanes_lt)];
+                            RTG_CHECK(r0 + na + __popc(hhi) <= nq && nq < kQCap + 64, "queue run index");
                             RTG_CHECK(gia >= 0 && gia < g.nrec && gib >= 0 && gib < g.nrec, "record index");
                             const GRec Ga = grec[(unsigned)gia], Gb = grec[(unsigned)gib];
                             float guard_a, guard_b;
