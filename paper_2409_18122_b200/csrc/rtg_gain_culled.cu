@@ -40,7 +40,11 @@ namespace {
 constexpr unsigned kFullG = 0xffffffffu;
 constexpr int kWarpsG = 4;     // warps per CTA; RTG_GAIN_MINB CTAs per SM: 36 warps at 56 registers
 constexpr int kQCap = 256;    // queued runs per warp
-constexpr int kQFlush = 192;  // test the queue once more runs than this are waiting (an append adds <= 64)
+#ifndef RTG_QFLUSH
+#define RTG_QFLUSH 192
+#endif
+constexpr int kQFlush = RTG_QFLUSH;  // test the queue once more runs than this are waiting (an append adds <= 64)
+static_assert(kQFlush + 64 <= kQCap, "the flush prefix takes 8 runs per lane: at most 256 queued runs");
 constexpr int kMaxUnits = 1024;   // units of a row chunk with a shared-memory owner table (else: search)
 constexpr int kHeadWords = (64 * 63 + 64 + 32) / 32 + 1;   // a flush chunk (kFlushPasses passes) + the window tail
 
