@@ -57,6 +57,9 @@ long long scan_i32_scratch_ints(long long n);
 cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* scratch, cudaStream_t st);
 // copy-B records' (u_q, nH | nL << 32) pairs (from GRec::uc) scanned into out[0 .. 2n+1]
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st);
+// exclusive scan over the ncols = ny * nx columns (row-major) of their record counts (all z-cells), read
+// from the z-fastest start table tab [ny][nx + 1][nz]; out[ncols] = total
+cudaError_t exclusive_scan_col_counts(const int* tab, int nx, int nz, long long ncols, int* out, cudaStream_t st);
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
@@ -87,12 +90,14 @@ struct rtg_map_s {
     // original-order inputs kept for (re)classification
     float* w_orig = nullptr;             // [n]
     unsigned char* flags = nullptr;      // [n] or null
-    // visibility records: copy A at [0, n_gain) (sorted by (iy, ix)), padded to n_gain_pad (a
-    // multiple of kTile) with NaN means, then copy B at [n_gain_pad, n_gain_pad + n_gain) (sorted
-    // by (iy, iz, ix)), padded likewise.  gidx is parallel to grec.
+    // visibility records, two copies, each padded to n_gain_pad (a multiple of kTile, >= n_gain + 64)
+    // with NaN means: copy A at [0, n_gain) sorted by (iy, ix, iz) -- whole columns for the flank runs;
+    // copy B at [n_gain_pad, n_gain_pad + n_gain) sorted by (iy, iz, ix) -- x-contiguous z-slabs.
+    // Copy B is counting-sorted from the inputs; copy A is derived from it (cell blocks moved in
+    // z-fastest order).  gidx is parallel to copy B.
     long long n_gain_pad = 0;
     rtg::GRec* grec = nullptr;           // [2 * n_gain_pad]
-    int* gidx = nullptr;                 // original index per record
+    int* gidx = nullptr;                 // [n_gain_pad] original index per copy-B record
     int* gstartA = nullptr;              // [ncellsA + 1] first copy-A record of column (iy, ix)
     int* gtabB = nullptr;                // [ny][nx + 1][nz] first copy-B record (relative to n_gain_pad) of
                                          // cell (iy, iz, ix); ix = nx: end of the z-slab (iy, iz)

@@ -5,12 +5,13 @@
 //      r_b = max_i a_i; stored as FP32 records (+ an FP64 copy of M for the re-decision branch).
 //      Records are placed by a counting sort into two uniform grids:
 //        * visibility grid: rows (hy) x x-cells (hx) x z-cells (hz), gain-eligible Gaussians only,
-//          two copies: A sorted by (row, x-cell) (whole columns), B by (row, z-cell, x-cell)
-//          (x-contiguous z-slabs) with exact per-record prefixes of u_q and the class counts;
+//          two copies: B sorted by (row, z-cell, x-cell) (x-contiguous z-slabs) with exact per-record
+//          prefixes of u_q and the class counts, counting-sorted from the inputs; A sorted by (row,
+//          x-cell, z-cell) (whole columns) derived from B by moving cell blocks in z-fastest order;
 //        * collision grid: cubic cells (h), x fastest, collidable (non-ground) Gaussians only.
 //  a2  classification over the gain-eligible set in ORIGINAL input order (deterministic FP64
 //      two-pass mean / population std), class increments and exact fixed-point u per
-//      record, and the exclusive prefixes over copy B that let the culled kernel add whole x-runs.
+//      record, and the exclusive prefixes over the records that let the culled kernel add whole x-runs.
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -216,14 +217,13 @@ __global__ void k_zocc_init(int2* zocc, long long n) {
     if (i < n) zocc[i] = make_int2(INT_MAX, -1);
 }
 
-// cell keys: visibility copy B key (iy, iz, ix) (copy A's (iy, ix) follows from it), collision key
-// (iz, iy, ix); per-cell counts, each Gaussian's rank in its cells (the counting-sort slot within
-// the cell, so the scatter needs no second atomic) and the occupied z-range of every row block
+// cell keys: visibility key (iy, iz, ix), collision key (iz, iy, ix); per-cell counts, each
+// Gaussian's rank in its cells (the counting-sort slot within the cell, so the scatter needs no second
+// atomic) and the occupied z-range of every row block
 __global__ void k_keys(long long n, const float* __restrict__ means, const unsigned char* __restrict__ flags,
                        GainGrid gg, ColGrid cg, int* __restrict__ gkey, int* __restrict__ ckey,
-                       int2* __restrict__ grank, int* __restrict__ crank,
-                       int* __restrict__ gcountA, int* __restrict__ gcountB, int2* __restrict__ zocc,
-                       int* __restrict__ ccount) {
+                       int* __restrict__ grank, int* __restrict__ crank, int* __restrict__ gcountB,
+                       int2* __restrict__ zocc, int* __restrict__ ccount) {
     const double igx = 1.0 / gg.hx, igy = 1.0 / gg.hy, igz = 1.0 / gg.hz, icg = 1.0 / cg.h;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -235,9 +235,7 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
             int iy = cell_coord(y, gg.oy, igy, gg.ny);
             int iz = cell_coord(z, gg.oz, igz, gg.nz);
             gk = (int)(((long long)iy * gg.nz + iz) * gg.nx + ix);
-            const int rb = atomicAdd(&gcountB[gk], 1);
-            const int ra = atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);
-            grank[i] = make_int2(ra, rb);
+            grank[i] = atomicAdd(&gcountB[gk], 1);
             int2* zo = zocc + (long long)iy * gg.nxb + ix / kZoccX;
             if (iz < zo->x) atomicMin(&zo->x, iz);
             if (iz > zo->y) atomicMax(&zo->y, iz);
@@ -267,36 +265,28 @@ __device__ __forceinline__ unsigned class_of(float w, int variant, const ClassSt
     return (unsigned)llrint(u * cs->scale) | (c << kUqBits);
 }
 
-// both visibility copies: A at cursorA (relative to 0), B at offB + cursorB, with their packed
-// class and fixed-point u (the classification statistics are computed before the scatter)
+// the visibility records, sorted by (row, z-cell, x-cell), with their packed class and fixed-point u
+// (the classification statistics are computed before the scatter)
 __global__ void k_scatter_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
-                               const int* __restrict__ gkey, const int2* __restrict__ grank, GainGrid gg,
-                               const int* __restrict__ startA, const int* __restrict__ startB, long long offB,
-                               GRec* __restrict__ grec,
-                               int* __restrict__ gidx, int variant, const ClassState* __restrict__ cs) {
+                               const int* __restrict__ gkey, const int* __restrict__ grank,
+                               const int* __restrict__ startB, GRec* __restrict__ grec, int* __restrict__ gidx,
+                               int variant, const ClassState* __restrict__ cs) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int k = gkey[i];
         if (k < 0) continue;
-        const long long nzx = (long long)gg.nz * gg.nx;
-        const long long iy = k / nzx, ix = k % gg.nx;
         const GRec r{means[i], means[n + i], means[2 * n + i], class_of(w[i], variant, cs)};
-        const int2 rk = grank[i];
-        const int sa = startA[iy * gg.nx + ix] + rk.x;
-        const int sb = startB[k] + rk.y;
-        grec[sa] = r;
-        gidx[sa] = (int)i;
-        grec[offB + sb] = r;
-        gidx[offB + sb] = (int)i;
+        const int sb = startB[k] + grank[i];
+        grec[sb] = r;
+        gidx[sb] = (int)i;
     }
 }
 
 // large maps: the visibility records in two coalesced passes instead of the scatter above (whose
-// partial 16-byte sectors cost read-modify-writes once the two copies exceed L2): (1) the permutation -- each eligible
-// Gaussian writes its index into its copy-A slot and its copy-B slot (offB + ...); (2) every slot,
-// in order, gathers its record, packed beforehand in input order with the class word (a2)
-// the scatter's record copies up to this size (measured: 2M Gaussians = 64 MB scatter in 0.59 ms vs
-// 0.67 ms gathered; 5M = 160 MB: 1.45 vs 1.23 ms for the whole map build)
+// partial 16-byte sectors cost read-modify-writes once the records exceed L2): (1) the permutation -- each
+// eligible Gaussian writes its index into its slot; (2) every slot, in order, gathers its record, packed
+// beforehand in input order with the class word (a2).  The scatter up to this many record bytes (r1,
+// with two record copies: 64 MB scattered in 0.59 ms vs 0.67 ms gathered; 160 MB: 1.45 vs 1.23 ms)
 constexpr double kScatterMaxBytes = 96.0 * 1024 * 1024;
 
 __global__ void k_pack_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
@@ -306,28 +296,21 @@ __global__ void k_pack_gain(long long n, const float* __restrict__ means, const 
         rec[i] = GRec{means[i], means[n + i], means[2 * n + i], class_of(w[i], variant, cs)};
 }
 
-__global__ void k_perm_gain(long long n, const int* __restrict__ gkey, const int2* __restrict__ grank, GainGrid gg,
-                            const int* __restrict__ startA, const int* __restrict__ startB, long long offB,
-                            int* __restrict__ gidx) {
+__global__ void k_perm_gain(long long n, const int* __restrict__ gkey, const int* __restrict__ grank,
+                            const int* __restrict__ startB, int* __restrict__ gidx) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const int k = gkey[i];
         if (k < 0) continue;
-        const long long nzx = (long long)gg.nz * gg.nx;
-        const long long iy = k / nzx, ix = k % gg.nx;
-        const int2 rk = grank[i];
-        gidx[startA[iy * gg.nx + ix] + rk.x] = (int)i;
-        gidx[offB + startB[k] + rk.y] = (int)i;
+        gidx[startB[k] + grank[i]] = (int)i;
     }
 }
 
-__global__ void k_fill_gain(long long n_gain, long long offB, const int* __restrict__ gidx,
-                            const GRec* __restrict__ rec, GRec* __restrict__ grec) {
-    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < 2 * n_gain;
-         j += (long long)gridDim.x * blockDim.x) {
-        const long long s = j < n_gain ? j : offB + (j - n_gain);
-        grec[s] = rec[gidx[s]];
-    }
+__global__ void k_fill_gain(long long n_gain, const int* __restrict__ gidx, const GRec* __restrict__ rec,
+                            GRec* __restrict__ grec) {
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n_gain;
+         j += (long long)gridDim.x * blockDim.x)
+        grec[j] = rec[gidx[j]];
 }
 
 // FP64 packing of the collision record (a1)
@@ -360,16 +343,30 @@ __global__ void k_scatter_col(long long n, const float* __restrict__ means, cons
     }
 }
 
-// NaN padding of both copies: [from, to) and [offB + from, offB + to)
-__global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to, long long offB) {
+// NaN padding of the records [from, to) (gidx: NULL for copy A)
+__global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to) {
     long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < to) {
-        float nan = __int_as_float(0x7fc00000);
-        for (int c = 0; c < 2; ++c) {
-            long long j = i + c * offB;
-            grec[j] = GRec{nan, nan, nan, 0u};
-            gidx[j] = -1;
-        }
+        const float nan = __int_as_float(0x7fc00000);
+        grec[i] = GRec{nan, nan, nan, 0u};
+        if (gidx) gidx[i] = -1;
+    }
+}
+
+// copy A from copy B: copy A is sorted by (iy, x, iz), so column (iy, x) starts at gstartA (the
+// exclusive scan of the column counts) and holds its cells (iy, iz, x) in iz order, each a contiguous
+// block of copy B at tabB[(iy, x, iz)]; one thread per column moves them
+__global__ void k_derive_cols(long long ncols, int nx, int nz, const int* __restrict__ tabB,
+                              const int* __restrict__ gstartA, const GRec* __restrict__ recB,
+                              GRec* __restrict__ recA) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= ncols) return;
+    const long long iy = col / nx, x = col - iy * nx;
+    const int* t = tabB + (iy * (nx + 1) + x) * nz;
+    int dst = gstartA[col];
+    for (int iz = 0; iz < nz; ++iz) {
+        const int src = t[iz], end = t[nz + iz];
+        for (int k = src; k < end; ++k) recA[dst++] = recB[k];
     }
 }
 
@@ -558,6 +555,19 @@ static cudaError_t class_stats(long long n, const float* w, const unsigned char*
     return cudaGetLastError();
 }
 
+// copy A (and gstartA) from copy B and its start table, in z-fastest cell order (map build and every
+// reclassification: copy A carries the class words too)
+static cudaError_t derive_copy_a(rtg_map_s* m, cudaStream_t st) {
+    if (m->n_gain <= 0) return cudaSuccess;
+    const GainGrid& gg = m->gg;
+    const long long ncols = gg.ncellsA;
+    cudaError_t e = exclusive_scan_col_counts(m->gtabB, gg.nx, gg.nz, ncols, m->gstartA, st);
+    if (e != cudaSuccess) return e;
+    note_launch(), k_derive_cols<<<nblocks(ncols, 256), 256, 0, st>>>(ncols, gg.nx, gg.nz, m->gtabB, m->gstartA,
+                                                                      m->grec + m->n_gain_pad, m->grec);
+    return cudaGetLastError();
+}
+
 // exact prefixes of copy B's (u_q, packed class count) pairs, gathered at the table entries
 // startB (map build only): the key-order start table; gtabB is then written in the same pass
 static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB = nullptr) {
@@ -576,6 +586,7 @@ static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB
         e = cudaGetLastError();
     }
     dev_free(pqhl, st);
+    if (e == cudaSuccess) e = derive_copy_a(m, st);
     return e;
 }
 
@@ -595,9 +606,10 @@ rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi
         m->cls_tl_nan == !has_lo && (!has_hi || m->cls_th == tau_hi) && (!has_lo || m->cls_tl == tau_lo))
         return RTG_OK;
     cudaError_t e = class_stats(m->n, m->w_orig, m->flags, variant, k_sigma, tau_hi, tau_lo, m->cls, m->red_scratch, st);
-    const long long nrec = 2 * m->n_gain_pad;
+    const long long nrec = m->n_gain_pad;   // copy B (copy A is re-derived by class_prefix)
     if (e == cudaSuccess && m->n_gain > 0) {
-        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->grec, m->gidx, m->w_orig, variant,
+        note_launch(), k_class_records<<<nblocks(nrec, 256), 256, 0, st>>>(nrec, m->grec + m->n_gain_pad, m->gidx,
+                                                                           m->w_orig, variant,
                                                                            m->cls);
         e = cudaGetLastError();
     }
@@ -743,11 +755,11 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     cg.h = (float)hc;
     cg.ncells = (long long)cg.nx * cg.ny * cg.nz;
     // --- allocations
-    // >= 64 NaN records after each copy: the culled kernel's sentinel run (items past its queue)
+    // >= 64 NaN records after the copy: the culled kernel's sentinel run (items past its queue)
     m->n_gain_pad = m->n_gain > 0 ? ((m->n_gain + 64 + kTile - 1) / kTile) * kTile : 0;
     m->n_col_pad = ((m->n_col + kTile - 1) / kTile) * kTile;
     MAP_CK(map_alloc(m, &m->grec, 2 * m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->gidx, 2 * m->n_gain_pad, st));
+    MAP_CK(map_alloc(m, &m->gidx, m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gstartA, gg.ncellsA + 1, st));
     MAP_CK(map_alloc(m, &m->gtabB, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
     MAP_CK(map_alloc(m, &m->zocc, (size_t)gg.ny * gg.nxb, st));
@@ -757,49 +769,50 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->csrc, m->n_col_pad, st));
     MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
     // --- counting sort into both grids
-    int *gkey = nullptr, *ckey = nullptr, *gcountA = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
+    int *gkey = nullptr, *ckey = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
     MAP_CK(dev_alloc((void**)&gkey, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&ckey, sizeof(int) * (n > 0 ? n : 1), st));
-    int2* grank = nullptr;
+    int* grank = nullptr;
     int* crank = nullptr;
-    MAP_CK(dev_alloc((void**)&grank, sizeof(int2) * (n > 0 ? n : 1), st));
+    MAP_CK(dev_alloc((void**)&grank, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&crank, sizeof(int) * (n > 0 ? n : 1), st));
-    // the three cell-count arrays in one block, cleared by one memset
-    const long long ncnt = (gg.ncellsA + 1) + (gg.ncellsB + 1) + (cg.ncells + 1);
-    MAP_CK(dev_alloc((void**)&gcountA, sizeof(int) * ncnt, st));
-    gcountB = gcountA + (gg.ncellsA + 1);
+    // both cell-count arrays in one block, cleared by one memset
+    const long long ncnt = (gg.ncellsB + 1) + (cg.ncells + 1);
+    MAP_CK(dev_alloc((void**)&gcountB, sizeof(int) * ncnt, st));
     ccount = gcountB + (gg.ncellsB + 1);
     MAP_CK(dev_alloc((void**)&gstartB, sizeof(int) * (gg.ncellsB + 1), st));
-    MAP_CK(cudaMemsetAsync(gcountA, 0, sizeof(int) * ncnt, st));
+    MAP_CK(cudaMemsetAsync(gcountB, 0, sizeof(int) * ncnt, st));
     note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc, (long long)gg.ny * gg.nxb);
     unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
     if (n > 0)
-        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, grank, crank, gcountA, gcountB,
-                                                  m->zocc, ccount);
+        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, grank, crank, gcountB, m->zocc,
+                                                  ccount);
     MAP_CK(cudaGetLastError());
-    MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));
     MAP_CK(exclusive_scan_i32(gcountB, gstartB, gg.ncellsB, st));
     MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
     if (n > 0) {
-        if (2.0 * (double)m->n_gain * sizeof(GRec) <= kScatterMaxBytes) {
-            note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, grank, gg, m->gstartA, gstartB,
-                                                              m->n_gain_pad, m->grec, m->gidx, RTG_VARIANT_XI, m->cls);
+        if ((double)m->n_gain * sizeof(GRec) <= kScatterMaxBytes) {
+            note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, grank, gstartB,
+                                                              m->grec + m->n_gain_pad, m->gidx, RTG_VARIANT_XI,
+                                                              m->cls);
         } else {
             GRec* rec = nullptr;
             MAP_CK(dev_alloc((void**)&rec, sizeof(GRec) * n, st));
             note_launch(), k_pack_gain<<<nb, 256, 0, st>>>(n, means, w, rec, RTG_VARIANT_XI, m->cls);
-            note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gg, m->gstartA, gstartB, m->n_gain_pad,
-                                                           m->gidx);
-            const unsigned fb = nblocks(2 * m->n_gain, 256) > 8192 ? 8192 : nblocks(2 * m->n_gain, 256);
-            note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, m->n_gain_pad, m->gidx, rec, m->grec);
+            note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gstartB, m->gidx);
+            const unsigned fb = nblocks(m->n_gain, 256) > 8192 ? 8192 : nblocks(m->n_gain, 256);
+            note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, m->gidx, rec, m->grec + m->n_gain_pad);
             dev_free(rec, st);
         }
         note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq, m->crec,
                                                          m->cmat, m->csrc);
     }
-    if (m->n_gain_pad > m->n_gain)
+    if (m->n_gain_pad > m->n_gain) {
         note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
-                           m->grec, m->gidx, m->n_gain, m->n_gain_pad, m->n_gain_pad);
+                           m->grec + m->n_gain_pad, m->gidx, m->n_gain, m->n_gain_pad);
+        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
+                           m->grec, nullptr, m->n_gain, m->n_gain_pad);
+    }
     if (m->n_col_pad > m->n_col)
         note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, m->n_col,
                                                                          m->n_col_pad);
@@ -808,7 +821,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     dev_free(ckey, st);
     dev_free(grank, st);
     dev_free(crank, st);
-    dev_free(gcountA, st);   // (gcountB, ccount live in the same block)
+    dev_free(gcountB, st);   // (ccount lives in the same block)
     // --- default classification (k = 1/2, derived thresholds)
     MAP_CK(class_prefix(m, st, gstartB));
     dev_free(gstartB, st);

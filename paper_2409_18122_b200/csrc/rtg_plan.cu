@@ -98,7 +98,7 @@ __global__ void k_region_scale(const int* __restrict__ wmax_bits, const int* __r
     sc[1] = ldexp(1.0, -s);
 }
 
-// pass 2: each thread walks kRegionRun consecutive records (copy A is sorted by visibility cell, so
+// pass 2: each thread walks kRegionRun consecutive records (copy B is sorted by visibility cell, so
 // neighbours mostly share a region) and issues one pair of atomics per run of equal regions
 constexpr int kRegionRun = 16;
 __global__ void k_region_acc(long long n, const int* __restrict__ rid, const int* __restrict__ gidx,
@@ -238,10 +238,11 @@ cudaError_t launch_region_utility(rtg_map_s* m, const double origin[3], double s
     e = cudaMemsetAsync(scratch, 0, qb + 64, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(count, 0, sizeof(int) * (size_t)nr, st);
     if (e != cudaSuccess) return e;
-    const long long n = m->n_gain;   // copy A: the gain-eligible Gaussians (ground plane excluded)
+    const long long n = m->n_gain;   // copy B (gidx is parallel to it): the gain-eligible Gaussians
+    const GRec* recB = m->grec + m->n_gain_pad;
     const unsigned nb = nblk(n, 256) > 2048 ? 2048 : nblk(n, 256);
     if (n > 0) {
-        note_launch(), k_region_max<<<nb, 256, 0, st>>>(n, m->grec, m->gidx, m->w_orig, g, mx, cnt, rid);
+        note_launch(), k_region_max<<<nb, 256, 0, st>>>(n, recB, m->gidx, m->w_orig, g, mx, cnt, rid);
         note_launch(), k_region_scale<<<1, 1, 0, st>>>(mx, cnt, sc);
         note_launch(), k_region_acc<<<nblk((n + kRegionRun - 1) / kRegionRun, 256), 256, 0, st>>>(
                            n, rid, m->gidx, m->w_orig, sc, qsum, count);

@@ -76,6 +76,19 @@ struct LoadArr {
     const T* __restrict__ p;
     __device__ T operator()(long long j) const { return p[j]; }
 };
+// column (iy, x) of the visibility grid -> its records over all z-cells, from the z-fastest start table
+// tab [ny][nx + 1][nz] (entry (iy, x, iz) = first record of cell (iy, iz, x); x + 1 = its end)
+struct LoadColCount {
+    const int* __restrict__ tab;
+    int nx, nz;
+    __device__ int operator()(long long col) const {
+        const long long iy = col / nx, x = col - iy * nx;
+        const int* t = tab + (iy * (nx + 1) + x) * nz;
+        int c = 0;
+        for (int iz = 0; iz < nz; ++iz) c += t[nz + iz] - t[iz];
+        return c;
+    }
+};
 // copy-B record -> (u_q, packed class count nH | nL << 32)
 struct LoadUc {
     const GRec* __restrict__ p;
@@ -319,6 +332,9 @@ cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* s
     note_launch(), k_scan<int, LoadArr<int>><<<(unsigned)nt, kScanThreads, 0, st>>>(LoadArr<int>{in}, out, n, ticket,
                                                                                    flags, agg, inc);
     return cudaGetLastError();
+}
+cudaError_t exclusive_scan_col_counts(const int* tab, int nx, int nz, long long ncols, int* out, cudaStream_t st) {
+    return scan_impl<int>(LoadColCount{tab, nx, nz}, out, ncols, st);
 }
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
     return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);
