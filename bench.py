@@ -352,6 +352,11 @@ def main():
         traffic = json.load(open(tpath)).get(f"{args.config}/{args.mode}/stride{args.stride}")
     roof = roofline(dom, phase_ms[dom], wl, int(feasible.sum()), args.stride, args.mode, clock,
                     hbm_peak, work, traffic)
+    executed_rate = None
+    if work is not None:
+        n_info = int(feasible.sum()) * (T // args.stride)
+        executed = n_info * work["tested"] + float(K) * T * work["col_tested"]
+        executed_rate = executed * world / (ms / 1000.0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:   # contract: rank 0 at N = 1 only
@@ -377,6 +382,9 @@ def main():
                 **({"best_view": {"score": res[2], "index": res[3]}} if len(res) > 2 else {}),
                 "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
                 "gpu_launches": int(round(launches_per_step)),
+                # SURVEY §8(d) metric 2, "executed": pairs actually tested one by one (visibility tests
+                # of the info waypoints + collision candidates), from the debug counters of a sample
+                **({"executed_pair_tests_per_s": executed_rate} if executed_rate is not None else {}),
                 "clocks": clock, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
         print(json.dumps(line), flush=True)
     if world > 1:
