@@ -31,6 +31,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "rtg_host.hpp"
 
@@ -106,12 +107,12 @@ __device__ __forceinline__ void add_if(bool p, unsigned& w, unsigned uc, unsigne
     }
 }
 
-template <bool kStats>
+template <bool kStats, bool kLongRuns>
 __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw,
     const float* __restrict__ Yaw, const int* __restrict__ list, const int* __restrict__ list_count,
     const double2* __restrict__ trig, const GRec* __restrict__ grec, const int* __restrict__ gstartA,
-    const int* __restrict__ gtabB, const int2* __restrict__ zocc, const TabP* __restrict__ gtabP, const GainK g,
+    const int2* __restrict__ zocc, const TabP* __restrict__ gtabP, const GainK g,
     const CamK cam, long long* __restrict__ wp_gq, int* __restrict__ wp_nh, int* __restrict__ wp_nl,
     int* __restrict__ counter, unsigned long long* __restrict__ stats) {
     // per-warp state, one struct per warp so a single base register addresses all of it
@@ -228,23 +229,34 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         // z-fastest table: entry (uy, x, iz) at (uy * (nx + 1) + x) * nz + iz
                         // all lookups independent: one memory round trip per unit
                         const int ub0 = uy * (g.nx + 1) * g.nz + iz;
-                        const int* sb = gtabB + ub0;
+                        const int4* tp = reinterpret_cast<const int4*>(gtabP) + ub0;
                         const bool in = j0 <= j1;
                         RTG_CHECK(uy >= 0 && uy < g.ny && iz >= 0 && iz < g.nz && q0 >= 0 && q1 + 1 <= g.nx &&
                                       (long long)ub0 + (long long)(q1 + 1) * g.nz < g.ntabB,
                                   "unit table index");
-                        const int a0 = __ldg(sb + q0 * g.nz), a3 = __ldg(sb + (q1 + 1) * g.nz);
-                        const int a1 = !in ? a3 : (j0 == q0 ? a0 : __ldg(sb + j0 * g.nz));
-                        const int a2 = !in ? a3 : (j1 == q1 ? a3 : __ldg(sb + (j1 + 1) * g.nz));
+                        // 128-bit entries {start, prefixes}: the x-run ends' starts come with the prefixes
+                        const int4 e0 = __ldg(tp + q0 * g.nz), e3 = __ldg(tp + (q1 + 1) * g.nz);
+                        const int a0 = e0.x, a3 = e3.x;
+                        int a1 = a3, a2 = a3;   // no inside run: [q0, q1] is tested whole
                         if (in) {
-                            // one 128-bit load per TabP entry {q (FP64 integer), nh, nl}
-                            const int4 hi = __ldg(reinterpret_cast<const int4*>(gtabP + ub0 + (j1 + 1) * g.nz));
-                            const int4 lo = __ldg(reinterpret_cast<const int4*>(gtabP + ub0 + j0 * g.nz));
-                            acc += (unsigned long long)__double2ll_rn(__hiloint2double(hi.y, hi.x) -
-                                                                      __hiloint2double(lo.y, lo.x));
-                            acch += hi.z - lo.z;
-                            accl += hi.w - lo.w;
+                            const int4 lo = j0 == q0 ? e0 : __ldg(tp + j0 * g.nz);
+                            const int4 hi = j1 == q1 ? e3 : __ldg(tp + (j1 + 1) * g.nz);
+                            // the modular differences are exact for runs of < 2^24 records: always when
+                            // the map has fewer gain-eligible Gaussians (kLongRuns = false); otherwise a
+                            // longer inside run is tested record by record instead
+                            if (!kLongRuns || hi.x - lo.x < (1 << 24)) {
+                            a1 = lo.x;
+                            a2 = hi.x;
+                            // differences of the packed prefixes, modulo 2^48 / 2^24 (exact: one x-run)
+                            const unsigned long long qh = ((unsigned long long)((unsigned)hi.z & 0xffffu) << 32) | (unsigned)hi.y;
+                            const unsigned long long ql = ((unsigned long long)((unsigned)lo.z & 0xffffu) << 32) | (unsigned)lo.y;
+                            acc += (qh - ql) & 0xffffffffffffull;
+                            const unsigned nhh = ((unsigned)hi.z >> 16) | (((unsigned)hi.w & 0xffu) << 16);
+                            const unsigned nhl = ((unsigned)lo.z >> 16) | (((unsigned)lo.w & 0xffu) << 16);
+                            acch += (int)((nhh - nhl) & 0xffffffu);
+                            accl += (int)((((unsigned)hi.w >> 8) - ((unsigned)lo.w >> 8)) & 0xffffffu);
                             if (kStats) nagg += 1;
+                            }
                         }
                         s0 = g.offB + a0;
                         l0 = a1 - a0;
@@ -534,7 +546,7 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     }
     if (!g_sms_g) {
         cudaDeviceGetAttribute(&g_sms_g, cudaDevAttrMultiProcessorCount, m->device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false>, kWarpsG * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_g, k_gain_culled<false, false>, kWarpsG * 32, 0);
         if (g_occ_g < 1) g_occ_g = 1;
     }
     const GainGrid& gg = m->gg;
@@ -565,14 +577,22 @@ cudaError_t launch_gain_culled(rtg_map_s* m, rtg_traj_s* tr, const CamK& cam, co
     long long cap = (long long)g_sms_g * g_occ_g;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    if (stats)
-        note_launch(), k_gain_culled<true><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, trig, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
-            cam, wp_gq, wp_nh, wp_nl, counter, stats);
-    else
-        note_launch(), k_gain_culled<false><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(
-            tr->x, tr->y, tr->z, tr->yaw, list, count, trig, m->grec, m->gstartA, m->gtabB, m->zocc, m->gtabP, g,
-            cam, wp_gq, wp_nh, wp_nl, counter, stats);
+    // packed table prefixes are exact for x-runs of < 2^24 records, guaranteed below 2^24 records in all
+    // (RTG_LONG_RUNS=1 forces the guarded variant: the parity tests run it on small maps)
+    static const bool force_long = getenv("RTG_LONG_RUNS") && getenv("RTG_LONG_RUNS")[0] == '1';
+    const bool long_runs = force_long || m->n_gain >= (1LL << 24);
+#define RTG_GAIN_LAUNCH(S, LR)                                                                                  \
+    note_launch(), k_gain_culled<S, LR><<<(unsigned)blocks, kWarpsG * 32, 0, st>>>(                             \
+                       tr->x, tr->y, tr->z, tr->yaw, list, count, trig, m->grec, m->gstartA, m->zocc,          \
+                       m->gtabP, g, cam, wp_gq, wp_nh, wp_nl, counter, stats)
+    if (stats) {
+        if (long_runs) RTG_GAIN_LAUNCH(true, true);
+        else RTG_GAIN_LAUNCH(true, false);
+    } else {
+        if (long_runs) RTG_GAIN_LAUNCH(false, true);
+        else RTG_GAIN_LAUNCH(false, false);
+    }
+#undef RTG_GAIN_LAUNCH
     cudaError_t e2 = cudaGetLastError();
     dev_free(trig, st);
     return e2;

@@ -58,8 +58,13 @@ cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* s
 // copy-B records' (u_q, nH | nL << 32) pairs (from GRec::uc) scanned into out[0 .. 2n+1]
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st);
 // exclusive scan over the ncols = ny * nx columns (row-major) of their record counts (all z-cells), read
-// from the z-fastest start table tab [ny][nx + 1][nz]; out[ncols] = total
-cudaError_t exclusive_scan_col_counts(const int* tab, int nx, int nz, long long ncols, int* out, cudaStream_t st);
+// from the z-fastest table [ny][nx + 1][nz] of `stride`-int entries led by the cell's first record;
+// out[ncols] = total
+cudaError_t exclusive_scan_col_counts(const int* tab, int stride, int nx, int nz, long long ncols, int* out,
+                                      cudaStream_t st);
+// the same from the key-order cell counts countB [ny][nz][nx]
+cudaError_t exclusive_scan_col_counts_b(const int* countB, int nx, int nz, long long ncols, int* out,
+                                        cudaStream_t st);
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
@@ -99,11 +104,11 @@ struct rtg_map_s {
     rtg::GRec* grec = nullptr;           // [2 * n_gain_pad]
     int* gidx = nullptr;                 // [n_gain_pad] original index per copy-B record
     int* gstartA = nullptr;              // [ncellsA + 1] first copy-A record of column (iy, ix)
-    int* gtabB = nullptr;                // [ny][nx + 1][nz] first copy-B record (relative to n_gain_pad) of
-                                         // cell (iy, iz, ix); ix = nx: end of the z-slab (iy, iz)
     int2* zocc = nullptr;                // [ny][nxb] occupied z-cell range {lo, hi} of each row block of
                                          // kZoccX x-cells (lo > hi: empty)
-    rtg::TabP* gtabP = nullptr;          // [ny][nx + 1][nz] exact exclusive prefixes at the gtabB entries
+    rtg::TabP* gtabP = nullptr;          // [ny][nx + 1][nz], z-fastest: entry (iy, ix, iz) = the first copy-B
+                                         // record (relative to n_gain_pad) of cell (iy, iz, ix) (ix = nx: end
+                                         // of the z-slab) and the exclusive prefixes there (packed, TabP)
     rtg::GainGrid gg{};
     // collision records (sorted by collision cell), padded likewise
     long long n_col_pad = 0;

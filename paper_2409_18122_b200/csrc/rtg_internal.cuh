@@ -40,9 +40,10 @@ __device__ __forceinline__ int uc_inc(unsigned uc) {
 struct __align__(16) CRec { float x, y, z, rb2; };
 // M rows (FP32): m[0..8] row-major, m[9] = original index (as int bits), pad
 struct __align__(16) CMat { float m[12]; };
-// exact exclusive prefixes at a copy-B cell boundary (z-fastest table entry): sum of u_q (an
-// integer < 2^53, exact in FP64) and the class counts nH, nL
-struct __align__(16) TabP { double q; int nh, nl; };
+// z-fastest table entry at a copy-B cell boundary: the cell's first record and the exact exclusive
+// prefixes there, packed modulo 2^48 (sum of u_q) and 2^24 (class counts nH, nL):
+// {start, q[31:0], q[47:32] | nH[15:0] << 16, nH[23:16] | nL << 8}
+struct __align__(16) TabP { int start; unsigned qlo, qhi_nh, nh_nl; };
 // the fp32 inputs M is packed from (sorted like the collision records): the rare FP64
 // re-decision recomputes M from them with the same code as the packing (pack_m64)
 struct __align__(32) CSrc { float q[4]; float s[3]; float pad; };

@@ -356,16 +356,31 @@ __global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to) 
 // copy A from copy B: copy A is sorted by (iy, x, iz), so column (iy, x) starts at gstartA (the
 // exclusive scan of the column counts) and holds its cells (iy, iz, x) in iz order, each a contiguous
 // block of copy B at tabB[(iy, x, iz)]; one thread per column moves them
+// map build: the cells' copy-B starts and counts in key order [ny][nz][nx] (coalesced over x)
+__global__ void k_derive_cols_b(long long ncols, int nx, int nz, const int* __restrict__ startB,
+                                const int* __restrict__ countB, const int* __restrict__ gstartA,
+                                const GRec* __restrict__ recB, GRec* __restrict__ recA) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= ncols) return;
+    const long long iy = col / nx, x = col - iy * nx;
+    const long long k0 = iy * nz * (long long)nx + x;
+    int dst = gstartA[col];
+    for (int iz = 0; iz < nz; ++iz) {
+        const int src = startB[k0 + (long long)iz * nx], c = countB[k0 + (long long)iz * nx];
+        for (int k = 0; k < c; ++k) recA[dst++] = recB[src + k];
+    }
+}
+
 __global__ void k_derive_cols(long long ncols, int nx, int nz, const int* __restrict__ tabB,
                               const int* __restrict__ gstartA, const GRec* __restrict__ recB,
                               GRec* __restrict__ recA) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= ncols) return;
     const long long iy = col / nx, x = col - iy * nx;
-    const int* t = tabB + (iy * (nx + 1) + x) * nz;
+    const int* t = tabB + (iy * (nx + 1) + x) * nz * 4;   // 4-int TabP entries, start first
     int dst = gstartA[col];
     for (int iz = 0; iz < nz; ++iz) {
-        const int src = t[iz], end = t[nz + iz];
+        const int src = t[iz * 4], end = t[(nz + iz) * 4];
         for (int k = src; k < end; ++k) recA[dst++] = recB[k];
     }
 }
@@ -511,28 +526,39 @@ __global__ void k_class_records(long long n_rec, GRec* __restrict__ grec, const 
 }
 
 
+// one z-fastest table entry: the cell's first copy-B record and the exclusive prefixes there, modulo
+// 2^48 (sum of u_q) and 2^24 (n_H, n_L) -- the culled kernel only takes differences of two entries of
+// one (row, z-slab), exact while such an x-run holds fewer than 2^24 records (u_q < 2^24)
+__device__ __forceinline__ TabP pack_tab(int start, const longlong2 v) {
+    const unsigned long long q = (unsigned long long)v.x;
+    const unsigned nh = (unsigned)(v.y & 0xffffff), nl = (unsigned)((v.y >> 32) & 0xffffff);
+    TabP t;
+    t.start = start;
+    t.qlo = (unsigned)q;
+    t.qhi_nh = (unsigned)((q >> 32) & 0xffff) | (nh << 16);
+    t.nh_nl = (nh >> 16) | (nl << 8);
+    return t;
+}
+
 // both z-fastest tables in one pass at map build: the copy-B start of the cell (key order scan)
 // and the exact prefixes there
 __global__ void k_build_tabs(GainGrid gg, const int* __restrict__ startB, const longlong2* __restrict__ pqhl,
-                             int* __restrict__ tabB, TabP* __restrict__ tabP) {
+                             TabP* __restrict__ tabP) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long nx1 = gg.nx + 1;
     if (e >= (long long)gg.ny * nx1 * gg.nz) return;
     const long long iz = e % gg.nz, r = e / gg.nz;
     const long long ix = r % nx1, iy = r / nx1;
     const int s = startB[(iy * gg.nz + iz) * gg.nx + ix];
-    tabB[e] = s;
-    const longlong2 v = pqhl[s];
-    tabP[e] = TabP{(double)v.x, (int)(v.y & 0xffffffffLL), (int)(v.y >> 32)};
+    tabP[e] = pack_tab(s, pqhl[s]);
 }
 
-// prefixes at every copy-B table entry (same z-fastest layout as gtabB): one lookup per x-run end
-__global__ void k_pack_tabP(long long nt, const int* __restrict__ tabB, const longlong2* __restrict__ pqhl,
-                            TabP* __restrict__ tabP) {
+// reclassification: new prefixes at every z-fastest table entry (its start unchanged)
+__global__ void k_pack_tabP(long long nt, const longlong2* __restrict__ pqhl, TabP* __restrict__ tabP) {
     long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= nt) return;
-    const longlong2 v = pqhl[tabB[e]];
-    tabP[e] = TabP{(double)v.x, (int)(v.y & 0xffffffffLL), (int)(v.y >> 32)};
+    const int t = tabP[e].start;   // the starts stay; the prefixes follow the new classes
+    tabP[e] = pack_tab(t, pqhl[t]);
 }
 
 inline unsigned nblocks(long long n, int t) {
@@ -557,20 +583,32 @@ static cudaError_t class_stats(long long n, const float* w, const unsigned char*
 
 // copy A (and gstartA) from copy B and its start table, in z-fastest cell order (map build and every
 // reclassification: copy A carries the class words too)
-static cudaError_t derive_copy_a(rtg_map_s* m, cudaStream_t st) {
+static cudaError_t derive_copy_a(rtg_map_s* m, cudaStream_t st, const int* startB = nullptr,
+                                 const int* countB = nullptr) {
     if (m->n_gain <= 0) return cudaSuccess;
     const GainGrid& gg = m->gg;
     const long long ncols = gg.ncellsA;
-    cudaError_t e = exclusive_scan_col_counts(m->gtabB, gg.nx, gg.nz, ncols, m->gstartA, st);
-    if (e != cudaSuccess) return e;
-    note_launch(), k_derive_cols<<<nblocks(ncols, 256), 256, 0, st>>>(ncols, gg.nx, gg.nz, m->gtabB, m->gstartA,
-                                                                      m->grec + m->n_gain_pad, m->grec);
+    const GRec* recB = m->grec + m->n_gain_pad;
+    cudaError_t e;
+    if (startB && countB) {   // map build: the key-order cell starts and counts are at hand
+        e = exclusive_scan_col_counts_b(countB, gg.nx, gg.nz, ncols, m->gstartA, st);
+        if (e != cudaSuccess) return e;
+        note_launch(), k_derive_cols_b<<<nblocks(ncols, 256), 256, 0, st>>>(ncols, gg.nx, gg.nz, startB, countB,
+                                                                            m->gstartA, recB, m->grec);
+    } else {                  // reclassification: the starts from the table entries
+        const int* tab = reinterpret_cast<const int*>(m->gtabP);   // TabP::start leads each 4-int entry
+        e = exclusive_scan_col_counts(tab, 4, gg.nx, gg.nz, ncols, m->gstartA, st);
+        if (e != cudaSuccess) return e;
+        note_launch(), k_derive_cols<<<nblocks(ncols, 256), 256, 0, st>>>(ncols, gg.nx, gg.nz, tab, m->gstartA,
+                                                                          recB, m->grec);
+    }
     return cudaGetLastError();
 }
 
 // exact prefixes of copy B's (u_q, packed class count) pairs, gathered at the table entries
-// startB (map build only): the key-order start table; gtabB is then written in the same pass
-static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB = nullptr) {
+// startB (map build only): the key-order start table; the entries' starts are written in the same pass
+static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB = nullptr,
+                                const int* countB = nullptr) {
     const long long ng = m->n_gain;
     long long* pqhl = nullptr;
     cudaError_t e = dev_alloc((void**)&pqhl, 2 * sizeof(long long) * (ng + 1), st);
@@ -579,14 +617,14 @@ static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB
     if (e == cudaSuccess) {
         const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
         if (startB)
-            note_launch(), k_build_tabs<<<nblocks(nt, 256), 256, 0, st>>>(m->gg, startB, (const longlong2*)pqhl, m->gtabB,
+            note_launch(), k_build_tabs<<<nblocks(nt, 256), 256, 0, st>>>(m->gg, startB, (const longlong2*)pqhl,
                                                                           m->gtabP);
         else
-            note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, m->gtabB, (const longlong2*)pqhl, m->gtabP);
+            note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, (const longlong2*)pqhl, m->gtabP);
         e = cudaGetLastError();
     }
     dev_free(pqhl, st);
-    if (e == cudaSuccess) e = derive_copy_a(m, st);
+    if (e == cudaSuccess) e = derive_copy_a(m, st, startB, countB);
     return e;
 }
 
@@ -761,7 +799,6 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->grec, 2 * m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gidx, m->n_gain_pad, st));
     MAP_CK(map_alloc(m, &m->gstartA, gg.ncellsA + 1, st));
-    MAP_CK(map_alloc(m, &m->gtabB, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
     MAP_CK(map_alloc(m, &m->zocc, (size_t)gg.ny * gg.nxb, st));
     MAP_CK(map_alloc(m, &m->gtabP, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
     MAP_CK(map_alloc(m, &m->crec, m->n_col_pad, st));
@@ -821,10 +858,10 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     dev_free(ckey, st);
     dev_free(grank, st);
     dev_free(crank, st);
-    dev_free(gcountB, st);   // (ccount lives in the same block)
-    // --- default classification (k = 1/2, derived thresholds)
-    MAP_CK(class_prefix(m, st, gstartB));
+    // --- default classification (k = 1/2, derived thresholds); copy A derived from copy B
+    MAP_CK(class_prefix(m, st, gstartB, gcountB));
     dev_free(gstartB, st);
+    dev_free(gcountB, st);   // (ccount lives in the same block)
     set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
     return RTG_OK;
 }

@@ -76,16 +76,17 @@ struct LoadArr {
     const T* __restrict__ p;
     __device__ T operator()(long long j) const { return p[j]; }
 };
-// column (iy, x) of the visibility grid -> its records over all z-cells, from the z-fastest start table
-// tab [ny][nx + 1][nz] (entry (iy, x, iz) = first record of cell (iy, iz, x); x + 1 = its end)
+// column (iy, x) of the visibility grid -> its records over all z-cells, from the z-fastest table
+// [ny][nx + 1][nz] whose entries start with the first record of cell (iy, iz, x) (x + 1: its end);
+// `stride` ints per entry
 struct LoadColCount {
     const int* __restrict__ tab;
-    int nx, nz;
+    int nx, nz, stride;
     __device__ int operator()(long long col) const {
         const long long iy = col / nx, x = col - iy * nx;
-        const int* t = tab + (iy * (nx + 1) + x) * nz;
+        const int* t = tab + (iy * (nx + 1) + x) * nz * stride;
         int c = 0;
-        for (int iz = 0; iz < nz; ++iz) c += t[nz + iz] - t[iz];
+        for (int iz = 0; iz < nz; ++iz) c += t[(nz + iz) * stride] - t[iz * stride];
         return c;
     }
 };
@@ -333,8 +334,25 @@ cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* s
                                                                                    flags, agg, inc);
     return cudaGetLastError();
 }
-cudaError_t exclusive_scan_col_counts(const int* tab, int nx, int nz, long long ncols, int* out, cudaStream_t st) {
-    return scan_impl<int>(LoadColCount{tab, nx, nz}, out, ncols, st);
+cudaError_t exclusive_scan_col_counts(const int* tab, int stride, int nx, int nz, long long ncols, int* out,
+                                      cudaStream_t st) {
+    return scan_impl<int>(LoadColCount{tab, nx, nz, stride}, out, ncols, st);
+}
+// same from the key-order cell counts countB [ny][nz][nx] (map build: coalesced over x)
+struct LoadColCountB {
+    const int* __restrict__ cnt;
+    int nx, nz;
+    __device__ int operator()(long long col) const {
+        const long long iy = col / nx, x = col - iy * nx;
+        const int* t = cnt + iy * nz * (long long)nx + x;
+        int c = 0;
+        for (int iz = 0; iz < nz; ++iz) c += t[(long long)iz * nx];
+        return c;
+    }
+};
+cudaError_t exclusive_scan_col_counts_b(const int* countB, int nx, int nz, long long ncols, int* out,
+                                        cudaStream_t st) {
+    return scan_impl<int>(LoadColCountB{countB, nx, nz}, out, ncols, st);
 }
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
     return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);

@@ -728,3 +728,39 @@ def test_sparse_diagonal_waypoints_collision(R):
     assert np.array_equal(b["wp_col"].reshape(K, T)[idx].reshape(-1).astype(bool), wp["col"])
     g = gpu_run(R, wl, "culled", flags=0, x=x, y=y, z=z, yaw=yaw, debug=False)
     assert np.array_equal(g["first_col"], b["first_col"])
+
+
+def test_culled_long_run_guard_variant(R):
+    """The packed z-fastest table holds prefixes modulo 2^48 / 2^24, exact for x-runs of
+    fewer than 2^24 records -- guaranteed when the map has fewer gain-eligible Gaussians.  Larger maps run
+    a guarded kernel variant that tests longer runs record by record; RTG_LONG_RUNS=1 forces it here, in a
+    subprocess, and it must equal the default kernel bit for bit (and the dense kernel)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2409_18122_b200 import rtg as R, workloads as W
+wl = W.room()
+idx = np.arange(0, wl.K, 8)
+out = []
+for mode in (R.MODE_CULLED, R.MODE_DENSE):
+    m = R.map_from_workload(wl)
+    tr = R.traj_from_workload(wl, x=wl.x[idx], y=wl.y[idx], z=wl.z[idx], yaw=wl.yaw[idx])
+    d = R.score_debug(m, tr, wl.camera, R.make_params(mode=mode, flags=R.SCORE_FULL_GAIN))
+    out.append(np.concatenate([d["wp_gain"].cpu().numpy().view(np.int64), d["wp_nh"].cpu().numpy(), d["wp_nl"].cpu().numpy()]))
+    m.close(); tr.close()
+assert np.array_equal(out[0], out[1])
+np.save(sys.argv[1], out[0])
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    res = {}
+    for flag in ("0", "1"):
+        f = tempfile.mktemp(suffix=".npy")
+        env = dict(os.environ, RTG_LONG_RUNS=flag)
+        p = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[flag] = np.load(f)
+        os.unlink(f)
+    assert np.array_equal(res["0"], res["1"])
