@@ -62,9 +62,6 @@ cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n,
 // out[ncols] = total
 cudaError_t exclusive_scan_col_counts(const int* tab, int stride, int nx, int nz, long long ncols, int* out,
                                       cudaStream_t st);
-// the same from the key-order cell counts countB [ny][nz][nx]
-cudaError_t exclusive_scan_col_counts_b(const int* countB, int nx, int nz, long long ncols, int* out,
-                                        cudaStream_t st);
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);

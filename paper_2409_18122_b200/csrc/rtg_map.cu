@@ -223,7 +223,7 @@ __global__ void k_zocc_init(int2* zocc, long long n) {
 __global__ void k_keys(long long n, const float* __restrict__ means, const unsigned char* __restrict__ flags,
                        GainGrid gg, ColGrid cg, int* __restrict__ gkey, int* __restrict__ ckey,
                        int* __restrict__ grank, int* __restrict__ crank, int* __restrict__ gcountB,
-                       int2* __restrict__ zocc, int* __restrict__ ccount) {
+                       int* __restrict__ gcountA, int2* __restrict__ zocc, int* __restrict__ ccount) {
     const double igx = 1.0 / gg.hx, igy = 1.0 / gg.hy, igz = 1.0 / gg.hz, icg = 1.0 / cg.h;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -236,6 +236,7 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
             int iz = cell_coord(z, gg.oz, igz, gg.nz);
             gk = (int)(((long long)iy * gg.nz + iz) * gg.nx + ix);
             grank[i] = atomicAdd(&gcountB[gk], 1);
+            atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);   // column totals (copy A), no rank needed
             int2* zo = zocc + (long long)iy * gg.nxb + ix / kZoccX;
             if (iz < zo->x) atomicMin(&zo->x, iz);
             if (iz > zo->y) atomicMax(&zo->y, iz);
@@ -589,10 +590,8 @@ static cudaError_t derive_copy_a(rtg_map_s* m, cudaStream_t st, const int* start
     const GainGrid& gg = m->gg;
     const long long ncols = gg.ncellsA;
     const GRec* recB = m->grec + m->n_gain_pad;
-    cudaError_t e;
-    if (startB && countB) {   // map build: the key-order cell starts and counts are at hand
-        e = exclusive_scan_col_counts_b(countB, gg.nx, gg.nz, ncols, m->gstartA, st);
-        if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (startB && countB) {   // map build: gstartA is scanned from the column counts; cell starts at hand
         note_launch(), k_derive_cols_b<<<nblocks(ncols, 256), 256, 0, st>>>(ncols, gg.nx, gg.nz, startB, countB,
                                                                             m->gstartA, recB, m->grec);
     } else {                  // reclassification: the starts from the table entries
@@ -813,20 +812,22 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     int* crank = nullptr;
     MAP_CK(dev_alloc((void**)&grank, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&crank, sizeof(int) * (n > 0 ? n : 1), st));
-    // both cell-count arrays in one block, cleared by one memset
-    const long long ncnt = (gg.ncellsB + 1) + (cg.ncells + 1);
+    // the cell-count arrays in one block, cleared by one memset
+    const long long ncnt = (gg.ncellsB + 1) + (cg.ncells + 1) + (gg.ncellsA + 1);
     MAP_CK(dev_alloc((void**)&gcountB, sizeof(int) * ncnt, st));
     ccount = gcountB + (gg.ncellsB + 1);
+    int* gcountA = ccount + (cg.ncells + 1);
     MAP_CK(dev_alloc((void**)&gstartB, sizeof(int) * (gg.ncellsB + 1), st));
     MAP_CK(cudaMemsetAsync(gcountB, 0, sizeof(int) * ncnt, st));
     note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc, (long long)gg.ny * gg.nxb);
     unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
     if (n > 0)
-        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, grank, crank, gcountB, m->zocc,
-                                                  ccount);
+        note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, grank, crank, gcountB, gcountA,
+                                                  m->zocc, ccount);
     MAP_CK(cudaGetLastError());
     MAP_CK(exclusive_scan_i32(gcountB, gstartB, gg.ncellsB, st));
     MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
+    MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));   // copy A's column starts
     if (n > 0) {
         if ((double)m->n_gain * sizeof(GRec) <= kScatterMaxBytes) {
             note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, grank, gstartB,
@@ -861,7 +862,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     // --- default classification (k = 1/2, derived thresholds); copy A derived from copy B
     MAP_CK(class_prefix(m, st, gstartB, gcountB));
     dev_free(gstartB, st);
-    dev_free(gcountB, st);   // (ccount lives in the same block)
+    dev_free(gcountB, st);   // (ccount, gcountA live in the same block)
     set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
     return RTG_OK;
 }

@@ -338,22 +338,6 @@ cudaError_t exclusive_scan_col_counts(const int* tab, int stride, int nx, int nz
                                       cudaStream_t st) {
     return scan_impl<int>(LoadColCount{tab, nx, nz, stride}, out, ncols, st);
 }
-// same from the key-order cell counts countB [ny][nz][nx] (map build: coalesced over x)
-struct LoadColCountB {
-    const int* __restrict__ cnt;
-    int nx, nz;
-    __device__ int operator()(long long col) const {
-        const long long iy = col / nx, x = col - iy * nx;
-        const int* t = cnt + iy * nz * (long long)nx + x;
-        int c = 0;
-        for (int iz = 0; iz < nz; ++iz) c += t[(long long)iz * nx];
-        return c;
-    }
-};
-cudaError_t exclusive_scan_col_counts_b(const int* countB, int nx, int nz, long long ncols, int* out,
-                                        cudaStream_t st) {
-    return scan_impl<int>(LoadColCountB{countB, nx, nz}, out, ncols, st);
-}
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
     return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);
 }
