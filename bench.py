@@ -249,11 +249,14 @@ def main():
         map_opts = (hy, hz, 0.0, hx)
 
     aux = torch.cuda.Stream(device=dev)
+    vstream = torch.cuda.Stream(device=dev)
 
     def step(host: bool):
         src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
         m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
                   device=local_dev, options=map_opts)
+        if Kv:
+            vstream.wait_stream(stream)   # the views need the map build only
         if host:
             # rtg_map_create returns once the map is on the device and its build is enqueued: the
             # waypoint upload then overlaps the build on a second stream
@@ -262,13 +265,18 @@ def main():
         else:
             tr = R.Traj.wrap(*src_traj, device=local_dev)   # resident waypoints: borrowed, no copy
         R.score(m, tr, cam, params, *outs)
+        tv = None
+        if Kv:   # the scale config's gain-only views (T = 1, no collision), scored concurrently on a
+            # third stream: their one-waypoint-per-warp launch would otherwise be a serial tail
+            tv = (R.Traj.upload(*hviews, device=local_dev, stream=vstream) if host
+                  else R.Traj.wrap(*dviews, device=local_dev))
+            R.score(m, tv, cam, vparams, *vouts, stream=vstream)
         s, i = R.best(outs[3])
         res = global_best(s, i)
-        if Kv:   # the scale config's gain-only views (T = 1, no collision): best view by xi
-            tv = R.Traj.upload(*hviews, device=local_dev) if host else R.Traj.wrap(*dviews, device=local_dev)
-            R.score(m, tv, cam, vparams, *vouts)
-            vs, vi = R.best(vouts[3])
+        if Kv:   # best view by xi
+            vs, vi = R.best(vouts[3], stream=vstream)
             res = res + global_best(vs, vi)
+            stream.wait_stream(vstream)
             tv.close()
         m.close()
         if host:

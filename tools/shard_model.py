@@ -39,6 +39,7 @@ def main():
     vparams = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
     flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
+    vstream = torch.cuda.Stream(device=dev)
     opts = None
     if args.cells:
         hy, hx, hz = (float(v) for v in args.cells.split(","))
@@ -58,13 +59,17 @@ def main():
         def step():
             m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
                       options=opts)
+            if views is not None:
+                vstream.wait_stream(st)   # views: the map build only, then concurrent (as bench.py)
             tr = R.Traj.wrap(*traj)
             R.score(m, tr, cam, params, *outs)
-            r = R.best(outs[3])
             if views is not None:
                 tv = R.Traj.wrap(*views)
-                fc, fe, g, u = R.score(m, tv, cam, vparams)
-                R.best(u)
+                fc, fe, g, u = R.score(m, tv, cam, vparams, stream=vstream)
+            r = R.best(outs[3])
+            if views is not None:
+                R.best(u, stream=vstream)
+                st.wait_stream(vstream)
                 tv.close()
             tr.close()
             m.close()
