@@ -361,9 +361,9 @@ __global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to) 
 __global__ void k_derive_cols_b(long long ncols, int nx, int nz, const int* __restrict__ startB,
                                 const int* __restrict__ countB, const int* __restrict__ gstartA,
                                 const GRec* __restrict__ recB, GRec* __restrict__ recA) {
-    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (col >= ncols) return;
-    const long long iy = col / nx, x = col - iy * nx;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;   // grid: x = columns of one row, y = rows
+    if (x >= nx) return;
+    const long long iy = blockIdx.y, col = iy * nx + x;
     const long long k0 = iy * nz * (long long)nx + x;
     int dst = gstartA[col];
     for (int iz = 0; iz < nz; ++iz) {
@@ -543,15 +543,16 @@ __device__ __forceinline__ TabP pack_tab(int start, const longlong2 v) {
 
 // both z-fastest tables in one pass at map build: the copy-B start of the cell (key order scan)
 // and the exact prefixes there
+// (grid: x = entries of one row, y = rows, so the index arithmetic is 32-bit within a row)
 __global__ void k_build_tabs(GainGrid gg, const int* __restrict__ startB, const longlong2* __restrict__ pqhl,
                              TabP* __restrict__ tabP) {
-    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long nx1 = gg.nx + 1;
-    if (e >= (long long)gg.ny * nx1 * gg.nz) return;
-    const long long iz = e % gg.nz, r = e / gg.nz;
-    const long long ix = r % nx1, iy = r / nx1;
+    const int er = blockIdx.x * blockDim.x + threadIdx.x;   // entry within the row: (ix, iz), iz fastest
+    const int nrow = (gg.nx + 1) * gg.nz;
+    if (er >= nrow) return;
+    const long long iy = blockIdx.y;
+    const int ix = er / gg.nz, iz = er - ix * gg.nz;
     const int s = startB[(iy * gg.nz + iz) * gg.nx + ix];
-    tabP[e] = pack_tab(s, pqhl[s]);
+    tabP[iy * nrow + er] = pack_tab(s, pqhl[s]);
 }
 
 // reclassification: new prefixes at every z-fastest table entry (its start unchanged)
@@ -592,8 +593,8 @@ static cudaError_t derive_copy_a(rtg_map_s* m, cudaStream_t st, const int* start
     const GRec* recB = m->grec + m->n_gain_pad;
     cudaError_t e = cudaSuccess;
     if (startB && countB) {   // map build: gstartA is scanned from the column counts; cell starts at hand
-        note_launch(), k_derive_cols_b<<<nblocks(ncols, 256), 256, 0, st>>>(ncols, gg.nx, gg.nz, startB, countB,
-                                                                            m->gstartA, recB, m->grec);
+        note_launch(), k_derive_cols_b<<<dim3((unsigned)((gg.nx + 255) / 256), (unsigned)gg.ny), 256, 0, st>>>(
+                           ncols, gg.nx, gg.nz, startB, countB, m->gstartA, recB, m->grec);
     } else {                  // reclassification: the starts from the table entries
         const int* tab = reinterpret_cast<const int*>(m->gtabP);   // TabP::start leads each 4-int entry
         e = exclusive_scan_col_counts(tab, 4, gg.nx, gg.nz, ncols, m->gstartA, st);
@@ -616,8 +617,8 @@ static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB
     if (e == cudaSuccess) {
         const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
         if (startB)
-            note_launch(), k_build_tabs<<<nblocks(nt, 256), 256, 0, st>>>(m->gg, startB, (const longlong2*)pqhl,
-                                                                          m->gtabP);
+            note_launch(), k_build_tabs<<<dim3((unsigned)(((m->gg.nx + 1) * m->gg.nz + 255) / 256), (unsigned)m->gg.ny),
+                                          256, 0, st>>>(m->gg, startB, (const longlong2*)pqhl, m->gtabP);
         else
             note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, (const longlong2*)pqhl, m->gtabP);
         e = cudaGetLastError();
