@@ -251,6 +251,8 @@ def main():
     aux = torch.cuda.Stream(device=dev)
     vstream = torch.cuda.Stream(device=dev)
 
+    prof_state = {"on": False}
+
     def step(host: bool):
         src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
         m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
@@ -267,14 +269,23 @@ def main():
         R.score(m, tr, cam, params, *outs)
         tv = None
         if Kv:   # the scale config's gain-only views (T = 1, no collision), scored concurrently on a
-            # third stream: their one-waypoint-per-warp launch would otherwise be a serial tail
+            # third stream: their one-waypoint-per-warp launch would otherwise be a serial tail.  The
+            # per-phase events skip them (their phases would count the wait for free SMs).
+            if prof_state["on"]:
+                R.profile_enable(False)
             tv = (R.Traj.upload(*hviews, device=local_dev, stream=vstream) if host
                   else R.Traj.wrap(*dviews, device=local_dev))
             R.score(m, tv, cam, vparams, *vouts, stream=vstream)
+            if prof_state["on"]:
+                R.profile_enable(True)
         s, i = R.best(outs[3])
         res = global_best(s, i)
         if Kv:   # best view by xi
+            if prof_state["on"]:
+                R.profile_enable(False)
             vs, vi = R.best(vouts[3], stream=vstream)
+            if prof_state["on"]:
+                R.profile_enable(True)
             res = res + global_best(vs, vi)
             stream.wait_stream(vstream)
             tv.close()
@@ -291,6 +302,7 @@ def main():
         if profile:                      # per-phase CUDA events over the timed steps only
             R.profile_read(reset=True)
             R.profile_enable(True)
+            prof_state["on"] = True
         total_ms = 0.0
         per_step = []
         res = None
@@ -309,6 +321,7 @@ def main():
             per_step.append(a.elapsed_time(b))
         if profile:
             R.profile_enable(False)
+            prof_state["on"] = False
         t = torch.tensor([total_ms] + per_step, dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)   # total and every step: max over ranks
@@ -385,7 +398,9 @@ def main():
                            "N": N, "K": K_glob, "K_per_gpu": K, "views": Kv_glob, "T": T, "mode": args.mode,
                            "info_stride": args.stride,
                            "parallelism": f"traj-shard x{world}, map replicated",
-                           "l2": "flushed (512 MiB write) between timed steps"},
+                           "l2": "flushed (512 MiB write) between timed steps",
+                           **({"views_stream": "views scored concurrently on a second stream; phase_ms covers "
+                                               "the trajectories' calls only"} if Kv_glob else {})},
                 "best": {"score": res[0], "index": res[1]},
                 **({"best_view": {"score": res[2], "index": res[3]}} if len(res) > 2 else {}),
                 "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
