@@ -555,6 +555,27 @@ __global__ void k_build_tabs(GainGrid gg, const int* __restrict__ startB, const 
     tabP[iy * nrow + er] = pack_tab(s, pqhl[s]);
 }
 
+// the same through shared memory: a CTA takes tx columns of one row over all z-cells, reads the
+// key-order starts and gathers the prefixes x-fastest (neighbouring cells share or neighbour their
+// starts: coalesced), and stores the entries z-fastest (one contiguous range)
+constexpr int kTabEntries = 1536;   // entries per CTA (24 KB of shared memory)
+__global__ void __launch_bounds__(256) k_build_tabs_tile(GainGrid gg, int tx, const int* __restrict__ startB,
+                                                         const longlong2* __restrict__ pqhl,
+                                                         TabP* __restrict__ tabP) {
+    __shared__ TabP sm[kTabEntries];
+    const long long iy = blockIdx.y;
+    const int x0 = blockIdx.x * tx, nz = gg.nz;
+    const int ncol = min(tx, gg.nx + 1 - x0);
+    for (int t = threadIdx.x; t < ncol * nz; t += blockDim.x) {
+        const int iz = t / ncol, xl = t - iz * ncol;
+        const int s = startB[(iy * nz + iz) * gg.nx + x0 + xl];   // x = nx: the slab's end
+        sm[xl * nz + iz] = pack_tab(s, pqhl[s]);
+    }
+    __syncthreads();
+    TabP* out = tabP + (iy * (gg.nx + 1) + x0) * nz;
+    for (int t = threadIdx.x; t < ncol * nz; t += blockDim.x) out[t] = sm[t];
+}
+
 // reclassification: new prefixes at every z-fastest table entry (its start unchanged)
 __global__ void k_pack_tabP(long long nt, const longlong2* __restrict__ pqhl, TabP* __restrict__ tabP) {
     long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -617,8 +638,16 @@ static cudaError_t class_prefix(rtg_map_s* m, cudaStream_t st, const int* startB
     if (e == cudaSuccess) {
         const long long nt = (long long)m->gg.ny * (m->gg.nx + 1) * m->gg.nz;
         if (startB)
-            note_launch(), k_build_tabs<<<dim3((unsigned)(((m->gg.nx + 1) * m->gg.nz + 255) / 256), (unsigned)m->gg.ny),
-                                          256, 0, st>>>(m->gg, startB, (const longlong2*)pqhl, m->gtabP);
+        {
+            const int tx = kTabEntries / m->gg.nz;
+            if (tx >= 8)
+                note_launch(), k_build_tabs_tile<<<dim3((unsigned)((m->gg.nx + 1 + tx - 1) / tx), (unsigned)m->gg.ny),
+                                                   256, 0, st>>>(m->gg, tx, startB, (const longlong2*)pqhl, m->gtabP);
+            else
+                note_launch(), k_build_tabs<<<dim3((unsigned)(((m->gg.nx + 1) * m->gg.nz + 255) / 256),
+                                                   (unsigned)m->gg.ny), 256, 0, st>>>(m->gg, startB,
+                                                                                      (const longlong2*)pqhl, m->gtabP);
+        }
         else
             note_launch(), k_pack_tabP<<<nblocks(nt, 256), 256, 0, st>>>(nt, (const longlong2*)pqhl, m->gtabP);
         e = cudaGetLastError();
