@@ -263,7 +263,7 @@ rtg_status rtg_best(const double* utility, int K, long long index_base, void* st
  * (= 12) counters {collision pairs FP64-redecided, visibility pairs FP64-redecided, visibility
  * pairs tested individually, (row, z-cell) x-runs added whole, collision candidates tested,
  * visibility pairs tested in the horizontally straddling flanks of rows, (row, z-cell) units cut,
- * individually tested pairs visible, footprint rows classified, test segments, 0, 0}
+ * individually tested pairs visible, footprint rows classified, 0, 0, 0 (reserved)}
  * (culled mode; dense mode fills the first two).  Synchronises the stream.
  */
 enum { RTG_DEBUG_STATS = 12 };
