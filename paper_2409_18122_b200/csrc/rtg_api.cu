@@ -82,15 +82,6 @@ void dev_free(void* p, cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
 }
 
-// frees a stream-ordered device block on every return path (the API_CK early returns included)
-struct DevFreeGuard {
-    void** p;
-    cudaStream_t st;
-    ~DevFreeGuard() {
-        if (*p) dev_free(*p, st);
-        *p = nullptr;
-    }
-};
 
 // defined in rtg_map.cu / rtg_score.cu
 rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const float* scales, const float* opacity,

@@ -65,6 +65,15 @@ cudaError_t exclusive_scan_col_counts(const int* tab, int stride, int nx, int nz
 // device allocation through the stream-ordered pool
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
+// frees a stream-ordered device block on every return path (the early error returns included)
+struct DevFreeGuard {
+    void** p;
+    cudaStream_t st;
+    ~DevFreeGuard() {
+        if (*p) dev_free(*p, st);
+        *p = nullptr;
+    }
+};
 // (re)classification of a built map (rtg_map.cu); force: even when the parameters are unchanged
 rtg_status classify_map(rtg_map_s* m, int variant, double k_sigma, double tau_hi, double tau_lo,
                         cudaStream_t st, bool force = false);

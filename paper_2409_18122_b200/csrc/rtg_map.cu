@@ -723,6 +723,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     const rtg_robot rb = m->robot;
     // --- bounds + validation (one sync)
     DevBounds* db = nullptr;
+    DevFreeGuard db_guard{(void**)&db, st};
     MAP_CK(dev_alloc((void**)&db, sizeof(DevBounds), st));
     // the map's own weights and flags (input order), written by the validation pass
     MAP_CK(map_alloc(m, &m->w_orig, n, st));
@@ -760,6 +761,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
         MAP_CK(es);
     }
     dev_free(db, st);
+    db = nullptr;
     if (hb.err) {
         set_error("rtg_map_create: invalid element(s):%s%s%s%s%s", (hb.err & 1) ? " non-finite mean" : "",
                   (hb.err & 2) ? " quaternion norm < 1e-12" : "", (hb.err & 4) ? " scale <= 0 or non-finite" : "",
@@ -836,10 +838,14 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
     // --- counting sort into both grids
     int *gkey = nullptr, *ckey = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
+    // temporaries of the sort: freed (stream-ordered) on every return path
+    DevFreeGuard g_gkey{(void**)&gkey, st}, g_ckey{(void**)&ckey, st}, g_gcount{(void**)&gcountB, st},
+        g_gstart{(void**)&gstartB, st};
     MAP_CK(dev_alloc((void**)&gkey, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&ckey, sizeof(int) * (n > 0 ? n : 1), st));
     int* grank = nullptr;
     int* crank = nullptr;
+    DevFreeGuard g_grank{(void**)&grank, st}, g_crank{(void**)&crank, st};
     MAP_CK(dev_alloc((void**)&grank, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&crank, sizeof(int) * (n > 0 ? n : 1), st));
     // the cell-count arrays in one block, cleared by one memset
@@ -865,12 +871,12 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
                                                               m->cls);
         } else {
             GRec* rec = nullptr;
+            DevFreeGuard g_rec{(void**)&rec, st};
             MAP_CK(dev_alloc((void**)&rec, sizeof(GRec) * n, st));
             note_launch(), k_pack_gain<<<nb, 256, 0, st>>>(n, means, w, rec, RTG_VARIANT_XI, m->cls);
             note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gstartB, m->gidx);
             const unsigned fb = nblocks(m->n_gain, 256) > 8192 ? 8192 : nblocks(m->n_gain, 256);
             note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, m->gidx, rec, m->grec + m->n_gain_pad);
-            dev_free(rec, st);
         }
         note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq, m->crec,
                                                          m->cmat, m->csrc);
@@ -885,14 +891,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
         note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, m->n_col,
                                                                          m->n_col_pad);
     MAP_CK(cudaGetLastError());
-    dev_free(gkey, st);
-    dev_free(ckey, st);
-    dev_free(grank, st);
-    dev_free(crank, st);
     // --- default classification (k = 1/2, derived thresholds); copy A derived from copy B
     MAP_CK(class_prefix(m, st, gstartB, gcountB));
-    dev_free(gstartB, st);
-    dev_free(gcountB, st);   // (ccount, gcountA live in the same block)
+    // (the guards free gkey, ckey, grank, crank, gstartB and gcountB with ccount, gcountA in its block)
     set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
     return RTG_OK;
 }
