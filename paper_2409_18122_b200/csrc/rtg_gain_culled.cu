@@ -417,14 +417,14 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                     int r0 = 0;   // run holding item gb
                     for (int gb0 = 0; gb0 < tot; gb0 += 64 * kFlushPasses) {   // 32-bit sums: flushed
                         const int gend = min(tot, gb0 + 64 * kFlushPasses);
-                        // head bitmap of this chunk: bit b <=> a run (or the sentinel) starts at item gb0 + b
+                        // head bitmap of this chunk: bit b <=> a run (or the sentinel) starts at item gb0 + b + 1
                         __syncwarp();
                         {
                             const int4 ea = *reinterpret_cast<const int4*>(qe + 8 * lane);
                             const int4 eb = *reinterpret_cast<const int4*>(qe + 8 * lane + 4);
                             const unsigned span = (unsigned)(kHeadWords * 32);
-                            auto mark = [&](int e) {
-                                const unsigned b = (unsigned)(e - gb0);
+                            auto mark = [&](int e) {   // bit e - 1 - gb0: the window needs no shift
+                                const unsigned b = (unsigned)(e - 1 - gb0);
                                 if (b < span) atomicOr(&sw.head[b >> 5], 1u << (b & 31));
                             };
                             mark(ea.x); mark(ea.y); mark(ea.z); mark(ea.w);
@@ -434,13 +434,11 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         __syncwarp();
                         unsigned w = 0, pc = 0;
                         for (int gb = gb0; gb < gend; gb += 64) {
-                            // head bit k of (hhi:hlo) <=> a run starts at item gb + k + 1
+                            // head bit k of (hhi:hlo) <=> a run starts at item gb + k + 1 (bits gb - gb0 ..)
                             const int hw = (gb - gb0) >> 5;
-                            RTG_CHECK(hw + 2 < kHeadWords, "head bitmap window");
+                            RTG_CHECK(hw + 1 < kHeadWords, "head bitmap window");
                             const uint2 h01 = *reinterpret_cast<const uint2*>(sw.head + hw);
-                            const unsigned h2 = sw.head[hw + 2];
-                            const unsigned hlo = __funnelshift_r(h01.x, h01.y, 1);
-                            const unsigned hhi = __funnelshift_r(h01.y, h2, 1);
+                            const unsigned hlo = h01.x, hhi = h01.y;
                             const int na = __popc(hlo);
                             const int gpa = gb + lane, gpb = gpa + 32;
                             const int gia = gpa + qs[r0 + __popc(hlo & lanes_lt)];
