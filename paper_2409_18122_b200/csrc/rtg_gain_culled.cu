@@ -11,21 +11,22 @@
 //      four horizontal constraints give the x-interval P of possibly visible columns and its
 //      sub-interval I of columns whose whole column box is horizontally inside;
 //   2. the flanks P \ I are tested Gaussian by Gaussian from record copy A (sorted by
-//      (row, x-cell)): each flank is ONE contiguous record run (all z);
+//      (row, x-cell, z-cell)): each flank is ONE contiguous record run (all z);
 //   3. the inside columns I are walked z-cell by z-cell from copy B (sorted by (row, z-cell,
 //      x-cell), so a row's z-slab is x-contiguous): per (row, z-cell) unit (lanes flattened over the
 //      chunk's units through a shared-memory owner table) the two vertical constraints cut I into an
-//      x-run fully inside (added from the exact prefixes of the z-fastest table: two loads) and at
-//      most two straddling x-runs (tested); the z-cells a row can see come from the vertical wedge
-//      at the row's largest depth and the row's occupied z-range;
+//      x-run fully inside (added from the exact prefixes of the z-fastest table: the difference of
+//      two 16-byte entries {start, prefixes mod 2^48 / 2^24}) and at most two straddling x-runs
+//      (tested); the z-cells a row can see come from the vertical wedge at the row's largest depth
+//      and the row's occupied z-range;
 //   4. tested runs go to a per-warp queue; a flush tests 64 items per pass, two per lane, whatever
-//      the run lengths: a shared-memory bitmap marks the items where runs start, so each lane finds
-//      its run from a 64-bit window of it (one broadcast load, two funnel shifts, popc); items past
-//      the queue fall in a sentinel run of NaN padding records (never visible, so no bound check).
+//      the run lengths: a shared-memory bitmap marks the items where runs start (shifted by one), so
+//      each lane finds its run from a 64-bit window of it (one broadcast load, popc); items past the
+//      queue fall in a sentinel run of NaN padding records (never visible, so no bound check).
 //      The pair test is the shared exact one (packed FP32 + FP64 re-decision inside the proven
 //      guard band).
 // Sums are exact integers (24-bit u_q and a class byte per record, 32-bit per-lane sums flushed
-// into 64-bit ones; FP64-exact prefixes): order free, so the result is bit-identical to the dense
+// into 64-bit ones; integer prefixes): order free, so the result is bit-identical to the dense
 // kernel.  eps (>> FP32 error of the cell tests) keeps "inside" strictly inside and "possible" a
 // superset.
 #include <cfloat>
