@@ -55,6 +55,8 @@ cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, cudaStream_
 long long scan_i32_zero_ints(long long n);
 long long scan_i32_scratch_ints(long long n);
 cudaError_t exclusive_scan_i32_into(const int* in, int* out, long long n, int* scratch, cudaStream_t st);
+// pairs of 64-bit sums (in: 2n long longs; out: 2(n + 1), the total last)
+cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st);
 // copy-B records' (u_q, nH | nL << 32) pairs (from GRec::uc) scanned into out[0 .. 2n+1]
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st);
 // exclusive scan over the ncols = ny * nx columns (row-major) of their record counts (all z-cells), read

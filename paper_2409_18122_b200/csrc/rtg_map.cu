@@ -15,6 +15,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "rtg_host.hpp"
@@ -236,10 +237,12 @@ __global__ void k_keys(long long n, const float* __restrict__ means, const unsig
             int iz = cell_coord(z, gg.oz, igz, gg.nz);
             gk = (int)(((long long)iy * gg.nz + iz) * gg.nx + ix);
             grank[i] = atomicAdd(&gcountB[gk], 1);
-            atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);   // column totals (copy A), no rank needed
-            int2* zo = zocc + (long long)iy * gg.nxb + ix / kZoccX;
-            if (iz < zo->x) atomicMin(&zo->x, iz);
-            if (iz > zo->y) atomicMax(&zo->y, iz);
+            if (gcountA) {   // scan path only (k_tabs_cols derives both from the cell starts)
+                atomicAdd(&gcountA[(long long)iy * gg.nx + ix], 1);   // column totals (copy A), no rank needed
+                int2* zo = zocc + (long long)iy * gg.nxb + ix / kZoccX;
+                if (iz < zo->x) atomicMin(&zo->x, iz);
+                if (iz > zo->y) atomicMax(&zo->y, iz);
+            }
         }
         if (!(f & RTG_G_NO_COLLIDE)) {
             int ix = cell_coord(x, cg.ox, icg, cg.nx);
@@ -266,12 +269,29 @@ __device__ __forceinline__ unsigned class_of(float w, int variant, const ClassSt
     return (unsigned)llrint(u * cs->scale) | (c << kUqBits);
 }
 
+// map build, per-cell tables by (row, kTabsX-column tile) (k_tabs_cols) up to kTabsMaxZ z-cells
+constexpr int kTabsX = 2 * kZoccX;   // columns per CTA: two z-occupancy blocks
+constexpr int kTabsMaxZ = 32;
+
+// the record's (u_q, nH | nL << 32) pair added to the sum of its (z-slab, kTabsX-column tile) segment of copy B
+// (fire-and-forget atomics; k_tabs_cols turns the scanned segment sums into the table's prefixes)
+__device__ __forceinline__ void add_tile_sum(unsigned long long* __restrict__ tsum, int ntl, int nx, int key,
+                                             unsigned uc) {
+    const int slab = key / nx, tl = (key - slab * nx) / kTabsX;
+    unsigned long long* t = tsum + 2 * ((long long)slab * ntl + tl);
+    const unsigned q = uc & kUqMask, c = uc >> kUqBits;
+    if (q) atomicAdd(t, (unsigned long long)q);
+    if (c == kClsH) atomicAdd(t + 1, 1ull);
+    else if (c == kClsL) atomicAdd(t + 1, 1ull << 32);
+}
+
 // the visibility records, sorted by (row, z-cell, x-cell), with their packed class and fixed-point u
-// (the classification statistics are computed before the scatter)
+// (the classification statistics are computed before the scatter); tsum: the segment sums (or NULL)
 __global__ void k_scatter_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
                                const int* __restrict__ gkey, const int* __restrict__ grank,
                                const int* __restrict__ startB, GRec* __restrict__ grec, int* __restrict__ gidx,
-                               int variant, const ClassState* __restrict__ cs) {
+                               int variant, const ClassState* __restrict__ cs, unsigned long long* __restrict__ tsum,
+                               int ntl, int nx) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int k = gkey[i];
@@ -280,6 +300,7 @@ __global__ void k_scatter_gain(long long n, const float* __restrict__ means, con
         const int sb = startB[k] + grank[i];
         grec[sb] = r;
         gidx[sb] = (int)i;
+        if (tsum) add_tile_sum(tsum, ntl, nx, k, r.uc);
     }
 }
 
@@ -298,12 +319,14 @@ __global__ void k_pack_gain(long long n, const float* __restrict__ means, const 
 }
 
 __global__ void k_perm_gain(long long n, const int* __restrict__ gkey, const int* __restrict__ grank,
-                            const int* __restrict__ startB, int* __restrict__ gidx) {
+                            const int* __restrict__ startB, int* __restrict__ gidx, const GRec* __restrict__ rec,
+                            unsigned long long* __restrict__ tsum, int ntl, int nx) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const int k = gkey[i];
         if (k < 0) continue;
         gidx[startB[k] + grank[i]] = (int)i;
+        if (tsum) add_tile_sum(tsum, ntl, nx, k, rec[i].uc);
     }
 }
 
@@ -574,6 +597,204 @@ __global__ void __launch_bounds__(256) k_build_tabs_tile(GainGrid gg, int tx, co
     __syncthreads();
     TabP* out = tabP + (iy * (gg.nx + 1) + x0) * nz;
     for (int t = threadIdx.x; t < ncol * nz; t += blockDim.x) out[t] = sm[t];
+}
+
+// map build, the per-cell tables in one pass per (row, kTabsX-column tile), from the cell starts (key
+// order) and the scanned sums of the tile's z-slab segments of copy B:
+//  - copy A's column starts: the row's first record plus, per z-slab, the slab's records left of the
+//    column (rows and slabs are contiguous in copy B);
+//  - copy A: each cell's records moved to their column, z-cells in order (what k_derive_cols_b does),
+//    one record per thread over the tile's slab segments (coalesced reads; a cell's records are found
+//    by binary search in the starts, so dense cells do not serialise a thread);
+//  - the z-fastest entries {start, exact prefixes} (what the record prefix scan + k_build_tabs* do):
+//    the segment's scanned base plus the sums of the cells to its left, stored as one contiguous range;
+//  - the tile's z-occupancy block (what the key pass's atomics do on the other path).
+// The map it builds is identical to the other path's.  nz <= kTabsMaxZ.
+constexpr int kTabsThreads = 256;
+static_assert(kTabsThreads > kTabsX && kTabsX % kZoccX == 0 && kTabsX % 32 == 0, "tile shape");
+// shared-memory rows of kTabsX + 1 (odd) elements: a warp's accesses along z (the z-fastest entries)
+// fall in distinct banks; the 16-byte sums are further skewed by one slot per 4 columns (kTabsSW, odd)
+// so that lanes taking 4 consecutive columns each (the per-slab prefix) do too
+constexpr int kTabsW = kTabsX + 1;
+constexpr int kTabsSW = kTabsX + kTabsX / 4 + 1;
+__device__ __forceinline__ int tabs_sx(int iz, int j) { return iz * kTabsSW + j + (j >> 2); }
+inline size_t tabs_smem(int nz) {
+    return sizeof(unsigned long long) * 2 * nz * kTabsSW  // per cell (u, nH | nL << 32), then its prefix
+           + sizeof(longlong2) * nz                      // the slab segments' scanned bases
+           + sizeof(int) * nz * kTabsW                   // cell starts
+           + sizeof(int) * nz * kTabsX                   // cells' first copy-A slot
+           + sizeof(int) * (2 * nz + 1);                 // slab starts, flattened segment offsets
+}
+__global__ void __launch_bounds__(kTabsThreads, 6) k_tabs_cols(GainGrid gg, int ntl, const int* __restrict__ startB,
+                                                            const longlong2* __restrict__ tpre,
+                                                            const GRec* __restrict__ recB, GRec* __restrict__ recA,
+                                                            TabP* __restrict__ tabP, int* __restrict__ gstartA,
+                                                            int2* __restrict__ zocc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ int s_zlo[kTabsX / kZoccX], s_zhi[kTabsX / kZoccX];
+    const int nx = gg.nx, nz = gg.nz, tile = blockIdx.x, x0 = tile * kTabsX;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    constexpr int W = kTabsW;
+    ulonglong2* s_sum = reinterpret_cast<ulonglong2*>(smraw);                     // [nz][kTabsSW], skewed
+    longlong2* s_base = reinterpret_cast<longlong2*>(s_sum + nz * kTabsSW);        // [nz]
+    int* s_st = reinterpret_cast<int*>(s_base + nz);                              // [nz][W]
+    int* s_dA = s_st + nz * W;                                                    // [nz][kTabsX]
+    int* s_slab0 = s_dA + nz * kTabsX;                                            // [nz]
+    int* s_seg = s_slab0 + nz;                                                    // [nz + 1]
+    const long long iy = blockIdx.y;
+    const int ncol = max(0, min(kTabsX, nx - x0));   // columns of the tile
+    const int nent = min(kTabsX, nx + 1 - x0);       // its table entries (x = nx: the slabs' ends)
+    const long long kb = iy * nz * (long long)nx;    // key of cell (iy, 0, 0)
+    if (threadIdx.x < kTabsX / kZoccX) {
+        s_zlo[threadIdx.x] = INT_MAX;
+        s_zhi[threadIdx.x] = -1;
+    }
+    // a warp per z-slab: its cell starts (coalesced, all loads in flight before the first use), the
+    // slab start and scanned base
+    constexpr int kLd = (kTabsX + 1 + 31) / 32;
+    for (int iz = wid; iz < nz; iz += nw) {
+        const int* src = startB + kb + (long long)iz * nx + x0;
+        int v[kLd];
+#pragma unroll
+        for (int c = 0; c < kLd; ++c) v[c] = lane + 32 * c <= ncol ? __ldg(src + lane + 32 * c) : 0;
+        int s0 = 0;
+        longlong2 bs = make_longlong2(0, 0);
+        if (lane == 0) {
+            s0 = __ldg(startB + kb + (long long)iz * nx);
+            bs = tpre[((long long)iy * nz + iz) * ntl + tile];
+        }
+#pragma unroll
+        for (int c = 0; c < kLd; ++c)
+            if (lane + 32 * c <= ncol) s_st[iz * W + lane + 32 * c] = v[c];
+        if (lane == 0) {
+            s_slab0[iz] = s0;
+            s_base[iz] = bs;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x <= ncol) {
+        const int j = threadIdx.x;
+        int a = s_slab0[0];
+        for (int iz = 0; iz < nz; ++iz) a += s_st[iz * W + j] - s_slab0[iz];
+        gstartA[iy * nx + x0 + j] = a;   // j = ncol: the next column's start (its tile writes the same)
+        if (j < ncol) {
+            int zlo = INT_MAX, zhi = -1;
+            for (int iz = 0; iz < nz; ++iz) {
+                s_dA[iz * kTabsX + j] = a;
+                s_sum[tabs_sx(iz, j)] = make_ulonglong2(0ull, 0ull);
+                const int c = s_st[iz * W + j + 1] - s_st[iz * W + j];
+                a += c;
+                if (c > 0) {
+                    zlo = min(zlo, iz);
+                    zhi = iz;
+                }
+            }
+            if (zhi >= 0) {
+                atomicMin(&s_zlo[j / kZoccX], zlo);
+                atomicMax(&s_zhi[j / kZoccX], zhi);
+            }
+        }
+    } else if (threadIdx.x == blockDim.x - 1) {
+        int o = 0;
+        for (int iz = 0; iz < nz; ++iz) {
+            s_seg[iz] = o;
+            o += s_st[iz * W + ncol] - s_st[iz * W];
+        }
+        s_seg[nz] = o;
+    }
+    __syncthreads();
+    // records, one per thread over the tile's slab segments: moved to copy A and summed per cell
+    const int total = s_seg[nz];
+    for (int fb = threadIdx.x - lane; fb < total; fb += blockDim.x) {   // warp-uniform trip count
+        const int f = fb + lane;
+        int cell = -1;
+        unsigned q = 0u, hl = 0u;
+        if (f < total) {
+            int iz = 0;   // the slab: the last with s_seg[iz] <= f (empty slabs share their offset)
+            for (int lo = 0, hi = nz - 1; lo < hi;) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_seg[mid] <= f) lo = mid; else hi = mid - 1;
+                iz = lo;
+            }
+            const int* st = s_st + iz * W;
+            const int k = st[0] + (f - s_seg[iz]);
+            int j = 0;    // the cell: the last with st[j] <= k
+            for (int lo = 0, hi = ncol - 1; lo < hi;) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (st[mid] <= k) lo = mid; else hi = mid - 1;
+                j = lo;
+            }
+            const GRec r = recB[k];
+            recA[s_dA[iz * kTabsX + j] + (k - st[j])] = r;
+            const unsigned c = r.uc >> kUqBits;
+            cell = tabs_sx(iz, j);
+            q = r.uc & kUqMask;
+            hl = c == kClsH ? 1u : (c == kClsL ? 0x10000u : 0u);
+        }
+        // a cell's records sit in consecutive lanes (cells ascend with f): segmented sums (exact, < 2^29
+        // and < 2^16 per warp), one shared-memory add per cell and warp by the segment's last lane
+        const int prev = __shfl_up_sync(0xffffffffu, cell, 1), next = __shfl_down_sync(0xffffffffu, cell, 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != cell);
+        const int seg0 = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));   // this lane's segment head
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned pq = __shfl_up_sync(0xffffffffu, q, o), ph = __shfl_up_sync(0xffffffffu, hl, o);
+            if (lane - o >= seg0) {
+                q += pq;
+                hl += ph;
+            }
+        }
+        if (cell >= 0 && (lane == 31 || next != cell)) {
+            unsigned long long* sm = reinterpret_cast<unsigned long long*>(s_sum + cell);
+            if (q) atomicAdd(sm, (unsigned long long)q);
+            if (hl) atomicAdd(sm + 1, (unsigned long long)(hl & 0xffffu) | ((unsigned long long)(hl >> 16) << 32));
+        }
+    }
+    __syncthreads();
+    // exclusive prefixes along x within each z-slab from the segment's base (a warp per slab, 4
+    // consecutive columns per lane summed serially, one warp scan of the lane totals)
+    static_assert(kTabsX == 128, "4 columns per lane");
+    for (int iz = wid; iz < nz; iz += nw) {
+        ulonglong2 v[4];
+        unsigned long long a = 0ull, b = 0ull;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = 4 * lane + i;
+            v[i] = j < ncol ? s_sum[tabs_sx(iz, j)] : make_ulonglong2(0ull, 0ull);
+            a += v[i].x;
+            b += v[i].y;
+        }
+        const unsigned long long ta = a, tb = b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long pa = __shfl_up_sync(0xffffffffu, a, o), pb = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) {
+                a += pa;
+                b += pb;
+            }
+        }
+        unsigned long long ea = (unsigned long long)s_base[iz].x + a - ta,
+                           eb = (unsigned long long)s_base[iz].y + b - tb;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = 4 * lane + i;
+            if (j < nent) s_sum[tabs_sx(iz, j)] = make_ulonglong2(ea, eb);
+            ea += v[i].x;
+            eb += v[i].y;
+        }
+    }
+    __syncthreads();
+    // the z-fastest entries (iy, x0 .. x0 + nent - 1, all z): one contiguous range; t -> (j, iz) by a
+    // float reciprocal (exact: t < 2^13, and t / nz is at least 1 / nz from the next integer)
+    TabP* out = tabP + (iy * (nx + 1) + x0) * nz;
+    const float rnz = 1.0f / (float)nz;
+    for (int t = threadIdx.x; t < nent * nz; t += blockDim.x) {
+        const int j = (int)(((float)t + 0.5f) * rnz), iz = t - j * nz;
+        const ulonglong2 v = s_sum[tabs_sx(iz, j)];
+        out[t] = pack_tab(s_st[iz * W + j], make_longlong2((long long)v.x, (long long)v.y));
+    }
+    if (threadIdx.x < kTabsX / kZoccX && x0 + threadIdx.x * kZoccX < nx)
+        zocc[iy * gg.nxb + tile * (kTabsX / kZoccX) + threadIdx.x] = make_int2(s_zlo[threadIdx.x], s_zhi[threadIdx.x]);
 }
 
 // reclassification: new prefixes at every z-fastest table entry (its start unchanged)
@@ -848,14 +1069,27 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     DevFreeGuard g_grank{(void**)&grank, st}, g_crank{(void**)&crank, st};
     MAP_CK(dev_alloc((void**)&grank, sizeof(int) * (n > 0 ? n : 1), st));
     MAP_CK(dev_alloc((void**)&crank, sizeof(int) * (n > 0 ? n : 1), st));
-    // the cell-count arrays in one block, cleared by one memset
-    const long long ncnt = (gg.ncellsB + 1) + (cg.ncells + 1) + (gg.ncellsA + 1);
-    MAP_CK(dev_alloc((void**)&gcountB, sizeof(int) * ncnt, st));
+    // the per-cell tables, copy A and the z-occupancy from one pass per (row, 128-column tile)
+    // (k_tabs_cols) unless the grid has more than kTabsMaxZ z-cells (then: column counts and z-occupancy
+    // by atomics in the key pass, the record prefix scan, k_build_tabs*, k_derive_cols_b).
+    // RTG_MAP_TABLES=scan forces the latter (the parity tests compare the two).
+    static const bool force_scan = getenv("RTG_MAP_TABLES") && strcmp(getenv("RTG_MAP_TABLES"), "scan") == 0;
+    const bool tiles = gg.nz <= kTabsMaxZ && !force_scan;
+    const int ntl = gg.nx / kTabsX + 1;   // tiles per row (the last holds the x = nx end entries)
+    const long long nseg = (long long)gg.ny * gg.nz * ntl;
+    // the cell-count arrays in one block, cleared by one memset (with the tile path's segment sums)
+    const long long ncnt = (gg.ncellsB + 1) + (cg.ncells + 1) + (tiles ? 0 : gg.ncellsA + 1);
+    const size_t cnt_bytes = (sizeof(int) * ncnt + 15) & ~(size_t)15;
+    const size_t seg_bytes = tiles ? 2 * sizeof(long long) * nseg : 0;
+    MAP_CK(dev_alloc((void**)&gcountB, cnt_bytes + seg_bytes, st));
     ccount = gcountB + (gg.ncellsB + 1);
-    int* gcountA = ccount + (cg.ncells + 1);
+    int* gcountA = tiles ? nullptr : ccount + (cg.ncells + 1);
+    unsigned long long* tsum = tiles ? reinterpret_cast<unsigned long long*>((char*)gcountB + cnt_bytes) : nullptr;
     MAP_CK(dev_alloc((void**)&gstartB, sizeof(int) * (gg.ncellsB + 1), st));
-    MAP_CK(cudaMemsetAsync(gcountB, 0, sizeof(int) * ncnt, st));
-    note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc, (long long)gg.ny * gg.nxb);
+    MAP_CK(cudaMemsetAsync(gcountB, 0, cnt_bytes + seg_bytes, st));
+    if (!tiles)
+        note_launch(), k_zocc_init<<<nblocks((long long)gg.ny * gg.nxb, 256), 256, 0, st>>>(m->zocc,
+                                                                                            (long long)gg.ny * gg.nxb);
     unsigned nb = nblocks(n, 256) > 8192 ? 8192 : nblocks(n, 256);
     if (n > 0)
         note_launch(), k_keys<<<nb, 256, 0, st>>>(n, means, flags, gg, cg, gkey, ckey, grank, crank, gcountB, gcountA,
@@ -863,18 +1097,18 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(cudaGetLastError());
     MAP_CK(exclusive_scan_i32(gcountB, gstartB, gg.ncellsB, st));
     MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
-    MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));   // copy A's column starts
+    if (!tiles) MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));   // copy A's column starts
     if (n > 0) {
         if ((double)m->n_gain * sizeof(GRec) <= kScatterMaxBytes) {
             note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, grank, gstartB,
                                                               m->grec + m->n_gain_pad, m->gidx, RTG_VARIANT_XI,
-                                                              m->cls);
+                                                              m->cls, tsum, ntl, gg.nx);
         } else {
             GRec* rec = nullptr;
             DevFreeGuard g_rec{(void**)&rec, st};
             MAP_CK(dev_alloc((void**)&rec, sizeof(GRec) * n, st));
             note_launch(), k_pack_gain<<<nb, 256, 0, st>>>(n, means, w, rec, RTG_VARIANT_XI, m->cls);
-            note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gstartB, m->gidx);
+            note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gstartB, m->gidx, rec, tsum, ntl, gg.nx);
             const unsigned fb = nblocks(m->n_gain, 256) > 8192 ? 8192 : nblocks(m->n_gain, 256);
             note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, m->gidx, rec, m->grec + m->n_gain_pad);
         }
@@ -892,7 +1126,25 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
                                                                          m->n_col_pad);
     MAP_CK(cudaGetLastError());
     // --- default classification (k = 1/2, derived thresholds); copy A derived from copy B
-    MAP_CK(class_prefix(m, st, gstartB, gcountB));
+    if (tiles) {
+        long long* tpre = nullptr;
+        DevFreeGuard g_tpre{(void**)&tpre, st};
+        MAP_CK(dev_alloc((void**)&tpre, 2 * sizeof(long long) * (nseg + 1), st));
+        MAP_CK(exclusive_scan_i64x2(reinterpret_cast<const long long*>(tsum), tpre, nseg, st));
+        const size_t smem = tabs_smem(gg.nz);
+        static bool smem_set = false;   // (> 48 KB of dynamic shared memory only for nz > 15)
+        if (smem > 48 * 1024 && !smem_set) {
+            MAP_CK(cudaFuncSetAttribute(k_tabs_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tabs_smem(kTabsMaxZ)));
+            smem_set = true;
+        }
+        note_launch(), k_tabs_cols<<<dim3((unsigned)ntl, (unsigned)gg.ny), kTabsThreads, smem, st>>>(
+                           gg, ntl, gstartB, reinterpret_cast<const longlong2*>(tpre), m->grec + m->n_gain_pad,
+                           m->grec, m->gtabP, m->gstartA, m->zocc);
+        MAP_CK(cudaGetLastError());
+    } else {
+        MAP_CK(class_prefix(m, st, gstartB, gcountB));
+    }
     // (the guards free gkey, ckey, grank, crank, gstartB and gcountB with ccount, gcountA in its block)
     set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
     return RTG_OK;

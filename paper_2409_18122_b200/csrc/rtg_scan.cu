@@ -338,6 +338,9 @@ cudaError_t exclusive_scan_col_counts(const int* tab, int stride, int nx, int nz
                                       cudaStream_t st) {
     return scan_impl<int>(LoadColCount{tab, nx, nz, stride}, out, ncols, st);
 }
+cudaError_t exclusive_scan_i64x2(const long long* in, long long* out, long long n, cudaStream_t st) {
+    return scan_impl<I64x2>(LoadArr<I64x2>{reinterpret_cast<const I64x2*>(in)}, reinterpret_cast<I64x2*>(out), n, st);
+}
 cudaError_t exclusive_scan_grec_uc(const GRec* rec, long long* out, long long n, cudaStream_t st) {
     return scan_impl<I64x2>(LoadUc{rec}, reinterpret_cast<I64x2*>(out), n, st);
 }

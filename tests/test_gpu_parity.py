@@ -764,3 +764,52 @@ np.save(sys.argv[1], out[0])
         res[flag] = np.load(f)
         os.unlink(f)
     assert np.array_equal(res["0"], res["1"])
+
+
+@pytest.mark.gpu
+def test_map_table_paths_identical():
+    """The map build derives copy A, the z-fastest tables and the z-occupancy in one pass per (row,
+    64-column tile) (k_tabs_cols) when the grid has <= 32 z-cells; RTG_MAP_TABLES=scan forces the other
+    path (record prefix scan, k_build_tabs*, k_derive_cols_b, atomics in the key pass), which maps with
+    more z-cells take.  Both must give the same scores bit for bit, and equal the dense kernel, on grids
+    whose x-cell count is a multiple of 64 (a tile holding only the slab ends), one more, and ragged."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    code = r'''
+import sys, dataclasses, numpy as np
+sys.path.insert(0, %r)
+from paper_2409_18122_b200 import rtg as R, workloads as W
+room = W.room()
+idx = np.arange(0, room.K, 16)
+res = []
+for span, hz in ((4.75, 1.5), (9.6 - 0.075 + 0.03, 0.5), (7.3, 0.09), (None, 1.5)):
+    wl = room
+    if span is not None:   # x extent chosen so that nx = floor(span / 0.075) + 1 is 64, 128 or 98
+        m = room.means.copy()
+        m[0] = (m[0] - m[0].min()) / (m[0].max() - m[0].min()) * span
+        wl = dataclasses.replace(room, means=m.astype(np.float32))
+    opts = (0.3, hz, 0.0, 0.075)
+    outs = []
+    for mode in (R.MODE_CULLED, R.MODE_DENSE):
+        mp = R.map_from_workload(wl, options=opts if mode == R.MODE_CULLED else None)
+        tr = R.traj_from_workload(wl, x=wl.x[idx], y=wl.y[idx], z=wl.z[idx], yaw=wl.yaw[idx])
+        d = R.score_debug(mp, tr, wl.camera, R.make_params(mode=mode, flags=R.SCORE_FULL_GAIN))
+        outs.append(np.concatenate([d["wp_gain"].cpu().numpy().view(np.int64), d["wp_nh"].cpu().numpy(),
+                                    d["wp_nl"].cpu().numpy(), d["wp_col"].cpu().numpy()]))
+        mp.close(); tr.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert outs[0][len(idx) * room.T:].sum() > 0
+    res.append(outs[0])
+np.save(sys.argv[1], np.concatenate(res))
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("tiles", "scan"):
+        f = tempfile.mktemp(suffix=".npy")
+        env = dict(os.environ, RTG_MAP_TABLES=flag)
+        p = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=900)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[flag] = np.load(f)
+        os.unlink(f)
+    assert np.array_equal(res["tiles"], res["scan"])
