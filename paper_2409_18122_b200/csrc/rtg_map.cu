@@ -285,31 +285,13 @@ __device__ __forceinline__ void add_tile_sum(unsigned long long* __restrict__ ts
     else if (c == kClsL) atomicAdd(t + 1, 1ull << 32);
 }
 
-// the visibility records, sorted by (row, z-cell, x-cell), with their packed class and fixed-point u
-// (the classification statistics are computed before the scatter); tsum: the segment sums (or NULL)
-__global__ void k_scatter_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
-                               const int* __restrict__ gkey, const int* __restrict__ grank,
-                               const int* __restrict__ startB, GRec* __restrict__ grec, int* __restrict__ gidx,
-                               int variant, const ClassState* __restrict__ cs, unsigned long long* __restrict__ tsum,
-                               int ntl, int nx) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        int k = gkey[i];
-        if (k < 0) continue;
-        const GRec r{means[i], means[n + i], means[2 * n + i], class_of(w[i], variant, cs)};
-        const int sb = startB[k] + grank[i];
-        grec[sb] = r;
-        gidx[sb] = (int)i;
-        if (tsum) add_tile_sum(tsum, ntl, nx, k, r.uc);
-    }
-}
-
 // large maps: the visibility records in two coalesced passes instead of the scatter above (whose
 // partial 16-byte sectors cost read-modify-writes once the records exceed L2): (1) the permutation -- each
 // eligible Gaussian writes its index into its slot; (2) every slot, in order, gathers its record, packed
 // beforehand in input order with the class word (a2).  The scatter up to this many record bytes (r1,
 // with two record copies: 64 MB scattered in 0.59 ms vs 0.67 ms gathered; 160 MB: 1.45 vs 1.23 ms)
 constexpr double kScatterMaxBytes = 96.0 * 1024 * 1024;
+constexpr double kScatterBothMaxBytes = 200.0 * 1024 * 1024;
 
 __global__ void k_pack_gain(long long n, const float* __restrict__ means, const float* __restrict__ w,
                             GRec* __restrict__ rec, int variant, const ClassState* __restrict__ cs) {
@@ -338,6 +320,30 @@ __global__ void k_fill_gain(long long n_gain, const int* __restrict__ gidx, cons
 }
 
 // FP64 packing of the collision record (a1)
+__device__ __forceinline__ void scatter_col_one(long long i, long long n, const float* __restrict__ means,
+                                                const float* __restrict__ quats, const float* __restrict__ scales,
+                                                int k, const int* __restrict__ crank, const int* __restrict__ cstart,
+                                                const rtg_robot& rb, double guard, CRec* __restrict__ crec,
+                                                CMat* __restrict__ cmat, CSrc* __restrict__ csrc) {
+    const int slot = cstart[k] + crank[i];
+    CSrc src;
+    src.q[0] = quats[i]; src.q[1] = quats[n + i]; src.q[2] = quats[2 * n + i]; src.q[3] = quats[3 * n + i];
+    src.s[0] = scales[i]; src.s[1] = scales[n + i]; src.s[2] = scales[2 * n + i];
+    src.pad = 0.f;
+    double a[3], M[9];
+    pack_m64(src.q[0], src.q[1], src.q[2], src.q[3], src.s[0], src.s[1], src.s[2], rb, M, a);
+    double amax = fmax(a[0], fmax(a[1], a[2]));
+    float rb2 = __double2float_ru(amax * amax * (1.0 + guard) * (1.0 + 1.0e-6));
+    crec[slot] = CRec{means[i], means[n + i], means[2 * n + i], rb2};
+    CMat cm;
+    for (int j = 0; j < 9; ++j) cm.m[j] = (float)M[j];
+    cm.m[9] = __int_as_float((int)i);
+    cm.m[10] = 0.f;
+    cm.m[11] = 0.f;
+    cmat[slot] = cm;
+    csrc[slot] = src;
+}
+
 __global__ void k_scatter_col(long long n, const float* __restrict__ means, const float* __restrict__ quats,
                               const float* __restrict__ scales, const int* __restrict__ ckey,
                               const int* __restrict__ crank, const int* __restrict__ cstart, rtg_robot rb,
@@ -345,25 +351,34 @@ __global__ void k_scatter_col(long long n, const float* __restrict__ means, cons
                               CMat* __restrict__ cmat, CSrc* __restrict__ csrc) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        int k = ckey[i];
-        if (k < 0) continue;
-        const int slot = cstart[k] + crank[i];
-        CSrc src;
-        src.q[0] = quats[i]; src.q[1] = quats[n + i]; src.q[2] = quats[2 * n + i]; src.q[3] = quats[3 * n + i];
-        src.s[0] = scales[i]; src.s[1] = scales[n + i]; src.s[2] = scales[2 * n + i];
-        src.pad = 0.f;
-        double a[3], M[9];
-        pack_m64(src.q[0], src.q[1], src.q[2], src.q[3], src.s[0], src.s[1], src.s[2], rb, M, a);
-        double amax = fmax(a[0], fmax(a[1], a[2]));
-        float rb2 = __double2float_ru(amax * amax * (1.0 + guard) * (1.0 + 1.0e-6));
-        crec[slot] = CRec{means[i], means[n + i], means[2 * n + i], rb2};
-        CMat cm;
-        for (int j = 0; j < 9; ++j) cm.m[j] = (float)M[j];
-        cm.m[9] = __int_as_float((int)i);
-        cm.m[10] = 0.f;
-        cm.m[11] = 0.f;
-        cmat[slot] = cm;
-        csrc[slot] = src;
+        const int k = ckey[i];
+        if (k >= 0) scatter_col_one(i, n, means, quats, scales, k, crank, cstart, rb, guard, crec, cmat, csrc);
+    }
+}
+
+// both record scatters in one pass: the visibility records, sorted by (row, z-cell, x-cell), with their
+// packed class and fixed-point u (the classification statistics are computed before) and their segment
+// sums (tsum, or NULL), and the collision records as k_scatter_col: one read of the means and keys, both
+// streams of random writes in flight together (crank NULL: the visibility records only)
+__global__ void k_scatter_both(long long n, const float* __restrict__ means, const float* __restrict__ w,
+                               const float* __restrict__ quats, const float* __restrict__ scales,
+                               const int* __restrict__ gkey, const int* __restrict__ grank,
+                               const int* __restrict__ startB, GRec* __restrict__ grec, int* __restrict__ gidx,
+                               int variant, const ClassState* __restrict__ cs, unsigned long long* __restrict__ tsum,
+                               int ntl, int nx, const int* __restrict__ ckey, const int* __restrict__ crank,
+                               const int* __restrict__ cstart, rtg_robot rb, double guard, CRec* __restrict__ crec,
+                               CMat* __restrict__ cmat, CSrc* __restrict__ csrc) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int k = gkey[i], kc = crank ? ckey[i] : -1;
+        if (k >= 0) {
+            const GRec r{means[i], means[n + i], means[2 * n + i], class_of(w[i], variant, cs)};
+            const int sb = startB[k] + grank[i];
+            grec[sb] = r;
+            gidx[sb] = (int)i;
+            if (tsum) add_tile_sum(tsum, ntl, nx, k, r.uc);
+        }
+        if (kc >= 0) scatter_col_one(i, n, means, quats, scales, kc, crank, cstart, rb, guard, crec, cmat, csrc);
     }
 }
 
@@ -1099,10 +1114,23 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     MAP_CK(exclusive_scan_i32(ccount, m->cstart, cg.ncells, st));
     if (!tiles) MAP_CK(exclusive_scan_i32(gcountA, m->gstartA, gg.ncellsA, st));   // copy A's column starts
     if (n > 0) {
-        if ((double)m->n_gain * sizeof(GRec) <= kScatterMaxBytes) {
-            note_launch(), k_scatter_gain<<<nb, 256, 0, st>>>(n, means, w, gkey, grank, gstartB,
+        // both scatters in one pass while the records they write stay near L2 size (outdoor, 136 MB:
+        // 0.387 -> 0.377 ms); above, two passes (scale, 340 MB: the fused pass 17 us slower)
+        const double col_bytes = (double)m->n_col * (sizeof(CRec) + sizeof(CMat) + sizeof(CSrc));
+        const double gain_bytes = (double)m->n_gain * (sizeof(GRec) + sizeof(int));
+        const bool scatter_gain = (double)m->n_gain * sizeof(GRec) <= kScatterMaxBytes;
+        if (scatter_gain && gain_bytes + col_bytes <= kScatterBothMaxBytes) {
+            note_launch(), k_scatter_both<<<nb, 256, 0, st>>>(n, means, w, quats, scales, gkey, grank, gstartB,
                                                               m->grec + m->n_gain_pad, m->gidx, RTG_VARIANT_XI,
-                                                              m->cls, tsum, ntl, gg.nx);
+                                                              m->cls, tsum, ntl, gg.nx, ckey, crank, m->cstart, rb,
+                                                              gq, m->crec, m->cmat, m->csrc);
+        } else if (scatter_gain) {
+            note_launch(), k_scatter_both<<<nb, 256, 0, st>>>(n, means, w, quats, scales, gkey, grank, gstartB,
+                                                              m->grec + m->n_gain_pad, m->gidx, RTG_VARIANT_XI,
+                                                              m->cls, tsum, ntl, gg.nx, ckey, nullptr, m->cstart,
+                                                              rb, gq, m->crec, m->cmat, m->csrc);
+            note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq,
+                                                             m->crec, m->cmat, m->csrc);
         } else {
             GRec* rec = nullptr;
             DevFreeGuard g_rec{(void**)&rec, st};
@@ -1111,9 +1139,9 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
             note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gstartB, m->gidx, rec, tsum, ntl, gg.nx);
             const unsigned fb = nblocks(m->n_gain, 256) > 8192 ? 8192 : nblocks(m->n_gain, 256);
             note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, m->gidx, rec, m->grec + m->n_gain_pad);
+            note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq,
+                                                             m->crec, m->cmat, m->csrc);
         }
-        note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq, m->crec,
-                                                         m->cmat, m->csrc);
     }
     if (m->n_gain_pad > m->n_gain) {
         note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
