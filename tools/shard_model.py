@@ -56,6 +56,8 @@ def main():
         outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
                 torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
 
+        prof_on = [False]
+
         def step():
             m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
                       options=opts)
@@ -63,12 +65,20 @@ def main():
                 vstream.wait_stream(st)   # views: the map build only, then concurrent (as bench.py)
             tr = R.Traj.wrap(*traj)
             R.score(m, tr, cam, params, *outs)
-            if views is not None:
+            if views is not None:   # (phase timers on the trajectories' stream only, as bench.py)
+                if prof_on[0]:
+                    R.profile_enable(False)
                 tv = R.Traj.wrap(*views)
                 fc, fe, g, u = R.score(m, tv, cam, vparams, stream=vstream)
+                if prof_on[0]:
+                    R.profile_enable(True)
             r = R.best(outs[3])
             if views is not None:
+                if prof_on[0]:
+                    R.profile_enable(False)
                 R.best(u, stream=vstream)
+                if prof_on[0]:
+                    R.profile_enable(True)
                 st.wait_stream(vstream)
                 tv.close()
             tr.close()
@@ -80,6 +90,7 @@ def main():
         ms = []
         R.profile_read(reset=True)
         R.profile_enable(True)
+        prof_on[0] = True
         for _ in range(args.steps):
             flush.fill_(1.0)
             torch.cuda.synchronize()
@@ -90,6 +101,7 @@ def main():
             torch.cuda.synchronize()
             ms.append(a.elapsed_time(b))
         R.profile_enable(False)
+        prof_on[0] = False
         prof = R.profile_read(reset=True)
         med = statistics.median(ms)
         base = med if base is None else base
