@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--mode", default="culled", choices=["culled", "dense"])
     ap.add_argument("--stride", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay of the scoring part")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=-1, help="steps timed per phase (default: all)")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
@@ -351,6 +352,44 @@ def main():
         e2e = {"value": pairs / (ms_e2e / 1000.0), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 16 + 68}
 
+    # ---- the scoring part of the cycle (rtg_score + rtg_best_async on a built map) eager vs one CUDA-graph
+    # replay (R.ScoreGraph): the launch gaps a graph removes.  The map build cannot be captured (it reads
+    # the validated bounds back to size its grids), so it is outside both.
+    graph = None
+    if args.mode == "culled" and not args.no_graph:
+        m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
+                  device=local_dev, options=map_opts)
+        tr = R.Traj.wrap(*dtraj, device=local_dev)
+        g = R.ScoreGraph(m, tr, cam, params)
+        bo = torch.empty(2, dtype=torch.float64, device=dev)
+
+        def eager():
+            R.score(m, tr, cam, params, *outs)
+            R.best_async(outs[3], bo)
+
+        def t_of(fn):
+            for _ in range(args.warmup):
+                fn()
+            vals = []
+            for _ in range(args.steps):
+                flush.fill_(1.0)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                vals.append(a.elapsed_time(b))
+            return statistics.median(vals)
+
+        ms_eager, ms_graph = t_of(eager), t_of(g.replay)
+        assert R.read_best(bo) == R.read_best(g.best)
+        graph = {"scope": "rtg_score + rtg_best_async on a built map (the cycle minus the map build)",
+                 "eager_ms_median": ms_eager, "graph_ms_median": ms_graph}
+        del g
+        tr.close()
+        m.close()
+
     # ---- roofline of the dominant phase
     phase_ms = {k: v / nprof for k, v in prof["ms"].items()}
     dom = max(("collision", "visibility_gain", "map_build"), key=lambda k: phase_ms[k])
@@ -408,7 +447,8 @@ def main():
                 # SURVEY §8(d) metric 2, "executed": pairs actually tested one by one (visibility tests
                 # of the info waypoints + collision candidates), from the debug counters of a sample
                 **({"executed_pair_tests_per_s": executed_rate} if executed_rate is not None else {}),
-                "clocks": clock, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
+                "clocks": clock, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                **({"cuda_graph": graph} if graph is not None else {})}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -23,6 +23,11 @@
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is
  *    enqueued on it.  Only rtg_map_create (sizes its grids from the data),
  *    rtg_best (returns a host result) and rtg_score_debug synchronise it.
+ *  - CUDA graphs: rtg_score in RTG_MODE_CULLED (when it does not reclassify)
+ *    and rtg_best_async enqueue device work only (kernels, memsets and
+ *    stream-ordered allocations freed within the call), so a capturing stream
+ *    records them; the graph keeps the handles' device pointers, so a replay
+ *    scores whatever the trajectory buffers then hold against the same map.
  *  - Handles own their device memory until *_destroy.  Handles are not
  *    thread-safe; distinct handles on distinct streams are.
  *  - A CUDA error inside a call returns RTG_ERR_CUDA; if the error is sticky
@@ -253,6 +258,14 @@ rtg_status rtg_score(rtg_map map, rtg_traj traj, const rtg_camera* cam, const rt
  */
 rtg_status rtg_best(const double* utility, int K, long long index_base, void* stream,
                     rtg_best_result* out);
+
+/*
+ * rtg_best_async -- rtg_best without the host result: the same argmax written to
+ * out_device (one rtg_best_result in caller-owned, 8-byte aligned DEVICE memory; index -1
+ * and score -inf when nothing is feasible).  Does not synchronise (capturable).
+ */
+rtg_status rtg_best_async(const double* utility, int K, long long index_base, rtg_best_result* out_device,
+                          void* stream);
 
 /*
  * rtg_score_debug -- parity/debug: per-waypoint outputs for EVERY waypoint (no early exit,

@@ -102,6 +102,7 @@ cudaError_t launch_start_setup(const float pose[4], StartState* st_dev, cudaStre
 cudaError_t launch_debug_wp(long long n, const long long* wp_gq, const ClassState* cs, double* out, cudaStream_t st);
 cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaStream_t st);
 cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st);
+cudaError_t launch_set_cam64(const rtg_camera& c, double* dst, cudaStream_t st);
 cudaError_t launch_sampler_di(int K, int T, double dt, const float* start, const float* v0, const float* ax,
                               const float* ay, rtg_traj_s* tr, cudaStream_t st);
 cudaError_t launch_sampler(int K, int T, double dt, const float* start, const float* v, const float* om,
@@ -585,9 +586,9 @@ static cudaError_t scratch_alloc(Scratch& s, long long K, long long T, long long
     s.cam64 = (double*)(b + o_cam);
     s.ranked = (int*)(b + o_ranked);
     s.start = (StartState*)(b + o_start);
-    // the FP64 camera (8 doubles) for the re-decision branch: pageable copy, stream-ordered
-    double c64[8] = {(double)cam->width, (double)cam->height, cam->fx, cam->fy, cam->cx, cam->cy, cam->z_near, cam->z_far};
-    cudaError_t e2 = cudaMemcpyAsync(s.cam64, c64, sizeof(c64), cudaMemcpyHostToDevice, st);
+    // the FP64 camera (8 doubles) for the re-decision branch (a kernel parameter, not a host copy:
+    // rtg_score enqueues device work only and can be captured into a CUDA graph)
+    cudaError_t e2 = launch_set_cam64(*cam, s.cam64, st);
     if (e2 != cudaSuccess) return e2;
     return cudaMemsetAsync(b + o_ints, 0, o_stats + al(sizeof(unsigned long long) * RTG_DEBUG_STATS) - o_ints, st);
 }
@@ -696,6 +697,17 @@ rtg_status rtg_best(const double* utility, int K, long long index_base, void* st
         set_error("rtg_best: no feasible trajectory");
         return RTG_ERR_NO_FEASIBLE;
     }
+    return RTG_OK;
+}
+
+rtg_status rtg_best_async(const double* utility, int K, long long index_base, rtg_best_result* out_device,
+                          void* stream) {
+    if (!out_device || ((uintptr_t)out_device & 7u)) return invalid("out_device must be an 8-byte aligned device pointer");
+    if (!utility || K < 1) return invalid("utility must be a device array of K >= 1 values");
+    cudaStream_t st = (cudaStream_t)stream;
+    prof_begin(PH_BEST, st);
+    API_CK(launch_best(utility, K, index_base, out_device, st), nullptr);
+    prof_end(PH_BEST, st);
     return RTG_OK;
 }
 

@@ -708,6 +708,19 @@ cudaError_t launch_pair_mask(rtg_map_s* m, rtg_traj_s* tr, unsigned* mask, cudaS
     return cudaGetLastError();
 }
 
+// the FP64 camera for the re-decision branch, written by a kernel (its values travel as launch
+// parameters, so rtg_score stays capturable in a CUDA graph: no pageable host copy)
+struct Cam64Args { double v[8]; };
+__global__ void k_set_cam64(Cam64Args a, double* __restrict__ dst) {
+    if (threadIdx.x < 8) dst[threadIdx.x] = a.v[threadIdx.x];
+}
+
+cudaError_t launch_set_cam64(const rtg_camera& c, double* dst, cudaStream_t st) {
+    const Cam64Args a{{(double)c.width, (double)c.height, c.fx, c.fy, c.cx, c.cy, c.z_near, c.z_far}};
+    note_launch(), k_set_cam64<<<1, 32, 0, st>>>(a, dst);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_best(const double* u, int K, long long base, void* out_dev, cudaStream_t st) {
     note_launch(), k_best<<<1, 1024, 0, st>>>(u, K, base, (BestDev*)out_dev);
     return cudaGetLastError();

@@ -112,6 +112,7 @@ _SIGS = {
     "rtg_traj_destroy": (_S, [_P]),
     "rtg_score": (_S, [_P, _P, ctypes.POINTER(Camera), ctypes.POINTER(ScoreParams), _P, _P, _P, _P, _P]),
     "rtg_best": (_S, [_P, _I, _LL, _P, ctypes.POINTER(BestResult)]),
+    "rtg_best_async": (_S, [_P, _I, _LL, _P, _P]),
     "rtg_score_debug": (_S, [_P, _P, ctypes.POINTER(Camera), ctypes.POINTER(ScoreParams), _P, _P, _P, _P, _P,
                              _P, _P]),
     "rtg_ledger_update": (_S, [_I, _LL, _I, _P, _P, _P, _P, _P]),
@@ -438,6 +439,59 @@ def best(utility, index_base: int = 0, stream=None):
     _check(_lib.rtg_best(p, int(utility.numel()), int(index_base), _stream(stream), ctypes.byref(out)),
            "rtg_best", allow=(ERR_NO_FEASIBLE,))
     return out.score, out.index
+
+
+def best_async(utility, out, index_base: int = 0, stream=None):
+    """rtg_best_async: the argmax written into `out` (a CUDA float64 tensor of 2 elements holding one
+    rtg_best_result: score, then the index's int64 bits); no synchronisation (capturable)."""
+    if len(utility.shape) != 1:
+        raise ValueError("utility: expected [K]")
+    p = _arg("utility", utility, "float64", cuda=True)
+    o = _arg("out", out, "float64", (2,), cuda=True)
+    _check(_lib.rtg_best_async(p, int(utility.numel()), int(index_base), o, _stream(stream)), "rtg_best_async")
+    return out
+
+
+def read_best(out):
+    """(score, index) from a best_async result tensor (synchronises through the copy)."""
+    h = out.detach().cpu()
+    return float(h[0]), int(h.view(_torch().int64)[1])
+
+
+class ScoreGraph:
+    """rtg_score (culled mode) + rtg_best_async on one map and one trajectory handle, captured once into a
+    CUDA graph (torch.cuda.CUDAGraph) and replayed.  The graph keeps the handles' device pointers: a replay
+    scores what the trajectory buffers then hold (refill them in place, e.g. through Traj.wrap) against
+    the same map.  The capture is preceded by one eager call (a reclassification, if the params ask for
+    one, happens there, outside the graph)."""
+
+    def __init__(self, m: Map, tr: Traj, camera, params: ScoreParams, index_base: int = 0):
+        torch = _torch()
+        if params.mode != MODE_CULLED:
+            raise ValueError("ScoreGraph: culled mode only (dense mode reads the list length on the host)")
+        dev = torch.device("cuda", m.device)
+        K = tr.K
+        self.outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
+                     torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
+        self.best = torch.empty(2, dtype=torch.float64, device=dev)
+        self._keep = (m, tr)   # the graph holds their device pointers
+        cam = camera if isinstance(camera, Camera) else make_camera(camera)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            score(m, tr, cam, params, *self.outs)
+            best_async(self.outs[3], self.best, index_base)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            score(m, tr, cam, params, *self.outs)
+            best_async(self.outs[3], self.best, index_base)
+
+    def replay(self):
+        """Enqueue one replay on the current stream; returns (first_col, feasible, gain, utility, best)."""
+        self.graph.replay()
+        return self.outs + (self.best,)
 
 
 def ledger_update(mu_prev, mu_cur, w_prev, w_out=None, device=0, stream=None):

@@ -68,6 +68,12 @@ def test_invalid_arguments_rejected_before_any_launch(rtg):
     out = rtg.BestResult()
     assert lib.rtg_best(None, 0, 0, None, ctypes.byref(out)) == rtg.ERR_INVALID_ARGUMENT
     assert out.index == -1
+    # best_async: NULL / misaligned result pointer, NULL utility, K < 1 (checked before any launch)
+    buf = (ctypes.c_double * 4)()
+    assert lib.rtg_best_async(buf, 1, 0, None, None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_best_async(buf, 1, 0, ctypes.c_void_p(ctypes.addressof(buf) + 4), None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_best_async(None, 1, 0, buf, None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_best_async(buf, 0, 0, buf, None) == rtg.ERR_INVALID_ARGUMENT
     # score with NULL handles
     cam = rtg.Camera(64, 48, 50, 50, 32, 24, 0.1, 5.0)
     par = rtg.make_params()

@@ -813,3 +813,38 @@ np.save(sys.argv[1], np.concatenate(res))
         res[flag] = np.load(f)
         os.unlink(f)
     assert np.array_equal(res["tiles"], res["scan"])
+
+
+@pytest.mark.gpu
+def test_score_graph_replay_equals_eager(R, room):
+    """rtg_score (culled) + rtg_best_async captured into one CUDA graph (R.ScoreGraph): every replay equals
+    the eager calls bit for bit, also after the borrowed waypoint buffers are refilled in place (the
+    graph keeps the handles' device pointers), and best_async equals rtg_best."""
+    import torch
+    dev = torch.device("cuda", 0)
+    k = np.arange(0, room.K, 3)
+    m = R.map_from_workload(room)
+    bufs = [torch.from_numpy(np.ascontiguousarray(a[k])).to(dev) for a in (room.x, room.y, room.z, room.yaw)]
+    tr = R.Traj.wrap(*bufs)
+    p = R.make_params()
+    g = R.ScoreGraph(m, tr, room.camera, p)
+    rng = np.random.default_rng(5)
+    for it in range(3):
+        if it:   # new waypoints in the same buffers: shuffled trajectories of the workload
+            perm = rng.permutation(room.K)[:len(k)]
+            for b, a in zip(bufs, (room.x, room.y, room.z, room.yaw)):
+                b.copy_(torch.from_numpy(np.ascontiguousarray(a[perm])))
+        outs = g.replay()
+        torch.cuda.synchronize()
+        eager = R.score(m, tr, room.camera, p)
+        for a, b in zip(outs[:4], eager):
+            assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+        s, i = R.best(eager[3])
+        assert R.read_best(outs[4]) == (s, i)
+        bo = torch.empty(2, dtype=torch.float64, device=dev)
+        R.best_async(eager[3], bo)
+        assert R.read_best(bo) == (s, i)
+    assert (eager[1] == 1).any()
+    del g
+    tr.close()
+    m.close()

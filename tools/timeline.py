@@ -1,7 +1,7 @@
 """GPU timeline of one outdoor planning cycle (torch.profiler / CUPTI kernel activity): every kernel
 and memcpy/memset with its start offset and duration, and the idle gaps between them.
 
-usage: python tools/timeline.py [--config outdoor] [--tree]
+usage: python tools/timeline.py [--config outdoor] [--tree | --score eager|graph]
   --tree: one rtg_plan_tree call (depth 8, beam 4096, goal 5 m ahead) on the config's map instead
 """
 import argparse
@@ -20,6 +20,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="outdoor")
     ap.add_argument("--tree", action="store_true")
+    ap.add_argument("--score", choices=("eager", "graph"), default=None,
+                    help="only the scoring part (rtg_score + rtg_best_async) on a built map, eager or as one "
+                         "CUDA-graph replay (R.ScoreGraph)")
     args = ap.parse_args()
     wl = W.make(args.config)
     dev = torch.device("cuda", 0)
@@ -40,9 +43,22 @@ def main():
         t2, _, _, _ = R.plan_tree(tree_map, (0.0, 0.0, 0.0), (5.0, 0.0), tp)
         t2.close()
 
+    score_map = score_tr = sg = None
+    if args.score:
+        score_map = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
+        score_tr = R.Traj.wrap(*dtraj)
+        bo = torch.empty(2, dtype=torch.float64, device=dev)
+        if args.score == "graph":
+            sg = R.ScoreGraph(score_map, score_tr, cam, params)
+
     def step():
         if args.tree:
             return tree_step()
+        if sg is not None:
+            return sg.replay()
+        if args.score:
+            R.score(score_map, score_tr, cam, params, *outs)
+            return R.best_async(outs[3], bo)
         m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
         tr = R.Traj.upload(*dtraj)
         R.score(m, tr, cam, params, *outs)
@@ -62,7 +78,7 @@ def main():
             torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     ev.sort(key=lambda e: e.time_range.start)
-    first = "k_tree_init" if args.tree else "k_bounds_init"
+    first = "k_tree_init" if args.tree else ("k_set_cam64" if args.score else "k_bounds_init")
     starts = [i for i, e in enumerate(ev) if first in e.name]
     ev = ev[starts[-1]:]
     t0 = ev[0].time_range.start
