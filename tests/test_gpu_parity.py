@@ -848,3 +848,43 @@ def test_score_graph_replay_equals_eager(R, room):
     del g
     tr.close()
     m.close()
+
+
+def test_max_size_inside_run_beyond_2p24_records(R):
+    """Maximum sizes: 2^24 + 2^20 gain-eligible Gaussians in ONE row and ONE z-cell of the visibility grid,
+    all inside the frustum of the waypoints and all of class H (caller thresholds tau_hi = -1, tau_lo = -2,
+    weights near 1), so the fully inside x-run holds more H records (2^24) and more fixed-point weight
+    (2^48) than the packed table's modular prefixes resolve.  The map selects the guarded
+    kernel variant by itself (it has >= 2^24 gain-eligible Gaussians), which tests such runs record by
+    record: culled must equal dense bit for bit, and both the oracle."""
+    n = (1 << 24) + (1 << 20)
+    rng = np.random.default_rng(21)
+    means = np.empty((3, n), np.float32)
+    means[0] = rng.uniform(2.0, 12.0, n)      # 2..12 m ahead of the cameras at x <= 0.5
+    means[1] = rng.uniform(0.0, 0.28, n)      # one row (hy = 0.3 from the lowest y)
+    means[2] = rng.uniform(0.0, 1.4, n)       # one z-cell (hz = 1.5 from the lowest z)
+    quats = np.zeros((4, n), np.float32)
+    quats[0] = 1.0
+    scales = np.full((3, n), 0.01, np.float32)
+    w = rng.uniform(0.9, 1.0, n).astype(np.float32)
+    flags = np.full(n, 1, np.uint8)           # NO_COLLIDE: the gain path only
+    cam = W.Camera(640, 480, 500.0, 500.0, 320.0, 240.0, 0.2, 15.0)
+    K, T = 2, 3
+    px = np.array([[0.0, 0.25, 0.5], [-0.5, 0.0, 0.5]], np.float32)
+    py = np.full((K, T), 0.14, np.float32)
+    pz = np.full((K, T), 0.7, np.float32)
+    yaw = np.array([[0.0, 0.0, 0.0], [0.01, -0.01, 0.0]], np.float32)
+    wl = W.Workload("max_run", means, quats, scales, np.ones(n, np.float32), w, flags, px, py, pz, yaw,
+                    W.Robot(0.2, 1.0), cam, 0.1)
+    tau = (-1.0, -2.0)
+    out = {mode: gpu_run(R, wl, mode, tau=tau) for mode in MODES}
+    assert out["culled"]["info"].n_gain == n
+    for k in ("wp_nh", "wp_nl", "wp_col", "first_col"):
+        assert np.array_equal(out["dense"][k], out["culled"][k]), k
+    assert np.array_equal(out["dense"]["wp_gain"].view(np.int64), out["culled"]["wp_gain"].view(np.int64))
+    nh = out["culled"]["wp_nh"]
+    assert nh.max() >= (1 << 24) and np.all(out["culled"]["wp_nl"] == 0)
+    assert out["culled"]["stats"]["tested"] >= (1 << 24)   # the long run was tested record by record
+    orc = O.score(wl, tau_hi=tau[0], tau_lo=tau[1])
+    check_waypoints(out["culled"], orc, out["culled"]["info"].fixed_point_shift)
+    check_trajectories(out["culled"], orc, T)
