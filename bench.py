@@ -387,8 +387,32 @@ def main():
         graph = {"scope": "rtg_score + rtg_best_async on a built map (the cycle minus the map build)",
                  "eager_ms_median": ms_eager, "graph_ms_median": ms_graph}
         del g
-        tr.close()
         m.close()
+        # the whole cycle on a layout map (grids from the workload's extents, rebuilt without a host
+        # synchronisation): eager, and captured with the score and the argmax into one graph
+        gbox, cbox, rb_b, rho_b = layout_bounds(wl)
+        lm = R.LayoutMap(N, gbox, cbox, rb_b, rho_b, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g,
+                         collide_rule=wl.robot.rule, device=local_dev, options=map_opts)
+
+        def eager_cycle():
+            lm.rebuild(*dmap)
+            R.score(lm, tr, cam, params, *outs)
+            R.best_async(outs[3], bo)
+
+        cg = R.CycleGraph(lm, dmap, tr, cam, params)
+        ms_ce, ms_cg = t_of(eager_cycle), t_of(cg.replay)
+        lm.check()
+        assert R.read_best(bo) == R.read_best(cg.best)
+        if world == 1:
+            assert R.read_best(cg.best) == (res[0], res[1])
+        graph["cycle"] = {"scope": "layout-map rebuild + rtg_score + rtg_best_async: the whole planning cycle "
+                                   "without a host synchronisation (rtg_map_create_layout, grids from the "
+                                   "workload's extents)",
+                          "eager_ms_median": ms_ce, "graph_ms_median": ms_cg,
+                          "standard_cycle_ms_median": step_stats["median"]}
+        del cg
+        tr.close()
+        lm.close()
 
     # ---- roofline of the dominant phase
     phase_ms = {k: v / nprof for k, v in prof["ms"].items()}
@@ -453,6 +477,26 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def layout_bounds(wl, margin=0.05):
+    """A layout for rtg_map_create_layout from the workload's extents (what a robot knows of its map):
+    boxes around the gain-eligible and collidable means, bounds on the largest collision semi-axis
+    a = lambda_g s + r_robot and its anisotropy, with margins."""
+    import numpy as np
+    f = wl.flags if wl.flags is not None else np.zeros(wl.N, np.uint8)
+    gain, col = (f & 2) == 0, (f & 1) == 0
+    m = wl.means.astype(np.float64)
+
+    def box(sel):
+        if not sel.any():
+            return [0.0] * 3, [1.0] * 3
+        return (m[:, sel].min(1) - margin).tolist(), (m[:, sel].max(1) + margin).tolist()
+
+    a = wl.robot.lambda_g * wl.scales[:, col].astype(np.float64) + wl.robot.r_robot
+    rb = float(a.max()) * 1.01 + 1e-3 if col.any() else 1.0
+    rho = float((a.max(0) / a.min(0)).max()) * 1.01 if col.any() else 1.0
+    return box(gain), box(col), rb, rho
 
 
 # Algorithmic work per unit, SURVEY §8(d) (SURVEY.md:709, [A5]): ~10 lane-instructions per individually

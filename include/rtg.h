@@ -23,11 +23,12 @@
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is
  *    enqueued on it.  Only rtg_map_create (sizes its grids from the data),
  *    rtg_best (returns a host result) and rtg_score_debug synchronise it.
- *  - CUDA graphs: rtg_score in RTG_MODE_CULLED (when it does not reclassify)
- *    and rtg_best_async enqueue device work only (kernels, memsets and
- *    stream-ordered allocations freed within the call), so a capturing stream
- *    records them; the graph keeps the handles' device pointers, so a replay
- *    scores whatever the trajectory buffers then hold against the same map.
+ *  - CUDA graphs: rtg_map_rebuild (layout maps), rtg_score in RTG_MODE_CULLED
+ *    (when it does not reclassify) and rtg_best_async enqueue device work only
+ *    (kernels, memsets and stream-ordered allocations freed within the call),
+ *    so a capturing stream records the whole planning cycle; the graph keeps
+ *    the handles' and arrays' device pointers, so a replay rebuilds from and
+ *    scores whatever those buffers then hold.
  *  - Handles own their device memory until *_destroy.  Handles are not
  *    thread-safe; distinct handles on distinct streams are.
  *  - A CUDA error inside a call returns RTG_ERR_CUDA; if the error is sticky
@@ -180,6 +181,44 @@ rtg_status rtg_map_create_ex(int device, long long n, rtg_mem kind,
                              const rtg_robot* robot, const rtg_map_options* opts,
                              void* stream, rtg_map* out);
 rtg_status rtg_map_destroy(rtg_map map);
+
+/*
+ * Layout maps: a map whose grids and capacity are fixed at creation from caller bounds, rebuilt
+ * from new data with device work only -- no host synchronisation, so a CUDA graph can capture
+ * rtg_map_rebuild + rtg_score + rtg_best_async (the whole planning cycle) and replay it.
+ * The grids cover the layout boxes (cell sizes as rtg_map_options); rb_max and rho_max set the
+ * collision search radius and the FP32 guard (larger bounds cost time, not correctness).  Scores of
+ * a rebuilt map equal those of rtg_map_create on the same data (decisions and exact sums do not
+ * depend on the grid).
+ */
+typedef struct {
+    long long capacity;  /* most Gaussians a rebuild may hold, 1 <= capacity < 2^30 - 4096      */
+    float gain_lo[3];    /* box holding every gain-eligible mean of every rebuild (world, m)   */
+    float gain_hi[3];
+    float col_lo[3];     /* box holding every collidable mean                                   */
+    float col_hi[3];
+    float rb_max;        /* bound on a collidable Gaussian's largest semi-axis a = lambda_g s + r_robot */
+    float rho_max;       /* bound on its a_max / a_min (>= 1)                                    */
+} rtg_map_layout;
+
+/* Allocates a layout map on `device` (an empty map until the first rebuild).  Synchronous
+ * allocation; RTG_ERR_INVALID_ARGUMENT for non-finite or empty boxes, bounds out of range. */
+rtg_status rtg_map_create_layout(int device, const rtg_map_layout* layout, const rtg_robot* robot,
+                                 const rtg_map_options* opts, void* stream, rtg_map* out);
+
+/* Rebuilds a layout map from n <= capacity Gaussians (DEVICE arrays as rtg_map_create's, read in
+ * place; flags may be NULL) with the default classification.  Enqueues device work only
+ * (capturable).  The validation of rtg_map_create plus the layout (means inside the boxes, radius and
+ * anisotropy within the bounds) is recorded on the device: rtg_map_check reports it.  A rebuild
+ * whose data breaks the layout gives undefined scores (memory-safe: cells clamp). */
+rtg_status rtg_map_rebuild(rtg_map map, long long n, const float* means, const float* quats,
+                           const float* scales, const float* opacity, const float* info_w,
+                           const unsigned char* flags, void* stream);
+
+/* Synchronises `stream` and returns RTG_ERR_INVALID_ARGUMENT (detail in rtg_last_error) if the last
+ * rebuild's data was invalid or broke the layout; RTG_OK otherwise (always for rtg_map_create maps).
+ * Afterwards rtg_map_info reports the rebuild's record counts. */
+rtg_status rtg_map_check(rtg_map map, void* stream);
 rtg_status rtg_map_info(rtg_map map, rtg_map_info_t* out);
 
 /*

@@ -84,6 +84,10 @@ void dev_free(void* p, cudaStream_t st) {
 
 
 // defined in rtg_map.cu / rtg_score.cu
+rtg_status create_layout_map(rtg_map_s* m, const rtg_map_layout* L, const rtg_map_options* opt, cudaStream_t st);
+rtg_status rebuild_map(rtg_map_s* m, long long n, const float* means, const float* quats, const float* scales,
+                       const float* opacity, const float* w, const unsigned char* flags, cudaStream_t st);
+rtg_status check_layout_map(rtg_map_s* m, cudaStream_t st);
 rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const float* scales, const float* opacity,
                      const float* w, const unsigned char* flags, const rtg_map_options* opt, cudaStream_t st);
 CamK make_cam(const rtg_camera& c, const double* cam64_dev);
@@ -323,6 +327,84 @@ rtg_status rtg_map_create(int device, long long n, rtg_mem kind, const float* me
                              out);
 }
 
+static rtg_status check_robot_opts(const rtg_robot* robot, const rtg_map_options* opts) {
+    if (!robot) return invalid("robot is NULL");
+    if (!(robot->r_robot >= 0) || !finite_f(robot->r_robot)) return invalid("r_robot must be finite and >= 0");
+    if (!(robot->lambda_g > 0) || !finite_f(robot->lambda_g)) return invalid("lambda_g must be finite and > 0");
+    if (robot->collide_rule != RTG_COLLIDE_ELLIPSOID && robot->collide_rule != RTG_COLLIDE_PRINCIPAL_AXIS)
+        return invalid("unknown collide_rule");
+    if (opts && (!std::isfinite(opts->gain_cell_xy) || !std::isfinite(opts->gain_cell_z) || !std::isfinite(opts->col_cell) ||
+                 !std::isfinite(opts->gain_cell_x)))
+        return invalid("grid options must be finite");
+    return RTG_OK;
+}
+
+rtg_status rtg_map_create_layout(int device, const rtg_map_layout* layout, const rtg_robot* robot,
+                                 const rtg_map_options* opts, void* stream, rtg_map* out) {
+    if (!out) return invalid("out is NULL");
+    *out = nullptr;
+    if (!layout) return invalid("layout is NULL");
+    const rtg_map_layout& L = *layout;
+    if (L.capacity < 1 || L.capacity >= (1LL << 30) - 4096) return invalid("capacity must satisfy 1 <= capacity < 2^30 - 4096");
+    for (int d = 0; d < 3; ++d)
+        if (!finite_f(L.gain_lo[d]) || !finite_f(L.gain_hi[d]) || !(L.gain_lo[d] <= L.gain_hi[d]) ||
+            !finite_f(L.col_lo[d]) || !finite_f(L.col_hi[d]) || !(L.col_lo[d] <= L.col_hi[d]))
+            return invalid("layout boxes must be finite with lo <= hi");
+    if (!(L.rb_max > 0) || !finite_f(L.rb_max)) return invalid("layout rb_max must be finite and > 0");
+    if (!(L.rho_max >= 1) || !finite_f(L.rho_max)) return invalid("layout rho_max must be finite and >= 1");
+    rtg_status s = check_robot_opts(robot, opts);
+    if (s != RTG_OK) return s;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return invalid("invalid device ordinal (no CUDA device?)");
+    }
+    API_CK(cudaSetDevice(device), nullptr);
+    ensure_pool(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    rtg_map_s* m = new (std::nothrow) rtg_map_s();
+    if (!m) return RTG_ERR_OUT_OF_MEMORY;
+    m->device = device;
+    m->stream = st;
+    m->robot = *robot;
+    s = create_layout_map(m, layout, opts, st);
+    cudaError_t e = s == RTG_OK ? cudaGetLastError() : cudaSuccess;
+    if (s == RTG_OK && e != cudaSuccess) s = cuda_fail(e, "rtg_map_create_layout", nullptr);
+    if (s != RTG_OK) {
+        for (void* p : m->allocs) dev_free(p, st);
+        delete m;
+        return s;
+    }
+    *out = m;
+    return RTG_OK;
+}
+
+rtg_status rtg_map_rebuild(rtg_map m, long long n, const float* means, const float* quats, const float* scales,
+                           const float* opacity, const float* info_w, const unsigned char* flags, void* stream) {
+    rtg_status s = check_map(m);
+    if (s != RTG_OK) return s;
+    if (!m->layout) return invalid("rtg_map_rebuild needs a map from rtg_map_create_layout");
+    if (n < 0 || n > m->cap) return invalid("n must satisfy 0 <= n <= the layout's capacity");
+    if (n > 0 && (!means || !quats || !scales || !info_w)) return invalid("means, quats, scales and info_w are required");
+    API_CK(cudaSetDevice(m->device), nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    prof_begin(PH_MAP, st);
+    s = rebuild_map(m, n, means, quats, scales, opacity, info_w, flags, st);
+    prof_end(PH_MAP, st);
+    if (s != RTG_OK) return s;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "rtg_map_rebuild", &m->poisoned);
+    return RTG_OK;
+}
+
+rtg_status rtg_map_check(rtg_map m, void* stream) {
+    rtg_status s = check_map(m);
+    if (s != RTG_OK) return s;
+    if (!m->layout) return RTG_OK;   // rtg_map_create validated its data before returning
+    API_CK(cudaSetDevice(m->device), nullptr);
+    return check_layout_map(m, (cudaStream_t)stream);
+}
+
 rtg_status rtg_map_destroy(rtg_map m) {
     if (!m) return invalid("map handle is NULL");
     cudaSetDevice(m->device);
@@ -336,6 +418,10 @@ rtg_status rtg_map_info(rtg_map m, rtg_map_info_t* out) {
     if (s != RTG_OK) return s;
     if (!out) return invalid("out is NULL");
     cudaSetDevice(m->device);
+    if (m->layout) {   // the counts of the last rebuild (and its validation)
+        s = check_layout_map(m, m->stream);
+        if (s != RTG_OK) return s;
+    }
     ClassState cs;
     cudaError_t e = cudaMemcpyAsync(&cs, m->cls, sizeof(cs), cudaMemcpyDeviceToHost, m->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);

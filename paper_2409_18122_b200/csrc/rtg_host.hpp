@@ -127,6 +127,14 @@ struct rtg_map_s {
     rtg::ColGrid cg{};
     float rb_max = 0.f;
     float gq = 0.f;                      // FP32 collision guard
+    double gq64 = 0.0;                   // (the same before rounding: the collision records' radius margin)
+    // layout maps (rtg_map_create_layout): grids and capacity fixed at creation, rebuilt from new data
+    // without a host synchronisation (rtg_map_rebuild); n_gain / n_col then hold the capacity until
+    // rtg_map_check reads the counts of the last rebuild, which stay on the device with its validation
+    bool layout = false;
+    long long cap = 0;
+    rtg_map_layout lay{};
+    void* dbounds = nullptr;             // device: validation flags, counts and bounds of the last rebuild
     // classification
     rtg::ClassState* cls = nullptr;      // device
     double* red_scratch = nullptr;       // device partials for the FP64 reductions

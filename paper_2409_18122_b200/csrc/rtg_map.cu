@@ -208,6 +208,24 @@ __global__ void k_bounds(long long n, const float* __restrict__ means, const flo
 
 // cell of coordinate v on a grid with origin o and inverse cell size ih (FP64; the culled kernels
 // allow for eps around the cell boundaries, so ih may be rounded)
+// layout maps: the rebuild's data must lie inside the caller's boxes and bounds (the grids were fixed by
+// them), else the map is flagged (rtg_map_check): 32 gain-eligible mean outside, 64 collidable mean
+// outside, 128 a_max above rb_max, 256 a_max / a_min above rho_max
+__global__ void k_layout_check(DevBounds* __restrict__ b, rtg_map_layout L) {
+    if (threadIdx.x != 0) return;
+    int err = 0;
+    if (b->n_gain > 0)
+        for (int d = 0; d < 3; ++d)
+            if (b->gmin[d] < f2o(L.gain_lo[d]) || b->gmax[d] > f2o(L.gain_hi[d])) err |= 32;
+    if (b->n_col > 0) {
+        for (int d = 0; d < 3; ++d)
+            if (b->cmin[d] < f2o(L.col_lo[d]) || b->cmax[d] > f2o(L.col_hi[d])) err |= 64;
+        if (b->rbmax > f2o(L.rb_max)) err |= 128;
+        if (b->rhomax > f2o(L.rho_max)) err |= 256;
+    }
+    b->err |= err;
+}
+
 __device__ __forceinline__ int cell_coord(float v, double o, double ih, int nmax) {
     int c = (int)floor(((double)v - o) * ih);
     return c < 0 ? 0 : (c >= nmax ? nmax - 1 : c);
@@ -312,9 +330,10 @@ __global__ void k_perm_gain(long long n, const int* __restrict__ gkey, const int
     }
 }
 
-__global__ void k_fill_gain(long long n_gain, const int* __restrict__ gidx, const GRec* __restrict__ rec,
-                            GRec* __restrict__ grec) {
-    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n_gain;
+__global__ void k_fill_gain(long long n_gain, const int* __restrict__ dn_gain, const int* __restrict__ gidx,
+                            const GRec* __restrict__ rec, GRec* __restrict__ grec) {
+    const long long ng = dn_gain ? *dn_gain : n_gain;   // (a layout map: the device count)
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < ng;
          j += (long long)gridDim.x * blockDim.x)
         grec[j] = rec[gidx[j]];
 }
@@ -382,10 +401,10 @@ __global__ void k_scatter_both(long long n, const float* __restrict__ means, con
     }
 }
 
-// NaN padding of the records [from, to) (gidx: NULL for copy A)
-__global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to) {
+// NaN padding of the records [from, to) (gidx: NULL for copy A); dfrom: a device count raising from
+__global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to, const int* __restrict__ dfrom) {
     long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < to) {
+    if (i < to && (!dfrom || i >= *dfrom)) {
         const float nan = __int_as_float(0x7fc00000);
         grec[i] = GRec{nan, nan, nan, 0u};
         if (gidx) gidx[i] = -1;
@@ -424,9 +443,10 @@ __global__ void k_derive_cols(long long ncols, int nx, int nz, const int* __rest
     }
 }
 
-__global__ void k_pad_col(CRec* crec, CMat* cmat, CSrc* csrc, long long from, long long to) {
+__global__ void k_pad_col(CRec* crec, CMat* cmat, CSrc* csrc, long long from, long long to,
+                          const int* __restrict__ dfrom) {
     long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < to) {
+    if (i < to && (!dfrom || i >= *dfrom)) {
         float nan = __int_as_float(0x7fc00000);
         crec[i] = CRec{nan, nan, nan, -1.f};
         CMat z;
@@ -952,11 +972,105 @@ static void pick_dims(float lo, float hi, double h, int& n) {
 }
 
 // Builds everything of rtg_map_create from device-resident inputs.
+// grid geometry and the FP32 collision guard from bounds: the data's own (rtg_map_create) or a caller's
+// layout (rtg_map_create_layout); rho bounds a_max / a_min of the collidable Gaussians
+static void plan_grids(rtg_map_s* m, bool have_gain, const float glo[3], const float ghi[3], bool have_col,
+                       const float clo[3], const float chi[3], double rb_max, double rho,
+                       const rtg_map_options* opt) {
+    m->rb_max = have_col ? (float)rb_max : 0.f;
+    const double u32 = ldexp(1.0, -24);
+    m->gq64 = (104.0 * (have_col ? rho : 1.0) + 6.0) * u32;   // FP32 error bound of q near 1, x2
+    m->gq = (float)m->gq64;
+    double hy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.3;
+    double hx = (opt && opt->gain_cell_x > 0) ? opt->gain_cell_x : 0.25 * hy;
+    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 1.5;
+    GainGrid& gg = m->gg;
+    if (have_gain) {
+        for (;;) {
+            pick_dims(glo[0], ghi[0], hx, gg.nx);
+            pick_dims(glo[1], ghi[1], hy, gg.ny);
+            pick_dims(glo[2], ghi[2], hz, gg.nz);
+            // (the culled kernel packs cell indices in 16 bits)
+            if ((double)gg.nx * gg.ny * gg.nz <= 96.0e6 && gg.nx < 65535 && gg.ny < 65535 && gg.nz < 65535) break;
+            hx *= 2.0;
+            hy *= 2.0;
+            hz *= 2.0;
+        }
+        gg.ox = glo[0]; gg.oy = glo[1]; gg.oz = glo[2];
+    } else {
+        gg.nx = gg.ny = gg.nz = 1;
+        gg.ox = gg.oy = gg.oz = 0.f;
+    }
+    gg.hx = (float)hx;
+    gg.hy = (float)hy;
+    gg.hz = (float)hz;
+    gg.ncellsA = (long long)gg.nx * gg.ny;
+    gg.nxb = (gg.nx + kZoccX - 1) / kZoccX;
+    gg.ncellsB = (long long)gg.nx * gg.ny * gg.nz;
+    ColGrid& cg = m->cg;
+    double hc = (opt && opt->col_cell > 0) ? opt->col_cell : fmax(0.5, 0.5 * (double)m->rb_max);
+    if (have_col) {
+        for (;;) {
+            pick_dims(clo[0], chi[0], hc, cg.nx);
+            pick_dims(clo[1], chi[1], hc, cg.ny);
+            pick_dims(clo[2], chi[2], hc, cg.nz);
+            if ((double)cg.nx * cg.ny * cg.nz <= 64.0e6) break;
+            hc *= 2.0;
+        }
+        cg.ox = clo[0]; cg.oy = clo[1]; cg.oz = clo[2];
+    } else {
+        cg.nx = cg.ny = cg.nz = 1;
+        cg.ox = cg.oy = cg.oz = 0.f;
+    }
+    cg.h = (float)hc;
+    cg.ncells = (long long)cg.nx * cg.ny * cg.nz;
+}
+
+// the map's persistent arrays for up to n_gain visibility and n_col collision records
+static cudaError_t alloc_records(rtg_map_s* m, long long n_gain, long long n_col, cudaStream_t st) {
+    const GainGrid& gg = m->gg;
+    // >= 64 NaN records after the copy: the culled kernel's sentinel run (items past its queue)
+    m->n_gain_pad = n_gain > 0 ? ((n_gain + 64 + kTile - 1) / kTile) * kTile : 0;
+    m->n_col_pad = ((n_col + kTile - 1) / kTile) * kTile;
+    cudaError_t e = map_alloc(m, &m->grec, 2 * m->n_gain_pad, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->gidx, m->n_gain_pad, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->gstartA, gg.ncellsA + 1, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->zocc, (size_t)gg.ny * gg.nxb, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->gtabP, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->crec, m->n_col_pad, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->cmat, m->n_col_pad, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->csrc, m->n_col_pad, st);
+    if (e == cudaSuccess) e = map_alloc(m, &m->cstart, m->cg.ncells + 1, st);
+    return e;
+}
+
+// the validation pass: bounds, counts and the map's copies of the weights and flags into db
+static void launch_bounds(rtg_map_s* m, long long n, const float* means, const float* quats, const float* scales,
+                          const float* opacity, const float* w, const unsigned char* flags, DevBounds* db,
+                          cudaStream_t st) {
+    note_launch(), k_bounds_init<<<1, 1, 0, st>>>(db);
+    if (n <= 0) return;
+    const rtg_robot rb = m->robot;
+    auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
+    const bool vec = (n % 4 == 0) && al16(means) && al16(quats) && al16(scales) && al16(opacity) && al16(w) &&
+                     ((uintptr_t)flags & 3u) == 0 && al16(m->w_orig) && ((uintptr_t)m->flags & 3u) == 0;
+    if (vec)
+        note_launch(), k_bounds<true><<<nblocks(n / 4, 256) > 1184 ? 1184 : nblocks(n / 4, 256), 256, 0, st>>>(
+                           n, means, quats, scales, opacity, w, flags, rb, m->w_orig, m->flags, db);
+    else
+        note_launch(), k_bounds<false><<<nblocks(n, 256) > 1184 ? 1184 : nblocks(n, 256), 256, 0, st>>>(
+                           n, means, quats, scales, opacity, w, flags, rb, m->w_orig, m->flags, db);
+}
+
+static rtg_status build_records(rtg_map_s* m, const float* means, const float* quats, const float* scales,
+                                const float* w, const unsigned char* flags, const int* dn_gain, const int* dn_col,
+                                cudaStream_t st);
+
+// Builds everything of rtg_map_create from device-resident inputs.
 rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const float* scales,
                      const float* opacity, const float* w, const unsigned char* flags, const rtg_map_options* opt,
                      cudaStream_t st) {
     long long n = m->n;
-    const rtg_robot rb = m->robot;
     // --- bounds + validation (one sync)
     DevBounds* db = nullptr;
     DevFreeGuard db_guard{(void**)&db, st};
@@ -969,18 +1083,7 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     // records (class increments, fixed-point u)
     MAP_CK(map_alloc(m, &m->cls, 1, st));
     MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
-    note_launch(), k_bounds_init<<<1, 1, 0, st>>>(db);
-    if (n > 0) {
-        auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
-        const bool vec = (n % 4 == 0) && al16(means) && al16(quats) && al16(scales) && al16(opacity) && al16(w) &&
-                         ((uintptr_t)flags & 3u) == 0 && al16(m->w_orig) && ((uintptr_t)m->flags & 3u) == 0;
-        if (vec)
-            note_launch(), k_bounds<true><<<nblocks(n / 4, 256) > 1184 ? 1184 : nblocks(n / 4, 256), 256, 0, st>>>(
-                               n, means, quats, scales, opacity, w, flags, rb, m->w_orig, m->flags, db);
-        else
-            note_launch(), k_bounds<false><<<nblocks(n, 256) > 1184 ? 1184 : nblocks(n, 256), 256, 0, st>>>(
-                               n, means, quats, scales, opacity, w, flags, rb, m->w_orig, m->flags, db);
-    }
+    launch_bounds(m, n, means, quats, scales, opacity, w, flags, db, st);
     // pinned staging (one per host thread) keeps the readback asynchronous: the classification
     // statistics below are enqueued while it is in flight
     thread_local DevBounds* hbp = nullptr;
@@ -1006,72 +1109,28 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     }
     m->n_gain = hb.n_gain;
     m->n_col = hb.n_col;
-    m->rb_max = m->n_col > 0 ? o2f(hb.rbmax) : 0.f;
-    double rho = m->n_col > 0 ? (double)o2f(hb.rhomax) : 1.0;
-    const double u32 = ldexp(1.0, -24);
-    double gq = (104.0 * rho + 6.0) * u32;   // FP32 error bound of q near 1, x2
-    m->gq = (float)gq;
-    // --- grid geometry
-    double hy = (opt && opt->gain_cell_xy > 0) ? opt->gain_cell_xy : 0.3;
-    double hx = (opt && opt->gain_cell_x > 0) ? opt->gain_cell_x : 0.25 * hy;
-    double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 1.5;
-    GainGrid& gg = m->gg;
-    if (m->n_gain > 0) {
-        float lo[3], hi[3];
-        for (int d = 0; d < 3; ++d) { lo[d] = o2f(hb.gmin[d]); hi[d] = o2f(hb.gmax[d]); }
-        for (;;) {
-            pick_dims(lo[0], hi[0], hx, gg.nx);
-            pick_dims(lo[1], hi[1], hy, gg.ny);
-            pick_dims(lo[2], hi[2], hz, gg.nz);
-            // (the culled kernel packs cell indices in 16 bits)
-            if ((double)gg.nx * gg.ny * gg.nz <= 96.0e6 && gg.nx < 65535 && gg.ny < 65535 && gg.nz < 65535) break;
-            hx *= 2.0;
-            hy *= 2.0;
-            hz *= 2.0;
-        }
-        gg.ox = lo[0]; gg.oy = lo[1]; gg.oz = lo[2];
-    } else {
-        gg.nx = gg.ny = gg.nz = 1;
-        gg.ox = gg.oy = gg.oz = 0.f;
+    float glo[3], ghi[3], clo[3], chi[3];
+    for (int d = 0; d < 3; ++d) {
+        glo[d] = o2f(hb.gmin[d]); ghi[d] = o2f(hb.gmax[d]);
+        clo[d] = o2f(hb.cmin[d]); chi[d] = o2f(hb.cmax[d]);
     }
-    gg.hx = (float)hx;
-    gg.hy = (float)hy;
-    gg.hz = (float)hz;
-    gg.ncellsA = (long long)gg.nx * gg.ny;
-    gg.nxb = (gg.nx + kZoccX - 1) / kZoccX;
-    gg.ncellsB = (long long)gg.nx * gg.ny * gg.nz;
-    ColGrid& cg = m->cg;
-    double hc = (opt && opt->col_cell > 0) ? opt->col_cell : fmax(0.5, 0.5 * (double)m->rb_max);
-    if (m->n_col > 0) {
-        float lo[3], hi[3];
-        for (int d = 0; d < 3; ++d) { lo[d] = o2f(hb.cmin[d]); hi[d] = o2f(hb.cmax[d]); }
-        for (;;) {
-            pick_dims(lo[0], hi[0], hc, cg.nx);
-            pick_dims(lo[1], hi[1], hc, cg.ny);
-            pick_dims(lo[2], hi[2], hc, cg.nz);
-            if ((double)cg.nx * cg.ny * cg.nz <= 64.0e6) break;
-            hc *= 2.0;
-        }
-        cg.ox = lo[0]; cg.oy = lo[1]; cg.oz = lo[2];
-    } else {
-        cg.nx = cg.ny = cg.nz = 1;
-        cg.ox = cg.oy = cg.oz = 0.f;
-    }
-    cg.h = (float)hc;
-    cg.ncells = (long long)cg.nx * cg.ny * cg.nz;
-    // --- allocations
-    // >= 64 NaN records after the copy: the culled kernel's sentinel run (items past its queue)
-    m->n_gain_pad = m->n_gain > 0 ? ((m->n_gain + 64 + kTile - 1) / kTile) * kTile : 0;
-    m->n_col_pad = ((m->n_col + kTile - 1) / kTile) * kTile;
-    MAP_CK(map_alloc(m, &m->grec, 2 * m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->gidx, m->n_gain_pad, st));
-    MAP_CK(map_alloc(m, &m->gstartA, gg.ncellsA + 1, st));
-    MAP_CK(map_alloc(m, &m->zocc, (size_t)gg.ny * gg.nxb, st));
-    MAP_CK(map_alloc(m, &m->gtabP, (size_t)gg.ny * (gg.nx + 1) * gg.nz, st));
-    MAP_CK(map_alloc(m, &m->crec, m->n_col_pad, st));
-    MAP_CK(map_alloc(m, &m->cmat, m->n_col_pad, st));
-    MAP_CK(map_alloc(m, &m->csrc, m->n_col_pad, st));
-    MAP_CK(map_alloc(m, &m->cstart, cg.ncells + 1, st));
+    plan_grids(m, m->n_gain > 0, glo, ghi, m->n_col > 0, clo, chi, m->n_col > 0 ? o2f(hb.rbmax) : 0.0,
+               m->n_col > 0 ? (double)o2f(hb.rhomax) : 1.0, opt);
+    MAP_CK(alloc_records(m, m->n_gain, m->n_col, st));
+    return build_records(m, means, quats, scales, w, flags, nullptr, nullptr, st);
+}
+
+// the counting sorts into both grids, the record scatters, the tables (device work only).  dn_gain /
+// dn_col: the record counts on the device when the host knows only upper bounds (layout maps: m->n_gain,
+// m->n_col are then the capacities), else NULL and m->n_gain / m->n_col are exact.
+static rtg_status build_records(rtg_map_s* m, const float* means, const float* quats, const float* scales,
+                                const float* w, const unsigned char* flags, const int* dn_gain, const int* dn_col,
+                                cudaStream_t st) {
+    const long long n = m->n;
+    const rtg_robot rb = m->robot;
+    const GainGrid& gg = m->gg;
+    const ColGrid& cg = m->cg;
+    const double gq = m->gq64;
     // --- counting sort into both grids
     int *gkey = nullptr, *ckey = nullptr, *gcountB = nullptr, *ccount = nullptr, *gstartB = nullptr;
     // temporaries of the sort: freed (stream-ordered) on every return path
@@ -1138,20 +1197,24 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
             note_launch(), k_pack_gain<<<nb, 256, 0, st>>>(n, means, w, rec, RTG_VARIANT_XI, m->cls);
             note_launch(), k_perm_gain<<<nb, 256, 0, st>>>(n, gkey, grank, gstartB, m->gidx, rec, tsum, ntl, gg.nx);
             const unsigned fb = nblocks(m->n_gain, 256) > 8192 ? 8192 : nblocks(m->n_gain, 256);
-            note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, m->gidx, rec, m->grec + m->n_gain_pad);
+            note_launch(), k_fill_gain<<<fb, 256, 0, st>>>(m->n_gain, dn_gain, m->gidx, rec, m->grec + m->n_gain_pad);
             note_launch(), k_scatter_col<<<nb, 256, 0, st>>>(n, means, quats, scales, ckey, crank, m->cstart, rb, gq,
                                                              m->crec, m->cmat, m->csrc);
         }
     }
-    if (m->n_gain_pad > m->n_gain) {
-        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
-                           m->grec + m->n_gain_pad, m->gidx, m->n_gain, m->n_gain_pad);
-        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - m->n_gain, 256), 256, 0, st>>>(
-                           m->grec, nullptr, m->n_gain, m->n_gain_pad);
+    // NaN padding after the records (from the device counts on a layout map: all of [0, pad) is launched)
+    if (m->n_gain_pad > (dn_gain ? 0 : m->n_gain)) {
+        const long long from = dn_gain ? 0 : m->n_gain;
+        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - from, 256), 256, 0, st>>>(
+                           m->grec + m->n_gain_pad, m->gidx, from, m->n_gain_pad, dn_gain);
+        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - from, 256), 256, 0, st>>>(
+                           m->grec, nullptr, from, m->n_gain_pad, dn_gain);
     }
-    if (m->n_col_pad > m->n_col)
-        note_launch(), k_pad_col<<<nblocks(m->n_col_pad - m->n_col, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, m->n_col,
-                                                                         m->n_col_pad);
+    if (m->n_col_pad > (dn_col ? 0 : m->n_col)) {
+        const long long from = dn_col ? 0 : m->n_col;
+        note_launch(), k_pad_col<<<nblocks(m->n_col_pad - from, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, from,
+                                                                                    m->n_col_pad, dn_col);
+    }
     MAP_CK(cudaGetLastError());
     // --- default classification (k = 1/2, derived thresholds); copy A derived from copy B
     if (tiles) {
@@ -1175,6 +1238,62 @@ rtg_status build_map(rtg_map_s* m, const float* means, const float* quats, const
     }
     // (the guards free gkey, ckey, grank, crank, gstartB and gcountB with ccount, gcountA in its block)
     set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
+    return RTG_OK;
+}
+
+// ---------------------------------------------------------------- layout maps (capturable rebuilds)
+
+rtg_status rebuild_map(rtg_map_s* m, long long n, const float* means, const float* quats, const float* scales,
+                       const float* opacity, const float* w, const unsigned char* flags, cudaStream_t st);
+
+rtg_status create_layout_map(rtg_map_s* m, const rtg_map_layout* L, const rtg_map_options* opt, cudaStream_t st) {
+    const long long cap = L->capacity;
+    m->layout = true;
+    m->cap = cap;
+    m->lay = *L;
+    m->n = 0;
+    MAP_CK(map_alloc(m, &m->w_orig, cap, st));
+    MAP_CK(map_alloc(m, &m->flags, cap, st));
+    MAP_CK(map_alloc(m, &m->cls, 1, st));
+    MAP_CK(map_alloc(m, &m->red_scratch, 3 * kRedBlocks, st));
+    DevBounds* db = nullptr;
+    MAP_CK(map_alloc(m, &db, 1, st));
+    m->dbounds = db;
+    plan_grids(m, true, L->gain_lo, L->gain_hi, true, L->col_lo, L->col_hi, L->rb_max, L->rho_max, opt);
+    MAP_CK(alloc_records(m, cap, cap, st));
+    // an empty map until the first rebuild (every array written)
+    return rebuild_map(m, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+}
+
+rtg_status rebuild_map(rtg_map_s* m, long long n, const float* means, const float* quats, const float* scales,
+                       const float* opacity, const float* w, const unsigned char* flags, cudaStream_t st) {
+    DevBounds* db = static_cast<DevBounds*>(m->dbounds);
+    m->n = n;
+    m->n_gain = m->n_col = m->cap;   // upper bounds until rtg_map_check reads the counts
+    if (!flags && n > 0) MAP_CK(cudaMemsetAsync(m->flags, 0, (size_t)n, st));
+    launch_bounds(m, n, means, quats, scales, opacity, w, flags, db, st);
+    note_launch(), k_layout_check<<<1, 32, 0, st>>>(db, m->lay);
+    MAP_CK(class_stats(n, m->w_orig, m->flags, RTG_VARIANT_XI, 0.5, NAN, NAN, m->cls, m->red_scratch, st));
+    set_class_params(m, RTG_VARIANT_XI, 0.5, NAN, NAN);
+    return build_records(m, means, quats, scales, m->w_orig, m->flags, &db->n_gain, &db->n_col, st);
+}
+
+rtg_status check_layout_map(rtg_map_s* m, cudaStream_t st) {
+    DevBounds hb;
+    MAP_CK(cudaMemcpyAsync(&hb, m->dbounds, sizeof(DevBounds), cudaMemcpyDeviceToHost, st));
+    MAP_CK(cudaStreamSynchronize(st));
+    if (hb.err) {
+        set_error("rtg_map_check: the last rebuild's data is invalid:%s%s%s%s%s%s%s%s%s",
+                  (hb.err & 1) ? " non-finite mean" : "", (hb.err & 2) ? " quaternion norm < 1e-12" : "",
+                  (hb.err & 4) ? " scale <= 0 or non-finite" : "", (hb.err & 8) ? " info_w < 0 or non-finite" : "",
+                  (hb.err & 16) ? " opacity outside [0,1]" : "",
+                  (hb.err & 32) ? " gain-eligible mean outside the layout box" : "",
+                  (hb.err & 64) ? " collidable mean outside the layout box" : "",
+                  (hb.err & 128) ? " semi-axis above rb_max" : "", (hb.err & 256) ? " anisotropy above rho_max" : "");
+        return RTG_ERR_INVALID_ARGUMENT;
+    }
+    m->n_gain = hb.n_gain;
+    m->n_col = hb.n_col;
     return RTG_OK;
 }
 

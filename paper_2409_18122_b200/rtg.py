@@ -61,6 +61,12 @@ class MapOptions(ctypes.Structure):
                 ("gain_cell_x", ctypes.c_float)]
 
 
+class MapLayout(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_longlong), ("gain_lo", ctypes.c_float * 3), ("gain_hi", ctypes.c_float * 3),
+                ("col_lo", ctypes.c_float * 3), ("col_hi", ctypes.c_float * 3), ("rb_max", ctypes.c_float),
+                ("rho_max", ctypes.c_float)]
+
+
 class MapInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_longlong), ("n_collide", ctypes.c_longlong), ("n_gain", ctypes.c_longlong),
                 ("tau_hi", ctypes.c_double), ("tau_lo", ctypes.c_double), ("u_mean", ctypes.c_double),
@@ -100,6 +106,10 @@ _SIGS = {
     "rtg_map_create_ex": (_S, [_I, _LL, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Robot),
                                ctypes.POINTER(MapOptions), _P, ctypes.POINTER(_P)]),
     "rtg_map_destroy": (_S, [_P]),
+    "rtg_map_create_layout": (_S, [_I, ctypes.POINTER(MapLayout), ctypes.POINTER(Robot), ctypes.POINTER(MapOptions),
+                                   _P, ctypes.POINTER(_P)]),
+    "rtg_map_rebuild": (_S, [_P, _LL, _P, _P, _P, _P, _P, _P, _P]),
+    "rtg_map_check": (_S, [_P, _P]),
     "rtg_map_info": (_S, [_P, ctypes.POINTER(MapInfo)]),
     "rtg_traj_upload": (_S, [_I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.POINTER(_P)]),
     "rtg_traj_wrap": (_S, [_I, _I, _I, _P, _P, _P, _P, ctypes.POINTER(_P)]),
@@ -294,6 +304,92 @@ class Map:
             self.close()
         except Exception:
             pass
+
+
+class LayoutMap(Map):
+    """rtg_map_create_layout handle: grids and capacity fixed from caller bounds; `rebuild` refills it
+    from new CUDA arrays with device work only (capturable, e.g. by CycleGraph); `check` synchronises and
+    raises RTGError if the last rebuild's data was invalid or broke the layout."""
+
+    def __init__(self, capacity, gain_box, col_box, rb_max, rho_max, r_robot=0.3, lambda_g=3.0,
+                 collide_rule=COLLIDE_ELLIPSOID, device=0, stream=None, options=None):
+        lay = MapLayout()
+        lay.capacity = int(capacity)
+        for d in range(3):
+            lay.gain_lo[d], lay.gain_hi[d] = float(gain_box[0][d]), float(gain_box[1][d])
+            lay.col_lo[d], lay.col_hi[d] = float(col_box[0][d]), float(col_box[1][d])
+        lay.rb_max, lay.rho_max = float(rb_max), float(rho_max)
+        self._layout = lay
+        self._robot = Robot(float(r_robot), float(lambda_g), int(collide_rule))
+        self.handle = _P()
+        self.n = 0
+        self.capacity = int(capacity)
+        self.device = device
+        self._keep = ()
+        opt = MapOptions(*[float(x) for x in options]) if options is not None else None
+        _check(_lib.rtg_map_create_layout(device, ctypes.byref(lay), ctypes.byref(self._robot),
+                                          ctypes.byref(opt) if opt is not None else None, _stream(stream),
+                                          ctypes.byref(self.handle)), "rtg_map_create_layout")
+
+    def rebuild(self, means, quats, scales, opacity, info_w, flags=None, stream=None) -> None:
+        """rtg_map_rebuild from CUDA arrays (read when the stream reaches the call: keep them alive)."""
+        n = int(means.shape[-1])
+        for nm, a in (("means", means), ("quats", quats), ("scales", scales), ("opacity", opacity),
+                      ("info_w", info_w), ("flags", flags)):
+            if a is not None and (isinstance(a, np.ndarray) or not a.is_cuda):
+                raise ValueError(f"{nm}: rtg_map_rebuild reads CUDA arrays")
+        ptrs = (_arg("means", means, "float32", (3, n), self.device), _arg("quats", quats, "float32", (4, n), self.device),
+                _arg("scales", scales, "float32", (3, n), self.device),
+                _arg("opacity", opacity, "float32", (n,), self.device),
+                _arg("info_w", info_w, "float32", (n,), self.device),
+                _arg("flags", flags, "uint8", (n,), self.device, optional=True))
+        _check(_lib.rtg_map_rebuild(self.handle, n, *ptrs, _stream(stream)), "rtg_map_rebuild")
+        self.n = n
+        self._keep = (means, quats, scales, opacity, info_w, flags)
+
+    def check(self, stream=None) -> None:
+        _check(_lib.rtg_map_check(self.handle, _stream(stream)), "rtg_map_check")
+
+
+class CycleGraph:
+    """The whole planning cycle -- rtg_map_rebuild of a LayoutMap from CUDA map arrays, rtg_score (culled) of
+    a trajectory handle, rtg_best_async -- captured once into one CUDA graph and replayed.  The graph keeps
+    every device pointer: a replay rebuilds from what the map arrays then hold and scores what the
+    trajectory buffers then hold (refill both in place; the Gaussian count n is fixed).  One eager cycle
+    precedes the capture."""
+
+    def __init__(self, lmap: "LayoutMap", map_arrays, tr: "Traj", camera, params: ScoreParams, index_base: int = 0):
+        torch = _torch()
+        if params.mode != MODE_CULLED:
+            raise ValueError("CycleGraph: culled mode only (dense mode reads the list length on the host)")
+        dev = torch.device("cuda", lmap.device)
+        K = tr.K
+        self.outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
+                     torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
+        self.best = torch.empty(2, dtype=torch.float64, device=dev)
+        self._keep = (lmap, tuple(map_arrays), tr)
+        cam = camera if isinstance(camera, Camera) else make_camera(camera)
+
+        def cycle():
+            lmap.rebuild(*map_arrays)
+            score(lmap, tr, cam, params, *self.outs)
+            best_async(self.outs[3], self.best, index_base)
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            cycle()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        lmap.check()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            cycle()
+
+    def replay(self):
+        """Enqueue one replay on the current stream; returns (first_col, feasible, gain, utility, best)."""
+        self.graph.replay()
+        return self.outs + (self.best,)
 
 
 class Traj:

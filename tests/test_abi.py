@@ -68,6 +68,31 @@ def test_invalid_arguments_rejected_before_any_launch(rtg):
     out = rtg.BestResult()
     assert lib.rtg_best(None, 0, 0, None, ctypes.byref(out)) == rtg.ERR_INVALID_ARGUMENT
     assert out.index == -1
+    # layout maps: every argument is checked before the device is touched
+    rob = rtg.Robot(0.2, 3.0, 0)
+    lay = rtg.MapLayout()
+    lay.capacity = 100
+    for d in range(3):
+        lay.gain_lo[d], lay.gain_hi[d], lay.col_lo[d], lay.col_hi[d] = -1.0, 1.0, -1.0, 1.0
+    lay.rb_max, lay.rho_max = 1.0, 4.0
+    assert lib.rtg_map_create_layout(0, ctypes.byref(lay), ctypes.byref(rob), None, None, None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_map_create_layout(0, None, ctypes.byref(rob), None, None, ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_map_create_layout(0, ctypes.byref(lay), None, None, None, ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    for field, bad in (("capacity", 0), ("rb_max", 0.0), ("rb_max", float("inf")), ("rho_max", 0.5)):
+        old_v = getattr(lay, field)
+        setattr(lay, field, bad)
+        assert lib.rtg_map_create_layout(0, ctypes.byref(lay), ctypes.byref(rob), None, None,
+                                         ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT, field
+        setattr(lay, field, old_v)
+    lay.gain_lo[1] = 2.0   # lo > hi
+    assert lib.rtg_map_create_layout(0, ctypes.byref(lay), ctypes.byref(rob), None, None,
+                                     ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    lay.gain_lo[1] = -1.0
+    lay.col_hi[2] = float("nan")
+    assert lib.rtg_map_create_layout(0, ctypes.byref(lay), ctypes.byref(rob), None, None,
+                                     ctypes.byref(h)) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_map_rebuild(None, 0, None, None, None, None, None, None, None) == rtg.ERR_INVALID_ARGUMENT
+    assert lib.rtg_map_check(None, None) == rtg.ERR_INVALID_ARGUMENT
     # best_async: NULL / misaligned result pointer, NULL utility, K < 1 (checked before any launch)
     buf = (ctypes.c_double * 4)()
     assert lib.rtg_best_async(buf, 1, 0, None, None) == rtg.ERR_INVALID_ARGUMENT

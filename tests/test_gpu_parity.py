@@ -888,3 +888,148 @@ def test_max_size_inside_run_beyond_2p24_records(R):
     orc = O.score(wl, tau_hi=tau[0], tau_lo=tau[1])
     check_waypoints(out["culled"], orc, out["culled"]["info"].fixed_point_shift)
     check_trajectories(out["culled"], orc, T)
+
+
+# ----------------------------------------------------------------- layout maps and the whole-cycle graph
+
+def _layout_of(wl, margin=0.05):
+    """Generous layout bounds for a workload (the caller's knowledge of its map extents): boxes around the
+    gain-eligible and collidable means, bounds on the largest semi-axis and its anisotropy."""
+    f = wl.flags if wl.flags is not None else np.zeros(wl.N, np.uint8)
+    gain, col = (f & 2) == 0, (f & 1) == 0
+    m = wl.means.astype(np.float64)
+    box = lambda sel: ((m[:, sel].min(1) - margin).tolist(), (m[:, sel].max(1) + margin).tolist()) \
+        if sel.any() else ([0.0] * 3, [1.0] * 3)
+    a = wl.robot.lambda_g * wl.scales[:, col].astype(np.float64) + wl.robot.r_robot
+    rb = float(a.max()) * 1.01 + 1e-3 if col.any() else 1.0
+    rho = float((a.max(0) / a.min(0)).max()) * 1.01 if col.any() else 1.0
+    return box(gain), box(col), rb, rho
+
+
+def _dev_map_arrays(wl, dev):
+    t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    return [t(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)]
+
+
+@pytest.mark.parametrize("which", ["room", "fuzz"])
+def test_layout_map_rebuild_equals_create(R, room, which):
+    """rtg_map_create_layout + rtg_map_rebuild (grids from the caller's bounds, no host synchronisation)
+    score exactly like rtg_map_create on the same data: per-waypoint counts, gains and collision bits bit
+    for bit (decisions and exact sums do not depend on the grid), and the same record counts."""
+    dev = torch.device("cuda", 0)
+    if which == "room":
+        wl = room
+        k = np.arange(0, room.K, 7)
+        x, y, z, yaw = (np.ascontiguousarray(a[k]) for a in (room.x, room.y, room.z, room.yaw))
+    else:
+        rng = np.random.default_rng(77)
+        n = 2500
+        means = (rng.uniform(-6, 6, (3, n))).astype(np.float32)
+        q = rng.normal(size=(4, n))
+        quats = (q / np.linalg.norm(q, axis=0)).astype(np.float32)
+        scales = np.exp(rng.uniform(np.log(0.01), np.log(0.5), (3, n))).astype(np.float32)
+        flags = (rng.integers(0, 4, n) * (rng.random(n) < 0.3)).astype(np.uint8)
+        K, T = 8, 9
+        x, y = rng.uniform(-7, 7, (2, K, T)).astype(np.float32)
+        z = rng.uniform(-2, 2, (K, T)).astype(np.float32)
+        yaw = rng.uniform(-np.pi, np.pi, (K, T)).astype(np.float32)
+        wl = W.Workload("layout_fuzz", means, quats, scales, rng.random(n).astype(np.float32),
+                        rng.random(n).astype(np.float32), flags, x, y, z, yaw, W.Robot(0.2, 2.0), room.camera, 0.1)
+    gbox, cbox, rb, rho = _layout_of(wl)
+    arrs = _dev_map_arrays(wl, dev)
+    p = R.make_params(flags=R.SCORE_FULL_GAIN)
+    ref = R.map_from_workload(wl)
+    lm = R.LayoutMap(wl.N + 100, gbox, cbox, rb, rho, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g,
+                     collide_rule=wl.robot.rule)
+    lm.rebuild(*arrs)
+    lm.check()
+    tr = R.traj_from_workload(wl, x=x, y=y, z=z, yaw=yaw)
+    outs = [R.score_debug(mp, tr, wl.camera, p) for mp in (ref, lm)]
+    for key in ("wp_gain", "wp_nh", "wp_nl", "wp_col"):
+        a, b = (o[key].cpu().numpy() for o in outs)
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), key
+    ia, ib = ref.info(), lm.info()
+    assert (ia.n_gain, ia.n_collide, ia.n) == (ib.n_gain, ib.n_collide, ib.n)
+    assert outs[0]["wp_nh"].sum() > 0
+    # the same handle rebuilt empty, then again from the data
+    lm.rebuild(*[None if a is None else a[..., :0] for a in arrs])
+    lm.check()
+    fc, fe, g, u = R.score(lm, tr, wl.camera, p)
+    assert bool((fe == 1).all()) and float(g.abs().max()) == 0.0
+    lm.rebuild(*arrs)
+    again = R.score_debug(lm, tr, wl.camera, p)
+    assert torch.equal(again["wp_gain"], outs[1]["wp_gain"]) and torch.equal(again["wp_col"], outs[1]["wp_col"])
+    for h in (tr, lm, ref):
+        h.close()
+
+
+def test_layout_map_check_reports_broken_layout(R, room):
+    """rtg_map_check reports what the rebuild recorded on the device: a mean outside the layout box, a
+    semi-axis above rb_max, an invalid element; a valid rebuild clears it."""
+    dev = torch.device("cuda", 0)
+    gbox, cbox, rb, rho = _layout_of(room)
+    arrs = _dev_map_arrays(room, dev)
+    lm = R.LayoutMap(room.N, gbox, cbox, rb, rho, r_robot=room.robot.r_robot, lambda_g=room.robot.lambda_g)
+    lm.rebuild(*arrs)
+    lm.check()
+    bad = [a.clone() if a is not None else None for a in arrs]
+    bad[0][0, 5] = gbox[1][0] + 1.0                     # outside the gain box (and the collision box)
+    lm.rebuild(*bad)
+    with pytest.raises(R.RTGError, match="outside the layout box"):
+        lm.check()
+    small = R.LayoutMap(room.N, gbox, cbox, 0.5 * rb, rho, r_robot=room.robot.r_robot, lambda_g=room.robot.lambda_g)
+    small.rebuild(*arrs)
+    with pytest.raises(R.RTGError, match="rb_max"):
+        small.check()
+    bad = [a.clone() if a is not None else None for a in arrs]
+    bad[2][1, 3] = -1.0                                 # invalid scale
+    lm.rebuild(*bad)
+    with pytest.raises(R.RTGError, match="scale"):
+        lm.check()
+    lm.rebuild(*arrs)
+    lm.check()
+    for h in (lm, small):
+        h.close()
+
+
+def test_cycle_graph_replay_equals_eager(R, room):
+    """The whole planning cycle -- layout-map rebuild + score + best_async -- captured into one CUDA graph
+    (R.CycleGraph): replays equal the eager rtg_map_create path bit for bit, also after the map arrays and
+    the waypoint buffers are refilled in place with other data of the same size."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(9)
+    k = np.arange(0, room.K, 5)
+    # a second map of the same size: the room mirrored in x (inside a box covering both)
+    room2 = dataclasses.replace(room, means=(room.means * np.array([[-1.0], [1.0], [1.0]], np.float32)).astype(np.float32),
+                                info_w=rng.permutation(room.info_w))
+    g1, c1, rb, rho = _layout_of(room)
+    g2, c2, _, _ = _layout_of(room2)
+    join = lambda a, b: ([min(u, v) for u, v in zip(a[0], b[0])], [max(u, v) for u, v in zip(a[1], b[1])])
+    lm = R.LayoutMap(room.N, join(g1, g2), join(c1, c2), rb, rho, r_robot=room.robot.r_robot,
+                     lambda_g=room.robot.lambda_g)
+    arrs = _dev_map_arrays(room, dev)
+    bufs = [torch.from_numpy(np.ascontiguousarray(a[k])).to(dev) for a in (room.x, room.y, room.z, room.yaw)]
+    tr = R.Traj.wrap(*bufs)
+    p = R.make_params()
+    cg = R.CycleGraph(lm, arrs, tr, room.camera, p)
+    for it, wl in enumerate((room, room2, room)):
+        src = _dev_map_arrays(wl, dev)
+        for dst, a in zip(arrs, src):
+            if dst is not None:
+                dst.copy_(a)
+        if it:
+            perm = rng.permutation(room.K)[:len(k)]
+            for b, a in zip(bufs, (room.x, room.y, room.z, room.yaw)):
+                b.copy_(torch.from_numpy(np.ascontiguousarray(a[perm])))
+        outs = cg.replay()
+        torch.cuda.synchronize()
+        lm.check()
+        ref = R.map_from_workload(wl)
+        eager = R.score(ref, tr, room.camera, p)
+        for a, b in zip(outs[:4], eager):
+            assert torch.equal(a.view(torch.uint8), b.view(torch.uint8)), it
+        assert R.read_best(outs[4]) == R.best(eager[3])
+        ref.close()
+    del cg
+    tr.close()
+    lm.close()
