@@ -352,9 +352,9 @@ def main():
         e2e = {"value": pairs / (ms_e2e / 1000.0), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 16 + 68}
 
-    # ---- the scoring part of the cycle (rtg_score + rtg_best_async on a built map) eager vs one CUDA-graph
-    # replay (R.ScoreGraph): the launch gaps a graph removes.  The map build cannot be captured (it reads
-    # the validated bounds back to size its grids), so it is outside both.
+    # ---- CUDA graphs: the scoring part of the cycle (rtg_score + rtg_best_async on a built
+    # map) eager vs one graph replay (R.ScoreGraph), and -- without views -- the whole cycle on a layout
+    # map (rtg_map_rebuild needs no host synchronisation, so R.CycleGraph captures rebuild + score + best)
     graph = None
     if args.mode == "culled" and not args.no_graph:
         m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
@@ -388,6 +388,7 @@ def main():
                  "eager_ms_median": ms_eager, "graph_ms_median": ms_graph}
         del g
         m.close()
+    if graph is not None and not Kv:
         # the whole cycle on a layout map (grids from the workload's extents, rebuilt without a host
         # synchronisation): eager, and captured with the score and the argmax into one graph
         gbox, cbox, rb_b, rho_b = layout_bounds(wl)
@@ -411,8 +412,9 @@ def main():
                           "eager_ms_median": ms_ce, "graph_ms_median": ms_cg,
                           "standard_cycle_ms_median": step_stats["median"]}
         del cg
-        tr.close()
         lm.close()
+    if graph is not None:
+        tr.close()
 
     # ---- roofline of the dominant phase
     phase_ms = {k: v / nprof for k, v in prof["ms"].items()}
