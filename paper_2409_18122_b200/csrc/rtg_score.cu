@@ -209,49 +209,31 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
 }
 
 // ===================================================================== info-waypoint list
-// list = { k*T + t : trajectory k computed, (t+1) % stride == 0 }, k ascending, t ascending
-__global__ void k_build_list(const int* __restrict__ first_col, int K, int T, int stride, int full_gain,
-                             int* __restrict__ list, int* __restrict__ count) {
-    __shared__ int s_warp[32];
-    __shared__ int s_carry;
-    const int per = T / stride;   // number of info waypoints per trajectory
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int k0 = 0; k0 < K; k0 += blockDim.x) {
-        int k = k0 + threadIdx.x;
-        int inc = (k < K && (full_gain || first_col[k] == T)) ? 1 : 0;
-        // block exclusive scan of inc
-        int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        int x = inc;
-        for (int o = 1; o < 32; o <<= 1) {
-            int v = __shfl_up_sync(kFull, x, o);
-            if (lane >= o) x += v;
-        }
-        if (lane == 31) s_warp[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            int w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(kFull, w, o);
-                if (lane >= o) w += v;
-            }
-            s_warp[lane] = w;
-        }
-        __syncthreads();
-        int rank = s_carry + (wid > 0 ? s_warp[wid - 1] : 0) + x - inc;
-        if (inc) list[rank] = k;      // ranked trajectories; expanded by k_fill_list
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += s_warp[(blockDim.x >> 5) - 1];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *count = s_carry * per;
+// list = { k*T + t : trajectory k computed, (t+1) % stride == 0 }: the computed trajectories ranked by one
+// warp-aggregated atomic per warp (k ascending within each warp's 32; the warps' order is the order they
+// ran -- the list order only schedules work, every output is indexed by waypoint), each expanded to its
+// info waypoints by k_fill_list
+__global__ void k_build_list(const int* __restrict__ first_col, int K, int T, int full_gain,
+                             int* __restrict__ list, int* __restrict__ nranked) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool inc = k < K && (full_gain || first_col[k] == T);
+    const unsigned b = __ballot_sync(kFull, inc);
+    if (!b) return;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(nranked, __popc(b));
+    base = __shfl_sync(kFull, base, 0);
+    if (inc) list[base + __popc(b & ((1u << lane) - 1u))] = k;
 }
 
-// list[e] = ranked[e / per] * T + (e % per + 1) * stride - 1 for e < count (= ranked count * per)
-__global__ void k_fill_list(const int* __restrict__ ranked, const int* __restrict__ count, int per, int T, int stride,
-                            int* __restrict__ list) {
+// list[e] = ranked[e / per] * T + (e % per + 1) * stride - 1 for e < count = ranked count * per (written
+// here for the gain kernels)
+__global__ void k_fill_list(const int* __restrict__ ranked, const int* __restrict__ nranked, int per, int T,
+                            int stride, int* __restrict__ list, int* __restrict__ count) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (e >= *count) return;
+    const long long n = (long long)*nranked * per;
+    if (e == 0) *count = (int)n;
+    if (e >= n) return;
     const int r = (int)(e / per), j = (int)(e - (long long)r * per);
     list[e] = ranked[r] * T + (j + 1) * stride - 1;
 }
@@ -617,11 +599,13 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
 
 cudaError_t launch_list(const int* first_col, int K, int T, int stride, int full_gain, int* list, int* count,
                         int* ranked, cudaStream_t st) {
-    note_launch(), k_build_list<<<1, 1024, 0, st>>>(first_col, K, T, stride, full_gain, ranked, count);
+    // count[4]: the ranked trajectories (zeroed with the scratch; count[1], count[2] are the collision and
+    // gain kernels' work counters), count[0]: the list length
+    note_launch(), k_build_list<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(first_col, K, T, full_gain, ranked,
+                                                                             count + 4);
     const long long per = T / stride, n = (long long)K * per;
-    if (n > 0)
-        note_launch(), k_fill_list<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ranked, count, (int)per, T, stride,
-                                                                                  list);
+    note_launch(), k_fill_list<<<(unsigned)(n > 0 ? (n + 255) / 256 : 1), 256, 0, st>>>(ranked, count + 4, (int)per,
+                                                                                       T, stride, list, count);
     return cudaGetLastError();
 }
 
