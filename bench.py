@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: exercise the multi-rank code path with "
                          "several ranks on one GPU; the (score, index) exchange then runs on the host)")
+    ap.add_argument("--z-centre", default="none",
+                    help="visibility z-cells: 'none' starts them at the lowest mean (default), 'camera' centres one "
+                         "on the waypoints' median camera height (rtg_map_options.gain_z_centre), or a height [m]")
     ap.add_argument("--cells", default=None,
                     help="visibility grid cells 'hy,hx,hz' [m] (rtg_map_options; default: library defaults)")
     return ap.parse_args()
@@ -248,6 +251,13 @@ def main():
     if args.cells:
         hy, hx, hz = (float(v) for v in args.cells.split(","))
         map_opts = (hy, hz, 0.0, hx)
+    z_centre = None
+    if args.z_centre == "camera":   # the planner's camera height: its waypoints share it (ground robot)
+        z_centre = float(np.median(wl.z))
+    elif args.z_centre != "none":
+        z_centre = float(args.z_centre)
+    if z_centre is not None:
+        map_opts = (map_opts or (0.0, 0.0, 0.0, 0.0)) + (z_centre,)
 
     aux = torch.cuda.Stream(device=dev)
     vstream = torch.cuda.Stream(device=dev)
@@ -462,6 +472,7 @@ def main():
                 "config": {"workload": "outdoor (BASELINE.json configs[3])" if args.config == "outdoor" else args.config,
                            "N": N, "K": K_glob, "K_per_gpu": K, "views": Kv_glob, "T": T, "mode": args.mode,
                            "info_stride": args.stride,
+                           "gain_z_centre": z_centre,
                            "parallelism": f"traj-shard x{world}, map replicated",
                            "l2": "flushed (512 MiB write) between timed steps",
                            **({"views_stream": "views scored concurrently on a second stream; phase_ms covers "

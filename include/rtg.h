@@ -137,15 +137,23 @@ typedef struct {
     long long index;     /* index_base + local index, -1 when none   */
 } rtg_best_result;
 
-/* Grid options for rtg_map_create_ex; any field <= 0 selects the default.  The visibility
- * grid has rows of height gain_cell_xy along y, cells of width gain_cell_x along x and
- * z-cells of height gain_cell_z (the culled gain kernel tests individually only Gaussians of
- * cells that straddle the frustum, so thinner rows mean fewer tests but more rows). */
+/* Grid options for rtg_map_create_ex / rtg_map_create_layout; any size <= 0 selects the default.
+ * The visibility grid has rows of height gain_cell_xy along y, cells of width gain_cell_x along x
+ * and z-cells of height gain_cell_z (the culled gain kernel tests individually only Gaussians of
+ * cells that straddle the frustum, so thinner rows mean fewer tests but more rows).  The z-cells
+ * start at the lowest mean unless gain_z_centred is set: then one z-cell is centred on
+ * gain_z_centre, e.g. the camera height of a ground robot, whose waypoints share it.  The cell
+ * holding the camera straddles the frustum's top and bottom planes out to the depth where the
+ * vertical field of view spans it -- hz / (2 k) with the camera at its centre, up to hz / k at an
+ * edge (k = the slope of the planes) -- so centring it minimises the near-field tests.  Results do
+ * not depend on any of these options. */
 typedef struct {
     float gain_cell_xy;  /* visibility grid row height (y) [m]    (default 0.3)            */
     float gain_cell_z;   /* visibility grid cell height (z) [m]   (default 1.5)            */
     float col_cell;      /* collision grid cell edge [m]          (default max(0.5, r_b/2)) */
     float gain_cell_x;   /* visibility grid cell width (x) [m]    (default gain_cell_xy/4) */
+    int gain_z_centred;  /* nonzero: centre a z-cell on gain_z_centre                      */
+    float gain_z_centre; /* [m], finite                                                    */
 } rtg_map_options;
 
 /* Read-only facts about a built map (rtg_map_info). */

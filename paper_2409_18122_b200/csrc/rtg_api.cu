@@ -269,7 +269,8 @@ rtg_status rtg_map_create_ex(int device, long long n, rtg_mem kind, const float*
     if (!(robot->lambda_g > 0) || !finite_f(robot->lambda_g)) return invalid("lambda_g must be finite and > 0");
     if (robot->collide_rule != RTG_COLLIDE_ELLIPSOID && robot->collide_rule != RTG_COLLIDE_PRINCIPAL_AXIS)
         return invalid("unknown collide_rule");
-    if (opts && (!std::isfinite(opts->gain_cell_xy) || !std::isfinite(opts->gain_cell_z) || !std::isfinite(opts->col_cell)))
+    if (opts && (!std::isfinite(opts->gain_cell_xy) || !std::isfinite(opts->gain_cell_z) || !std::isfinite(opts->col_cell) ||
+                 !std::isfinite(opts->gain_cell_x) || (opts->gain_z_centred && !std::isfinite(opts->gain_z_centre))))
         return invalid("grid options must be finite");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
@@ -334,7 +335,7 @@ static rtg_status check_robot_opts(const rtg_robot* robot, const rtg_map_options
     if (robot->collide_rule != RTG_COLLIDE_ELLIPSOID && robot->collide_rule != RTG_COLLIDE_PRINCIPAL_AXIS)
         return invalid("unknown collide_rule");
     if (opts && (!std::isfinite(opts->gain_cell_xy) || !std::isfinite(opts->gain_cell_z) || !std::isfinite(opts->col_cell) ||
-                 !std::isfinite(opts->gain_cell_x)))
+                 !std::isfinite(opts->gain_cell_x) || (opts->gain_z_centred && !std::isfinite(opts->gain_z_centre))))
         return invalid("grid options must be finite");
     return RTG_OK;
 }

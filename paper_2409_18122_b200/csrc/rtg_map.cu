@@ -986,17 +986,25 @@ static void plan_grids(rtg_map_s* m, bool have_gain, const float glo[3], const f
     double hz = (opt && opt->gain_cell_z > 0) ? opt->gain_cell_z : 1.5;
     GainGrid& gg = m->gg;
     if (have_gain) {
+        float oz = glo[2];
         for (;;) {
             pick_dims(glo[0], ghi[0], hx, gg.nx);
             pick_dims(glo[1], ghi[1], hy, gg.ny);
-            pick_dims(glo[2], ghi[2], hz, gg.nz);
+            if (opt && opt->gain_z_centred) {
+                // z-cell boundaries at gain_z_centre +- (j + 1/2) hz: the origin moves down to the first
+                // of them at or below the lowest mean (at most one more z-cell)
+                const double c0 = (double)opt->gain_z_centre - 0.5 * hz;
+                oz = (float)(c0 - ceil((c0 - (double)glo[2]) / hz) * hz);
+                if ((double)oz > (double)glo[2]) oz = glo[2];   // (rounding: never above a mean)
+            }
+            pick_dims(oz, ghi[2], hz, gg.nz);
             // (the culled kernel packs cell indices in 16 bits)
             if ((double)gg.nx * gg.ny * gg.nz <= 96.0e6 && gg.nx < 65535 && gg.ny < 65535 && gg.nz < 65535) break;
             hx *= 2.0;
             hy *= 2.0;
             hz *= 2.0;
         }
-        gg.ox = glo[0]; gg.oy = glo[1]; gg.oz = glo[2];
+        gg.ox = glo[0]; gg.oy = glo[1]; gg.oz = oz;
     } else {
         gg.nx = gg.ny = gg.nz = 1;
         gg.ox = gg.oy = gg.oz = 0.f;

@@ -58,7 +58,15 @@ class BestResult(ctypes.Structure):
 
 class MapOptions(ctypes.Structure):
     _fields_ = [("gain_cell_xy", ctypes.c_float), ("gain_cell_z", ctypes.c_float), ("col_cell", ctypes.c_float),
-                ("gain_cell_x", ctypes.c_float)]
+                ("gain_cell_x", ctypes.c_float), ("gain_z_centred", ctypes.c_int), ("gain_z_centre", ctypes.c_float)]
+
+
+def make_map_options(options) -> "MapOptions":
+    """rtg_map_options from (gain_cell_xy, gain_cell_z, col_cell, gain_cell_x[, gain_z_centre]); sizes <= 0 take
+    the defaults, a gain_z_centre of None leaves the z-cells at the lowest mean."""
+    v = list(options)
+    zc = v[4] if len(v) > 4 else None
+    return MapOptions(*[float(x) for x in v[:4]], int(zc is not None), float(zc) if zc is not None else 0.0)
 
 
 class MapLayout(ctypes.Structure):
@@ -269,7 +277,7 @@ class Map:
         self._keep = (means, quats, scales, opacity, info_w, flags)
         st = _stream(stream)
         if options is not None:
-            opt = MapOptions(*[float(x) for x in options])
+            opt = make_map_options(options)
             s = _lib.rtg_map_create_ex(device, n, kind, *ptrs, ctypes.byref(self._robot), ctypes.byref(opt), st,
                                        ctypes.byref(self.handle))
         else:
@@ -326,7 +334,7 @@ class LayoutMap(Map):
         self.capacity = int(capacity)
         self.device = device
         self._keep = ()
-        opt = MapOptions(*[float(x) for x in options]) if options is not None else None
+        opt = make_map_options(options) if options is not None else None
         _check(_lib.rtg_map_create_layout(device, ctypes.byref(lay), ctypes.byref(self._robot),
                                           ctypes.byref(opt) if opt is not None else None, _stream(stream),
                                           ctypes.byref(self.handle)), "rtg_map_create_layout")

@@ -474,7 +474,8 @@ def test_determinism_and_shard_emulation(R, room):
 
 # ----------------------------------------------------------------- culled kernel geometry edge cases
 
-@pytest.mark.parametrize("cells", [None, (0.5, 0.5, 0.5, 0.5), (0.1, 3.0, 0.0, 0.3), (1.0, 0.25, 0.0, 0.05)])
+@pytest.mark.parametrize("cells", [None, (0.5, 0.5, 0.5, 0.5), (0.1, 3.0, 0.0, 0.3), (1.0, 0.25, 0.0, 0.05),
+                                   (0.3, 1.5, 0.0, 0.075, 0.04), (0.3, 0.5, 0.0, 0.075, 1.25), (0.3, 1.0, 0.0, 0.1, -3.0)])
 def test_culled_equals_dense_axis_yaws_offcentre_cameras(R, room, cells):
     """The culled kernel's row / column intervals divide by the x-coefficient of each frustum plane,
     which is exactly 0 at axis-aligned yaws; its cell classification must still be exact for any
@@ -569,6 +570,8 @@ def test_fuzz_random_maps_cameras_grids(R, seed):
                     W.Robot(float(rng.uniform(0, 0.5)), float(rng.uniform(1, 3))), cam, 0.1)
     cells = (float(rng.uniform(0.05, 2)), float(rng.uniform(0.1, 3)), float(rng.uniform(0.3, 3)),
              float(rng.uniform(0.02, 1)))
+    if seed % 2:   # a z-cell centred on a random height (rtg_map_options.gain_z_centre)
+        cells = cells + (float(lo[2] + ext[2] * rng.uniform(-0.5, 1.5)),)
     out = {}
     for mode in MODES:
         m = R.map_from_workload(wl, options=cells if mode == "culled" else None)

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--cells", default=None, help="visibility grid 'hy,hx,hz' [m] (rtg_map_options)")
+    ap.add_argument("--z-centre", default="none", help="as bench.py: 'none', 'camera' or a height [m]")
     args = ap.parse_args()
     wl = W.make(args.config)
     dev = torch.device("cuda", 0)
@@ -44,6 +45,10 @@ def main():
     if args.cells:
         hy, hx, hz = (float(v) for v in args.cells.split(","))
         opts = (hy, hz, 0.0, hx)
+    zc = None if args.z_centre == "none" else (float(np.median(wl.z)) if args.z_centre == "camera"
+                                                 else float(args.z_centre))
+    if zc is not None:
+        opts = (opts or (0.0, 0.0, 0.0, 0.0)) + (zc,)
     base = None
     for n in (int(v) for v in args.ranks.split(",")):
         idx = np.arange(0, wl.K, n)
@@ -105,7 +110,7 @@ def main():
         prof = R.profile_read(reset=True)
         med = statistics.median(ms)
         base = med if base is None else base
-        print(json.dumps({"config": args.config, "cells": args.cells, "ranks": n, "trajectories_per_rank": K,
+        print(json.dumps({"config": args.config, "cells": args.cells, "gain_z_centre": zc, "ranks": n, "trajectories_per_rank": K,
                           "views_per_rank": len(views[0]) if views is not None else 0,
                           "per_rank_ms_median": med, "per_rank_ms_min": min(ms),
                           "modelled_speedup": base / med,
