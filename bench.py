@@ -542,6 +542,48 @@ def work_sample(R, m, wl, cam, params, feasible, n=96):
     return {k: v / nwp for k, v in d["stats"].items()}
 
 
+# Algorithmic L2 -> SM bytes of the culled gain kernel per info waypoint:
+# a 16-byte record per individually tested Gaussian, two 16-byte z-fastest table entries per (row, z-cell)
+# unit plus two more per unit whose inside x-run is added whole, four 4-byte copy-A column starts per
+# footprint row, and the waypoint's pose (16 B) and FP64 yaw sine / cosine (16 B).
+B_REC, B_TAB, B_ROW, B_WP = 16.0, 16.0, 16.0, 32.0
+
+
+def l2_roofline(n_info, work, ms, k_ncu):
+    """Second roof of the culled gain kernel: its records and tables are L2-resident (ncu: DRAM bytes are
+    < 0.1 % of the L2 reads), so the memory roof is the L2 -> SM read bandwidth, measured on B200 by
+    tools/l2_peak.cu (profiles/r2j_l2_peak.json): sequential 16-byte loads through L2 (the hardware roof)
+    and the kernel's own access pattern (runs of 8 consecutive 16-byte records at random offsets)."""
+    bytes_wp = (B_REC * work["tested"] + B_TAB * 2.0 * (work["units"] + work["cells_aggregated"])
+                + B_ROW * work.get("rows", 0.0) + B_WP)
+    ach = n_info * bytes_wp / (ms / 1e3) / 1e9
+    mean_run = (work["tested"] / work["runs"]) if work.get("runs") else None
+    peak = pattern = pattern_run = None
+    try:
+        res = json.load(open(os.path.join(ROOT, "profiles", "r2j_l2_peak.json")))["results"]
+        peak = max(r["GBps"] for r in res if r["pattern"] == "seq_cg")
+        # the runs pattern at the longest measured run length not above the kernel's mean run length
+        runs = sorted((r["run_records"], r["GBps"]) for r in res if r["pattern"] == "runs")
+        pattern_run, pattern = ([x for x in runs if mean_run is None or x[0] <= mean_run] or runs[:1])[-1]
+    except Exception:
+        pass
+    out = {"bound": "l2", "achieved": ach, "peak": peak, "unit": "GB/s",
+           "frac": ach / peak if peak else None,
+           "peak_basis": "measured L2->SM read bandwidth, sequential ld.global.cg 16-byte loads over a 64 MB "
+                         "L2-resident buffer (tools/l2_peak.cu, profiles/r2j_l2_peak.json)",
+           "pattern_peak": pattern, "frac_of_pattern_peak": ach / pattern if pattern else None,
+           "pattern_basis": f"the same tool: 16-byte records in runs of {pattern_run} consecutive records at random "
+                            "offsets, 32 lanes on 32 consecutive items of the flattened runs (the test passes' "
+                            "access pattern; the longest measured run length not above mean_run_records)",
+           "mean_run_records": mean_run,
+           "bytes_per_wp": bytes_wp, "per_unit_bytes": {"record": B_REC, "table_entry": B_TAB, "row": B_ROW,
+                                                      "waypoint": B_WP}}
+    if k_ncu and k_ncu.get("l2_read_bytes"):
+        out["ncu_l2_read_bytes"] = k_ncu["l2_read_bytes"]
+        out["algorithmic_share_of_l2_reads"] = n_info * bytes_wp / k_ncu["l2_read_bytes"]
+    return out
+
+
 def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, ncu):
     """Roofline object of the dominant phase (achieved = algorithmic work per launch / launch time).
     `ncu` holds the committed ncu --set full figures of the same kernel (profiles/traffic.json)."""
@@ -578,6 +620,8 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, ncu
            "traffic": tr, "phase": phase, "kernel": kname, "kernel_ms": ms,
            "peak_basis": "148 SMs x 128 FP32 lanes x measured SM clock (B200_PROFILING.md unit counts)",
            "work_units": units, "work_per_waypoint": work}
+    if phase == "visibility_gain" and mode == "culled" and work is not None:
+        out["l2"] = l2_roofline(n_info, work, ms, k_ncu)
     if k_ncu:
         out["ncu"] = {k: v for k, v in k_ncu.items() if k != "dram_bytes"}
         wi = k_ncu.get("warp_inst")

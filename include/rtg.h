@@ -323,7 +323,8 @@ rtg_status rtg_best_async(const double* utility, int K, long long index_base, rt
  * (= 12) counters {collision pairs FP64-redecided, visibility pairs FP64-redecided, visibility
  * pairs tested individually, (row, z-cell) x-runs added whole, collision candidates tested,
  * visibility pairs tested in the horizontally straddling flanks of rows, (row, z-cell) units cut,
- * individually tested pairs visible, footprint rows classified, 0, 0, 0 (reserved)}
+ * individually tested pairs visible, footprint rows classified, tested runs (contiguous record
+ * ranges queued for individual tests), 0, 0 (reserved)}
  * (culled mode; dense mode fills the first two).  Synchronises the stream.
  */
 enum { RTG_DEBUG_STATS = 12 };

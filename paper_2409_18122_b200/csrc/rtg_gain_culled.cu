@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     __syncwarp();
     const int L = *list_count;
     unsigned nref = 0;
-    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0, nrow = 0;
+    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0, nrow = 0, nruns = 0;
     for (;;) {
         int e = 0;
         if (lane == 0) e = atomicAdd(counter, 1);
@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         qe[slot] = l1;
                     }
                     nq += __popc(b0) + __popc(b1);
+                    if (kStats) nruns += (unsigned)(__popc(b0) + __popc(b1));
                 }
                 if (nq > kQFlush || (done && nq > 0)) {
                     // ---- test every queued item, 64 per pass (two per lane)
@@ -506,6 +507,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
             nflank += __shfl_xor_sync(kFullG, nflank, o);
             nvis += __shfl_xor_sync(kFullG, nvis, o);
             nrow += __shfl_xor_sync(kFullG, nrow, o);
+            nruns += __shfl_xor_sync(kFullG, nruns, o);
         }
         if (lane == 0) {
             if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
             atomicAdd(&stats[6], nunit);
             atomicAdd(&stats[7], nvis);
             atomicAdd(&stats[8], nrow);
+            atomicAdd(&stats[9], nruns / 32);   // warp-uniform: every lane counted the warp's runs
         }
     }
 }

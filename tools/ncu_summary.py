@@ -90,7 +90,10 @@ def full(rep, out, key=None):
         traffic[short] = {"dram_bytes": b, "warp_inst": num("smsp__inst_executed.sum"),
                           "fma_pipe_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                           "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                          "ms": num("gpu__time_duration.sum")}
+                          "ms": num("gpu__time_duration.sum"),
+                          # L2 -> SM read bytes (32-byte sectors requested by the SMs' texture/LSU path)
+                          "l2_read_bytes": (32.0 * num("lts__t_sectors_srcunit_tex_op_read.sum")
+                                            if num("lts__t_sectors_srcunit_tex_op_read.sum") else None)}
         fp = [w for w in METRICS if "thread_inst_executed_op_f" in w and "per_cycle_elapsed" in w]
         pk = "sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained"
         if all(w in got for w in fp) and pk in got:
