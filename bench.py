@@ -563,7 +563,8 @@ def l2_roofline(n_info, work, ms, k_ncu):
         res = json.load(open(os.path.join(ROOT, "profiles", "r2j_l2_peak.json")))["results"]
         peak = max(r["GBps"] for r in res if r["pattern"] == "seq_cg")
         # the runs pattern at the longest measured run length not above the kernel's mean run length
-        runs = sorted((r["run_records"], r["GBps"]) for r in res if r["pattern"] == "runs")
+        runs = sorted((r["run_records"], r["GBps"]) for r in res
+                      if r["pattern"] == "runs" and r.get("warps_per_sm", 64) == 64)
         pattern_run, pattern = ([x for x in runs if mean_run is None or x[0] <= mean_run] or runs[:1])[-1]
     except Exception:
         pass

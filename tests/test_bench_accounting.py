@@ -22,7 +22,7 @@ WORK = {"tested": 3800.0, "units": 340.0, "cells_aggregated": 300.0, "rows": 60.
 def test_l2_roofline_bytes_and_fracs(bench):
     peaks = json.load(open(os.path.join(ROOT, "profiles", "r2j_l2_peak.json")))["results"]
     seq = max(r["GBps"] for r in peaks if r["pattern"] == "seq_cg")
-    runs = {r["run_records"]: r["GBps"] for r in peaks if r["pattern"] == "runs"}
+    runs = {r["run_records"]: r["GBps"] for r in peaks if r["pattern"] == "runs" and r.get("warps_per_sm") == 64}
     n_info, ms = 1000, 0.01
     out = bench.l2_roofline(n_info, WORK, ms, {"l2_read_bytes": 2.0e9})
     bpw = 16 * 3800 + 16 * 2 * (340 + 300) + 16 * 60 + 32      # record, table entries, row starts, pose
@@ -38,7 +38,7 @@ def test_l2_roofline_bytes_and_fracs(bench):
 
 def test_l2_pattern_roof_follows_run_length(bench):
     peaks = json.load(open(os.path.join(ROOT, "profiles", "r2j_l2_peak.json")))["results"]
-    runs = {r["run_records"]: r["GBps"] for r in peaks if r["pattern"] == "runs"}
+    runs = {r["run_records"]: r["GBps"] for r in peaks if r["pattern"] == "runs" and r.get("warps_per_sm") == 64}
     w = dict(WORK, runs=WORK["tested"] / 9.0)
     assert bench.l2_roofline(10, w, 1.0, None)["pattern_peak"] == runs[8]
     w = dict(WORK, runs=WORK["tested"] / 2.0)       # shorter than any measured run: the shortest

@@ -73,6 +73,67 @@ __global__ void k_runs(const uint4* __restrict__ rec, const int* __restrict__ st
     if (acc == 0x9e3779b9u) sink[0] = acc;
 }
 
+
+// ---- TMA variant of the runs pattern: per warp, each 64-item window's run segments are bulk-copied
+// (cp.async.bulk, one per segment, issued by one lane each) into a shared-memory ring of NBUF windows
+// tracked by one mbarrier per slot; the lanes then read items lane and lane + 32 of the window
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(unsigned long long* b, unsigned c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void bar_expect(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W_%=;\n\t}" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
+}
+
+template <int R, int NBUF, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_runs_tma(const uint4* __restrict__ rec, const int* __restrict__ starts,
+                                                       int nwin, int off, int passes, unsigned* __restrict__ sink) {
+    __shared__ __align__(128) uint4 buf[WPB][NBUF][64];
+    __shared__ __align__(8) unsigned long long bar[WPB][NBUF];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int warp = blockIdx.x * WPB + wid, nwarps = gridDim.x * WPB;
+    if (lane < NBUF) bar_init(&bar[wid][lane], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    unsigned acc = 0;
+    unsigned phase = 0;   // bit k: parity of slot k
+    auto issue = [&](int w, int slot) {
+        const int lo = w * 64 + off, hi = lo + 64;
+        const int r0 = lo / R, r1 = (hi - 1) / R;
+        if (lane == 0) bar_expect(&bar[wid][slot], 64 * 16);
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int r = r0 + lane;
+        if (r <= r1) {
+            const int a = max(lo, r * R), b = min(hi, (r + 1) * R);
+            bulk(&buf[wid][slot][a - lo], rec + __ldg(starts + r) + (a - r * R), (unsigned)(b - a) * 16u, &bar[wid][slot]);
+        }
+    };
+    for (int p = 0; p < passes; ++p) {
+        int k = 0;   // windows of this warp: w = warp + k * nwarps
+        for (int j = 0; j < NBUF - 1 && warp + j * nwarps < nwin; ++j) issue(warp + j * nwarps, j);
+        for (int w = warp; w < nwin; w += nwarps, ++k) {
+            const int slot = k % NBUF;
+            const int wn = w + (NBUF - 1) * nwarps;
+            if (wn < nwin) issue(wn, (k + NBUF - 1) % NBUF);
+            bar_wait(&bar[wid][slot], (phase >> slot) & 1u);
+            phase ^= 1u << slot;
+            const uint4 x = buf[wid][slot][lane], y = buf[wid][slot][lane + 32];
+            acc ^= x.x ^ x.w ^ y.y ^ y.z;
+            __syncwarp();
+        }
+    }
+    if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
 int main(int argc, char** argv) {
     int dev = 0;
     CK(cudaSetDevice(dev));
@@ -127,7 +188,7 @@ int main(int argc, char** argv) {
         uint4* rec;
         CK(cudaMalloc(&rec, nrec * 16));
         CK(cudaMemset(rec, 3, nrec * 16));
-        auto one = [&](int R, auto kern) {
+        auto one = [&](int R, auto kern, int bps = 8, int thr = 256) {
             const long long nruns = (16LL << 20) / R;   // 16M items per pass (256 MB of records read)
             std::vector<int> hs(nruns);
             unsigned long long x = 88172645463325252ull;
@@ -139,14 +200,14 @@ int main(int argc, char** argv) {
             CK(cudaMalloc(&ds, nruns * sizeof(int)));
             CK(cudaMemcpy(ds, hs.data(), nruns * sizeof(int), cudaMemcpyHostToDevice));
             const int nitems = (int)(nruns * R);
-            const int blocks = sms * 8;
+            const int blocks = sms * bps;
             const int passes = 64;
-            kern<<<blocks, threads>>>(rec, ds, nitems, 1, sink);
+            kern<<<blocks, thr>>>(rec, ds, nitems, 1, sink);
             CK(cudaDeviceSynchronize());
             float best = 1e30f;
             for (int rep = 0; rep < 3; ++rep) {
                 CK(cudaEventRecord(a));
-                kern<<<blocks, threads>>>(rec, ds, nitems, passes, sink);
+                kern<<<blocks, thr>>>(rec, ds, nitems, passes, sink);
                 CK(cudaEventRecord(b));
                 CK(cudaEventSynchronize(b));
                 float ms;
@@ -155,13 +216,57 @@ int main(int argc, char** argv) {
             }
             // record bytes only (the start lookups, 4 bytes per R records, are not counted)
             const double gbs = (double)nitems * 16 * passes / (best * 1e-3) / 1e9;
-            printf(", {\"pattern\": \"runs\", \"run_records\": %d, \"mb\": 32, \"blocks_per_sm\": 8, \"GBps\": %.1f}", R, gbs);
+            printf(", {\"pattern\": \"runs\", \"run_records\": %d, \"mb\": 32, \"warps_per_sm\": %d, \"GBps\": %.1f}", R,
+                   bps * thr / 32, gbs);
             CK(cudaFree(ds));
         };
+        auto tma = [&](int R, int nbuf, int wpb, int bps, auto kern) {
+            const int off = 37;
+            const long long nruns = (16LL << 20) / R;
+            std::vector<int> hs(nruns);
+            unsigned long long x = 88172645463325252ull;
+            for (auto& s : hs) {
+                x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+                s = (int)(x % (unsigned long long)(nrec - R));
+            }
+            int* ds;
+            CK(cudaMalloc(&ds, nruns * sizeof(int)));
+            CK(cudaMemcpy(ds, hs.data(), nruns * sizeof(int), cudaMemcpyHostToDevice));
+            const int nwin = (int)((nruns * R - off) / 64);
+            const int blocks = sms * bps;
+            const int passes = 64;
+            kern<<<blocks, wpb * 32>>>(rec, ds, nwin, off, 1, sink);
+            CK(cudaDeviceSynchronize());
+            float best = 1e30f;
+            for (int rep = 0; rep < 3; ++rep) {
+                CK(cudaEventRecord(a));
+                kern<<<blocks, wpb * 32>>>(rec, ds, nwin, off, passes, sink);
+                CK(cudaEventRecord(b));
+                CK(cudaEventSynchronize(b));
+                float ms;
+                CK(cudaEventElapsedTime(&ms, a, b));
+                best = std::min(best, ms);
+            }
+            const double gbs = (double)nwin * 64 * 16 * passes / (best * 1e-3) / 1e9;
+            printf(", {\"pattern\": \"runs_tma\", \"run_records\": %d, \"nbuf\": %d, \"warps_per_sm\": %d, \"GBps\": %.1f}",
+                   R, nbuf, wpb * bps, gbs);
+            CK(cudaFree(ds));
+        };
+        tma(8, 2, 4, 9, k_runs_tma<8, 2, 4>);
+        tma(8, 3, 4, 9, k_runs_tma<8, 3, 4>);
+        tma(8, 4, 4, 9, k_runs_tma<8, 4, 4>);
+        tma(16, 2, 4, 9, k_runs_tma<16, 2, 4>);
+        tma(16, 3, 4, 9, k_runs_tma<16, 3, 4>);
+        tma(16, 4, 4, 9, k_runs_tma<16, 4, 4>);
+        tma(4, 3, 4, 9, k_runs_tma<4, 3, 4>);
+        tma(64, 3, 4, 9, k_runs_tma<64, 3, 4>);
+        tma(16, 3, 8, 8, k_runs_tma<16, 3, 8>);
         one(4, k_runs<4>);
         one(8, k_runs<8>);
         one(16, k_runs<16>);
         one(64, k_runs<64>);
+        one(8, k_runs<8>, 9, 128);
+        one(16, k_runs<16>, 9, 128);
         CK(cudaFree(rec));
     }
     printf("], \"clock_attr_mhz\": %.0f}\n", clk_khz / 1000.0);
