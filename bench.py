@@ -543,9 +543,12 @@ def work_sample(R, m, wl, cam, params, feasible, n=96):
 
 
 # Algorithmic L2 -> SM bytes of the culled gain kernel per info waypoint:
-# a 16-byte record per individually tested Gaussian, two 16-byte z-fastest table entries per (row, z-cell)
-# unit plus two more per unit whose inside x-run is added whole, four 4-byte copy-A column starts per
-# footprint row, and the waypoint's pose (16 B) and FP64 yaw sine / cosine (16 B).
+# a 16-byte record per individually tested Gaussian, the 16-byte z-fastest table entries the (row, z-cell)
+# units need (the run ends: 2 per unit, up to 2 more where the inside x-run differs from them), the copy-A
+# column starts (4 bytes, 2 or 4 per footprint row) and z-occupancy blocks (8 bytes) of the rows -- all
+# three counted in the kernel by rtg_score_debug -- and the waypoint's pose (16 B) and FP64 yaw sine and
+# cosine (16 B).  Older stats without the table counters: 2 entries per unit + 2 per aggregated unit,
+# 16 bytes per row.
 B_REC, B_TAB, B_ROW, B_WP = 16.0, 16.0, 16.0, 32.0
 
 
@@ -554,8 +557,11 @@ def l2_roofline(n_info, work, ms, k_ncu):
     < 0.1 % of the L2 reads), so the memory roof is the L2 -> SM read bandwidth, measured on B200 by
     tools/l2_peak.cu (profiles/r2j_l2_peak.json): sequential 16-byte loads through L2 (the hardware roof)
     and the kernel's own access pattern (runs of 8 consecutive 16-byte records at random offsets)."""
-    bytes_wp = (B_REC * work["tested"] + B_TAB * 2.0 * (work["units"] + work["cells_aggregated"])
-                + B_ROW * work.get("rows", 0.0) + B_WP)
+    if "unit_table_entries" in work:   # counted in the kernel (rtg_score_debug)
+        bytes_wp = (B_REC * work["tested"] + B_TAB * work["unit_table_entries"] + work["row_table_bytes"] + B_WP)
+    else:
+        bytes_wp = (B_REC * work["tested"] + B_TAB * 2.0 * (work["units"] + work["cells_aggregated"])
+                    + B_ROW * work.get("rows", 0.0) + B_WP)
     ach = n_info * bytes_wp / (ms / 1e3) / 1e9
     mean_run = (work["tested"] / work["runs"]) if work.get("runs") else None
     peak = pattern = pattern_run = None
@@ -578,7 +584,9 @@ def l2_roofline(n_info, work, ms, k_ncu):
                             "access pattern; the longest measured run length not above mean_run_records)",
            "mean_run_records": mean_run,
            "bytes_per_wp": bytes_wp, "per_unit_bytes": {"record": B_REC, "table_entry": B_TAB, "row": B_ROW,
-                                                      "waypoint": B_WP}}
+                                                      "waypoint": B_WP},
+           "bytes_basis": "16 B per tested record + 16 B per unit table entry + row table bytes (kernel counters) "
+                          "+ 32 B pose and yaw trig per waypoint"}
     if k_ncu and k_ncu.get("l2_read_bytes"):
         out["ncu_l2_read_bytes"] = k_ncu["l2_read_bytes"]
         out["algorithmic_share_of_l2_reads"] = n_info * bytes_wp / k_ncu["l2_read_bytes"]

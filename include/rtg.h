@@ -324,7 +324,8 @@ rtg_status rtg_best_async(const double* utility, int K, long long index_base, rt
  * pairs tested individually, (row, z-cell) x-runs added whole, collision candidates tested,
  * visibility pairs tested in the horizontally straddling flanks of rows, (row, z-cell) units cut,
  * individually tested pairs visible, footprint rows classified, tested runs (contiguous record
- * ranges queued for individual tests), 0, 0 (reserved)}
+ * ranges queued for individual tests), 16-byte table entries loaded by the (row, z-cell) units,
+ * bytes of column starts and z-occupancy blocks loaded by the footprint rows}
  * (culled mode; dense mode fills the first two).  Synchronises the stream.
  */
 enum { RTG_DEBUG_STATS = 12 };

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
     __syncwarp();
     const int L = *list_count;
     unsigned nref = 0;
-    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0, nrow = 0, nruns = 0;
+    unsigned long long ntest = 0, nagg = 0, nunit = 0, nflank = 0, nvis = 0, nrow = 0, nruns = 0, ntab = 0, nrowb = 0;
     for (;;) {
         int e = 0;
         if (lane == 0) e = atomicAdd(counter, 1);
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                         // 128-bit entries {start, prefixes}: the x-run ends' starts come with the prefixes
                         const int4 e0 = __ldg(tp + q0 * g.nz), e3 = __ldg(tp + (q1 + 1) * g.nz);
                         const int a0 = e0.x, a3 = e3.x;
+                        if (kStats) ntab += 2u + (unsigned)(in && j0 != q0) + (unsigned)(in && j1 != q1);
                         int a1 = a3, a2 = a3;   // no inside run: [q0, q1] is tested whole
                         if (in) {
                             const int4 lo = j0 == q0 ? e0 : __ldg(tp + j0 * g.nz);
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                                   "flank table index");
                         s0 = __ldg(sa + p0);
                         l0 = __ldg(sa + (in ? ri0 : p1 + 1)) - s0;
+                        if (kStats) nrowb += in ? 16u : 8u;   // copy-A column starts (4 bytes each)
                         if (in) {
                             s1 = __ldg(sa + ri1 + 1);
                             l1 = __ldg(sa + p1 + 1) - s1;
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
                                     ohi = max(ohi, o[u].y);
                                 }
                             }
+                            if (kStats) nrowb += 8u * (unsigned)(bend - ri0 / kZoccX + 1);   // z-occupancy blocks
                             izlo = max(zlo, olo);
                             nu = max(0, min(zhi, ohi) - izlo + 1);
                         }
@@ -508,6 +511,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
             nvis += __shfl_xor_sync(kFullG, nvis, o);
             nrow += __shfl_xor_sync(kFullG, nrow, o);
             nruns += __shfl_xor_sync(kFullG, nruns, o);
+            ntab += __shfl_xor_sync(kFullG, ntab, o);
+            nrowb += __shfl_xor_sync(kFullG, nrowb, o);
         }
         if (lane == 0) {
             if (nref) atomicAdd(&stats[1], (unsigned long long)nref);
@@ -518,6 +523,8 @@ __global__ void __launch_bounds__(kWarpsG * 32, RTG_GAIN_MINB) k_gain_culled(
             atomicAdd(&stats[7], nvis);
             atomicAdd(&stats[8], nrow);
             atomicAdd(&stats[9], nruns / 32);   // warp-uniform: every lane counted the warp's runs
+            atomicAdd(&stats[10], ntab);
+            atomicAdd(&stats[11], nrowb);
         }
     }
 }

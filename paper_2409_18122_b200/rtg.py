@@ -673,7 +673,8 @@ def score_debug(m: Map, tr: Traj, camera, params: ScoreParams, pair_mask: bool =
     return dict(wp_col=wp_col, wp_gain=wp_gain, wp_nh=wp_nh, wp_nl=wp_nl, pair_mask=mask,
                 stats=dict(col_refined=stats[0], vis_refined=stats[1], tested=stats[2], cells_aggregated=stats[3],
                            col_tested=stats[4], tested_flank=stats[5], units=stats[6], tested_visible=stats[7],
-                           rows=stats[8], runs=stats[9]))
+                           rows=stats[8], runs=stats[9], unit_table_entries=stats[10],
+                           row_table_bytes=stats[11]))
 
 
 def unpack_pair_mask(mask, KT: int, N: int) -> np.ndarray:

@@ -36,6 +36,12 @@ def test_l2_roofline_bytes_and_fracs(bench):
     assert out["algorithmic_share_of_l2_reads"] == pytest.approx(n_info * bpw / 2.0e9)
 
 
+def test_l2_roofline_counted_table_bytes(bench):
+    w = dict(WORK, unit_table_entries=700.0, row_table_bytes=1500.0)
+    out = bench.l2_roofline(1000, w, 0.01, None)
+    assert out["bytes_per_wp"] == pytest.approx(16 * 3800 + 16 * 700 + 1500 + 32)
+
+
 def test_l2_pattern_roof_follows_run_length(bench):
     peaks = json.load(open(os.path.join(ROOT, "profiles", "r2j_l2_peak.json")))["results"]
     runs = {r["run_records"]: r["GBps"] for r in peaks if r["pattern"] == "runs" and r.get("warps_per_sm") == 64}

@@ -178,6 +178,13 @@ def test_dense_equals_culled_bitwise(R, room):
     assert np.array_equal(a["wp_gain"].view(np.int64), b["wp_gain"].view(np.int64))
     assert a["best"] == b["best"]
     assert b["stats"]["cells_aggregated"] > 0 and b["stats"]["units"] > 0
+    # the roofline's byte counters (bench.py roofline.l2): a unit with a possibly visible x-run loads its
+    # two run ends and at most two more entries; every tested run holds >= 1 record; a row with a
+    # possibly visible x-interval loads 2 or 4 column starts (+ z-occupancy blocks when it has an inside)
+    st = b["stats"]
+    assert 0 < st["unit_table_entries"] <= 4 * st["units"]
+    assert 0 < st["runs"] <= st["tested"]
+    assert 0 < st["row_table_bytes"]
 
 
 @pytest.mark.parametrize("variant,stride,lam,tau,rule", [
