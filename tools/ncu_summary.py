@@ -3,6 +3,7 @@
 usage:
   python tools/ncu_summary.py launches <launches.csv> <out.txt>
   python tools/ncu_summary.py full <report.ncu-rep> <out.txt> [traffic_key]
+  python tools/ncu_summary.py dram <metrics.csv> <out.txt>   (tools/ncu_mapbuild.sh: per-launch DRAM bytes)
 The `full` mode also records dram bytes per launch of the captured kernel into
 profiles/traffic.json under traffic_key (e.g. outdoor/culled/stride1), which bench.py reports
 as roofline.traffic.
@@ -121,6 +122,33 @@ def full(rep, out, key=None):
         lines.append("\n## hottest source lines: share of instructions executed, share of stall samples")
         for n, st, f, ln, txt in sorted(rows, reverse=True)[:25]:
             lines.append(f"{n / ti * 100:5.1f}% inst {st / ts * 100:5.1f}% stall  {f}:{ln}  {txt}")
+    # the L1 load path by source line: global tag requests and shared-memory wavefronts (both take
+    # l1tex LSU data-pipe wavefronts, the kernel's co-limit)
+    cur, hdr, lsu = None, None, []
+    for r in csv.reader(io.StringIO(src)):
+        if r and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if not r or not r[0].isdigit() or hdr is None:
+            continue
+        try:
+            tag = float(r[hdr.index("L1 Tag Requests Global")] or 0)
+            shw = float(r[hdr.index("L1 Wavefronts Shared")] or 0)
+            l2s = float(r[hdr.index("L2 Theoretical Sectors Global")] or 0)
+        except (ValueError, IndexError):
+            continue
+        if tag or shw:
+            lsu.append((tag + shw, tag, shw, l2s, cur, int(r[0]), r[1].strip()[:72]))
+    if lsu:
+        tt = sum(x[1] for x in lsu) or 1.0
+        tw = sum(x[2] for x in lsu) or 1.0
+        lines.append(f"\n## L1 load path by source line: global tag requests {tt:.3g} (share), shared wavefronts "
+                     f"{tw:.3g} (share), L2 sectors")
+        for tot, tag, shw, l2s, f, ln, txt in sorted(lsu, reverse=True)[:20]:
+            lines.append(f"{tag / tt * 100:5.1f}% tag {shw / tw * 100:5.1f}% shw {l2s:9.3g} sec  {f}:{ln}  {txt}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if key:
@@ -130,8 +158,35 @@ def full(rep, out, key=None):
         json.dump(t, open(tpath, "w"), indent=1, sort_keys=True)
 
 
+def dram(path, out):
+    """Per-launch duration and DRAM bytes of a `--metrics` capture (cold-cache, serialised launches)."""
+    rows = list(csv.reader(open(path)))
+    h0 = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[h0]
+    ix = {k: i for i, k in enumerate(hdr)}
+    per = collections.OrderedDict()
+    for r in rows[h0 + 1:]:
+        if len(r) < len(hdr):
+            continue
+        per.setdefault((int(r[ix["ID"]]), r[ix["Kernel Name"]].split("(")[0]), {})[r[ix["Metric Name"]]] = (
+            r[ix["Metric Unit"]], float(r[ix["Metric Value"]].replace(",", "")))
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6,
+            "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}
+    lines = [f"# per-launch DRAM traffic ({os.path.basename(path)}; ncu --metrics, cold cache, serialised)",
+             f"{'id':>4s} {'kernel':44s} {'us':>8s} {'rd MB':>8s} {'wr MB':>8s} {'TB/s':>6s}"]
+    for (i, name), m in per.items():
+        g = lambda k: m[k][1] * mult.get(m[k][0], 1) if k in m else 0.0
+        t, rd, wr = g("gpu__time_duration.sum"), g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
+        lines.append(f"{i:4d} {name.split('::')[-1][:44]:44s} {t * 1e6:8.1f} {rd / 1e6:8.1f} {wr / 1e6:8.1f} "
+                     f"{(rd + wr) / t / 1e12 if t else 0:6.2f}")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines[:30]))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "dram":
+        dram(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
