@@ -629,13 +629,32 @@ def roofline(phase, ms, wl, n_feasible, stride, mode, clock, hbm_peak, work, ncu
            "traffic": tr, "phase": phase, "kernel": kname, "kernel_ms": ms,
            "peak_basis": "148 SMs x 128 FP32 lanes x measured SM clock (B200_PROFILING.md unit counts)",
            "work_units": units, "work_per_waypoint": work}
+    l2 = None
     if phase == "visibility_gain" and mode == "culled" and work is not None:
-        out["l2"] = l2_roofline(n_info, work, ms, k_ncu)
+        l2 = out["l2"] = l2_roofline(n_info, work, ms, k_ncu)
     if k_ncu:
         out["ncu"] = {k: v for k, v in k_ncu.items() if k != "dram_bytes"}
         wi = k_ncu.get("warp_inst")
         if wi:   # executed lane slots per launch vs the algorithmic lane instructions above
             out["ncu"]["algorithmic_share_of_executed"] = lane_instr / (32.0 * wi)
+    if l2 is not None and l2.get("peak") and n_info > 0:
+        # "the roofline fraction is the achieved rate over min(FP32 peak, arithmetic intensity x
+        # bandwidth)"; the culled traversal's records and tables are L2-resident, so the bandwidth is the
+        # measured L2 -> SM roof.  When that product is the smaller roof the line reports it as the primary
+        # (frac = achieved bytes / L2 peak = achieved lane-instr / (AI x L2 peak)); the FP32 one stays under "alu"
+        ai = lane_instr / (n_info * l2["bytes_per_wp"])            # lane instructions per algorithmic byte
+        roof_l2 = ai * l2["peak"] * 1e9 / 1e12                     # T lane-instr/s
+        rule = {"definition": "SURVEY 8(d): frac = achieved / min(FP32 peak, arithmetic intensity x bandwidth)",
+                "ai_lane_instr_per_byte": ai, "fp32_roof": peak_ti, "l2_roof": roof_l2, "unit": "T lane-instr/s",
+                "binding": "l2" if roof_l2 < peak_ti else "alu"}
+        if roof_l2 < peak_ti:
+            alu = {k: out.pop(k) for k in ("bound", "achieved", "peak", "unit", "frac", "peak_basis")}
+            prim = {k: l2[k] for k in ("bound", "achieved", "peak", "unit", "frac", "peak_basis")}
+            rest = {k: v for k, v in out.items() if k != "l2"}
+            out = dict(prim, traffic=tr, roof_rule=rule, alu=alu, l2=l2, **{k: v for k, v in rest.items()
+                                                                            if k != "traffic"})
+        else:
+            out["roof_rule"] = rule
     return out
 
 

@@ -61,8 +61,32 @@ def test_alu_roofline_uses_survey_units(bench):
     w = dict(WORK)
     out = bench.roofline("visibility_gain", 2.0, WL, 10, 1, "culled", {"sm_mhz": 1965.0}, 6544.0, w, None)
     lane = 10 * 100 * (10 * 3800 + 25 * 340 + 25 * 60)      # SURVEY.md:709: 10 / 25 / 25 per test / unit / row
-    assert out["bound"] == "alu"
-    assert out["achieved"] == pytest.approx(lane / 2e-3 / 1e12)
-    assert out["peak"] == pytest.approx(148 * 128 * 1965e6 / 1e12)
-    assert out["frac"] == pytest.approx(out["achieved"] / out["peak"])
+    alu = out["alu"]
+    assert alu["bound"] == "alu"
+    assert alu["achieved"] == pytest.approx(lane / 2e-3 / 1e12)
+    assert alu["peak"] == pytest.approx(148 * 128 * 1965e6 / 1e12)
+    assert alu["frac"] == pytest.approx(alu["achieved"] / alu["peak"])
     assert out["l2"]["bound"] == "l2"
+
+
+def test_primary_roof_is_survey_min_roof(bench):
+    """frac = achieved / min(FP32 peak, arithmetic intensity x bandwidth); the culled gain
+    kernel's bandwidth is the measured L2 roof, and with SURVEY's per-unit costs (10 lane instructions per
+    16-byte record) its product with the intensity is the smaller roof."""
+    class WL:
+        T, N, K = 100, 1000, 10
+
+    out = bench.roofline("visibility_gain", 2.0, WL, 10, 1, "culled", {"sm_mhz": 1965.0}, 6544.0, dict(WORK), None)
+    rule, alu, l2 = out["roof_rule"], out["alu"], out["l2"]
+    n_info = 10 * 100
+    lane = n_info * (10 * 3800 + 25 * 340 + 25 * 60)
+    ai = lane / (n_info * l2["bytes_per_wp"])
+    assert rule["ai_lane_instr_per_byte"] == pytest.approx(ai)
+    assert rule["l2_roof"] == pytest.approx(ai * l2["peak"] * 1e9 / 1e12)
+    assert rule["fp32_roof"] == pytest.approx(alu["peak"])
+    assert rule["binding"] == "l2" and rule["l2_roof"] < rule["fp32_roof"]
+    # the primary fields are the L2 roof's; its fraction equals achieved lane instructions over AI x L2 peak
+    assert out["bound"] == "l2" and out["unit"] == "GB/s"
+    assert out["achieved"] == pytest.approx(l2["achieved"]) and out["peak"] == pytest.approx(l2["peak"])
+    assert out["frac"] == pytest.approx(alu["achieved"] / rule["l2_roof"])
+    assert out["frac"] == pytest.approx(min(1.0, alu["achieved"] / min(rule["fp32_roof"], rule["l2_roof"])))
