@@ -398,30 +398,46 @@ def main():
                  "eager_ms_median": ms_eager, "graph_ms_median": ms_graph}
         del g
         m.close()
-    if graph is not None and not Kv:
+    if graph is not None:
         # the whole cycle on a layout map (grids from the workload's extents, rebuilt without a host
-        # synchronisation): eager, and captured with the score and the argmax into one graph
+        # synchronisation): eager, and captured with the score and the argmax into one graph (the scale
+        # config's views on a second stream forked after the rebuild: concurrent branches of the graph)
         gbox, cbox, rb_b, rho_b = layout_bounds(wl)
         lm = R.LayoutMap(N, gbox, cbox, rb_b, rho_b, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g,
                          collide_rule=wl.robot.rule, device=local_dev, options=map_opts)
+        tvw = R.Traj.wrap(*dviews, device=local_dev) if Kv else None
+        vbo = torch.empty(2, dtype=torch.float64, device=dev) if Kv else None
 
         def eager_cycle():
             lm.rebuild(*dmap)
+            if Kv:
+                vstream.wait_stream(stream)
+                R.score(lm, tvw, cam, vparams, *vouts, stream=vstream)
+                R.best_async(vouts[3], vbo, stream=vstream)
             R.score(lm, tr, cam, params, *outs)
             R.best_async(outs[3], bo)
+            if Kv:
+                stream.wait_stream(vstream)
 
-        cg = R.CycleGraph(lm, dmap, tr, cam, params)
+        cg = R.CycleGraph(lm, dmap, tr, cam, params, views=tvw, vparams=vparams)
         ms_ce, ms_cg = t_of(eager_cycle), t_of(cg.replay)
         lm.check()
         assert R.read_best(bo) == R.read_best(cg.best)
+        if Kv:
+            assert R.read_best(vbo) == R.read_best(cg.vbest)
         if world == 1:
             assert R.read_best(cg.best) == (res[0], res[1])
-        graph["cycle"] = {"scope": "layout-map rebuild + rtg_score + rtg_best_async: the whole planning cycle "
+            if Kv:
+                assert R.read_best(cg.vbest) == (res[2], res[3])
+        graph["cycle"] = {"scope": "layout-map rebuild + rtg_score + rtg_best_async" + (" (+ the views on a forked "
+                                   "stream)" if Kv else "") + ": the whole planning cycle "
                                    "without a host synchronisation (rtg_map_create_layout, grids from the "
                                    "workload's extents)",
                           "eager_ms_median": ms_ce, "graph_ms_median": ms_cg,
                           "standard_cycle_ms_median": step_stats["median"]}
         del cg
+        if tvw is not None:
+            tvw.close()
         lm.close()
     if graph is not None:
         tr.close()

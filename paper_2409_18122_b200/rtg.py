@@ -366,22 +366,38 @@ class CycleGraph:
     trajectory buffers then hold (refill both in place; the Gaussian count n is fixed).  One eager cycle
     precedes the capture."""
 
-    def __init__(self, lmap: "LayoutMap", map_arrays, tr: "Traj", camera, params: ScoreParams, index_base: int = 0):
+    def __init__(self, lmap: "LayoutMap", map_arrays, tr: "Traj", camera, params: ScoreParams, index_base: int = 0,
+                 views: Optional["Traj"] = None, vparams: Optional[ScoreParams] = None, vindex_base: int = 0):
         torch = _torch()
-        if params.mode != MODE_CULLED:
+        if params.mode != MODE_CULLED or (views is not None and (vparams is None or vparams.mode != MODE_CULLED)):
             raise ValueError("CycleGraph: culled mode only (dense mode reads the list length on the host)")
         dev = torch.device("cuda", lmap.device)
-        K = tr.K
-        self.outs = (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
-                     torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
+
+        def outs_for(K):
+            return (torch.empty(K, dtype=torch.int32, device=dev), torch.empty(K, dtype=torch.uint8, device=dev),
+                    torch.empty(K, dtype=torch.float64, device=dev), torch.empty(K, dtype=torch.float64, device=dev))
+
+        self.outs = outs_for(tr.K)
         self.best = torch.empty(2, dtype=torch.float64, device=dev)
-        self._keep = (lmap, tuple(map_arrays), tr)
+        # gain-only views (the scale config): scored on a second stream forked after the rebuild, joined
+        # before the cycle ends -- inside the graph, the two scorings are concurrent branches
+        self.vouts = outs_for(views.K) if views is not None else None
+        self.vbest = torch.empty(2, dtype=torch.float64, device=dev) if views is not None else None
+        vstream = torch.cuda.Stream(device=dev) if views is not None else None
+        self._keep = (lmap, tuple(map_arrays), tr, views, vstream)
         cam = camera if isinstance(camera, Camera) else make_camera(camera)
 
         def cycle():
             lmap.rebuild(*map_arrays)
+            cur = torch.cuda.current_stream(dev)
+            if views is not None:
+                vstream.wait_stream(cur)
+                score(lmap, views, cam, vparams, *self.vouts, stream=vstream)
+                best_async(self.vouts[3], self.vbest, vindex_base, stream=vstream)
             score(lmap, tr, cam, params, *self.outs)
             best_async(self.outs[3], self.best, index_base)
+            if views is not None:
+                cur.wait_stream(vstream)
 
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
@@ -395,7 +411,8 @@ class CycleGraph:
             cycle()
 
     def replay(self):
-        """Enqueue one replay on the current stream; returns (first_col, feasible, gain, utility, best)."""
+        """Enqueue one replay on the current stream; returns (first_col, feasible, gain, utility, best)
+        (the views' outputs and best are in .vouts / .vbest)."""
         self.graph.replay()
         return self.outs + (self.best,)
 
@@ -593,7 +610,8 @@ class ScoreGraph:
             best_async(self.outs[3], self.best, index_base)
 
     def replay(self):
-        """Enqueue one replay on the current stream; returns (first_col, feasible, gain, utility, best)."""
+        """Enqueue one replay on the current stream; returns (first_col, feasible, gain, utility, best)
+        (the views' outputs and best are in .vouts / .vbest)."""
         self.graph.replay()
         return self.outs + (self.best,)
 

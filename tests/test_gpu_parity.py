@@ -1043,3 +1043,51 @@ def test_cycle_graph_replay_equals_eager(R, room):
     del cg
     tr.close()
     lm.close()
+
+
+@pytest.mark.gpu
+def test_cycle_graph_with_views_equals_eager(R, room):
+    """The cycle graph with gain-only views on a forked stream (the scale config's shape, R.CycleGraph
+    views=): the trajectories' and the views' outputs and bests equal eager rtg_map_create scoring bit for
+    bit, also after the view poses are refilled in place."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(11)
+    g, c, rb, rho = _layout_of(room)
+    lm = R.LayoutMap(room.N, g, c, rb, rho, r_robot=room.robot.r_robot, lambda_g=room.robot.lambda_g)
+    arrs = _dev_map_arrays(room, dev)
+    k = np.arange(0, room.K, 4)
+    tr = R.Traj.wrap(*[torch.from_numpy(np.ascontiguousarray(a[k])).to(dev) for a in (room.x, room.y, room.z, room.yaw)])
+    nv = 300
+
+    def poses():
+        lo, hi = room.means.min(1), room.means.max(1)
+        return [rng.uniform(lo[0] + 1, hi[0] - 1, (nv, 1)), rng.uniform(lo[1] + 1, hi[1] - 1, (nv, 1)),
+                np.full((nv, 1), 0.5), rng.uniform(-np.pi, np.pi, (nv, 1))]
+
+    vbufs = [torch.from_numpy(a.astype(np.float32)).to(dev) for a in poses()]
+    tv = R.Traj.wrap(*vbufs)
+    p = R.make_params()
+    vp = R.make_params(flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
+    cg = R.CycleGraph(lm, arrs, tr, room.camera, p, views=tv, vparams=vp)
+    ref = R.map_from_workload(room)
+    for it in range(3):
+        if it:
+            for b, a in zip(vbufs, poses()):
+                b.copy_(torch.from_numpy(a.astype(np.float32)))
+        outs = cg.replay()
+        torch.cuda.synchronize()
+        lm.check()
+        eager = R.score(ref, tr, room.camera, p)
+        veager = R.score(ref, tv, room.camera, vp)
+        for a, b in zip(outs[:4], eager):
+            assert torch.equal(a.view(torch.uint8), b.view(torch.uint8)), it
+        for a, b in zip(cg.vouts, veager):
+            assert torch.equal(a.view(torch.uint8), b.view(torch.uint8)), it
+        assert R.read_best(outs[4]) == R.best(eager[3])
+        assert R.read_best(cg.vbest) == R.best(veager[3])
+        assert int((veager[2] > 0).sum()) > nv // 4, "the views see the room"
+    ref.close()
+    del cg
+    tr.close()
+    tv.close()
+    lm.close()

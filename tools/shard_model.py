@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--cells", default=None, help="visibility grid 'hy,hx,hz' [m] (rtg_map_options)")
     ap.add_argument("--z-centre", default="none", help="as bench.py: 'none', 'camera' or a height [m]")
+    ap.add_argument("--graph", action="store_true",
+                    help="each rank's cycle as one CUDA graph: layout map rebuilt without a host synchronisation "
+                         "+ score + argmax (+ the views on a forked stream), R.CycleGraph")
     args = ap.parse_args()
     wl = W.make(args.config)
     dev = torch.device("cuda", 0)
@@ -90,12 +93,24 @@ def main():
             m.close()
             return r
 
+        cg = None
+        if args.graph:
+            # the rank's whole cycle as one CUDA graph (no host synchronisation: a layout map from the
+            # workload's extents, as bench.py's cuda_graph.cycle); per-phase timers do not run in a graph
+            import bench as BN
+            gbox, cbox, rb_b, rho_b = BN.layout_bounds(wl)
+            lm = R.LayoutMap(wl.N, gbox, cbox, rb_b, rho_b, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g,
+                             collide_rule=wl.robot.rule, options=opts)
+            gtr = R.Traj.wrap(*traj)
+            gtv = R.Traj.wrap(*views) if views is not None else None
+            cg = R.CycleGraph(lm, dmap, gtr, cam, params, views=gtv, vparams=vparams if views is not None else None)
+            step = cg.replay   # noqa: F811
         for _ in range(3):
             step()
         ms = []
         R.profile_read(reset=True)
-        R.profile_enable(True)
-        prof_on[0] = True
+        R.profile_enable(cg is None)
+        prof_on[0] = cg is None
         for _ in range(args.steps):
             flush.fill_(1.0)
             torch.cuda.synchronize()
@@ -108,9 +123,17 @@ def main():
         R.profile_enable(False)
         prof_on[0] = False
         prof = R.profile_read(reset=True)
+        if cg is not None:
+            lm.check()
+            del cg
+            gtr.close()
+            if gtv is not None:
+                gtv.close()
+            lm.close()
         med = statistics.median(ms)
         base = med if base is None else base
-        print(json.dumps({"config": args.config, "cells": args.cells, "gain_z_centre": zc, "ranks": n, "trajectories_per_rank": K,
+        print(json.dumps({"config": args.config, "cells": args.cells, "gain_z_centre": zc, "graph": args.graph,
+                          "ranks": n, "trajectories_per_rank": K,
                           "views_per_rank": len(views[0]) if views is not None else 0,
                           "per_rank_ms_median": med, "per_rank_ms_min": min(ms),
                           "modelled_speedup": base / med,
