@@ -12,6 +12,7 @@
 //  a2  classification over the gain-eligible set in ORIGINAL input order (deterministic FP64
 //      two-pass mean / population std), class increments and exact fixed-point u per
 //      record, and the exclusive prefixes over the records that let the culled kernel add whole x-runs.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -401,16 +402,6 @@ __global__ void k_scatter_both(long long n, const float* __restrict__ means, con
     }
 }
 
-// NaN padding of the records [from, to) (gidx: NULL for copy A); dfrom: a device count raising from
-__global__ void k_pad_gain(GRec* grec, int* gidx, long long from, long long to, const int* __restrict__ dfrom) {
-    long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < to && (!dfrom || i >= *dfrom)) {
-        const float nan = __int_as_float(0x7fc00000);
-        grec[i] = GRec{nan, nan, nan, 0u};
-        if (gidx) gidx[i] = -1;
-    }
-}
-
 // copy A from copy B: copy A is sorted by (iy, x, iz), so column (iy, x) starts at gstartA (the
 // exclusive scan of the column counts) and holds its cells (iy, iz, x) in iz order, each a contiguous
 // block of copy B at tabB[(iy, x, iz)]; one thread per column moves them
@@ -443,23 +434,23 @@ __global__ void k_derive_cols(long long ncols, int nx, int nz, const int* __rest
     }
 }
 
-__global__ void k_pad_col(CRec* crec, CMat* cmat, CSrc* csrc, long long from, long long to,
-                          const int* __restrict__ dfrom) {
-    long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < to && (!dfrom || i >= *dfrom)) {
-        float nan = __int_as_float(0x7fc00000);
-        crec[i] = CRec{nan, nan, nan, -1.f};
-        CMat z;
-        for (int j = 0; j < 12; ++j) z.m[j] = 0.f;
-        z.m[9] = __int_as_float(-1);
-        cmat[i] = z;
-        CSrc zs;
-        for (int j = 0; j < 4; ++j) zs.q[j] = 0.f;
-        zs.q[0] = 1.f;
-        for (int j = 0; j < 3; ++j) zs.s[j] = 1.f;
-        zs.pad = 0.f;
-        csrc[i] = zs;
+// NaN padding of the visibility records [g0, gto) of both copies (gidx -1) and of the collision records
+// [c0, cto) in one launch, g0 / c0 the device counts when given (a layout map's rebuild: grid-stride from
+// there, so a rebuild that fills its capacity pads nothing).  Only the collision record's sphere
+// {NaN, -1} is written: the matrix and FP32 sources are read only after a passed sphere test.
+__global__ void k_pad_records(GRec* __restrict__ recA, GRec* __restrict__ recB, int* __restrict__ gidx,
+                              long long gfrom, long long gto, const int* __restrict__ dg, CRec* __restrict__ crec,
+                              long long cfrom, long long cto, const int* __restrict__ dc) {
+    const long long g0 = dg ? max(gfrom, (long long)*dg) : gfrom;
+    const long long c0 = dc ? max(cfrom, (long long)*dc) : cfrom;
+    const long long stride = (long long)gridDim.x * blockDim.x, t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const float nan = __int_as_float(0x7fc00000);
+    for (long long i = g0 + t; i < gto; i += stride) {
+        recB[i] = GRec{nan, nan, nan, 0u};
+        recA[i] = GRec{nan, nan, nan, 0u};
+        gidx[i] = -1;
     }
+    for (long long i = c0 + t; i < cto; i += stride) crec[i] = CRec{nan, nan, nan, -1.f};
 }
 
 // ------------------------------------------------------------------ classification (a2)
@@ -1210,18 +1201,16 @@ static rtg_status build_records(rtg_map_s* m, const float* means, const float* q
                                                              m->crec, m->cmat, m->csrc);
         }
     }
-    // NaN padding after the records (from the device counts on a layout map: all of [0, pad) is launched)
-    if (m->n_gain_pad > (dn_gain ? 0 : m->n_gain)) {
-        const long long from = dn_gain ? 0 : m->n_gain;
-        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - from, 256), 256, 0, st>>>(
-                           m->grec + m->n_gain_pad, m->gidx, from, m->n_gain_pad, dn_gain);
-        note_launch(), k_pad_gain<<<nblocks(m->n_gain_pad - from, 256), 256, 0, st>>>(
-                           m->grec, nullptr, from, m->n_gain_pad, dn_gain);
-    }
-    if (m->n_col_pad > (dn_col ? 0 : m->n_col)) {
-        const long long from = dn_col ? 0 : m->n_col;
-        note_launch(), k_pad_col<<<nblocks(m->n_col_pad - from, 256), 256, 0, st>>>(m->crec, m->cmat, m->csrc, from,
-                                                                                    m->n_col_pad, dn_col);
+    // NaN padding after the records (a layout map: after its device counts, whatever the capacity)
+    {
+        const long long gfrom = dn_gain ? 0 : m->n_gain, cfrom = dn_col ? 0 : m->n_col;
+        const long long span = std::max(m->n_gain_pad - gfrom, m->n_col_pad - cfrom);
+        if (span > 0) {
+            const unsigned pb = nblocks(span, 256) > 1184 ? 1184 : nblocks(span, 256);
+            note_launch(), k_pad_records<<<pb, 256, 0, st>>>(m->grec, m->grec + m->n_gain_pad, m->gidx, gfrom,
+                                                             m->n_gain_pad, dn_gain, m->crec, cfrom, m->n_col_pad,
+                                                             dn_col);
+        }
     }
     MAP_CK(cudaGetLastError());
     // --- default classification (k = 1/2, derived thresholds); copy A derived from copy B

@@ -1,8 +1,10 @@
 """GPU timeline of one outdoor planning cycle (torch.profiler / CUPTI kernel activity): every kernel
 and memcpy/memset with its start offset and duration, and the idle gaps between them.
 
-usage: python tools/timeline.py [--config outdoor] [--tree | --score eager|graph]
+usage: python tools/timeline.py [--config outdoor] [--tree | --score eager|graph | --cycle eager|graph [--ranks N]]
   --tree: one rtg_plan_tree call (depth 8, beam 4096, goal 5 m ahead) on the config's map instead
+  --cycle: the whole cycle on a layout map (rebuild + score + best, views on a forked stream), eager or as
+           one CUDA graph (R.CycleGraph); --ranks N scores rank 0's interleaved 1/N shard (tools/shard_model.py)
 """
 import argparse
 import os
@@ -23,8 +25,12 @@ def main():
     ap.add_argument("--score", choices=("eager", "graph"), default=None,
                     help="only the scoring part (rtg_score + rtg_best_async) on a built map, eager or as one "
                          "CUDA-graph replay (R.ScoreGraph)")
+    ap.add_argument("--cycle", choices=("eager", "graph"), default=None)
+    ap.add_argument("--ranks", type=int, default=1)
     args = ap.parse_args()
     wl = W.make(args.config)
+    if args.ranks > 1:
+        wl = W.subset_trajectories(wl, np.arange(0, wl.K, args.ranks))
     dev = torch.device("cuda", 0)
     to_dev = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     dmap = [to_dev(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)]
@@ -51,7 +57,40 @@ def main():
         if args.score == "graph":
             sg = R.ScoreGraph(score_map, score_tr, cam, params)
 
+    cg = None
+    if args.cycle:
+        import bench as BN
+        gbox, cbox, rb_b, rho_b = BN.layout_bounds(wl)
+        lm = R.LayoutMap(wl.N, gbox, cbox, rb_b, rho_b, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g,
+                         collide_rule=wl.robot.rule)
+        ctr = R.Traj.wrap(*dtraj)
+        ctv = None
+        if wl.views is not None:
+            vi = np.arange(0, wl.views["x"].shape[0], args.ranks)
+            ctv = R.Traj.wrap(*[to_dev(wl.views[c][vi]) for c in ("x", "y", "z", "yaw")])
+        vparams = R.make_params(mode=R.MODE_CULLED, flags=R.SCORE_FULL_GAIN | R.SCORE_NO_COLLISION)
+        cg = R.CycleGraph(lm, dmap, ctr, cam, params, views=ctv, vparams=vparams if ctv is not None else None)
+        if args.cycle == "eager":
+            cycle_eager = cg.graph   # keep the graph alive; the eager path re-issues the same calls
+            vst = torch.cuda.Stream(device=dev)
+            vbo = torch.empty(2, dtype=torch.float64, device=dev)
+            bo2 = torch.empty(2, dtype=torch.float64, device=dev)
+
     def step():
+        if cg is not None:
+            if args.cycle == "graph":
+                return cg.replay()
+            cur = torch.cuda.current_stream()
+            lm.rebuild(*dmap)
+            if ctv is not None:
+                vst.wait_stream(cur)
+                R.score(lm, ctv, cam, vparams, *cg.vouts, stream=vst)
+                R.best_async(cg.vouts[3], vbo, stream=vst)
+            R.score(lm, ctr, cam, params, *outs)
+            R.best_async(outs[3], bo2)
+            if ctv is not None:
+                cur.wait_stream(vst)
+            return None
         if args.tree:
             return tree_step()
         if sg is not None:
@@ -80,6 +119,8 @@ def main():
     ev.sort(key=lambda e: e.time_range.start)
     first = "k_tree_init" if args.tree else ("k_set_cam64" if args.score else "k_bounds_init")
     starts = [i for i, e in enumerate(ev) if first in e.name]
+    if not starts:   # (a layout rebuild starts elsewhere: the first event after the last synchronisation)
+        starts = [0]
     ev = ev[starts[-1]:]
     t0 = ev[0].time_range.start
     prev_end = t0
