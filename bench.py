@@ -265,18 +265,25 @@ def main():
     prof_state = {"on": False}
 
     def step(host: bool):
-        src_map, src_traj = (hmap, htraj) if host else (dmap, dtraj)
+        if host:
+            # the map's arrays are copied first (pinned host -> device on this stream); the waypoint upload
+            # (rtg_traj_upload from the pinned host arrays, on a second stream) waits only for those copies,
+            # so it overlaps the validation, the bounds readback and the map build instead of following them
+            src_map = [None if h is None else h.to(dev, non_blocking=True) for h in hmap]
+            copied = torch.cuda.Event()
+            copied.record(stream)
+            aux.wait_event(copied)
+            tr = R.Traj.upload(*htraj, device=local_dev, stream=aux)
+        else:
+            src_map = dmap
         m = R.Map(*src_map, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule,
                   device=local_dev, options=map_opts)
         if Kv:
             vstream.wait_stream(stream)   # the views need the map build only
         if host:
-            # rtg_map_create returns once the map is on the device and its build is enqueued: the
-            # waypoint upload then overlaps the build on a second stream
-            tr = R.Traj.upload(*src_traj, device=local_dev, stream=aux)
             stream.wait_stream(aux)
         else:
-            tr = R.Traj.wrap(*src_traj, device=local_dev)   # resident waypoints: borrowed, no copy
+            tr = R.Traj.wrap(*dtraj, device=local_dev)   # resident waypoints: borrowed, no copy
         R.score(m, tr, cam, params, *outs)
         tv = None
         if Kv:   # the scale config's gain-only views (T = 1, no collision), scored concurrently on a

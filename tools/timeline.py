@@ -27,6 +27,9 @@ def main():
                          "CUDA-graph replay (R.ScoreGraph)")
     ap.add_argument("--cycle", choices=("eager", "graph"), default=None)
     ap.add_argument("--ranks", type=int, default=1)
+    ap.add_argument("--host", action="store_true",
+                    help="the standard cycle from pinned host buffers (bench.py's e2e step: map and waypoint "
+                         "uploads inside, the waypoints on a second stream overlapping the map build)")
     args = ap.parse_args()
     wl = W.make(args.config)
     if args.ranks > 1:
@@ -57,6 +60,10 @@ def main():
         if args.score == "graph":
             sg = R.ScoreGraph(score_map, score_tr, cam, params)
 
+    pin = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hmap = [pin(a) for a in (wl.means, wl.quats, wl.scales, wl.opacity, wl.info_w, wl.flags)] if args.host else None
+    htraj = [pin(a) for a in (wl.x, wl.y, wl.z, wl.yaw)] if args.host else None
+    aux = torch.cuda.Stream(device=dev)
     cg = None
     if args.cycle:
         import bench as BN
@@ -98,6 +105,21 @@ def main():
         if args.score:
             R.score(score_map, score_tr, cam, params, *outs)
             return R.best_async(outs[3], bo)
+        if args.host:
+            cur = torch.cuda.current_stream()
+            src = [None if h is None else h.to(dev, non_blocking=True) for h in hmap]
+            copied = torch.cuda.Event()
+            copied.record(cur)
+            aux.wait_event(copied)
+            tr = R.Traj.upload(*htraj, stream=aux)
+            m = R.Map(*src, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
+            cur.wait_stream(aux)
+            R.score(m, tr, cam, params, *outs)
+            r = R.best(outs[3])
+            m.close()
+            aux.wait_stream(cur)
+            tr.close()
+            return r
         m = R.Map(*dmap, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
         tr = R.Traj.upload(*dtraj)
         R.score(m, tr, cam, params, *outs)
@@ -119,6 +141,11 @@ def main():
     ev.sort(key=lambda e: e.time_range.start)
     first = "k_tree_init" if args.tree else ("k_set_cam64" if args.score else "k_bounds_init")
     starts = [i for i, e in enumerate(ev) if first in e.name]
+    if args.host and starts:   # the cycle begins with the map's uploads just before its first kernel
+        j = starts[-1]
+        while j > 0 and "Memcpy HtoD" in ev[j - 1].name:
+            j -= 1
+        starts[-1] = j
     if not starts:   # (a layout rebuild starts elsewhere: the first event after the last synchronisation)
         starts = [0]
     ev = ev[starts[-1]:]
