@@ -164,14 +164,16 @@ constexpr int kWarps = 8;   // warps per block of the persistent culled kernels
 constexpr int kColChunk = RTG_COL_CHUNK;
 static_assert(kColChunk >= 1 && kColChunk <= 32, "k_col_culled holds one waypoint of a chunk per lane");
 
+template <int kChunk>
 __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
     const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ Zw, int K, int T,
     const CRec* __restrict__ crec, const CMat* __restrict__ cmat, const CSrc* __restrict__ csrc, const rtg_robot rb,
     const int* __restrict__ cstart, ColGridK g, float gq, int* __restrict__ first_col,
     unsigned char* __restrict__ wp_col, int all_waypoints, int* __restrict__ counter,
     unsigned long long* __restrict__ stats) {
+    static_assert(kChunk >= 1 && kChunk <= 32, "k_col_culled holds one waypoint of a chunk per lane");
     const int lane = threadIdx.x & 31;
-    const int nch = (T + kColChunk - 1) / kColChunk;
+    const int nch = (T + kChunk - 1) / kChunk;
     const long long items = (long long)K * nch;
     unsigned nref = 0;
     unsigned long long ntest = 0;
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_col_culled(
         e = __shfl_sync(kFull, e, 0);
         if (e >= items) break;
         const int c = e / K, k = e - c * K;
-        const int t0 = c * kColChunk, t1 = min(T, t0 + kColChunk);
+        const int t0 = c * kChunk, t1 = min(T, t0 + kChunk);
         if (lane == 0) fc = *(volatile int*)(first_col + k);
         fc = __shfl_sync(kFull, fc, 0);
         if (!all_waypoints && fc < t0) continue;
@@ -539,7 +541,7 @@ int g_occ_col = 0, g_sms = 0;
 void occupancy(int dev) {
     if (g_sms) return;
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_col, k_col_culled, kWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ_col, k_col_culled<kColChunk>, kWarps * 32, 0);
     if (g_occ_col < 1) g_occ_col = 1;
 }
 }  // namespace
@@ -587,12 +589,33 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
         g.ox = m->cg.ox; g.oy = m->cg.oy; g.oz = m->cg.oz; g.h = m->cg.h;
         g.R = m->rb_max * (1.0f + 2e-5f) + 1e-4f;
         g.nx = m->cg.nx; g.ny = m->cg.ny; g.nz = m->cg.nz;
-        const long long items = (long long)K * ((T + kColChunk - 1) / kColChunk);
+        // waypoints per work item: kColChunk (10), or 5 / 3 when that would leave fewer than 20 work items per
+        // resident warp (small plans: the kernel is latency-bound, so the chunks' parallelism beats the shared
+        // candidate loads; measured: room 0.140 -> 0.067 ms at 3, multi-room 0.153 -> 0.101 at 5,
+        // outdoor and scale stay at 10)
+        const long long slots = (long long)g_sms * g_occ_col * kWarps;
+        int chunk = 3;
+        for (const int c : {kColChunk, 5}) {
+            if (c <= kColChunk && (long long)K * ((T + c - 1) / c) >= 20 * slots) {
+                chunk = c;
+                break;
+            }
+        }
+        if (chunk > kColChunk) chunk = kColChunk;
+        static const int chunk_env = getenv("RTG_COL_CHUNK_RT") ? atoi(getenv("RTG_COL_CHUNK_RT")) : 0;
+        if (chunk_env == 3 || chunk_env == 5 || chunk_env == kColChunk) chunk = chunk_env;   // (A/B measurements)
+        const long long items = (long long)K * ((T + chunk - 1) / chunk);
         int blocks = (int)std::min<long long>((items + kWarps - 1) / kWarps, 1LL << 30);
         int cap = g_sms * g_occ_col;
         if (blocks > cap) blocks = cap;
-        note_launch(), k_col_culled<<<blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat, m->csrc, m->robot,
-                                                     m->cstart, g, m->gq, first_col, wp_col, all_wp, counter, stats);
+#define RTG_COL_LAUNCH(C)                                                                                         \
+    note_launch(), k_col_culled<C><<<blocks, kWarps * 32, 0, st>>>(tr->x, tr->y, tr->z, K, T, m->crec, m->cmat,       \
+                                                                   m->csrc, m->robot, m->cstart, g, m->gq, first_col, \
+                                                                   wp_col, all_wp, counter, stats)
+        if (chunk == 3) RTG_COL_LAUNCH(3);
+        else if (chunk == 5) RTG_COL_LAUNCH(5);
+        else RTG_COL_LAUNCH(kColChunk);
+#undef RTG_COL_LAUNCH
     }
     return cudaGetLastError();
 }
