@@ -602,7 +602,8 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
             }
         }
         if (chunk > kColChunk) chunk = kColChunk;
-        static const int chunk_env = getenv("RTG_COL_CHUNK_RT") ? atoi(getenv("RTG_COL_CHUNK_RT")) : 0;
+        const char* chunk_var = getenv("RTG_COL_CHUNK_RT");   // (read per call: the parity test switches it)
+        const int chunk_env = chunk_var ? atoi(chunk_var) : 0;
         if (chunk_env == 3 || chunk_env == 5 || chunk_env == kColChunk) chunk = chunk_env;   // (A/B measurements)
         const long long items = (long long)K * ((T + chunk - 1) / chunk);
         int blocks = (int)std::min<long long>((items + kWarps - 1) / kWarps, 1LL << 30);

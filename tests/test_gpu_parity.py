@@ -11,6 +11,7 @@ Bars (BASELINE.json north_star):
 import ctypes
 import dataclasses
 import math
+import os
 
 import numpy as np
 import pytest
@@ -1091,3 +1092,32 @@ def test_cycle_graph_with_views_equals_eager(R, room):
     tr.close()
     tv.close()
     lm.close()
+
+
+@pytest.mark.gpu
+def test_collision_chunk_variants_identical(R, room):
+    """k_col_culled tests 10, 5 or 3 waypoints per work item (picked from the plan size); every
+    choice gives the same first collisions, feasibility, gains and utilities bit for bit, on the room map
+    (walls: many candidates per waypoint) and with all waypoints reported (debug path)."""
+    m = R.map_from_workload(room)
+    tr = R.traj_from_workload(room)
+    p = R.make_params()
+    res = {}
+    old = os.environ.get("RTG_COL_CHUNK_RT")
+    try:
+        for ch in ("10", "5", "3"):
+            os.environ["RTG_COL_CHUNK_RT"] = ch
+            res[ch] = [a.clone() for a in R.score(m, tr, room.camera, p)]
+            res[ch + "dbg"] = R.score_debug(m, tr, room.camera, p)["wp_col"].clone()
+    finally:
+        if old is None:
+            os.environ.pop("RTG_COL_CHUNK_RT", None)
+        else:
+            os.environ["RTG_COL_CHUNK_RT"] = old
+    for ch in ("5", "3"):
+        for a, b in zip(res["10"], res[ch]):
+            assert torch.equal(a.view(torch.uint8), b.view(torch.uint8)), ch
+        assert torch.equal(res["10dbg"], res[ch + "dbg"]), ch
+    assert 0 < int(res["10"][1].sum()) < room.K, "some trajectories collide, some do not"
+    m.close()
+    tr.close()
