@@ -591,7 +591,7 @@ cudaError_t launch_phase_a(rtg_map_s* m, rtg_traj_s* tr, int mode, int* first_co
         g.nx = m->cg.nx; g.ny = m->cg.ny; g.nz = m->cg.nz;
         // waypoints per work item: kColChunk (10), or 5 / 3 when that would leave fewer than 20 work items per
         // resident warp (small plans: the kernel is latency-bound, so the chunks' parallelism beats the shared
-        // candidate loads; measured: room 0.140 -> 0.067 ms at 3, multi-room 0.153 -> 0.101 at 5,
+        // candidate loads; measured: room 0.140 -> 0.069 ms at 3, multi-room 0.134 -> 0.090 at 5,
         // outdoor and scale stay at 10)
         const long long slots = (long long)g_sms * g_occ_col * kWarps;
         int chunk = 3;
