@@ -438,11 +438,22 @@ __global__ void k_best(const double* __restrict__ u, int K, long long base, Best
     __shared__ int si[1024];
     double bv = -INFINITY;
     int bi = -1;
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        double v = u[k];
-        if (v > bv) {   // strict: keeps the lowest index among equal values (k ascending per thread)
-            bv = v;
-            bi = k;
+    // eight loads in flight per thread (a single block reads all K: one dependent load per step would
+    // cost K / blockDim.x memory latencies), then compared in index order
+    constexpr int kU = 8;
+    for (int k0 = threadIdx.x; k0 < K; k0 += kU * blockDim.x) {
+        double v[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int k = k0 + j * (int)blockDim.x;
+            v[j] = k < K ? u[k] : -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            if (v[j] > bv) {   // strict: keeps the lowest index among equal values (k ascending per thread)
+                bv = v[j];
+                bi = k0 + j * (int)blockDim.x;
+            }
         }
     }
     sv[threadIdx.x] = bv;
