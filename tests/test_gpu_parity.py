@@ -1121,3 +1121,28 @@ def test_collision_chunk_variants_identical(R, room):
     assert 0 < int(res["10"][1].sum()) < room.K, "some trajectories collide, some do not"
     m.close()
     tr.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk", ["auto", "10", "5"])
+def test_long_trajectories_parity(R, chunk):
+    """Long plans: T = 997 waypoints (prime: no chunk of 3, 5 or 10 divides it) of slow unicycles that
+    leave the 12 x 10 m room, against the oracle waypoint by waypoint.  The collision kernel picks 3
+    waypoints per work item for this small plan (or the forced 10 / 5); first collisions may sit in any
+    chunk, and most waypoints lie outside the map."""
+    wl = W.room(N=30_000, K=6, T=997, traj_seed=5)
+    orc = O.score(wl)
+    old = os.environ.get("RTG_COL_CHUNK_RT")
+    try:
+        if chunk != "auto":
+            os.environ["RTG_COL_CHUNK_RT"] = chunk
+        gpu = gpu_run(R, wl, "culled")
+    finally:
+        if old is None:
+            os.environ.pop("RTG_COL_CHUNK_RT", None)
+        else:
+            os.environ["RTG_COL_CHUNK_RT"] = old
+    check_waypoints(gpu, orc, gpu["info"].fixed_point_shift)
+    check_trajectories(gpu, orc, wl.T)
+    assert np.any(gpu["first_col"] < wl.T), "some trajectory collides"
+    assert np.any((gpu["first_col"] > 10) & (gpu["first_col"] < wl.T)), "a collision after the first chunk"
