@@ -967,6 +967,22 @@ def test_layout_map_rebuild_equals_create(R, room, which):
     lm.check()
     fc, fe, g, u = R.score(lm, tr, wl.camera, p)
     assert bool((fe == 1).all()) and float(g.abs().max()) == 0.0
+    # dense mode reads every record slot up to the capacity: the stale records of the earlier rebuild
+    # must be padded away (the rebuild pads from its device counts)
+    pd = R.make_params(flags=R.SCORE_FULL_GAIN, mode=R.MODE_DENSE)
+    fc, fe, g, u = R.score(lm, tr, wl.camera, pd)
+    assert bool((fe == 1).all()) and float(g.abs().max()) == 0.0
+    # a smaller rebuild over the stale records: equal to rtg_map_create on the same half, in both modes
+    half = [None if a is None else a[..., : wl.N // 2].contiguous() for a in arrs]
+    lm.rebuild(*half)
+    lm.check()
+    ref_half = R.Map(*half, r_robot=wl.robot.r_robot, lambda_g=wl.robot.lambda_g, collide_rule=wl.robot.rule)
+    for params in (p, pd):
+        a = R.score_debug(ref_half, tr, wl.camera, params)
+        b = R.score_debug(lm, tr, wl.camera, params)
+        for key in ("wp_gain", "wp_nh", "wp_nl", "wp_col"):
+            assert torch.equal(a[key], b[key]), (key, params.mode)
+    ref_half.close()
     lm.rebuild(*arrs)
     again = R.score_debug(lm, tr, wl.camera, p)
     assert torch.equal(again["wp_gain"], outs[1]["wp_gain"]) and torch.equal(again["wp_col"], outs[1]["wp_col"])
